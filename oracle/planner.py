@@ -1,0 +1,139 @@
+"""Oracle planner: Temporal Adaptation (Eq. 4) + Spatial Adaptation (Eq. 5).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PAPER.md L179-185 (§III-C, Eq. 4):
+    M_i = M_base                         if a*v_max <  v_i <= v_max
+    M_i = 1/2 M_base + 1/2 M_warmup      if b*v_max <  v_i <= a*v_max
+    (excluded)                           if v_i <= b*v_max
+PAPER.md L187-198 (§III-D, Eq. 5):
+    P_i = (v_i/M_i) / sum_j (v_j/M_j) * P_total
+Alg. 1 L114-119 apply them per GPU.  L284: M_base=100, M_warmup=4,
+P_total=32, a=0.75, b=0.25.
+
+Readings:
+  R2  Eq. 4 boundaries as printed (v <= b*v_max is excluded), exact
+      rational comparisons.
+  R3  (M_base - M_warmup) must be even when a tier-2 GPU exists.
+  R4  "LCM-minimising": tier 2 runs stride 2 after warmup; sync_period =
+      lcm of post-warmup strides (1 or 2).
+  R5  Eq. 5 integerised by the D'Hondt divisor method on weights v_i/M_i,
+      >= 1 unit per included GPU, ties to the lowest rank.
+  R6  one unit = rows_per_unit latent rows.
+  R7  Eq. 5 uses M_i of Eq. 4 (flag SIZER_INTERVAL: per-round step counts).
+  R8  rank order, top to bottom.
+Written with plain Python integers and fractions.Fraction (exact).
+"""
+from __future__ import annotations
+
+from fractions import Fraction
+
+NO_TA = 1
+NO_SA = 2
+SIZER_INTERVAL = 4
+FORCE_UNITS = 8
+
+
+class PlanError(ValueError):
+    """Invalid parameters (maps to STADI_EINVAL at the C boundary)."""
+
+
+def tiers(speed, a=(3, 4), b=(1, 4), flags=0):
+    """Eq. 4 tier per GPU: 1 = M_base, 2 = reduced, 0 = excluded (R2)."""
+    vmax = max(speed)
+    out = []
+    for v in speed:
+        if flags & NO_TA:
+            out.append(1)
+        elif Fraction(v) > Fraction(a[0], a[1]) * vmax:       # a*v_max < v_i
+            out.append(1)
+        elif Fraction(v) > Fraction(b[0], b[1]) * vmax:       # b*v_max < v_i <= a*v_max
+            out.append(2)
+        else:                                                 # v_i <= b*v_max
+            out.append(0)
+    return out
+
+
+def steps_of(tier, m_base, m_warmup):
+    """Eq. 4 right-hand sides (L183)."""
+    if tier == 1:
+        return m_base
+    if tier == 2:
+        return Fraction(m_base, 2) + Fraction(m_warmup, 2)
+    return 0
+
+
+def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
+         flags=0, forced_units=None):
+    """Return the assignment (M_i, P_i) per GPU plus derived schedule facts."""
+    n = len(speed)
+    if n < 1 or n > 64:
+        raise PlanError("n_gpus out of range")
+    if any(int(v) <= 0 for v in speed):
+        raise PlanError("speed must be > 0")
+    if not (0 < b[0] * a[1] < a[0] * b[1] and a[0] < a[1] and b[0] > 0):
+        raise PlanError("need 0 < b < a < 1")
+    if not (1 <= m_warmup <= m_base):
+        raise PlanError("need 1 <= M_warmup <= M_base")
+    if p_total < 1 or rows_per_unit < 1:
+        raise PlanError("bad p_total / rows_per_unit")
+
+    tier = tiers(speed, a, b, flags)
+    any_slow = any(t == 2 for t in tier)
+    if any_slow and (m_base - m_warmup) % 2:
+        raise PlanError("R3: (M_base - M_warmup) must be even with a tier-2 GPU")
+    steps = [steps_of(t, m_base, m_warmup) for t in tier]
+    assert all(Fraction(s).denominator == 1 for s in steps)
+    steps = [int(s) for s in steps]
+    inc = [i for i in range(n) if tier[i] > 0]
+    if p_total < len(inc):
+        raise PlanError("P_total < number of included GPUs")
+
+    units = [0] * n
+    if flags & FORCE_UNITS:
+        if forced_units is None or len(forced_units) != n:
+            raise PlanError("forced units missing")
+        if sum(forced_units) != p_total:
+            raise PlanError("forced units must sum to P_total")
+        for i in range(n):
+            if (tier[i] == 0) != (forced_units[i] == 0):
+                raise PlanError("forced units: included GPUs need >= 1, excluded 0")
+        units = list(forced_units)
+    elif flags & NO_SA:
+        q, r = divmod(p_total, len(inc))
+        for k, i in enumerate(inc):
+            units[i] = q + (1 if k < r else 0)
+    else:
+        # Eq. 5 weights w_i = v_i / M'_i.  D'Hondt: every included GPU starts
+        # with one unit; each further unit goes to argmax w_i/(P_i+1), i.e.
+        # argmin (P_i+1) * M'_i / v_i, ties to the smallest rank (R5).
+        if flags & SIZER_INTERVAL:
+            mprime = [(2 if (tier[i] == 1 and any_slow) else 1) for i in range(n)]
+        else:
+            mprime = steps
+        for i in inc:
+            units[i] = 1
+        for _ in range(p_total - len(inc)):
+            best = None
+            best_val = None
+            for i in inc:
+                val = Fraction((units[i] + 1) * mprime[i], int(speed[i]))
+                if best_val is None or val < best_val:
+                    best, best_val = i, val
+            units[best] += 1
+
+    row_begin, rows = [0] * n, [0] * n
+    acc = 0
+    for i in range(n):                       # R8: rank order, top to bottom
+        row_begin[i] = acc * rows_per_unit
+        rows[i] = units[i] * rows_per_unit
+        acc += units[i]
+    makespan = max(Fraction(steps[i] * units[i], int(speed[i])) for i in inc)
+    sync_period = 2 if any_slow else 1
+    return dict(
+        n_gpus=n, m_base=m_base, m_warmup=m_warmup, p_total=p_total,
+        rows_per_unit=rows_per_unit, tier=tier, steps=steps, units=units,
+        row_begin=row_begin, rows=rows, sync_period=sync_period,
+        n_exchange_rounds=m_warmup + (m_base - m_warmup) // sync_period,
+        makespan=makespan,
+    )

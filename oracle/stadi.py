@@ -1,0 +1,116 @@
+"""Oracle STADI run: Algorithm 1 end to end, all GPUs simulated in one process.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PAPER.md Alg. 1 (L108-L155): Step 1 temporal adaptation (Eq. 4) ->
+Step 2 spatial adaptation (Eq. 5) -> Step 3 inference: warmup steps with the
+buffer updated synchronously (L122-L128), then per GPU: fast GPUs alternate
+"update buffer asynchronously + all-gather" (even) and "no update for buffer"
+(odd); slow GPUs update asynchronously every (stride-2) step (L130-L152).
+Each GPU denoises only its patch p_i (L125, L171, DistriFusion-style stale
+activations, L80).
+
+Protocol (SURVEY §8(c) O5/O6 and readings R9-R17):
+* "buffer" = per attention site, the K/V rows each GPU published for an
+  exchange version.  A step reads version ``read_ver`` for every *other* GPU's
+  rows and its own rows fresh (R14); it publishes its fresh K/V as
+  ``pub_ver``.  read_ver == pub_ver (warmup) is a layer-synchronous fresh
+  exchange (R9).
+* Steps are processed grouped by fast-grid index m ("phases"); inside a phase
+  every participating GPU runs in lock-step per layer: all publish, then all
+  read.  Only warmup phases depend on the lock-step; stale phases read only
+  versions published in earlier phases.
+* R12 owner-computes: each GPU updates only its own rows with its own grid;
+  the final (synchronous) all-gather concatenates the bands.  Intermediate
+  "Get x by synchronous All-Gather" lines do not change any band.
+"""
+from __future__ import annotations
+
+from . import diffusion, dit, planner, schedule
+
+
+def _group_phases(plan):
+    """All ranks' schedule entries grouped by fast-grid index m."""
+    phases = {}
+    for r in range(plan["n_gpus"]):
+        for st in schedule.schedule(plan, r):
+            phases.setdefault(st.m, []).append((r, st))
+    return [phases[m] for m in sorted(phases)]
+
+
+def run(cfg, weights, x_T, cond, plan, return_trace=False):
+    """Execute STADI for one request.  x_T: full noise [H, W, C] (any float).
+
+    Returns the final latent [H, W, C] (float64) assembled from the bands.
+    """
+    model = dit.DiT(cfg, weights)
+    abar = diffusion.alpha_bar("linear" if cfg["schedule"] == "linear" else "scaled_linear")
+    B = dit.batch_of(cfg)
+    y = model.caption(cond)
+    p = cfg["patch"]
+    inc = [r for r in range(plan["n_gpus"]) if plan["tier"][r] > 0]
+    band = {r: x_T[plan["row_begin"][r]:plan["row_begin"][r] + plan["rows"][r]].astype("float64")
+            for r in inc}
+    store = {}                                   # (version, layer, rank) -> (k, v)
+    trace = []
+    for phase in _group_phases(plan):
+        parts = []
+        for r, st in phase:
+            mods, fin = model.modulations(st.t, cond)
+            h = model.embed(band[r], plan["row_begin"][r] // p, B)
+            parts.append(dict(r=r, st=st, mods=mods, fin=fin, h=h))
+        for l in range(model.depth):
+            fresh = {}
+            for P in parts:                      # everyone computes + publishes first
+                q, k, v = model.block_qkv(l, P["h"], P["mods"][l])
+                fresh[P["r"]] = (q, k, v)
+                if P["st"].pub_ver != schedule.NONE:
+                    store[(P["st"].pub_ver, l, P["r"])] = (k, v)
+            for P in parts:                      # then reads version read_ver
+                r, st = P["r"], P["st"]
+                ks, vs = [], []
+                for j in inc:                    # full image K/V in row order
+                    if j == r:
+                        kj, vj = fresh[r][1], fresh[r][2]      # R14: own rows fresh
+                    else:
+                        kj, vj = store[(st.read_ver, l, j)]
+                    ks.append(kj)
+                    vs.append(vj)
+                P["h"] = model.block_rest(l, P["h"], fresh[r][0],
+                                          _cat(ks), _cat(vs), P["mods"][l], y)
+        for P in parts:                          # eps on own band + Eq. 3 on own rows
+            r, st = P["r"], P["st"]
+            eps = dit.guided_eps(cfg, model.final(P["h"], P["fin"], band[r].shape[0]))
+            band[r] = diffusion.ddim_step(abar, band[r], eps, st.t, st.t_prev)
+            if return_trace:
+                trace.append((st.m, r, st.kind, band[r].copy()))
+    import numpy as np
+    out = np.concatenate([band[r] for r in inc], axis=0)   # final synchronous all-gather
+    return (out, trace) if return_trace else out
+
+
+def _cat(xs):
+    import numpy as np
+    return np.concatenate(xs, axis=1)
+
+
+def sequential(cfg, weights, x_T, cond, m_base):
+    """Non-distributed DDIM with M_base steps on the fast grid (the "Origin"
+    method of Table II)."""
+    model = dit.DiT(cfg, weights)
+    abar = diffusion.alpha_bar("linear" if cfg["schedule"] == "linear" else "scaled_linear")
+    y = model.caption(cond)
+    x = x_T.astype("float64")
+    grid = schedule.fast_grid(m_base)
+    for m, t in enumerate(grid):
+        t_prev = grid[m + 1] if m + 1 < m_base else schedule.FINAL
+        eps = dit.guided_eps(cfg, model.forward_full(x, t, cond, y))
+        x = diffusion.ddim_step(abar, x, eps, t, t_prev)
+    return x
+
+
+def plan_for(cfg, speed, m_base, m_warmup, flags=0, forced_units=None):
+    """Planner call with the DiT unit (R6: one unit = one token row = p latent rows)."""
+    p = cfg["patch"]
+    return planner.plan(speed, m_base, m_warmup, cfg["latent_h"] // p, p,
+                        flags=flags, forced_units=forced_units)

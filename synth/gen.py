@@ -1,0 +1,75 @@
+"""Seeded input generators (numpy PCG64).  No method arithmetic here.
+
+SURVEY.md §8(d) "Common inputs": noise ~ N(0,1) fp32 (seed 1234), weights
+seed 0, conditioning seed 42.  R22: random init, not adaLN-Zero.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import configs
+
+
+def _rng(seed: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+def weights(cfg: dict, seed: int = configs.SEED_WEIGHTS) -> dict[str, np.ndarray]:
+    """Random-init weights in manifest order (float32, C-contiguous)."""
+    rng = _rng(seed)
+    depth = cfg["depth"]
+    out: dict[str, np.ndarray] = {}
+    for name, shape, kind in configs.manifest(cfg):
+        a = rng.standard_normal(shape, dtype=np.float32)
+        if kind == "w":
+            a *= np.float32(1.0 / np.sqrt(shape[1]))
+        elif kind == "wo":
+            a *= np.float32(1.0 / np.sqrt(shape[1]) / np.sqrt(2.0 * depth))
+        elif kind == "b":
+            a *= np.float32(0.02)
+        elif kind == "emb":
+            a *= np.float32(0.5)
+        elif kind == "table":
+            a *= np.float32(1.0 / np.sqrt(cfg["hidden"]))
+        else:  # pragma: no cover
+            raise ValueError(kind)
+        out[name] = np.ascontiguousarray(a)
+    return out
+
+
+def noise(cfg: dict, seed: int = configs.SEED_NOISE) -> np.ndarray:
+    """Initial latent x_T: [H, W, C_in] float32 ~ N(0, 1) (NHWC, full image)."""
+    return _rng(seed).standard_normal(
+        (cfg["latent_h"], cfg["latent_w"], cfg["c_in"]), dtype=np.float32)
+
+
+def cond(cfg: dict, seed: int = configs.SEED_COND) -> dict:
+    """Conditioning for the internal batch (index 0 = unconditional when CFG).
+
+    class-conditional: labels [B] (null class = num_classes for the uncond row).
+    text-conditional:  text [B, L_txt, D_txt] float32 ~ N(0,1) (R21: synthetic
+    T5-shaped embeddings; row 0 plays the null caption).
+    """
+    B = configs.batch(cfg)
+    if cfg["cond"] == "class":
+        lab = [cfg["class_label"]] if B == 1 else [cfg["num_classes"], cfg["class_label"]]
+        return {"labels": np.asarray(lab, dtype=np.int32)}
+    t = _rng(seed).standard_normal((B, cfg["text_len"], cfg["text_dim"]), dtype=np.float32)
+    return {"text": t}
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round float32 -> bfloat16 (round-to-nearest-even), returned as float32.
+
+    Input transform for bf16 parity runs (R22: the oracle consumes the same
+    bf16-rounded weights the device stores).  NaN/Inf are not expected here.
+    """
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    r = ((u + 0x7FFF + lsb) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32).reshape(a.shape)
+
+
+def weights_bf16(w: dict[str, np.ndarray]) -> dict[str, np.ndarray]:
+    return {k: bf16_round(v) for k, v in w.items()}

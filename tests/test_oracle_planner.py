@@ -1,0 +1,209 @@
+"""Pins for oracle/planner.py (Eq. 4 / Eq. 5) and oracle/schedule.py (Alg. 1).
+
+Pinned against: hand-checkable golden cases (tests/golden/*.json, cited),
+brute-force min-makespan enumeration, closed-form counts, L310's statement of
+which occupancy pairs trigger temporal adaptation, and Theorem 2's grid
+alignment.  No GPU.
+"""
+import itertools
+import json
+import os
+import random
+from fractions import Fraction
+
+import pytest
+
+from oracle import planner, schedule
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", _gold("planner_appA.json")["cases"], ids=lambda c: c["name"])
+def test_golden_cases(case):
+    p = planner.plan(case["speed"], case["m_base"], case["m_warmup"], case["p_total"])
+    assert p["steps"] == case["steps"]
+    assert p["units"] == case["units"]
+    q = planner.plan(case["speed"], case["m_base"], case["m_warmup"], case["p_total"],
+                     flags=planner.SIZER_INTERVAL)
+    assert q["units"] == case["units_interval"]
+
+
+def _brute_min_makespan(speed, steps, p_total):
+    """Enumerate every integer split (>=1 per included GPU) and return the
+    minimal max_i M_i P_i / v_i — Eq. 5's objective "all GPUs finish ... within
+    similar latency" (L198) made exact."""
+    inc = [i for i in range(len(speed)) if steps[i] > 0]
+    best = None
+    for split in itertools.product(range(1, p_total + 1), repeat=len(inc)):
+        if sum(split) != p_total:
+            continue
+        ms = max(Fraction(steps[i] * s, speed[i]) for i, s in zip(inc, split))
+        best = ms if best is None or ms < best else best
+    return best
+
+
+def test_dhondt_is_min_makespan():
+    rng = random.Random(7)
+    for _ in range(400):
+        n = rng.randint(1, 4)
+        speed = [rng.randint(1, 1 << 16) for _ in range(n)]
+        mb = rng.choice([10, 20, 50, 100])
+        mw = rng.choice([2, 4])
+        P = rng.randint(n, 12)
+        try:
+            p = planner.plan(speed, mb, mw, P)
+        except planner.PlanError:
+            continue
+        assert p["makespan"] == _brute_min_makespan(speed, p["steps"], P)
+
+
+def test_invariants_random():
+    rng = random.Random(11)
+    for _ in range(2000):
+        n = rng.randint(1, 16)
+        speed = [rng.randint(1, 1 << 40) for _ in range(n)]
+        P = rng.randint(n, 256)
+        for flags in (0, planner.NO_TA, planner.NO_SA, planner.NO_TA | planner.NO_SA,
+                      planner.SIZER_INTERVAL):
+            try:
+                p = planner.plan(speed, 50, 4, P, rows_per_unit=2, flags=flags)
+            except planner.PlanError:
+                continue
+            assert sum(p["units"]) == P
+            for i in range(n):
+                assert (p["tier"][i] == 0) == (p["units"][i] == 0)
+                assert p["rows"][i] == 2 * p["units"][i]
+            assert p["row_begin"][0] == 0
+            for i in range(1, n):
+                assert p["row_begin"][i] == p["row_begin"][i - 1] + p["rows"][i - 1]
+            # the fastest GPU is always tier 1 (Eq. 4: a*v_max < v_max)
+            assert p["tier"][speed.index(max(speed))] == 1
+            if flags & planner.NO_TA:
+                assert all(t == 1 for t in p["tier"])
+            if flags & planner.NO_SA:
+                u = [x for x in p["units"] if x]
+                assert max(u) - min(u) <= 1
+            # scale invariance: Eq. 4/5 depend only on speed ratios
+            k = rng.randint(2, 1000)
+            p2 = planner.plan([v * k for v in speed], 50, 4, P, rows_per_unit=2, flags=flags)
+            assert p2["units"] == p["units"] and p2["tier"] == p["tier"]
+
+
+def test_eq4_boundaries_exact():
+    # R2: v = a*v_max exactly is NOT tier 1 (needs a*v_max < v); v = b*v_max is excluded.
+    p = planner.plan([4, 3, 1], 100, 4, 8)
+    assert p["tier"] == [1, 2, 0] and p["steps"] == [100, 52, 0]
+    p = planner.plan([400, 301, 101], 100, 4, 8)
+    assert p["tier"] == [1, 1, 2]
+
+
+def test_l310_trigger_pattern():
+    # "[0%, 20%] and [35%, 45%] ... load balancing is achieved solely
+    # by adjusting the patch size"; the other Fig. 8 pairs trigger TA (Table III +TA).
+    def speeds(occ):
+        return [round((100 - o) * 65536 / 100) for o in occ]
+    no_ta = [(0, 20), (35, 45)]
+    ta = [(0, 40), (0, 60), (30, 50), (25, 55)]
+    for occ in no_ta:
+        assert 2 not in planner.plan(speeds(occ), 100, 4, 32)["tier"]
+    for occ in ta:
+        assert 2 in planner.plan(speeds(occ), 100, 4, 32)["tier"]
+
+
+def test_eq4_m_i_value():
+    # Eq. 4 second case: 1/2 M_base + 1/2 M_warmup (L183)
+    p = planner.plan([10, 6], 100, 4, 32)
+    assert p["steps"] == [100, 52]
+    p = planner.plan([10, 6], 50, 4, 32)
+    assert p["steps"] == [50, 27]
+
+
+def test_eq5_continuous_consistency():
+    # With divisible totals the integer split equals Eq. 5 exactly:
+    # v/M = [1/10, 1/10, 1/5] -> P = [1/4, 1/4, 1/2] * 16 = [4, 4, 8].
+    p = planner.plan([1, 1, 2], 10, 2, 16, flags=planner.NO_TA)
+    assert p["units"] == [4, 4, 8]
+
+
+def test_plan_errors():
+    bad = [
+        dict(speed=[], m_base=10, m_warmup=2, p_total=8),
+        dict(speed=[0, 1], m_base=10, m_warmup=2, p_total=8),
+        dict(speed=[1, 1], m_base=10, m_warmup=11, p_total=8),
+        dict(speed=[1, 1], m_base=10, m_warmup=0, p_total=8),
+        dict(speed=[1, 1, 1], m_base=10, m_warmup=2, p_total=2),
+        dict(speed=[10, 6], m_base=11, m_warmup=2, p_total=8),   # R3: odd K with tier 2
+    ]
+    for kw in bad:
+        with pytest.raises(planner.PlanError):
+            planner.plan(**kw)
+    with pytest.raises(planner.PlanError):
+        planner.plan([1, 1], 10, 2, 8, a=(1, 4), b=(3, 4))
+    with pytest.raises(planner.PlanError):
+        planner.plan([1, 1], 10, 2, 8, flags=planner.FORCE_UNITS, forced_units=[3, 4])
+
+
+def test_forced_units():
+    # Table II splits 24:8 / 16:16 / 8:24 of P_total = 32 (L294-L308)
+    for split in ([24, 8], [16, 16], [8, 24]):
+        p = planner.plan([10, 6], 100, 4, 32, flags=planner.FORCE_UNITS, forced_units=split)
+        assert p["units"] == split
+
+
+# ---------------------------------------------------------------- schedule
+def test_schedule_c1_golden():
+    g = _gold("schedule_C1.json")
+    p = planner.plan([65536, 32768], 10, 2, 8)
+    for r in (0, 1):
+        got = [[s.m, s.t, s.t_prev, s.kind, s.read_ver, s.pub_ver]
+               for s in schedule.schedule(p, r)]
+        assert got == g[f"rank{r}"]
+
+
+def test_fast_grid_leading_spacing():
+    assert schedule.fast_grid(10) == [901, 801, 701, 601, 501, 401, 301, 201, 101, 1]
+    assert schedule.fast_grid(50)[:3] == [981, 961, 941] and schedule.fast_grid(50)[-1] == 1
+    assert schedule.fast_grid(20)[0] == 951
+
+
+@pytest.mark.parametrize("mb,mw", [(10, 2), (50, 4), (100, 4), (20, 4)])
+def test_schedule_counts_and_alignment(mb, mw):
+    p = planner.plan([100, 60, 100, 30], mb, mw, 16)
+    assert p["tier"] == [1, 2, 1, 2]
+    fast = schedule.schedule(p, 0)
+    slow = schedule.schedule(p, 1)
+    # Eq. 4 step counts
+    assert len(fast) == mb and len(slow) == (mb + mw) // 2 == p["steps"][1]
+    # exchange rounds: M_warmup + K/2
+    pubs = {s.pub_ver for s in fast if s.pub_ver >= 0}
+    assert len(pubs) == mw + (mb - mw) // 2 == p["n_exchange_rounds"]
+    # Thm 2 (L234-L238): slow grid is a subsample of the fast grid, both end at final
+    fast_t = [s.t for s in fast]
+    assert all(s.t in fast_t for s in slow)
+    assert fast[-1].t_prev == slow[-1].t_prev == schedule.FINAL
+    # every slow step spans exactly the two fast steps starting at the same t
+    for s in slow:
+        if s.kind == schedule.SLOW:
+            i = fast_t.index(s.t)
+            assert fast[i].kind == schedule.FAST_EVEN and fast[i + 1].kind == schedule.FAST_ODD
+            assert s.t_prev == fast[i + 1].t_prev
+            assert s.read_ver == fast[i].read_ver and s.pub_ver == fast[i].pub_ver
+    # odd steps publish nothing and read the version their even step published
+    for a, b in zip(fast, fast[1:]):
+        if b.kind == schedule.FAST_ODD:
+            assert b.pub_ver == schedule.NONE and b.read_ver == a.pub_ver
+
+
+def test_schedule_uniform_and_excluded():
+    p = planner.plan([100, 90, 10], 10, 2, 8)        # third GPU excluded (v <= b v_max)
+    assert p["tier"] == [1, 1, 0] and p["sync_period"] == 1
+    assert schedule.schedule(p, 2) == []
+    s = schedule.schedule(p, 0)
+    assert [x.kind for x in s] == [schedule.WARMUP] * 2 + [schedule.UNIFORM] * 8
+    assert all(x.read_ver == x.pub_ver - 1 for x in s[2:])
+    assert p["n_exchange_rounds"] == 10
