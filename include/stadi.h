@@ -1,0 +1,247 @@
+/*
+ * stadi.h — C ABI of the B200-native STADI elastic patch-parallel denoiser.
+ *
+ * STADI = Spatio-Temporal Adaptive Diffusion Inference, arXiv 2509.04719
+ * (/root/reference/PAPER.md).  The boundary follows the paper's statement of
+ * the problem: inputs are an initial noise x_{t_0}, a model eps_theta, the
+ * effective speeds {v_i}, M_base and M_warmup (Alg. 1 inputs, L108-L112);
+ * outputs are the final image x_{t_M} (L113) and the assignment (M_i, P_i)
+ * per GPU (§III-B).
+ *
+ * The four north-star calls:
+ *   stadi_profile_warmup  per-GPU speed v_i from timed warm-up forwards
+ *                         (L179 "effective speed", L284-L286 "derived directly
+ *                         from historical inference time profiles")
+ *   stadi_plan            Eq. 4 step allocation + Eq. 5 patch sizing
+ *                         (L179-L198, Alg. 1 lines 1-6)
+ *   stadi_denoise_step    one patch-parallel model forward + Eq. 3 sampler
+ *                         update on this GPU's patch (Alg. 1 lines 9-24)
+ *   stadi_run             a full request (Alg. 1 end to end, line 25)
+ *
+ * Conventions (all calls):
+ *   - Every call returns stadi_status; nothing throws or aborts.
+ *     STADI_EINVAL: bad arguments (no state change).  STADI_ECUDA /
+ *     STADI_ENCCL: a CUDA / NCCL error; the context is poisoned and only
+ *     stadi_destroy is valid afterwards (later calls return STADI_ESTATE).
+ *     stadi_last_error(ctx) gives a human-readable message (ctx may be NULL:
+ *     thread-local message of the last context-less call).
+ *   - Ownership: the caller owns every pointer it passes; the library copies
+ *     what it keeps (plans, conditioning, weights).  Device pointers must be
+ *     on the context's device and stay valid until the enqueued work ends.
+ *     The context owns its weights, activations, exchange buffers, streams,
+ *     events and communicators.
+ *   - Streams are passed as `void *` holding a cudaStream_t (NULL = legacy
+ *     default stream).  denoise_step / gather are stream-ordered; stadi_run
+ *     synchronises before returning.
+ *   - "COLLECTIVE" calls must be made by every rank of the group in the same
+ *     order with identical plans (the plan is a pure function of speed[]).
+ *   - One host thread per context.
+ *
+ * Layouts: latents are NHWC float32, [H, W, C] row-major for the full image,
+ * a rank's patch p_i is the contiguous row band [row_begin_i, row_begin_i +
+ * rows_i) (rank order, top to bottom).
+ */
+#ifndef STADI_H_
+#define STADI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STADI_ABI_VERSION 1u
+#define STADI_MAX_GPUS 64
+
+typedef enum {
+  STADI_OK = 0,
+  STADI_EINVAL = 1,
+  STADI_ENOMEM = 2,
+  STADI_ECUDA = 3,
+  STADI_ENCCL = 4,
+  STADI_ESTATE = 5,        /* poisoned context or wrong call order          */
+  STADI_EUNSUPPORTED = 6
+} stadi_status;
+
+typedef struct stadi_ctx stadi_ctx;
+
+uint32_t stadi_abi_version(void);
+const char *stadi_status_str(stadi_status s);
+/* Last error message of ctx (or of this thread when ctx == NULL).  Valid until
+ * the next call on the same ctx / thread. */
+const char *stadi_last_error(const stadi_ctx *ctx);
+
+/* ======================================================================
+ * Planner — pure host, integer only, deterministic, re-entrant, no CUDA.
+ * ====================================================================== */
+enum {
+  STADI_NO_TA = 1u,           /* disable temporal adaptation (every GPU tier 1) */
+  STADI_NO_SA = 2u,           /* disable spatial adaptation (uniform units)     */
+  STADI_SIZER_INTERVAL = 4u,  /* Eq. 5 with per-round step counts (R7 variant)  */
+  STADI_FORCE_UNITS = 8u      /* use forced_units (Table II / Fig. 9 splits)    */
+};
+
+typedef struct {
+  uint32_t n_gpus;             /* N, 1..STADI_MAX_GPUS                           */
+  const uint64_t *speed;       /* [N] effective speeds v_i > 0, any common scale */
+  uint32_t m_base, m_warmup;   /* 1 <= M_warmup <= M_base (L284: 100 / 4)        */
+  uint32_t a_num, a_den;       /* a = a_num/a_den, 0 < b < a < 1 (L284: 3/4)     */
+  uint32_t b_num, b_den;       /* b (L284: 1/4)                                  */
+  uint32_t p_total;            /* P_total units (L284: 32); >= #included GPUs    */
+  uint32_t rows_per_unit;      /* latent rows per unit (R6)                      */
+  uint32_t flags;              /* STADI_NO_TA | STADI_NO_SA | ...                */
+  const uint32_t *forced_units;/* [N] with STADI_FORCE_UNITS, else ignored       */
+} stadi_plan_params;
+
+typedef struct {
+  uint32_t n_gpus, m_base, m_warmup, p_total, rows_per_unit;
+  uint8_t tier[STADI_MAX_GPUS];        /* Eq. 4: 1 = M_base, 2 = (M_base+M_warmup)/2,
+                                          0 = excluded (v_i <= b v_max)          */
+  uint32_t steps[STADI_MAX_GPUS];      /* M_i (0 when excluded)                   */
+  uint32_t units[STADI_MAX_GPUS];      /* P_i in units (Eq. 5, D'Hondt, R5)       */
+  uint32_t row_begin[STADI_MAX_GPUS];  /* first latent row of GPU i's band        */
+  uint32_t rows[STADI_MAX_GPUS];       /* latent rows of GPU i's band             */
+  uint32_t sync_period;                /* lcm of post-warmup DDIM strides: 1 or 2 */
+  uint32_t n_exchange_rounds;          /* M_warmup + (M_base-M_warmup)/sync_period */
+  uint64_t makespan_num, makespan_den; /* max_i M_i P_i / v_i, reduced fraction   */
+} stadi_plan_t;
+
+/* Eq. 4 (L179-L185) then Eq. 5 (L187-L198), as in Alg. 1 lines 1-6.
+ * Thresholds compared exactly in 128-bit integers (R2: v_i <= b v_max is
+ * excluded, tier 1 needs a v_max < v_i).  Eq. 5 is integerised with the
+ * D'Hondt divisor method (R5): one unit per included GPU, then each further
+ * unit to argmin (P_i + 1) M_i / v_i, ties to the lowest rank.
+ * EINVAL: N out of range, a zero speed, not 0<b<a<1, M_warmup out of range,
+ * (M_base - M_warmup) odd with a tier-2 GPU (R3), P_total < #included, bad
+ * forced units. */
+stadi_status stadi_plan(const stadi_plan_params *in, stadi_plan_t *out);
+
+enum {
+  STADI_STEP_WARMUP = 0,     /* Alg. 1: synchronous (fresh) exchange   */
+  STADI_STEP_UNIFORM = 1,    /* no slow GPU: every step exchanges (R13)          */
+  STADI_STEP_FAST_EVEN = 2,  /* L136-L140: async buffer update + all-gather      */
+  STADI_STEP_FAST_ODD = 3,   /* L142-L146: no buffer update, reads newest (R10)  */
+  STADI_STEP_SLOW = 4        /* L148-L152: stride-2 step, async buffer update    */
+};
+#define STADI_T_FINAL (-1)   /* t_prev of the last step: alpha_bar_0 (R18)       */
+#define STADI_VER_NONE (-1)  /* pub_ver of a step that publishes nothing         */
+
+typedef struct {
+  int32_t m;          /* fast-grid index                                        */
+  int32_t t, t_prev;  /* DDIM timesteps (leading spacing, offset 1, R18)         */
+  int32_t kind;       /* STADI_STEP_*                                            */
+  int32_t read_ver;   /* exchange version read at every site (== pub_ver: fresh) */
+  int32_t pub_ver;    /* version published, or STADI_VER_NONE                    */
+} stadi_step_t;
+
+/* Step table of one rank (Alg. 1, Thm 2 grid alignment L234-L238).
+ * Writes min(cap, n) entries to buf and the full count to *n_out (buf may be
+ * NULL with cap 0 to query the count). */
+stadi_status stadi_schedule(const stadi_plan_t *plan, uint32_t rank,
+                            stadi_step_t *buf, uint32_t cap, uint32_t *n_out);
+
+/* ======================================================================
+ * Model description and weights
+ * ====================================================================== */
+enum {
+  STADI_PRESET_TINY_DIT = 0,   /* C1: d 64, 4 heads, depth 2, 16x16x4 latent    */
+  STADI_PRESET_DIT_XL2 = 1,    /* C2: DiT-XL/2 shapes, 32x32x4 latent, CFG 4.0  */
+  STADI_PRESET_PIXART_ALPHA = 2/* C5: PixArt-alpha shapes, 256x256x4, CFG 4.5   */
+};
+enum { STADI_DTYPE_BF16 = 0, STADI_DTYPE_FP32_DEBUG = 1 };
+enum { STADI_SAMPLER_DDIM = 0, STADI_SAMPLER_DDPM = 1 /* NEXT: EUNSUPPORTED */ };
+
+typedef struct {
+  int32_t preset;          /* STADI_PRESET_*                                     */
+  int32_t dtype;           /* BF16: tcgen05 bf16 GEMM/attention, fp32 accumulate,
+                              fp32 residual + latent; FP32_DEBUG: SIMT fp32 (no
+                              TF32) kernels for the <=1e-4 parity build         */
+  int32_t sampler;         /* STADI_SAMPLER_DDIM                                 */
+  int32_t depth;           /* 0 = preset depth, >0 overrides (reduced variants)  */
+  int32_t latent_h, latent_w; /* 0 = preset resolution                           */
+} stadi_model_desc;
+
+/* Weight manifest: tensors in load order (same order as synth/configs.py
+ * manifest()).  Linear weights are [out, in] row-major float32. */
+stadi_status stadi_weight_count(const stadi_model_desc *desc, uint32_t *n_tensors);
+stadi_status stadi_weight_info(const stadi_model_desc *desc, uint32_t index,
+                               char *name_buf, uint32_t name_cap, uint64_t *numel);
+
+/* ======================================================================
+ * Runtime — one context per process; a context hosts one rank (world > 1,
+ * NCCL over NVLink) or n_local ranks on one device (world == 1; exchange by
+ * device copies — used to run the multi-rank protocol on a single GPU).
+ * ====================================================================== */
+typedef struct {
+  int32_t rank, world;       /* process rank / number of processes (1 GPU each)  */
+  int32_t device;            /* CUDA device ordinal                              */
+  int32_t n_local;           /* ranks hosted by this ctx (>1 only if world == 1) */
+  const uint8_t *nccl_id;    /* 128-byte ncclUniqueId from rank 0 when world > 1 */
+} stadi_dist_desc;
+
+typedef struct {
+  const int32_t *labels;     /* [B] class labels (class presets; B=2: null first) */
+  const float *text;         /* [B, L_txt, D_txt] host fp32 (text presets)        */
+} stadi_cond;
+
+typedef struct {
+  double ms_total;           /* device time of the request on this process       */
+  double ms_exchange_wait;   /* reserved (0)                                     */
+  uint64_t exchange_bytes;   /* bytes this process sent in exchange rounds       */
+  uint32_t kernel_launches;  /* kernels this process launched for the request    */
+  uint32_t steps_run;        /* program steps executed                           */
+} stadi_run_stats;
+
+stadi_status stadi_create(const stadi_model_desc *model, const stadi_dist_desc *dist,
+                          stadi_ctx **out);
+void stadi_destroy(stadi_ctx *ctx);
+
+/* Copy the weights (host float32, manifest order) to the device, converting
+ * GEMM operands to the context dtype.  EINVAL on count / numel mismatch. */
+stadi_status stadi_load_weights(stadi_ctx *ctx, uint32_t n_tensors,
+                                const float *const *host_tensors, const uint64_t *numels);
+
+/* COLLECTIVE.  Times n_steps compute-only forwards on a uniform band (no
+ * exchange waits), takes the median ms per step ms_i, all-gathers it and
+ * returns v_i = round(2^20 min_j ms_j / ms_i) (R1).  ms_out / speed_out: [G]
+ * where G = world * n_local. */
+stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, double *ms_out,
+                                  uint64_t *speed_out);
+
+/* COLLECTIVE.  Install a plan (n_gpus == G, p_total * rows_per_unit == latent
+ * height).  Allocates bands and exchange slots. */
+stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan);
+
+/* Start a request: take this context's rows of the full noise [H, W, C_in]
+ * (host or device pointer) and the conditioning; precompute per-timestep
+ * modulation and text K/V.  Stream-ordered on `stream`. */
+stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full, const stadi_cond *cond,
+                         void *stream);
+/* Number of program steps of the installed plan (local mode: steps grouped by
+ * fast-grid index m across the hosted ranks; NCCL mode: this rank's steps). */
+stadi_status stadi_num_steps(stadi_ctx *ctx, uint32_t *n);
+/* COLLECTIVE.  Program step i: patch-local forward with stale exchange + Eq. 3
+ * update of the hosted bands (Alg. 1 lines 9-24). */
+stadi_status stadi_denoise_step(stadi_ctx *ctx, uint32_t step, void *stream);
+/* COLLECTIVE.  Final synchronous all-gather of the bands into out_full [H, W, C]
+ * fp32 (host or device pointer). */
+stadi_status stadi_gather(stadi_ctx *ctx, float *out_full, void *stream);
+/* COLLECTIVE.  set_plan (if changed) + begin + every step + gather; synchronises.
+ * noise_full / out_full may be host or device pointers. */
+stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, const float *noise_full,
+                       const stadi_cond *cond, float *out_full, stadi_run_stats *stats,
+                       void *stream);
+
+/* Occupancy emulator: pin ceil(pct * SMs / 100) SMs with a
+ * persistent spin kernel until stopped (hard self-timeout 900 s). */
+stadi_status stadi_emulator_start(stadi_ctx *ctx, uint32_t occupancy_pct);
+stadi_status stadi_emulator_stop(stadi_ctx *ctx);
+
+/* ncclGetUniqueId through the library's NCCL (dlopen'ed; ENCCL if absent). */
+stadi_status stadi_nccl_unique_id(uint8_t out[128]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STADI_H_ */

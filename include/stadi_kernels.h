@@ -1,0 +1,68 @@
+/*
+ * stadi_kernels.h — kernel-level C entry points of libstadi, for parity tests
+ * and micro-benchmarks of the individual hot-path kernels.  All pointers are
+ * DEVICE pointers on the current device; all calls are stream-ordered on
+ * `stream` (a cudaStream_t, NULL = legacy default stream) and return
+ * STADI_EINVAL for unsupported shapes, STADI_ECUDA on a launch error.
+ *
+ * dtype: STADI_DTYPE_BF16 -> the tcgen05/TMA kernels (bf16 operands, fp32
+ * accumulation); STADI_DTYPE_FP32_DEBUG -> the SIMT fp32 kernels.
+ */
+#ifndef STADI_KERNELS_H_
+#define STADI_KERNELS_H_
+
+#include "stadi.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* GEMM epilogues, applied to acc = A[M,K] . W[N,K]^T:     */
+enum {
+  STADI_EPI_STORE = 0,      /* out[T] (ld ldo) = acc + bias                       */
+  STADI_EPI_GELU = 1,       /* out[T] = gelu_tanh(acc + bias)                     */
+  STADI_EPI_GATED_RES = 2,  /* res[f32] += gate[row % B][col] * (acc + bias)      */
+  STADI_EPI_RES = 3,        /* res[f32] += acc + bias                             */
+  STADI_EPI_QKV = 4,        /* cols < d: q[T]; cols >= d: K/V rows of the exchange
+                               slot(s) kv_a / kv_b at row kv_row0 + row            */
+  STADI_EPI_F32 = 5         /* out[f32] = acc + bias                              */
+};
+
+typedef struct {
+  const float *bias;   /* [N] or NULL                                          */
+  void *out;           /* output (T or f32), row stride ldo elements           */
+  int32_t ldo;
+  float *res;          /* residual (f32), row stride ldr                       */
+  int32_t ldr;
+  const float *gate;   /* gate row of batch b at gate + b * gate_bstride        */
+  int32_t gate_bstride;
+  int32_t B;           /* internal batch; rows are token-major, batch innermost */
+  void *q;             /* EPI_QKV: q [M, d]                                    */
+  void *kv_a, *kv_b;   /* EPI_QKV: slot(s) [N_tok, B, 2, d]; kv_b may be NULL  */
+  int64_t kv_row0;
+  int32_t d;
+} stadi_k_epi;
+
+/* out = epilogue(A[M,K] . W[N,K]^T).  BF16 path: K % 64 == 0, N % 64 == 0. */
+stadi_status stadi_k_gemm(int32_t dtype, const void *A, const void *W, int32_t M, int32_t N,
+                          int32_t K, int32_t epi, const stadi_k_epi *ep, void *stream);
+
+/* o = softmax(q k^T / sqrt(hd)) v per (batch b, head h).
+ * q, o: [Nq * B, H*hd] (row = token*B + b); kv: [Nkv, B, 2, H*hd].
+ * BF16 path: hd in {16, 64, 72, 80}. */
+stadi_status stadi_k_attention(int32_t dtype, const void *q, const void *kv, void *o, int32_t Nq,
+                               int32_t Nkv, int32_t B, int32_t H, int32_t hd, void *stream);
+
+/* y[row] = LayerNorm(x[row]) * (1 + scale[b]) + shift[b], b = row % B (eps 1e-6);
+ * x f32 [M, d], y T [M, d]. */
+stadi_status stadi_k_ln_modulate(int32_t dtype, const float *x, void *y, int32_t M, int32_t d,
+                                 int32_t B, const float *shift, const float *scale,
+                                 int32_t bstride, void *stream);
+
+/* Number of kernels launched by this process so far. */
+uint64_t stadi_k_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STADI_KERNELS_H_ */

@@ -1,0 +1,261 @@
+// Device helpers for sm_100a: dtype conversion, mbarrier, TMA, tcgen05 PTX.
+// Bit layouts of the UMMA shared-memory / instruction descriptors follow the
+// PTX ISA tcgen05 "matrix descriptor" and "instruction descriptor" tables.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace stadi {
+
+using bf16 = __nv_bfloat16;
+
+template <typename T> __device__ __forceinline__ float to_f(T v);
+template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f<bf16>(bf16 v) { return __bfloat162float(v); }
+template <typename T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float v) { return __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float silu(float x) { return x / (1.f + expf(-x)); }
+
+// ----------------------------------------------------------------- GEMM epilogues
+// Shared by the SIMT (fp32 debug) and the tcgen05 GEMM so both paths compute
+// exactly the same post-accumulation math.
+enum EpiKind : int {
+  EPI_STORE = 0,      // out[T]   = acc + bias
+  EPI_GELU = 1,       // out[T]   = gelu_tanh(acc + bias)
+  EPI_GATED_RES = 2,  // res[f32] += gate[row % B] * (acc + bias)   (adaLN gate, DiT ref [4])
+  EPI_RES = 3,        // res[f32] += acc + bias
+  EPI_QKV = 4,        // cols [0,d): q ; [d,3d): K/V into exchange slot(s)
+  EPI_F32 = 5,        // outf[f32] = acc + bias
+};
+
+struct EpiParams {
+  const float *bias;   // [N] or nullptr
+  void *out;           // T or float, row stride ldo
+  int ldo;
+  float *res;          // residual fp32, row stride ldr
+  int ldr;
+  const float *gate;   // gate row for batch b at gate + b * gate_bstride
+  int gate_bstride;
+  int B;               // internal batch (rows are token-major, batch innermost)
+  void *q;             // EPI_QKV: q [M, d]
+  void *kv_a;          // EPI_QKV: K/V slot base ([N_tok, B, 2, d]); own rows at kv_row0
+  void *kv_b;          // optional second slot (publish version), may be nullptr
+  long kv_row0;        // first own row of the slot = tok_begin * B
+  int d;
+};
+
+// Apply the epilogue to `n` consecutive columns col..col+n-1 of one row.
+template <typename T, int EPI>
+__device__ __forceinline__ void epi_apply(const EpiParams &p, int row, int col, float *v, int n) {
+  if (p.bias) {
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) v[i] += __ldg(p.bias + col + i);
+  }
+  if constexpr (EPI == EPI_STORE || EPI == EPI_GELU) {
+    T *o = reinterpret_cast<T *>(p.out) + (long)row * p.ldo + col;
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) o[i] = from_f<T>(EPI == EPI_GELU ? gelu_tanh(v[i]) : v[i]);
+  } else if constexpr (EPI == EPI_F32) {
+    float *o = reinterpret_cast<float *>(p.out) + (long)row * p.ldo + col;
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) o[i] = v[i];
+  } else if constexpr (EPI == EPI_GATED_RES || EPI == EPI_RES) {
+    float *r = p.res + (long)row * p.ldr + col;
+    if constexpr (EPI == EPI_GATED_RES) {
+      const float *g = p.gate + (row % p.B) * p.gate_bstride + col;
+#pragma unroll 8
+      for (int i = 0; i < n; ++i) r[i] += __ldg(g + i) * v[i];
+    } else {
+#pragma unroll 8
+      for (int i = 0; i < n; ++i) r[i] += v[i];
+    }
+  } else if constexpr (EPI == EPI_QKV) {
+    // n consecutive columns never straddle the q / kv boundary (d % n == 0).
+    if (col < p.d) {
+      T *o = reinterpret_cast<T *>(p.q) + (long)row * p.d + col;
+#pragma unroll 8
+      for (int i = 0; i < n; ++i) o[i] = from_f<T>(v[i]);
+    } else {
+      const long off = (p.kv_row0 + row) * 2L * p.d + (col - p.d);
+      T *a = reinterpret_cast<T *>(p.kv_a) + off;
+#pragma unroll 8
+      for (int i = 0; i < n; ++i) a[i] = from_f<T>(v[i]);
+      if (p.kv_b) {
+        T *b = reinterpret_cast<T *>(p.kv_b) + off;
+#pragma unroll 8
+        for (int i = 0; i < n; ++i) b[i] = from_f<T>(v[i]);
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Wait for the phase with the given parity to complete.  Watchdog: trap after
+// ~10 s so a protocol bug becomes a CUDA error instead of a hung GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t it = 0;
+  while (!mbar_try_wait(a, parity)) {
+    if ((++it & 0x3FFu) == 0 && globaltimer() - t0 > 10000000000ull) __trap();
+  }
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch(const void *tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const void *tmap, void *dst, uint64_t *bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(const void *tmap, void *dst, uint64_t *bar, int c0,
+                                            int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+// tcgen05 ------------------------------------------------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 in, fp32 accumulate)
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete.
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// 32 lanes x 16 columns
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory matrix descriptor (sm_100): start>>4 [0,14), LBO>>4
+// [16,30), SBO>>4 [32,46), version 1 [46,48), base offset 0, swizzle [61,64):
+// 0 none, 2 = 128B, 4 = 64B, 6 = 32B.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t swz) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | ((uint64_t)swz << 61);
+}
+constexpr uint32_t SWZ_128B = 2, SWZ_64B = 4, SWZ_32B = 6;
+
+// Instruction descriptor kind::f16: D f32, A/B bf16, K-major unless *_mn set.
+__host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+}  // namespace stadi

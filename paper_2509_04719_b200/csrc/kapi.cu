@@ -1,0 +1,79 @@
+// Kernel-level C entry points (include/stadi_kernels.h).
+#include "../../include/stadi_kernels.h"
+#include "common.h"
+#include "kernels.h"
+
+using namespace stadi;
+
+namespace {
+stadi_status cu(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return STADI_OK;
+  if (e == cudaErrorInvalidValue)
+    return fail(nullptr, STADI_EINVAL, "%s: unsupported shape / argument", what);
+  return fail(nullptr, STADI_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+}  // namespace
+
+extern "C" stadi_status stadi_k_gemm(int32_t dtype, const void *A, const void *W, int32_t M,
+                                     int32_t N, int32_t K, int32_t epi, const stadi_k_epi *e,
+                                     void *stream) {
+  if (!A || !W || !e || M < 0 || N <= 0 || K <= 0 || epi < 0 || epi > 5)
+    return fail(nullptr, STADI_EINVAL, "stadi_k_gemm: bad argument");
+  EpiParams ep{};
+  ep.bias = e->bias;
+  ep.out = e->out;
+  ep.ldo = e->ldo;
+  ep.res = e->res;
+  ep.ldr = e->ldr;
+  ep.gate = e->gate;
+  ep.gate_bstride = e->gate_bstride;
+  ep.B = e->B > 0 ? e->B : 1;
+  ep.q = e->q;
+  ep.kv_a = e->kv_a;
+  ep.kv_b = e->kv_b;
+  ep.kv_row0 = e->kv_row0;
+  ep.d = e->d;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == STADI_DTYPE_BF16) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return cu(tc_gemm_bf16((const bf16 *)A, (const bf16 *)W, M, N, K, epi, ep, sms, s),
+              "tc_gemm_bf16");
+  }
+  if (dtype == STADI_DTYPE_FP32_DEBUG)
+    return cu(simt_gemm<float>((const float *)A, (const float *)W, M, N, K, epi, ep, s),
+              "simt_gemm");
+  return fail(nullptr, STADI_EINVAL, "stadi_k_gemm: bad dtype");
+}
+
+extern "C" stadi_status stadi_k_attention(int32_t dtype, const void *q, const void *kv, void *o,
+                                          int32_t Nq, int32_t Nkv, int32_t B, int32_t H,
+                                          int32_t hd, void *stream) {
+  if (!q || !kv || !o || Nq < 0 || Nkv <= 0 || B <= 0 || H <= 0 || hd <= 0)
+    return fail(nullptr, STADI_EINVAL, "stadi_k_attention: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == STADI_DTYPE_BF16)
+    return cu(tc_attention_bf16((const bf16 *)q, (const bf16 *)kv, (bf16 *)o, Nq, Nkv, B, H, hd,
+                                s),
+              "tc_attention_bf16");
+  if (dtype == STADI_DTYPE_FP32_DEBUG)
+    return cu(simt_attention<float>((const float *)q, (const float *)kv, (float *)o, Nq, Nkv, B,
+                                    H, hd, s),
+              "simt_attention");
+  return fail(nullptr, STADI_EINVAL, "stadi_k_attention: bad dtype");
+}
+
+extern "C" stadi_status stadi_k_ln_modulate(int32_t dtype, const float *x, void *y, int32_t M,
+                                            int32_t d, int32_t B, const float *shift,
+                                            const float *scale, int32_t bstride, void *stream) {
+  if (!x || !y || !shift || !scale || M < 0 || d <= 0 || B <= 0)
+    return fail(nullptr, STADI_EINVAL, "stadi_k_ln_modulate: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == STADI_DTYPE_BF16)
+    return cu(ln_modulate<bf16>(x, (bf16 *)y, M, d, B, shift, scale, bstride, 1, s), "ln_modulate");
+  return cu(ln_modulate<float>(x, (float *)y, M, d, B, shift, scale, bstride, 1, s),
+            "ln_modulate");
+}
+
+extern "C" uint64_t stadi_k_launch_count(void) { return g_launches; }

@@ -1,0 +1,64 @@
+// Host launch functions of the libstadi kernels (all stream-ordered).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace stadi {
+
+// Global launch counter (kernels launched by this process).
+extern unsigned long long g_launches;
+
+// ---- GEMM  out = epilogue(A[M,K] . W[N,K]^T) ------------------------------
+// SIMT fp32-accumulate GEMM (the fp32 debug build, and tiny conditioning GEMMs).
+template <typename T>
+cudaError_t simt_gemm(const T *A, const T *W, int M, int N, int K, int epi, const EpiParams &ep,
+                      cudaStream_t s);
+// tcgen05 + TMA bf16 GEMM (persistent, warp-specialised).  Requires K % 64 == 0,
+// N % 64 == 0.  max_ctas bounds the grid (SMs not pinned by the emulator).
+cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
+                         const EpiParams &ep, int max_ctas, cudaStream_t s);
+
+// ---- attention  o = softmax(q k^T / sqrt(hd)) v  per (batch b, head h) ------
+// q, o: [Nq * B, H*hd] (row = token*B + b);  kv: [Nkv, B, 2, H*hd] (K then V).
+template <typename T>
+cudaError_t simt_attention(const T *q, const T *kv, T *o, int Nq, int Nkv, int B, int H, int hd,
+                           cudaStream_t s);
+cudaError_t tc_attention_bf16(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B,
+                              int H, int hd, cudaStream_t s);
+bool tc_attention_supported(int hd);
+
+// ---- elementwise / normalisation -------------------------------------------
+// y[row] = LN(x[row]) * (1 + scale[b]) + shift[b]   (b = row % B); do_norm = 0: y = x
+template <typename T>
+cudaError_t ln_modulate(const float *x, T *y, int M, int d, int B, const float *shift,
+                        const float *scale, int mod_bstride, int do_norm, cudaStream_t s);
+// Patchify a latent band + Linear(p*p*C -> d) + bias + positional embedding,
+// written for every batch row: x_res[(i*B+b), :].
+cudaError_t patch_embed(const float *x_band, int rows, int W, int C, int p, const float *w,
+                        const float *b, const float *pos_rows, int d, int B, float *x_res,
+                        cudaStream_t s);
+// CFG combine + unpatchify + Eq. 3 update of the band:  x = A x + Bc eps.
+// eps_raw row stride = ld (>= p*p*c_out).
+cudaError_t sampler_update(float *x_band, const float *eps_raw, int rows, int W, int C, int p,
+                           int c_out, int ld, int B, float guidance, float A, float Bc,
+                           cudaStream_t s);
+// Conditioning helpers
+cudaError_t silu_inplace(float *x, long n, cudaStream_t s);
+template <typename T>
+cudaError_t class_cond(const float *temb, const float *table, const int *labels, int n_t, int B,
+                       int d, T *out, cudaStream_t s);
+template <typename T>
+cudaError_t silu_cast(const float *x, T *y, long n, cudaStream_t s);
+template <typename T>
+cudaError_t cast_f32(const float *x, T *y, long n, cudaStream_t s);
+cudaError_t pixart_mods(const float *t0, const float *temb, const float *sst_all,
+                        const float *final_sst, int n_t, int B, int depth, int d, float *mod,
+                        float *fmod, cudaStream_t s);
+
+// ---- occupancy emulator ---------------------------------
+cudaError_t emulator_launch(int n_ctas, volatile int *stop_flag, cudaStream_t s);
+
+}  // namespace stadi

@@ -1,0 +1,447 @@
+// SIMT kernels: fp32-accumulate GEMM and attention (the fp32 debug build of
+// no tensor cores, no TF32 — and small conditioning GEMMs),
+// plus the HBM-bound elementwise kernels of the hot path (LN + adaLN modulate,
+// patch embedding, fused CFG + unpatchify + Eq. 3 sampler).
+#include <float.h>
+
+#include "../kernels.h"
+
+namespace stadi {
+
+unsigned long long g_launches = 0;
+
+// ------------------------------------------------------------------ GEMM
+namespace {
+constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 16;
+
+template <typename T, int EPI>
+__global__ void __launch_bounds__(256) simt_gemm_kernel(const T *__restrict__ A,
+                                                        const T *__restrict__ W, int M, int N,
+                                                        int K, EpiParams ep) {
+  __shared__ float As[SG_BK][SG_BM + 4];
+  __shared__ float Ws[SG_BK][SG_BN + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * SG_BM, n0 = blockIdx.x * SG_BN;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += SG_BK) {
+    for (int i = threadIdx.x; i < SG_BM * SG_BK; i += 256) {
+      const int r = i / SG_BK, c = i % SG_BK;
+      const int gm = m0 + r, gk = k0 + c;
+      As[c][r] = (gm < M && gk < K) ? to_f(A[(long)gm * K + gk]) : 0.f;
+      const int gn = n0 + r;
+      Ws[c][r] = (gn < N && gk < K) ? to_f(W[(long)gn * K + gk]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < SG_BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Ws[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + ty * 4 + i;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = n0 + tx * 4 + j;
+      if (col >= N) continue;
+      float v = acc[i][j];
+      epi_apply<T, EPI>(ep, row, col, &v, 1);
+    }
+  }
+}
+}  // namespace
+
+template <typename T>
+cudaError_t simt_gemm(const T *A, const T *W, int M, int N, int K, int epi, const EpiParams &ep,
+                      cudaStream_t s) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  dim3 grid((N + SG_BN - 1) / SG_BN, (M + SG_BM - 1) / SG_BM);
+  switch (epi) {
+    case EPI_STORE: simt_gemm_kernel<T, EPI_STORE><<<grid, 256, 0, s>>>(A, W, M, N, K, ep); break;
+    case EPI_GELU: simt_gemm_kernel<T, EPI_GELU><<<grid, 256, 0, s>>>(A, W, M, N, K, ep); break;
+    case EPI_GATED_RES:
+      simt_gemm_kernel<T, EPI_GATED_RES><<<grid, 256, 0, s>>>(A, W, M, N, K, ep);
+      break;
+    case EPI_RES: simt_gemm_kernel<T, EPI_RES><<<grid, 256, 0, s>>>(A, W, M, N, K, ep); break;
+    case EPI_QKV: simt_gemm_kernel<T, EPI_QKV><<<grid, 256, 0, s>>>(A, W, M, N, K, ep); break;
+    case EPI_F32: simt_gemm_kernel<T, EPI_F32><<<grid, 256, 0, s>>>(A, W, M, N, K, ep); break;
+    default: return cudaErrorInvalidValue;
+  }
+  ++g_launches;
+  return cudaGetLastError();
+}
+template cudaError_t simt_gemm<float>(const float *, const float *, int, int, int, int,
+                                      const EpiParams &, cudaStream_t);
+template cudaError_t simt_gemm<bf16>(const bf16 *, const bf16 *, int, int, int, int,
+                                     const EpiParams &, cudaStream_t);
+
+// ------------------------------------------------------------------ attention
+namespace {
+constexpr int SA_WARPS = 4;
+constexpr int SA_MAXC = 5;  // hd <= 160
+
+template <typename T>
+__global__ void __launch_bounds__(SA_WARPS * 32) simt_attn_kernel(const T *__restrict__ q,
+                                                                  const T *__restrict__ kv,
+                                                                  T *__restrict__ o, int Nq,
+                                                                  int Nkv, int B, int H, int hd) {
+  __shared__ float qs[SA_WARPS][160];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long job = (long)blockIdx.x * SA_WARPS + warp;  // (row, h)
+  const int d = H * hd;
+  if (job >= (long)Nq * B * H) return;
+  const long row = job / H;
+  const int h = (int)(job % H);
+  const int b = (int)(row % B);
+  const float scale = rsqrtf((float)hd);
+  for (int c = lane; c < hd; c += 32) qs[warp][c] = to_f(q[row * d + h * hd + c]) * scale;
+  __syncwarp();
+  const long kv_stride = 2L * B * d;  // per key token
+  const T *kbase = kv + (long)b * 2 * d + h * hd;
+  const T *vbase = kbase + d;
+  float m = -FLT_MAX, l = 0.f, acc[SA_MAXC] = {};
+  for (int j0 = 0; j0 < Nkv; j0 += 32) {
+    const int j = j0 + lane;
+    float sc = -FLT_MAX;
+    if (j < Nkv) {
+      const T *kj = kbase + (long)j * kv_stride;
+      float a = 0.f;
+      for (int c = 0; c < hd; ++c) a = fmaf(qs[warp][c], to_f(kj[c]), a);
+      sc = a;
+    }
+    float mc = sc;
+    for (int off = 16; off; off >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, off));
+    const float mn = fmaxf(m, mc);
+    const float p = (j < Nkv) ? expf(sc - mn) : 0.f;
+    const float alpha = expf(m - mn);
+    float ps = p;
+    for (int off = 16; off; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+    l = l * alpha + ps;
+#pragma unroll
+    for (int k = 0; k < SA_MAXC; ++k) acc[k] *= alpha;
+    const int jn = min(32, Nkv - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      const float pj = __shfl_sync(0xffffffffu, p, jj);
+      const T *vj = vbase + (long)(j0 + jj) * kv_stride;
+#pragma unroll
+      for (int k = 0; k < SA_MAXC; ++k) {
+        const int c = lane + 32 * k;
+        if (c < hd) acc[k] = fmaf(pj, to_f(vj[c]), acc[k]);
+      }
+    }
+    m = mn;
+  }
+  const float inv = 1.f / l;
+#pragma unroll
+  for (int k = 0; k < SA_MAXC; ++k) {
+    const int c = lane + 32 * k;
+    if (c < hd) o[row * d + h * hd + c] = from_f<T>(acc[k] * inv);
+  }
+}
+}  // namespace
+
+template <typename T>
+cudaError_t simt_attention(const T *q, const T *kv, T *o, int Nq, int Nkv, int B, int H, int hd,
+                           cudaStream_t s) {
+  if (hd > 160) return cudaErrorInvalidValue;
+  const long jobs = (long)Nq * B * H;
+  if (jobs == 0) return cudaSuccess;
+  simt_attn_kernel<T><<<(unsigned)((jobs + SA_WARPS - 1) / SA_WARPS), SA_WARPS * 32, 0, s>>>(
+      q, kv, o, Nq, Nkv, B, H, hd);
+  ++g_launches;
+  return cudaGetLastError();
+}
+template cudaError_t simt_attention<float>(const float *, const float *, float *, int, int, int,
+                                           int, int, cudaStream_t);
+template cudaError_t simt_attention<bf16>(const bf16 *, const bf16 *, bf16 *, int, int, int, int,
+                                          int, cudaStream_t);
+
+// ------------------------------------------------------------------ LN + modulate
+namespace {
+constexpr int LN_MAXV = 12;  // float4 per lane: d <= 1536
+
+template <typename T>
+__global__ void __launch_bounds__(256) ln_mod_kernel(const float *__restrict__ x, T *__restrict__ y,
+                                                     int M, int d, int B,
+                                                     const float *__restrict__ shift,
+                                                     const float *__restrict__ scale, int bs,
+                                                     int do_norm) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long row = (long)blockIdx.x * 8 + warp;
+  if (row >= M) return;
+  const int d4 = d / 4;
+  const float4 *xr = reinterpret_cast<const float4 *>(x + row * d);
+  float4 v[LN_MAXV];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < d4) {
+      v[i] = xr[c];
+      s += v[i].x + v[i].y + v[i].z + v[i].w;
+    }
+  }
+  T *yr = y + row * d;
+  if (!do_norm) {
+#pragma unroll
+    for (int i = 0; i < LN_MAXV; ++i) {
+      const int c = lane + 32 * i;
+      if (c < d4) {
+        yr[4 * c + 0] = from_f<T>(v[i].x);
+        yr[4 * c + 1] = from_f<T>(v[i].y);
+        yr[4 * c + 2] = from_f<T>(v[i].z);
+        yr[4 * c + 3] = from_f<T>(v[i].w);
+      }
+    }
+    return;
+  }
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  const float mean = s / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < d4) {
+      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, e = v[i].w - mean;
+      q += a * a + b * b + cc * cc + e * e;
+    }
+  }
+  for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+  const float rstd = rsqrtf(q / d + 1e-6f);
+  const int b = (int)(row % B);
+  const float *sh = shift + (long)b * bs, *sc = scale + (long)b * bs;
+#pragma unroll
+  for (int i = 0; i < LN_MAXV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < d4) {
+      const float4 s4 = reinterpret_cast<const float4 *>(sh)[c];
+      const float4 c4 = reinterpret_cast<const float4 *>(sc)[c];
+      yr[4 * c + 0] = from_f<T>((v[i].x - mean) * rstd * (1.f + c4.x) + s4.x);
+      yr[4 * c + 1] = from_f<T>((v[i].y - mean) * rstd * (1.f + c4.y) + s4.y);
+      yr[4 * c + 2] = from_f<T>((v[i].z - mean) * rstd * (1.f + c4.z) + s4.z);
+      yr[4 * c + 3] = from_f<T>((v[i].w - mean) * rstd * (1.f + c4.w) + s4.w);
+    }
+  }
+}
+}  // namespace
+
+template <typename T>
+cudaError_t ln_modulate(const float *x, T *y, int M, int d, int B, const float *shift,
+                        const float *scale, int mod_bstride, int do_norm, cudaStream_t s) {
+  if (d % 4 || d / 4 > 32 * LN_MAXV) return cudaErrorInvalidValue;
+  if (M <= 0) return cudaSuccess;
+  ln_mod_kernel<T><<<(M + 7) / 8, 256, 0, s>>>(x, y, M, d, B, shift, scale, mod_bstride, do_norm);
+  ++g_launches;
+  return cudaGetLastError();
+}
+template cudaError_t ln_modulate<float>(const float *, float *, int, int, int, const float *,
+                                        const float *, int, int, cudaStream_t);
+template cudaError_t ln_modulate<bf16>(const float *, bf16 *, int, int, int, const float *,
+                                       const float *, int, int, cudaStream_t);
+
+// ------------------------------------------------------------------ patch embedding
+namespace {
+__global__ void __launch_bounds__(256) patch_embed_kernel(const float *__restrict__ xb, int W,
+                                                          int C, int p, const float *__restrict__ w,
+                                                          const float *__restrict__ bias,
+                                                          const float *__restrict__ pos, int d,
+                                                          int B, float *__restrict__ xres) {
+  __shared__ float patch[64];
+  const int i = blockIdx.x;  // band-local token
+  const int wp = W / p;
+  const int r = i / wp, c = i % wp;
+  const int KP = C * p * p;
+  for (int k = threadIdx.x; k < KP; k += blockDim.x) {
+    const int ch = k / (p * p), dy = (k / p) % p, dx = k % p;  // column = c*p*p + dy*p + dx
+    patch[k] = xb[((long)(p * r + dy) * W + (p * c + dx)) * C + ch];
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < d; o += blockDim.x) {
+    float a = bias[o];
+    const float *wr = w + (long)o * KP;
+    for (int k = 0; k < KP; ++k) a = fmaf(wr[k], patch[k], a);
+    a += pos[(long)i * d + o];
+    for (int b = 0; b < B; ++b) xres[((long)i * B + b) * d + o] = a;
+  }
+}
+
+__global__ void sampler_kernel(float *__restrict__ xb, const float *__restrict__ eps, int rows,
+                               int W, int C, int p, int c_out, int ld, int B, float g, float A,
+                               float Bc) {
+  const long n = (long)rows * W * C;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  const int ch = (int)(idx % C);
+  const long pix = idx / C;
+  const int col = (int)(pix % W), row = (int)(pix / W);
+  const int wp = W / p;
+  const long tok = (long)(row / p) * wp + col / p;
+  const int j = ((row % p) * p + (col % p)) * c_out + ch;   // unpatchify column
+  const int ncol = ld;
+  float e = eps[(tok * B + 0) * ncol + j];
+  if (B == 2) {
+    const float ec = eps[(tok * B + 1) * ncol + j];
+    e = e + g * (ec - e);                                   // CFG (R20)
+  }
+  xb[idx] = A * xb[idx] + Bc * e;                           // Eq. 3
+}
+}  // namespace
+
+cudaError_t patch_embed(const float *x_band, int rows, int W, int C, int p, const float *w,
+                        const float *b, const float *pos_rows, int d, int B, float *x_res,
+                        cudaStream_t s) {
+  const int ntok = (rows / p) * (W / p);
+  if (C * p * p > 64) return cudaErrorInvalidValue;
+  if (ntok == 0) return cudaSuccess;
+  patch_embed_kernel<<<ntok, 256, 0, s>>>(x_band, W, C, p, w, b, pos_rows, d, B, x_res);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t sampler_update(float *x_band, const float *eps_raw, int rows, int W, int C, int p,
+                           int c_out, int ld, int B, float guidance, float A, float Bc,
+                           cudaStream_t s) {
+  const long n = (long)rows * W * C;
+  if (n == 0) return cudaSuccess;
+  sampler_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x_band, eps_raw, rows, W, C, p,
+                                                              c_out, ld, B, guidance, A, Bc);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ conditioning
+namespace {
+__global__ void silu_kernel(float *x, long n) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = silu(x[i]);
+}
+template <typename T>
+__global__ void silu_cast_kernel(const float *x, T *y, long n) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = from_f<T>(silu(x[i]));
+}
+template <typename T>
+__global__ void cast_kernel(const float *x, T *y, long n) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = from_f<T>(x[i]);
+}
+template <typename T>
+__global__ void class_cond_kernel(const float *temb, const float *table, const int *labels,
+                                  int n_t, int B, int d, T *out) {
+  const long n = (long)n_t * B * d;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = (int)(i % d);
+  const long tb = i / d;
+  const int b = (int)(tb % B);
+  const int ti = (int)(tb / B);
+  out[i] = from_f<T>(silu(temb[(long)ti * d + c] + table[(long)labels[b] * d + c]));
+}
+__global__ void pixart_mods_kernel(const float *t0, const float *temb, const float *sst,
+                                   const float *fsst, int n_t, int B, int depth, int d,
+                                   float *mod, float *fmod) {
+  const long nm = (long)n_t * B * depth * 6 * d;
+  const long nf = (long)n_t * B * 2 * d;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nm) {
+    const int kc = (int)(i % (6 * d));
+    const long r = i / (6 * d);
+    const int l = (int)(r % depth);
+    const int ti = (int)(r / depth / B);
+    mod[i] = sst[(long)l * 6 * d + kc] + t0[(long)ti * 6 * d + kc];
+  } else if (i < nm + nf) {
+    const long j = i - nm;
+    const int c = (int)(j % d);
+    const int k = (int)((j / d) % 2);
+    const int ti = (int)(j / (2 * d) / B);
+    fmod[j] = fsst[(long)k * d + c] + temb[(long)ti * d + c];
+  }
+}
+}  // namespace
+
+cudaError_t silu_inplace(float *x, long n, cudaStream_t s) {
+  silu_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, n);
+  ++g_launches;
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t silu_cast(const float *x, T *y, long n, cudaStream_t s) {
+  silu_cast_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, y, n);
+  ++g_launches;
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t cast_f32(const float *x, T *y, long n, cudaStream_t s) {
+  cast_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, y, n);
+  ++g_launches;
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t class_cond(const float *temb, const float *table, const int *labels, int n_t, int B,
+                       int d, T *out, cudaStream_t s) {
+  const long n = (long)n_t * B * d;
+  class_cond_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(temb, table, labels, n_t, B, d,
+                                                                   out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+cudaError_t pixart_mods(const float *t0, const float *temb, const float *sst_all,
+                        const float *final_sst, int n_t, int B, int depth, int d, float *mod,
+                        float *fmod, cudaStream_t s) {
+  const long n = (long)n_t * B * depth * 6 * d + (long)n_t * B * 2 * d;
+  pixart_mods_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(t0, temb, sst_all, final_sst,
+                                                                 n_t, B, depth, d, mod, fmod);
+  ++g_launches;
+  return cudaGetLastError();
+}
+template cudaError_t silu_cast<float>(const float *, float *, long, cudaStream_t);
+template cudaError_t silu_cast<bf16>(const float *, bf16 *, long, cudaStream_t);
+template cudaError_t cast_f32<float>(const float *, float *, long, cudaStream_t);
+template cudaError_t cast_f32<bf16>(const float *, bf16 *, long, cudaStream_t);
+template cudaError_t class_cond<float>(const float *, const float *, const int *, int, int, int,
+                                       float *, cudaStream_t);
+template cudaError_t class_cond<bf16>(const float *, const float *, const int *, int, int, int,
+                                      bf16 *, cudaStream_t);
+
+// ------------------------------------------------------------------ occupancy emulator
+namespace {
+// One CTA per SM (max shared memory + 1024 threads keep anything else off that
+// SM).  FMA spin until *stop is set or 900 s elapse.
+__global__ void __launch_bounds__(1024, 1) emulator_kernel(volatile int *stop) {
+  extern __shared__ float pad[];
+  const uint64_t t0 = globaltimer();
+  float a = threadIdx.x * 1e-3f, b = 1.0001f;
+  for (uint32_t it = 0;; ++it) {
+#pragma unroll 16
+    for (int k = 0; k < 256; ++k) a = fmaf(a, b, 1e-7f);
+    if ((it & 63) == 0) {
+      if (*stop) break;
+      if (globaltimer() - t0 > 900000000000ull) break;
+    }
+  }
+  if (a == 12345.f) pad[threadIdx.x] = a;  // keep the loop alive
+}
+}  // namespace
+
+cudaError_t emulator_launch(int n_ctas, volatile int *stop_flag, cudaStream_t s) {
+  if (n_ctas <= 0) return cudaSuccess;
+  const int smem = 200 * 1024;
+  cudaError_t e =
+      cudaFuncSetAttribute(emulator_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  emulator_kernel<<<n_ctas, 1024, smem, s>>>(stop_flag);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace stadi

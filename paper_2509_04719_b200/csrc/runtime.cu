@@ -1,0 +1,1086 @@
+// libstadi runtime: context, weights, plan install, per-request conditioning,
+// the patch-parallel DiT step with stale K/V exchange, final gather, run
+// loop, speed profiling and the occupancy emulator.
+//
+// PAPER.md Alg. 1 (L108-L155) is executed as a "program" of steps:
+//  * NCCL mode (world > 1, one rank per process): program = this rank's step
+//    table (stadi_schedule).  Exchange = grouped ncclBroadcast (one root per
+//    rank: an in-place variable-size all-gather, L288) on a side stream.
+//  * local mode (world == 1, n_local ranks on one device): program = every
+//    hosted rank's steps grouped by fast-grid index m, run layer-lock-step;
+//    exchange = device copies of the publisher's rows into the other ranks'
+//    slots.  Same kernels, same buffers; used to run the multi-rank protocol
+//    (and its parity tests) on one GPU.
+//
+// Exchange buffers: per attention site l and version
+// parity v%2 a full-image K/V slot [N_tok, B, 2, d] (token-major, batch
+// innermost, K then V).  A step reading version R publishing P: the QKV GEMM
+// epilogue writes the rank's fresh K/V rows into slot[R%2] (so attention sees
+// own-fresh + others-stale in one contiguous buffer) and into slot[P%2] (the
+// publish), and the exchange delivers the other ranks' rows of version P.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+#include "model.h"
+
+using namespace stadi;
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclCommSplit) CommSplit = nullptr;
+  decltype(&ncclBroadcast) Broadcast = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+NcclApi &nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+#define LD(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f))
+      LD(GetUniqueId); LD(CommInitRank); LD(CommDestroy); LD(CommSplit); LD(Broadcast);
+      LD(AllGather); LD(GroupStart); LD(GroupEnd); LD(GetErrorString);
+#undef LD
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast &&
+               api.AllGather && api.GroupStart && api.GroupEnd;
+    }
+  }
+  return api;
+}
+
+inline int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// One hosted rank: its band, activations and exchange slots.
+struct Rank {
+  int g = 0;                       // group rank (0..G-1)
+  int row_begin = 0, rows = 0;     // latent rows
+  int tok_begin = 0, n_tok = 0;    // tokens (token rows * wp)
+  int tier = 0;
+  std::vector<stadi_step_t> sched;
+  float *x_band = nullptr;         // [rows, W, C_in] fp32
+  float *x_res = nullptr;          // [n_tok*B, d] fp32 residual stream
+  void *xmod = nullptr, *q = nullptr, *o = nullptr, *h1 = nullptr;  // T activations
+  float *eps_raw = nullptr;        // [n_tok*B, fin_ld] fp32
+  std::vector<void *> kv;          // [depth*2] full-image slots
+};
+
+struct Part {  // one (hosted rank, schedule entry) executed in a program step
+  int li;      // index into ctx->ranks
+  stadi_step_t st;
+};
+
+}  // namespace
+
+struct stadi_ctx {
+  Dims dm;
+  int dtype = STADI_DTYPE_BF16;
+  int device = 0, rank = 0, world = 1, n_local = 1, G = 1;
+  int num_sms = 148;
+  std::string err;
+  bool poisoned = false;
+  size_t esz = 2;  // element size of T
+
+  // weights
+  bool weights_loaded = false;
+  std::vector<TensorSpec> man;
+  std::vector<void *> wT;    // compute-dtype copy of GEMM weights (nullptr otherwise)
+  std::vector<float *> wf;   // fp32 copy (bf16-rounded values in bf16 mode)
+  void *ada_all = nullptr;   // [depth*6d, d] T (class presets)
+  float *ada_all_b = nullptr;
+  float *sst_all = nullptr;  // [depth, 6, d] (text presets)
+  void *final_w = nullptr;   // [fin_ld, d] T, zero-padded rows
+  float *final_b = nullptr;  // [fin_ld]
+  int fin_ld = 64;
+  float *pos_full = nullptr; // [hp*wp, d]
+  std::vector<void *> allocs;
+
+  // plan
+  bool has_plan = false;
+  stadi_plan_t plan{};
+  std::vector<Rank> ranks;   // hosted ranks (included ones)
+  std::vector<std::vector<Part>> program;
+
+  // request state
+  bool begun = false;
+  int n_t = 0;               // = M_base: modulation precomputed for every fast-grid t
+  float *mod = nullptr;      // [n_t, B, depth, 6, d]
+  float *fmod = nullptr;     // [n_t, B, 2, d]
+  float *temb = nullptr, *tmp_f = nullptr, *tfreq = nullptr;
+  void *csilu = nullptr;
+  int *labels_dev = nullptr;
+  size_t cond_cap_nt = 0;
+  void *text_T = nullptr, *y1 = nullptr, *y = nullptr;
+  std::vector<void *> kv_text;
+  double abar[1000];
+
+  // streams / NCCL
+  cudaStream_t comm = nullptr;
+  ncclComm_t world_comm = nullptr, sub_comm = nullptr;
+  std::vector<cudaEvent_t> ev_done;  // [depth*2] exchange completion per (site, parity)
+  std::vector<char> ev_used;
+  cudaEvent_t ev_ready = nullptr;
+  uint64_t exch_bytes = 0;
+
+  // emulator
+  int *emu_flag_host = nullptr;
+  int *emu_flag_dev = nullptr;
+  cudaStream_t emu_stream = nullptr;
+  int emu_ctas = 0;
+};
+
+namespace {
+
+stadi_status ctx_fail(stadi_ctx *c, stadi_status st, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (st == STADI_ECUDA || st == STADI_ENCCL) c->poisoned = true;
+  }
+  tls_error() = buf;
+  return st;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return ctx_fail(ctx, STADI_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,     \
+                      cudaGetErrorString(e_));                                         \
+  } while (0)
+#define CKN(call)                                                                      \
+  do {                                                                                 \
+    ncclResult_t r_ = (call);                                                          \
+    if (r_ != ncclSuccess)                                                             \
+      return ctx_fail(ctx, STADI_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,     \
+                      nccl().GetErrorString ? nccl().GetErrorString(r_) : "nccl");     \
+  } while (0)
+#define ALIVE()                                                                        \
+  do {                                                                                 \
+    if (!ctx) return ctx_fail(nullptr, STADI_EINVAL, "NULL context");                  \
+    if (ctx->poisoned) return ctx_fail(ctx, STADI_ESTATE, "context poisoned: %s",      \
+                                       ctx->err.c_str());                              \
+  } while (0)
+
+template <typename P>
+cudaError_t dalloc(stadi_ctx *ctx, P **p, size_t bytes) {
+  void *q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
+  if (e != cudaSuccess) return e;
+  ctx->allocs.push_back(q);
+  *p = reinterpret_cast<P *>(q);
+  return cudaSuccess;
+}
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ---------------------------------------------------------------- host math (fp64)
+void alpha_bar(bool linear, double *ab) {
+  double acc = 1.0;
+  for (int t = 0; t < 1000; ++t) {
+    double beta;
+    if (linear) {
+      beta = 1e-4 + (0.02 - 1e-4) * t / 999.0;
+    } else {
+      const double a = std::sqrt(0.00085), b = std::sqrt(0.012);
+      const double s = a + (b - a) * t / 999.0;
+      beta = s * s;
+    }
+    acc *= 1.0 - beta;
+    ab[t] = acc;
+  }
+}
+// Eq. 3 as x' = A x + Bc eps: A = alpha'/alpha, Bc = -sigma'(e^h - 1).
+void ddim_coeffs(const double *ab, int t, int t_prev, float *A, float *Bc) {
+  const double a1 = ab[t], a2 = t_prev < 0 ? ab[0] : ab[t_prev];
+  const double al = std::sqrt(a1), si = std::sqrt(1 - a1), al2 = std::sqrt(a2),
+               si2 = std::sqrt(1 - a2);
+  const double h = std::log(al2 / si2) - std::log(al / si);
+  *A = (float)(al2 / al);
+  *Bc = (float)(-si2 * std::expm1(h));
+}
+
+// ---------------------------------------------------------------- kernel dispatch
+cudaError_t gemm(stadi_ctx *ctx, const void *A, const void *W, int M, int N, int K, int epi,
+                 const EpiParams &ep, cudaStream_t s) {
+  if (ctx->dtype == STADI_DTYPE_BF16)
+    return tc_gemm_bf16((const bf16 *)A, (const bf16 *)W, M, N, K, epi, ep,
+                        std::max(1, ctx->num_sms - ctx->emu_ctas), s);
+  return simt_gemm<float>((const float *)A, (const float *)W, M, N, K, epi, ep, s);
+}
+cudaError_t attention(stadi_ctx *ctx, const void *q, const void *kv, void *o, int Nq, int Nkv,
+                      cudaStream_t s) {
+  const Dims &m = ctx->dm;
+  if (ctx->dtype == STADI_DTYPE_BF16)
+    return tc_attention_bf16((const bf16 *)q, (const bf16 *)kv, (bf16 *)o, Nq, Nkv, m.B, m.H,
+                             m.hd, s);
+  return simt_attention<float>((const float *)q, (const float *)kv, (float *)o, Nq, Nkv, m.B,
+                               m.H, m.hd, s);
+}
+cudaError_t lnmod(stadi_ctx *ctx, const float *x, void *y, int M, const float *shift,
+                  const float *scale, int bs, int do_norm, cudaStream_t s) {
+  if (ctx->dtype == STADI_DTYPE_BF16)
+    return ln_modulate<bf16>(x, (bf16 *)y, M, ctx->dm.d, ctx->dm.B, shift, scale, bs, do_norm, s);
+  return ln_modulate<float>(x, (float *)y, M, ctx->dm.d, ctx->dm.B, shift, scale, bs, do_norm, s);
+}
+
+int widx(stadi_ctx *ctx, const std::string &name) {
+  for (size_t i = 0; i < ctx->man.size(); ++i)
+    if (ctx->man[i].name == name) return (int)i;
+  return -1;
+}
+void *WT(stadi_ctx *ctx, const std::string &n) { return ctx->wT[widx(ctx, n)]; }
+float *WF(stadi_ctx *ctx, const std::string &n) { return ctx->wf[widx(ctx, n)]; }
+
+void free_plan_buffers(stadi_ctx *ctx) {
+  for (auto &r : ctx->ranks) {
+    cudaFree(r.x_band); cudaFree(r.x_res); cudaFree(r.xmod); cudaFree(r.q); cudaFree(r.o);
+    cudaFree(r.h1); cudaFree(r.eps_raw);
+    for (void *p : r.kv) cudaFree(p);
+  }
+  ctx->ranks.clear();
+  ctx->program.clear();
+  for (auto e : ctx->ev_done) cudaEventDestroy(e);
+  ctx->ev_done.clear();
+  ctx->ev_used.clear();
+  if (ctx->sub_comm && ctx->sub_comm != ctx->world_comm && nccl().CommDestroy)
+    nccl().CommDestroy(ctx->sub_comm);
+  ctx->sub_comm = nullptr;
+  ctx->has_plan = false;
+  ctx->begun = false;
+}
+
+int64_t slot_elems(const Dims &m) { return (int64_t)m.hp * m.wp * m.B * 2 * m.d; }
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" const char *stadi_last_error(const stadi_ctx *ctx) {
+  return ctx ? ctx->err.c_str() : tls_error().c_str();
+}
+
+extern "C" stadi_status stadi_weight_count(const stadi_model_desc *desc, uint32_t *n) {
+  if (!desc || !n) return fail(nullptr, STADI_EINVAL, "NULL argument");
+  Dims d;
+  std::string e;
+  if (!make_dims(*desc, d, e)) return fail(nullptr, STADI_EINVAL, "%s", e.c_str());
+  *n = (uint32_t)manifest(d).size();
+  return STADI_OK;
+}
+
+extern "C" stadi_status stadi_weight_info(const stadi_model_desc *desc, uint32_t index,
+                                          char *name_buf, uint32_t name_cap, uint64_t *numel) {
+  if (!desc) return fail(nullptr, STADI_EINVAL, "NULL argument");
+  Dims d;
+  std::string e;
+  if (!make_dims(*desc, d, e)) return fail(nullptr, STADI_EINVAL, "%s", e.c_str());
+  auto man = manifest(d);
+  if (index >= man.size()) return fail(nullptr, STADI_EINVAL, "index out of range");
+  if (name_buf && name_cap) {
+    std::strncpy(name_buf, man[index].name.c_str(), name_cap - 1);
+    name_buf[name_cap - 1] = 0;
+  }
+  if (numel) *numel = (uint64_t)(man[index].rows * man[index].cols);
+  return STADI_OK;
+}
+
+extern "C" stadi_status stadi_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return fail(nullptr, STADI_EINVAL, "NULL argument");
+  if (!nccl().ok) return fail(nullptr, STADI_ENCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  ncclResult_t r = nccl().GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, STADI_ENCCL, "ncclGetUniqueId failed");
+  std::memcpy(out, &id, 128);
+  return STADI_OK;
+}
+
+extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_dist_desc *dist,
+                                     stadi_ctx **out) {
+  if (!model || !dist || !out) return fail(nullptr, STADI_EINVAL, "NULL argument");
+  *out = nullptr;
+  Dims dm;
+  std::string e;
+  if (!make_dims(*model, dm, e)) return fail(nullptr, STADI_EINVAL, "%s", e.c_str());
+  if (model->dtype != STADI_DTYPE_BF16 && model->dtype != STADI_DTYPE_FP32_DEBUG)
+    return fail(nullptr, STADI_EINVAL, "bad dtype");
+  if (model->sampler != STADI_SAMPLER_DDIM)
+    return fail(nullptr, STADI_EUNSUPPORTED, "only the DDIM sampler (Eq. 3) is implemented");
+  if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || dist->n_local < 1 ||
+      (dist->world > 1 && dist->n_local != 1) || dist->world * dist->n_local > STADI_MAX_GPUS)
+    return fail(nullptr, STADI_EINVAL, "bad dist desc (n_local > 1 requires world == 1)");
+  if (model->dtype == STADI_DTYPE_BF16 && !tc_attention_supported(dm.hd))
+    return fail(nullptr, STADI_EUNSUPPORTED, "head dim %d not supported by the tcgen05 kernel",
+                dm.hd);
+  auto ctx = std::make_unique<stadi_ctx>();
+  ctx->dm = dm;
+  ctx->dtype = model->dtype;
+  ctx->esz = model->dtype == STADI_DTYPE_BF16 ? 2 : 4;
+  ctx->device = dist->device;
+  ctx->rank = dist->rank;
+  ctx->world = dist->world;
+  ctx->n_local = dist->n_local;
+  ctx->G = dist->world * dist->n_local;
+  ctx->man = manifest(dm);
+  ctx->fin_ld = (int)rup(dm.p * dm.p * dm.c_out, 64);
+  alpha_bar(dm.schedule_linear != 0, ctx->abar);
+  stadi_ctx *c = ctx.get();
+  {
+    stadi_ctx *ctx = c;  // for CK
+    CK(cudaSetDevice(dist->device));
+    CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dist->device));
+    int lo, hi;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
+    // positional embedding of the full token grid, fp64 on the host (pins the
+    // values to 1 ulp of fp32), [sin(c w), cos(c w), sin(r w), cos(r w)]
+    const int q4 = dm.d / 4;
+    std::vector<float> pos((size_t)dm.hp * dm.wp * dm.d);
+    for (int r = 0; r < dm.hp; ++r)
+      for (int cc = 0; cc < dm.wp; ++cc) {
+        float *row = &pos[((size_t)r * dm.wp + cc) * dm.d];
+        for (int k = 0; k < q4; ++k) {
+          const double w = 1.0 / std::pow(10000.0, (double)k / q4);
+          row[k] = (float)std::sin(cc * w);
+          row[q4 + k] = (float)std::cos(cc * w);
+          row[2 * q4 + k] = (float)std::sin(r * w);
+          row[3 * q4 + k] = (float)std::cos(r * w);
+        }
+      }
+    CK(dalloc(ctx, &ctx->pos_full, pos.size() * 4));
+    CK(cudaMemcpy(ctx->pos_full, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice));
+    if (dist->world > 1) {
+      if (!nccl().ok) return ctx_fail(ctx, STADI_ENCCL, "libnccl.so.2 not loadable");
+      if (!dist->nccl_id) return ctx_fail(ctx, STADI_EINVAL, "nccl_id required when world > 1");
+      ncclUniqueId id;
+      std::memcpy(&id, dist->nccl_id, 128);
+      CKN(nccl().CommInitRank(&ctx->world_comm, dist->world, id, dist->rank));
+    }
+    CK(cudaHostAlloc(&ctx->emu_flag_host, 64, cudaHostAllocMapped));
+    *ctx->emu_flag_host = 0;
+    CK(cudaHostGetDevicePointer(&ctx->emu_flag_dev, ctx->emu_flag_host, 0));
+    CK(cudaStreamCreateWithFlags(&ctx->emu_stream, cudaStreamNonBlocking));
+  }
+  *out = ctx.release();
+  return STADI_OK;
+}
+
+extern "C" void stadi_destroy(stadi_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->emu_ctas) {
+    *ctx->emu_flag_host = 1;
+    cudaStreamSynchronize(ctx->emu_stream);
+  }
+  cudaDeviceSynchronize();
+  free_plan_buffers(ctx);
+  for (void *p : ctx->allocs) cudaFree(p);
+  for (void *p : ctx->wT) cudaFree(p);
+  for (float *p : ctx->wf) cudaFree(p);
+  if (ctx->world_comm && nccl().CommDestroy) nccl().CommDestroy(ctx->world_comm);
+  if (ctx->comm) cudaStreamDestroy(ctx->comm);
+  if (ctx->emu_stream) cudaStreamDestroy(ctx->emu_stream);
+  if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
+  if (ctx->emu_flag_host) cudaFreeHost(ctx->emu_flag_host);
+  cudaGetLastError();
+  delete ctx;
+}
+
+namespace {
+// fp32 -> T conversion on the device (bf16: round-to-nearest-even)
+cudaError_t upload_T(stadi_ctx *ctx, const float *host, int64_t n, void **dst_T, float **dst_f) {
+  float *f = nullptr;
+  cudaError_t e = cudaMalloc(&f, n * 4);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(f, host, n * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return e;
+  if (ctx->dtype == STADI_DTYPE_BF16) {
+    bf16 *t = nullptr;
+    e = cudaMalloc(&t, n * 2);
+    if (e != cudaSuccess) return e;
+    e = cast_f32<bf16>(f, t, n, 0);
+    if (e != cudaSuccess) return e;
+    // fp32 copy holds the bf16-rounded values (the oracle's bf16 parity weights)
+    std::vector<float> tmp;
+    (void)tmp;
+    if (dst_T) *dst_T = t;
+    else cudaFree(t);
+  } else if (dst_T) {
+    *dst_T = f;
+  }
+  *dst_f = f;
+  return cudaSuccess;
+}
+
+__global__ void round_bf16_inplace(float *x, long n) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
+}
+}  // namespace
+
+extern "C" stadi_status stadi_load_weights(stadi_ctx *ctx, uint32_t n_tensors,
+                                           const float *const *host, const uint64_t *numels) {
+  ALIVE();
+  if (!host || !numels) return ctx_fail(ctx, STADI_EINVAL, "NULL argument");
+  if (n_tensors != ctx->man.size())
+    return ctx_fail(ctx, STADI_EINVAL, "expected %zu tensors, got %u", ctx->man.size(), n_tensors);
+  for (uint32_t i = 0; i < n_tensors; ++i) {
+    const uint64_t want = (uint64_t)(ctx->man[i].rows * ctx->man[i].cols);
+    if (numels[i] != want || !host[i])
+      return ctx_fail(ctx, STADI_EINVAL, "tensor %u (%s): numel %llu, expected %llu", i,
+                      ctx->man[i].name.c_str(), (unsigned long long)numels[i],
+                      (unsigned long long)want);
+  }
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->weights_loaded) return ctx_fail(ctx, STADI_ESTATE, "weights already loaded");
+  const Dims &m = ctx->dm;
+  const bool bf = ctx->dtype == STADI_DTYPE_BF16;
+  ctx->wT.assign(n_tensors, nullptr);
+  ctx->wf.assign(n_tensors, nullptr);
+  for (uint32_t i = 0; i < n_tensors; ++i) {
+    const auto &ts = ctx->man[i];
+    const int64_t n = ts.rows * ts.cols;
+    CK(upload_T(ctx, host[i], n, ts.gemm_weight ? &ctx->wT[i] : nullptr, &ctx->wf[i]));
+    if (bf) {
+      round_bf16_inplace<<<(unsigned)((n + 255) / 256), 256>>>(ctx->wf[i], n);
+      CK(cudaGetLastError());
+    }
+  }
+  // contiguous per-block tensors for the batched conditioning GEMM
+  const int64_t d = m.d;
+  if (!m.text) {
+    CK(dalloc(ctx, &ctx->ada_all, m.depth * 6 * d * d * ctx->esz));
+    CK(dalloc(ctx, &ctx->ada_all_b, m.depth * 6 * d * 4));
+    for (int l = 0; l < m.depth; ++l) {
+      const std::string p = "blocks." + std::to_string(l) + ".";
+      CK(cudaMemcpy((char *)ctx->ada_all + l * 6 * d * d * ctx->esz, WT(ctx, p + "ada.w"),
+                    6 * d * d * ctx->esz, cudaMemcpyDeviceToDevice));
+      CK(cudaMemcpy(ctx->ada_all_b + l * 6 * d, WF(ctx, p + "ada.b"), 6 * d * 4,
+                    cudaMemcpyDeviceToDevice));
+    }
+  } else {
+    CK(dalloc(ctx, &ctx->sst_all, m.depth * 6 * d * 4));
+    for (int l = 0; l < m.depth; ++l)
+      CK(cudaMemcpy(ctx->sst_all + l * 6 * d, WF(ctx, "blocks." + std::to_string(l) + ".sst"),
+                    6 * d * 4, cudaMemcpyDeviceToDevice));
+  }
+  // final linear, rows zero-padded to fin_ld (tcgen05 N granularity)
+  const int nf = m.p * m.p * m.c_out;
+  CK(dalloc(ctx, &ctx->final_w, (size_t)ctx->fin_ld * d * ctx->esz));
+  CK(cudaMemset(ctx->final_w, 0, (size_t)ctx->fin_ld * d * ctx->esz));
+  CK(cudaMemcpy(ctx->final_w, WT(ctx, "final.linear.w"), (size_t)nf * d * ctx->esz,
+                cudaMemcpyDeviceToDevice));
+  CK(dalloc(ctx, &ctx->final_b, ctx->fin_ld * 4));
+  CK(cudaMemset(ctx->final_b, 0, ctx->fin_ld * 4));
+  CK(cudaMemcpy(ctx->final_b, WF(ctx, "final.linear.b"), nf * 4, cudaMemcpyDeviceToDevice));
+  CK(cudaDeviceSynchronize());
+  ctx->weights_loaded = true;
+  return STADI_OK;
+}
+
+// ---------------------------------------------------------------- plan install
+extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan) {
+  ALIVE();
+  if (!plan) return ctx_fail(ctx, STADI_EINVAL, "NULL plan");
+  const Dims &m = ctx->dm;
+  if ((int)plan->n_gpus != ctx->G)
+    return ctx_fail(ctx, STADI_EINVAL, "plan has %u GPUs, group has %d", plan->n_gpus, ctx->G);
+  if ((int64_t)plan->p_total * plan->rows_per_unit != m.lat_h || plan->rows_per_unit % m.p)
+    return ctx_fail(ctx, STADI_EINVAL,
+                    "plan covers %u x %u rows; latent has %d rows (unit must be a multiple of p)",
+                    plan->p_total, plan->rows_per_unit, m.lat_h);
+  if (plan->m_base > 1000) return ctx_fail(ctx, STADI_EINVAL, "M_base > 1000");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  free_plan_buffers(ctx);
+  ctx->plan = *plan;
+  const int g0 = ctx->rank * ctx->n_local;
+  for (int k = 0; k < ctx->n_local; ++k) {
+    const int g = g0 + k;
+    if (plan->tier[g] == 0) continue;  // excluded (Eq. 4 third case)
+    Rank r;
+    r.g = g;
+    r.tier = plan->tier[g];
+    r.row_begin = (int)plan->row_begin[g];
+    r.rows = (int)plan->rows[g];
+    r.tok_begin = r.row_begin / m.p * m.wp;
+    r.n_tok = r.rows / m.p * m.wp;
+    uint32_t n = 0;
+    if (stadi_schedule(plan, g, nullptr, 0, &n) != STADI_OK)
+      return ctx_fail(ctx, STADI_EINVAL, "bad plan: %s", tls_error().c_str());
+    r.sched.resize(n);
+    stadi_schedule(plan, g, r.sched.data(), n, &n);
+    const int64_t M = (int64_t)r.n_tok * m.B;
+    CK(cudaMalloc(&r.x_band, std::max<int64_t>(16, (int64_t)r.rows * m.lat_w * m.c_in * 4)));
+    CK(cudaMalloc(&r.x_res, std::max<int64_t>(16, M * m.d * 4)));
+    CK(cudaMalloc(&r.xmod, std::max<int64_t>(16, M * m.d * ctx->esz)));
+    CK(cudaMalloc(&r.q, std::max<int64_t>(16, M * m.d * ctx->esz)));
+    CK(cudaMalloc(&r.o, std::max<int64_t>(16, M * m.d * ctx->esz)));
+    CK(cudaMalloc(&r.h1, std::max<int64_t>(16, M * 4 * m.d * ctx->esz)));
+    CK(cudaMalloc(&r.eps_raw, std::max<int64_t>(16, M * ctx->fin_ld * 4)));
+    r.kv.assign(m.depth * 2, nullptr);
+    for (auto &p : r.kv) {
+      CK(cudaMalloc(&p, slot_elems(m) * ctx->esz));
+      CK(cudaMemset(p, 0, slot_elems(m) * ctx->esz));
+    }
+    ctx->ranks.push_back(std::move(r));
+  }
+  // program
+  if (ctx->world > 1) {
+    if (!ctx->ranks.empty())
+      for (auto &st : ctx->ranks[0].sched) ctx->program.push_back({Part{0, st}});
+  } else {
+    for (int mm = 0; mm < (int)plan->m_base; ++mm) {
+      std::vector<Part> ph;
+      for (int li = 0; li < (int)ctx->ranks.size(); ++li)
+        for (auto &st : ctx->ranks[li].sched)
+          if (st.m == mm) ph.push_back(Part{li, st});
+      if (!ph.empty()) ctx->program.push_back(ph);
+    }
+  }
+  // NCCL: communicator over the included ranks + exchange events
+  if (ctx->world > 1) {
+    const bool inc = !ctx->ranks.empty();
+    bool all_inc = true;
+    for (uint32_t i = 0; i < plan->n_gpus; ++i) all_inc &= plan->tier[i] != 0;
+    if (all_inc) {
+      ctx->sub_comm = ctx->world_comm;
+    } else {
+      if (!nccl().CommSplit) return ctx_fail(ctx, STADI_ENCCL, "ncclCommSplit unavailable");
+      CKN(nccl().CommSplit(ctx->world_comm, inc ? 0 : NCCL_SPLIT_NOCOLOR, ctx->rank,
+                           &ctx->sub_comm, nullptr));
+    }
+    ctx->ev_done.assign(m.depth * 2, nullptr);
+    ctx->ev_used.assign(m.depth * 2, 0);
+    for (auto &e : ctx->ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ctx->has_plan = true;
+  return STADI_OK;
+}
+
+// ---------------------------------------------------------------- request begin
+extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
+                                    const stadi_cond *cond, void *stream) {
+  ALIVE();
+  if (!ctx->has_plan) return ctx_fail(ctx, STADI_ESTATE, "stadi_begin before stadi_set_plan");
+  if (!ctx->weights_loaded) return ctx_fail(ctx, STADI_ESTATE, "weights not loaded");
+  if (!noise_full || !cond) return ctx_fail(ctx, STADI_EINVAL, "NULL argument");
+  const Dims &m = ctx->dm;
+  if (m.text ? !cond->text : !cond->labels)
+    return ctx_fail(ctx, STADI_EINVAL, "conditioning missing (%s)", m.text ? "text" : "labels");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(ctx->device));
+  // noise bands
+  const bool dev = is_device_ptr(noise_full);
+  const size_t row_bytes = (size_t)m.lat_w * m.c_in * 4;
+  for (auto &r : ctx->ranks)
+    CK(cudaMemcpyAsync(r.x_band, noise_full + (size_t)r.row_begin * m.lat_w * m.c_in,
+                       row_bytes * r.rows, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       s));
+  // ---- conditioning for every fast-grid timestep (one batched GEMM each)
+  const int nt = (int)ctx->plan.m_base;
+  const int64_t d = m.d;
+  const int B = m.B;
+  if (ctx->cond_cap_nt < (size_t)nt) {
+    // (re)allocate per-request conditioning buffers
+    for (void *p : {(void *)ctx->mod, (void *)ctx->fmod, (void *)ctx->temb, (void *)ctx->tmp_f,
+                    (void *)ctx->tfreq, ctx->csilu})
+      cudaFree(p);
+    CK(cudaMalloc(&ctx->mod, (size_t)nt * B * m.depth * 6 * d * 4));
+    CK(cudaMalloc(&ctx->fmod, (size_t)nt * B * 2 * d * 4));
+    CK(cudaMalloc(&ctx->temb, (size_t)nt * d * 4));
+    CK(cudaMalloc(&ctx->tmp_f, (size_t)nt * 6 * d * 4));
+    CK(cudaMalloc(&ctx->tfreq, (size_t)nt * 256 * 4));
+    CK(cudaMalloc(&ctx->csilu, (size_t)nt * B * d * ctx->esz));
+    ctx->cond_cap_nt = nt;
+  }
+  ctx->n_t = nt;
+  {
+    // sinusoidal timestep features on the host in fp64 (DiT TimestepEmbedder)
+    std::vector<float> tf((size_t)nt * 256);
+    const int ratio = 1000 / nt;
+    for (int i = 0; i < nt; ++i) {
+      const double t = ratio * (nt - 1 - i) + 1;  // fast grid (R18)
+      for (int k = 0; k < 128; ++k) {
+        const double f = std::exp(-std::log(10000.0) * k / 128.0);
+        tf[(size_t)i * 256 + k] = (float)std::cos(t * f);
+        tf[(size_t)i * 256 + 128 + k] = (float)std::sin(t * f);
+      }
+    }
+    CK(cudaMemcpyAsync(ctx->tfreq, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));  // tf is a host temporary
+  }
+  EpiParams ep{};
+  ep.B = 1;
+  ep.bias = WF(ctx, "t_embed.b1");
+  ep.out = ctx->tmp_f;
+  ep.ldo = (int)d;
+  CK(simt_gemm<float>(ctx->tfreq, WF(ctx, "t_embed.w1"), nt, (int)d, 256, EPI_F32, ep, s));
+  CK(silu_inplace(ctx->tmp_f, (long)nt * d, s));
+  ep.bias = WF(ctx, "t_embed.b2");
+  ep.out = ctx->temb;
+  CK(simt_gemm<float>(ctx->tmp_f, WF(ctx, "t_embed.w2"), nt, (int)d, (int)d, EPI_F32, ep, s));
+  if (!m.text) {
+    if (!ctx->labels_dev) CK(dalloc(ctx, &ctx->labels_dev, 64 * 4));
+    for (int b = 0; b < B; ++b)
+      if (cond->labels[b] < 0 || cond->labels[b] > m.num_classes)
+        return ctx_fail(ctx, STADI_EINVAL, "class label out of range");
+    CK(cudaMemcpyAsync(ctx->labels_dev, cond->labels, B * 4, cudaMemcpyHostToDevice, s));
+    if (ctx->dtype == STADI_DTYPE_BF16)
+      CK(class_cond<bf16>(ctx->temb, WF(ctx, "y_embed.table"), ctx->labels_dev, nt, B, (int)d,
+                          (bf16 *)ctx->csilu, s));
+    else
+      CK(class_cond<float>(ctx->temb, WF(ctx, "y_embed.table"), ctx->labels_dev, nt, B, (int)d,
+                           (float *)ctx->csilu, s));
+    // adaLN for all blocks and all timesteps: [nt*B, d] x [depth*6d, d]^T
+    ep.bias = ctx->ada_all_b;
+    ep.out = ctx->mod;
+    ep.ldo = (int)(m.depth * 6 * d);
+    CK(gemm(ctx, ctx->csilu, ctx->ada_all, nt * B, (int)(m.depth * 6 * d), (int)d, EPI_F32, ep,
+            s));
+    ep.bias = WF(ctx, "final.ada.b");
+    ep.out = ctx->fmod;
+    ep.ldo = (int)(2 * d);
+    CK(gemm(ctx, ctx->csilu, WT(ctx, "final.ada.w"), nt * B, (int)(2 * d), (int)d, EPI_F32, ep,
+            s));
+  } else {
+    // adaLN-single: t0 = W SiLU(t_emb) + b ; mod_l = sst_l + t0 ; final = sst_f + t_emb
+    if (ctx->dtype == STADI_DTYPE_BF16)
+      CK(silu_cast<bf16>(ctx->temb, (bf16 *)ctx->csilu, (long)nt * d, s));
+    else
+      CK(silu_cast<float>(ctx->temb, (float *)ctx->csilu, (long)nt * d, s));
+    ep.bias = WF(ctx, "t_block.b");
+    ep.out = ctx->tmp_f;
+    ep.ldo = (int)(6 * d);
+    CK(gemm(ctx, ctx->csilu, WT(ctx, "t_block.w"), nt, (int)(6 * d), (int)d, EPI_F32, ep, s));
+    CK(pixart_mods(ctx->tmp_f, ctx->temb, ctx->sst_all, WF(ctx, "final.sst"), nt, B, m.depth,
+                   (int)d, ctx->mod, ctx->fmod, s));
+    // caption projection + per-block cross-attention K/V (once per request)
+    const int L = m.txt_len, Dt = m.txt_dim;
+    const int64_t Mt = (int64_t)L * B;
+    if (!ctx->text_T) {
+      CK(dalloc(ctx, &ctx->text_T, Mt * Dt * ctx->esz));
+      CK(dalloc(ctx, &ctx->y1, Mt * d * ctx->esz));
+      CK(dalloc(ctx, &ctx->y, Mt * d * ctx->esz));
+      ctx->kv_text.assign(m.depth, nullptr);
+      for (auto &p : ctx->kv_text) CK(dalloc(ctx, &p, Mt * 2 * d * ctx->esz));
+    }
+    // host reorder [B, L, D] -> [L, B, D] (token-major, batch innermost)
+    std::vector<float> tx((size_t)Mt * Dt);
+    for (int b = 0; b < B; ++b)
+      for (int j = 0; j < L; ++j)
+        std::memcpy(&tx[((size_t)j * B + b) * Dt], cond->text + ((size_t)b * L + j) * Dt, Dt * 4);
+    float *tx_dev = nullptr;
+    CK(cudaMalloc(&tx_dev, tx.size() * 4));
+    CK(cudaMemcpyAsync(tx_dev, tx.data(), tx.size() * 4, cudaMemcpyHostToDevice, s));
+    if (ctx->dtype == STADI_DTYPE_BF16)
+      CK(cast_f32<bf16>(tx_dev, (bf16 *)ctx->text_T, (long)tx.size(), s));
+    else
+      CK(cudaMemcpyAsync(ctx->text_T, tx_dev, tx.size() * 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(tx_dev);
+    ep.bias = WF(ctx, "caption.b1");
+    ep.out = ctx->y1;
+    ep.ldo = (int)d;
+    CK(gemm(ctx, ctx->text_T, WT(ctx, "caption.w1"), (int)Mt, (int)d, Dt, EPI_GELU, ep, s));
+    ep.bias = WF(ctx, "caption.b2");
+    ep.out = ctx->y;
+    CK(gemm(ctx, ctx->y1, WT(ctx, "caption.w2"), (int)Mt, (int)d, (int)d, EPI_STORE, ep, s));
+    for (int l = 0; l < m.depth; ++l) {
+      const std::string p = "blocks." + std::to_string(l) + ".";
+      ep.bias = WF(ctx, p + "xkv.b");
+      ep.out = ctx->kv_text[l];
+      ep.ldo = (int)(2 * d);
+      CK(gemm(ctx, ctx->y, WT(ctx, p + "xkv.w"), (int)Mt, (int)(2 * d), (int)d, EPI_STORE, ep, s));
+    }
+  }
+  ctx->begun = true;
+  ctx->exch_bytes = 0;
+  return STADI_OK;
+}
+
+extern "C" stadi_status stadi_num_steps(stadi_ctx *ctx, uint32_t *n) {
+  ALIVE();
+  if (!n) return ctx_fail(ctx, STADI_EINVAL, "NULL argument");
+  if (!ctx->has_plan) return ctx_fail(ctx, STADI_ESTATE, "no plan installed");
+  *n = (uint32_t)ctx->program.size();
+  return STADI_OK;
+}
+
+// ---------------------------------------------------------------- exchange
+namespace {
+
+// Rows of group rank g in a slot (element offset, element count).
+void seg_of(stadi_ctx *ctx, int g, int64_t *off, int64_t *cnt) {
+  const Dims &m = ctx->dm;
+  const int64_t per_tok = (int64_t)m.B * 2 * m.d;
+  *off = (int64_t)ctx->plan.row_begin[g] / m.p * m.wp * per_tok;
+  *cnt = (int64_t)ctx->plan.rows[g] / m.p * m.wp * per_tok;
+}
+
+// Publish the own rows of version `ver` at site l (after the QKV GEMM wrote them).
+stadi_status publish(stadi_ctx *ctx, int li, int l, int ver, cudaStream_t s) {
+  Rank &r = ctx->ranks[li];
+  const int slot = l * 2 + (ver & 1);
+  int64_t off, cnt;
+  seg_of(ctx, r.g, &off, &cnt);
+  const size_t bytes = cnt * ctx->esz;
+  if (ctx->world == 1) {  // local mode: copy into every other hosted rank's slot
+    for (auto &o : ctx->ranks) {
+      if (o.g == r.g) continue;
+      CK(cudaMemcpyAsync((char *)o.kv[slot] + off * ctx->esz, (char *)r.kv[slot] + off * ctx->esz,
+                         bytes, cudaMemcpyDeviceToDevice, s));
+      ctx->exch_bytes += bytes;
+    }
+    return STADI_OK;
+  }
+  // NCCL mode: in-place variable-size all-gather = one broadcast per included root
+  CK(cudaEventRecord(ctx->ev_ready, s));
+  CK(cudaStreamWaitEvent(ctx->comm, ctx->ev_ready, 0));
+  const ncclDataType_t dt = ctx->dtype == STADI_DTYPE_BF16 ? ncclBfloat16 : ncclFloat32;
+  CKN(nccl().GroupStart());
+  int root = 0;
+  for (uint32_t g = 0; g < ctx->plan.n_gpus; ++g) {
+    if (!ctx->plan.tier[g]) continue;
+    int64_t o2, c2;
+    seg_of(ctx, (int)g, &o2, &c2);
+    void *p = (char *)r.kv[slot] + o2 * ctx->esz;
+    CKN(nccl().Broadcast(p, p, (size_t)c2, dt, root, ctx->sub_comm, ctx->comm));
+    ++root;
+  }
+  CKN(nccl().GroupEnd());
+  CK(cudaEventRecord(ctx->ev_done[slot], ctx->comm));
+  ctx->ev_used[slot] = 1;
+  ctx->exch_bytes += bytes;
+  return STADI_OK;
+}
+
+// Make stream s wait until version `ver` of site l is complete (NCCL mode).
+stadi_status wait_version(stadi_ctx *ctx, int l, int ver, cudaStream_t s) {
+  if (ctx->world == 1 || ver < 0) return STADI_OK;
+  const int slot = l * 2 + (ver & 1);
+  if (ctx->ev_used[slot]) CK(cudaStreamWaitEvent(s, ctx->ev_done[slot], 0));
+  return STADI_OK;
+}
+
+#define ST(call)                          \
+  do {                                    \
+    stadi_status s_ = (call);             \
+    if (s_ != STADI_OK) return s_;        \
+  } while (0)
+
+// One program step: patch-local forward of every part in layer lock-step,
+// exchange at every attention site, then the Eq. 3 update of each band.
+stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStream_t s) {
+  const Dims &m = ctx->dm;
+  const int64_t d = m.d;
+  const int B = m.B;
+  const int64_t mod_bs = (int64_t)m.depth * 6 * d;  // batch stride in mod
+  const int ntok_full = m.hp * m.wp;
+  for (const Part &P : phase) {  // x_res = patch embedding of the band (+ pos)
+    Rank &r = ctx->ranks[P.li];
+    CK(patch_embed(r.x_band, r.rows, m.lat_w, m.c_in, m.p, WF(ctx, "x_embed.w"),
+                   WF(ctx, "x_embed.b"), ctx->pos_full + (int64_t)r.tok_begin * d, (int)d, B,
+                   r.x_res, s));
+  }
+  for (int l = 0; l < m.depth; ++l) {
+    const std::string pre = "blocks." + std::to_string(l) + ".";
+    for (const Part &P : phase) {  // ---- LN/modulate + QKV (+ publish)
+      Rank &r = ctx->ranks[P.li];
+      const int M = r.n_tok * B;
+      const float *mb = ctx->mod + ((int64_t)P.st.m * B * m.depth + l) * 6 * d;
+      CK(lnmod(ctx, r.x_res, r.xmod, M, mb, mb + d, (int)mod_bs, 1, s));
+      // own rows may only be overwritten once this rank's earlier sends of
+      // the read version completed (NCCL mode)
+      if (P.st.pub_ver != P.st.read_ver) ST(wait_version(ctx, l, P.st.read_ver, s));
+      EpiParams ep{};
+      ep.bias = WF(ctx, pre + "qkv.b");
+      ep.B = B;
+      ep.q = r.q;
+      ep.d = (int)d;
+      ep.kv_a = r.kv[l * 2 + (P.st.read_ver & 1)];
+      ep.kv_b = (P.st.pub_ver >= 0 && P.st.pub_ver != P.st.read_ver)
+                    ? r.kv[l * 2 + (P.st.pub_ver & 1)]
+                    : nullptr;
+      ep.kv_row0 = (int64_t)r.tok_begin * B;
+      CK(gemm(ctx, r.xmod, WT(ctx, pre + "qkv.w"), M, (int)(3 * d), (int)d, EPI_QKV, ep, s));
+      if (P.st.pub_ver >= 0) ST(publish(ctx, P.li, l, P.st.pub_ver, s));
+      if (P.st.pub_ver == P.st.read_ver) ST(wait_version(ctx, l, P.st.read_ver, s));  // fresh
+    }
+    for (const Part &P : phase) {  // ---- attention + rest of the block
+      Rank &r = ctx->ranks[P.li];
+      const int M = r.n_tok * B;
+      const float *mb = ctx->mod + ((int64_t)P.st.m * B * m.depth + l) * 6 * d;
+      CK(attention(ctx, r.q, r.kv[l * 2 + (P.st.read_ver & 1)], r.o, r.n_tok, ntok_full, s));
+      EpiParams ep{};
+      ep.B = B;
+      ep.bias = WF(ctx, pre + "proj.b");
+      ep.res = r.x_res;
+      ep.ldr = (int)d;
+      ep.gate = mb + 2 * d;
+      ep.gate_bstride = (int)mod_bs;
+      CK(gemm(ctx, r.o, WT(ctx, pre + "proj.w"), M, (int)d, (int)d, EPI_GATED_RES, ep, s));
+      if (m.text) {  // cross-attention to the caption tokens (band-local)
+        CK(lnmod(ctx, r.x_res, r.xmod, M, nullptr, nullptr, 0, 0, s));
+        EpiParams eq{};
+        eq.B = B;
+        eq.bias = WF(ctx, pre + "xq.b");
+        eq.out = r.q;
+        eq.ldo = (int)d;
+        CK(gemm(ctx, r.xmod, WT(ctx, pre + "xq.w"), M, (int)d, (int)d, EPI_STORE, eq, s));
+        CK(attention(ctx, r.q, ctx->kv_text[l], r.o, r.n_tok, m.txt_len, s));
+        EpiParams er{};
+        er.B = B;
+        er.bias = WF(ctx, pre + "xproj.b");
+        er.res = r.x_res;
+        er.ldr = (int)d;
+        CK(gemm(ctx, r.o, WT(ctx, pre + "xproj.w"), M, (int)d, (int)d, EPI_RES, er, s));
+      }
+      CK(lnmod(ctx, r.x_res, r.xmod, M, mb + 3 * d, mb + 4 * d, (int)mod_bs, 1, s));
+      EpiParams e1{};
+      e1.B = B;
+      e1.bias = WF(ctx, pre + "fc1.b");
+      e1.out = r.h1;
+      e1.ldo = (int)(4 * d);
+      CK(gemm(ctx, r.xmod, WT(ctx, pre + "fc1.w"), M, (int)(4 * d), (int)d, EPI_GELU, e1, s));
+      EpiParams e2{};
+      e2.B = B;
+      e2.bias = WF(ctx, pre + "fc2.b");
+      e2.res = r.x_res;
+      e2.ldr = (int)d;
+      e2.gate = mb + 5 * d;
+      e2.gate_bstride = (int)mod_bs;
+      CK(gemm(ctx, r.h1, WT(ctx, pre + "fc2.w"), M, (int)d, (int)(4 * d), EPI_GATED_RES, e2, s));
+    }
+  }
+  for (const Part &P : phase) {  // ---- final layer + CFG + unpatchify + Eq. 3
+    Rank &r = ctx->ranks[P.li];
+    const int M = r.n_tok * B;
+    const float *fb = ctx->fmod + (int64_t)P.st.m * B * 2 * d;
+    CK(lnmod(ctx, r.x_res, r.xmod, M, fb, fb + d, (int)(2 * d), 1, s));
+    EpiParams ef{};
+    ef.B = B;
+    ef.bias = ctx->final_b;
+    ef.out = r.eps_raw;
+    ef.ldo = ctx->fin_ld;
+    CK(gemm(ctx, r.xmod, ctx->final_w, M, ctx->fin_ld, (int)d, EPI_F32, ef, s));
+    float A, Bc;
+    ddim_coeffs(ctx->abar, P.st.t, P.st.t_prev, &A, &Bc);
+    CK(sampler_update(r.x_band, r.eps_raw, r.rows, m.lat_w, m.c_in, m.p, m.c_out, ctx->fin_ld, B,
+                      m.guidance, A, Bc, s));
+  }
+  return STADI_OK;
+}
+
+}  // namespace
+
+extern "C" stadi_status stadi_denoise_step(stadi_ctx *ctx, uint32_t step, void *stream) {
+  ALIVE();
+  if (!ctx->begun) return ctx_fail(ctx, STADI_ESTATE, "stadi_denoise_step before stadi_begin");
+  if (step >= ctx->program.size()) return ctx_fail(ctx, STADI_EINVAL, "step out of range");
+  CK(cudaSetDevice(ctx->device));
+  return run_phase(ctx, ctx->program[step], (cudaStream_t)stream);
+}
+
+extern "C" stadi_status stadi_gather(stadi_ctx *ctx, float *out_full, void *stream) {
+  ALIVE();
+  if (!ctx->begun) return ctx_fail(ctx, STADI_ESTATE, "stadi_gather before stadi_begin");
+  if (!out_full) return ctx_fail(ctx, STADI_EINVAL, "NULL argument");
+  const Dims &m = ctx->dm;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(ctx->device));
+  const bool dev = is_device_ptr(out_full);
+  const size_t row_elems = (size_t)m.lat_w * m.c_in;
+  if (ctx->world == 1) {
+    for (auto &r : ctx->ranks)
+      CK(cudaMemcpyAsync(out_full + (size_t)r.row_begin * row_elems, r.x_band,
+                         (size_t)r.rows * row_elems * 4,
+                         dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    return STADI_OK;
+  }
+  // NCCL: every rank (excluded ones too) receives every band (world communicator)
+  float *full = nullptr;
+  CK(cudaMallocAsync(&full, (size_t)m.lat_h * row_elems * 4, s));
+  if (!ctx->ranks.empty())
+    CK(cudaMemcpyAsync(full + (size_t)ctx->ranks[0].row_begin * row_elems, ctx->ranks[0].x_band,
+                       (size_t)ctx->ranks[0].rows * row_elems * 4, cudaMemcpyDeviceToDevice, s));
+  CKN(nccl().GroupStart());
+  for (uint32_t g = 0; g < ctx->plan.n_gpus; ++g) {
+    if (!ctx->plan.rows[g]) continue;
+    float *p = full + (size_t)ctx->plan.row_begin[g] * row_elems;
+    CKN(nccl().Broadcast(p, p, (size_t)ctx->plan.rows[g] * row_elems, ncclFloat32, (int)g,
+                         ctx->world_comm, s));
+  }
+  CKN(nccl().GroupEnd());
+  CK(cudaMemcpyAsync(out_full, full, (size_t)m.lat_h * row_elems * 4,
+                     dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(full, s));
+  return STADI_OK;
+}
+
+extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, const float *noise_full,
+                                  const stadi_cond *cond, float *out_full, stadi_run_stats *stats,
+                                  void *stream) {
+  ALIVE();
+  if (!plan || !noise_full || !cond || !out_full)
+    return ctx_fail(ctx, STADI_EINVAL, "NULL argument");
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->has_plan || std::memcmp(plan, &ctx->plan, sizeof(stadi_plan_t)) != 0)
+    ST(stadi_set_plan(ctx, plan));
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const unsigned long long l0 = g_launches;
+  CK(cudaEventRecord(e0, s));
+  ST(stadi_begin(ctx, noise_full, cond, stream));
+  for (uint32_t i = 0; i < ctx->program.size(); ++i) ST(run_phase(ctx, ctx->program[i], s));
+  ST(stadi_gather(ctx, out_full, stream));
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (stats) {
+    stats->ms_total = ms;
+    stats->ms_exchange_wait = 0;
+    stats->exchange_bytes = ctx->exch_bytes;
+    stats->kernel_launches = (uint32_t)(g_launches - l0);
+    stats->steps_run = (uint32_t)ctx->program.size();
+  }
+  return STADI_OK;
+}
+
+// ---------------------------------------------------------------- profiling (a1)
+extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, double *ms_out,
+                                             uint64_t *speed_out) {
+  ALIVE();
+  if (!ms_out || !speed_out || n_steps == 0) return ctx_fail(ctx, STADI_EINVAL, "bad argument");
+  if (!ctx->weights_loaded) return ctx_fail(ctx, STADI_ESTATE, "weights not loaded");
+  const Dims &m = ctx->dm;
+  CK(cudaSetDevice(ctx->device));
+  // uniform probe plan over the whole group (Eq. 5 with equal speeds)
+  std::vector<uint64_t> ones(ctx->G, 1);
+  stadi_plan_params pp{};
+  pp.n_gpus = ctx->G;
+  pp.speed = ones.data();
+  pp.m_base = 10;
+  pp.m_warmup = 10;
+  pp.a_num = 3; pp.a_den = 4; pp.b_num = 1; pp.b_den = 4;
+  pp.rows_per_unit = m.p;
+  pp.p_total = m.lat_h / m.p;
+  pp.flags = STADI_NO_TA | STADI_NO_SA;
+  if ((int)pp.p_total < ctx->G) return ctx_fail(ctx, STADI_EINVAL, "latent too small for group");
+  stadi_plan_t probe;
+  if (stadi_plan(&pp, &probe) != STADI_OK)
+    return ctx_fail(ctx, STADI_EINVAL, "probe plan: %s", tls_error().c_str());
+  ST(stadi_set_plan(ctx, &probe));
+  std::vector<float> zeros((size_t)m.lat_h * m.lat_w * m.c_in, 0.f);
+  std::vector<int32_t> labels(m.B, 0);
+  std::vector<float> text;
+  stadi_cond cond{labels.data(), nullptr};
+  if (m.text) {
+    text.assign((size_t)m.B * m.txt_len * m.txt_dim, 0.f);
+    cond.text = text.data();
+  }
+  cudaStream_t s = nullptr;
+  ST(stadi_begin(ctx, zeros.data(), &cond, s));
+  std::vector<double> ms_local(ctx->ranks.size(), 0.0);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  for (size_t li = 0; li < ctx->ranks.size(); ++li) {
+    std::vector<double> v;
+    // compute-only probe step: reads version 0, publishes nothing (no waits)
+    Part P{(int)li, stadi_step_t{0, 901, 801, STADI_STEP_UNIFORM, 0, STADI_VER_NONE}};
+    for (uint32_t it = 0; it <= n_steps; ++it) {
+      CK(cudaEventRecord(e0, s));
+      ST(run_phase(ctx, {P}, s));
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (it > 0) v.push_back(ms);  // first one is a warm-up
+    }
+    std::sort(v.begin(), v.end());
+    ms_local[li] = v[v.size() / 2];
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  std::vector<double> all(ctx->G, 0.0);
+  if (ctx->world == 1) {
+    for (size_t li = 0; li < ctx->ranks.size(); ++li) all[ctx->ranks[li].g] = ms_local[li];
+  } else {
+    double *dsend = nullptr, *drecv = nullptr;
+    CK(cudaMalloc(&dsend, 8));
+    CK(cudaMalloc(&drecv, 8 * ctx->G));
+    CK(cudaMemcpy(dsend, ms_local.data(), 8, cudaMemcpyHostToDevice));
+    CKN(nccl().AllGather(dsend, drecv, 1, ncclFloat64, ctx->world_comm, s));
+    CK(cudaMemcpy(all.data(), drecv, 8 * ctx->G, cudaMemcpyDeviceToHost));
+    cudaFree(dsend);
+    cudaFree(drecv);
+  }
+  double mn = all[0];
+  for (double x : all) mn = std::min(mn, x);
+  for (int g = 0; g < ctx->G; ++g) {
+    ms_out[g] = all[g];
+    speed_out[g] = (uint64_t)std::llround(1048576.0 * mn / all[g]);
+    if (!speed_out[g]) speed_out[g] = 1;
+  }
+  free_plan_buffers(ctx);
+  return STADI_OK;
+}
+
+// ---------------------------------------------------------------- emulator (a9)
+extern "C" stadi_status stadi_emulator_start(stadi_ctx *ctx, uint32_t pct) {
+  ALIVE();
+  if (pct > 95) return ctx_fail(ctx, STADI_EINVAL, "occupancy must be <= 95%%");
+  if (ctx->emu_ctas) return ctx_fail(ctx, STADI_ESTATE, "emulator already running");
+  if (pct == 0) return STADI_OK;
+  CK(cudaSetDevice(ctx->device));
+  const int n = (int)std::ceil(pct * ctx->num_sms / 100.0);
+  *ctx->emu_flag_host = 0;
+  CK(emulator_launch(n, ctx->emu_flag_dev, ctx->emu_stream));
+  ctx->emu_ctas = n;
+  return STADI_OK;
+}
+
+extern "C" stadi_status stadi_emulator_stop(stadi_ctx *ctx) {
+  ALIVE();
+  if (!ctx->emu_ctas) return STADI_OK;
+  *ctx->emu_flag_host = 1;
+  CK(cudaStreamSynchronize(ctx->emu_stream));
+  ctx->emu_ctas = 0;
+  return STADI_OK;
+}

@@ -1,0 +1,164 @@
+"""Kernel-level parity (GPU): the tcgen05/TMA bf16 kernels and the SIMT fp32
+kernels against the oracle's plain fp64 definitions (oracle/dit.py), at
+sizes that span several tiles with ragged tails, plus the degenerate cases.
+
+Tolerances (max |x - ref| / max |ref|):
+  bf16 kernels: 1e-2 — operands are exact bf16 values, accumulation is fp32;
+    the error is the bf16 rounding of the output (2^-9 relative) and, for
+    attention, of P (2^-9) — 1e-2 leaves ~5x headroom.
+  fp32 SIMT kernels: 1e-5 (fp32 accumulation over K <= 4608).
+"""
+import numpy as np
+import pytest
+
+from oracle import dit as OD
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2509_04719_b200 import stadi
+    return stadi
+
+
+def _bf(x):  # numpy fp32 -> torch bf16 on GPU, and back the exact values
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda().to(torch.bfloat16)
+    return t, t.float().cpu().numpy().astype(np.float64)
+
+
+def _f32(x):
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+    return t, t.cpu().numpy().astype(np.float64)
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+GEMM_SHAPES = [(1, 64, 64), (77, 192, 256), (128, 128, 64), (300, 384, 1152), (1000, 256, 128),
+               (513, 3456, 1152), (64, 768, 64), (2048, 1152, 4608)]
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["bf16", "fp32"])
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_store_f32_gelu(S, dtype, M, N, K):
+    rng = np.random.default_rng(M * 7 + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    bias = (rng.standard_normal(N) * 0.1).astype(np.float32)
+    mk = _bf if dtype == 0 else _f32
+    tA, nA = mk(A)
+    tW, nW = mk(W)
+    tb = torch.from_numpy(bias).cuda()
+    ref = OD.linear(nA, nW, bias.astype(np.float64))
+    tol = 1e-2 if dtype == 0 else 1e-5
+    # fp32 output
+    out = torch.zeros(M, N, device="cuda")
+    S.k_gemm(dtype, tA, tW, M, N, K, S.EPI_F32, bias=tb, out=out, ldo=N, B=1)
+    torch.cuda.synchronize()
+    assert _rel(out.cpu().numpy(), ref) < (1e-5 if True else tol)
+    # T output, GELU
+    outT = torch.zeros(M, N, device="cuda", dtype=tA.dtype)
+    S.k_gemm(dtype, tA, tW, M, N, K, S.EPI_GELU, bias=tb, out=outT, ldo=N, B=1)
+    torch.cuda.synchronize()
+    assert _rel(outT.float().cpu().numpy(), OD.gelu_tanh(ref)) < tol
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["bf16", "fp32"])
+def test_gemm_gated_residual_and_qkv(S, dtype):
+    rng = np.random.default_rng(5)
+    B, ntok, d = 2, 150, 64
+    M, K = ntok * B, d
+    mk = _bf if dtype == 0 else _f32
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    # gated residual, gate row per batch
+    W = (rng.standard_normal((d, K)) / 8).astype(np.float32)
+    tA, nA = mk(A)
+    tW, nW = mk(W)
+    bias = (rng.standard_normal(d) * 0.1).astype(np.float32)
+    gate = rng.standard_normal((B, 7, d)).astype(np.float32)   # batch stride 7*d
+    res0 = rng.standard_normal((M, d)).astype(np.float32)
+    res = torch.from_numpy(res0.copy()).cuda()
+    S.k_gemm(dtype, tA, tW, M, d, K, S.EPI_GATED_RES, bias=torch.from_numpy(bias).cuda(),
+             res=res, ldr=d, gate=torch.from_numpy(gate).cuda(), gate_bstride=7 * d, B=B)
+    torch.cuda.synchronize()
+    lin = OD.linear(nA, nW, bias.astype(np.float64))
+    g = gate[np.arange(M) % B, 0, :].astype(np.float64)
+    ref = res0 + g * lin
+    assert _rel(res.cpu().numpy() - res0, ref - res0) < 1e-5 * (1 if dtype else 1)
+    # QKV scatter into two exchange slots at own rows
+    Wq = (rng.standard_normal((3 * d, K)) / 8).astype(np.float32)
+    tWq, nWq = mk(Wq)
+    ntok_full, tok0 = 400, 123
+    q = torch.zeros(M, d, device="cuda", dtype=tA.dtype)
+    kva = torch.zeros(ntok_full, B, 2, d, device="cuda", dtype=tA.dtype)
+    kvb = torch.zeros_like(kva)
+    bq = (rng.standard_normal(3 * d) * 0.1).astype(np.float32)
+    S.k_gemm(dtype, tA, tWq, M, 3 * d, K, S.EPI_QKV, bias=torch.from_numpy(bq).cuda(), q=q,
+             kv_a=kva, kv_b=kvb, kv_row0=tok0 * B, d=d, B=B)
+    torch.cuda.synchronize()
+    full = OD.linear(nA, nWq, bq.astype(np.float64))
+    tol = 1e-2 if dtype == 0 else 1e-5
+    assert _rel(q.float().cpu().numpy(), full[:, :d]) < tol
+    for kv in (kva, kvb):
+        got = kv.float().cpu().numpy()
+        own = got[tok0:tok0 + ntok].reshape(M, 2 * d)
+        assert _rel(own, full[:, d:]) < tol
+        assert np.all(got[:tok0] == 0) and np.all(got[tok0 + ntok:] == 0)
+
+
+ATTN_CASES = [  # Nq, Nkv, B, H, hd
+    (1, 64, 1, 4, 16), (32, 64, 1, 4, 16), (200, 1000, 2, 3, 64), (128, 256, 2, 2, 72),
+    (300, 777, 2, 2, 72), (128, 120, 2, 16, 72), (256, 384, 1, 1, 80), (1000, 2048, 2, 2, 72),
+]
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["bf16", "fp32"])
+@pytest.mark.parametrize("Nq,Nkv,B,H,hd", ATTN_CASES)
+def test_attention(S, dtype, Nq, Nkv, B, H, hd):
+    rng = np.random.default_rng(Nq + Nkv + hd)
+    d = H * hd
+    q = rng.standard_normal((Nq, B, d)).astype(np.float32)
+    kv = rng.standard_normal((Nkv, B, 2, d)).astype(np.float32)
+    mk = _bf if dtype == 0 else _f32
+    tq, nq = mk(q)
+    tkv, nkv = mk(kv)
+    o = torch.full((Nq * B, d), float("nan"), device="cuda", dtype=tq.dtype)
+    S.k_attention(dtype, tq, tkv, o, Nq, Nkv, B, H, hd)
+    torch.cuda.synchronize()
+    got = o.float().cpu().numpy().reshape(Nq, B, d)
+    # oracle layout [B, n, d]
+    ref = OD.attention(nq.transpose(1, 0, 2), nkv[:, :, 0].transpose(1, 0, 2),
+                       nkv[:, :, 1].transpose(1, 0, 2), H).transpose(1, 0, 2)
+    assert np.all(np.isfinite(got))
+    assert _rel(got, ref) < (1e-2 if dtype == 0 else 1e-5)
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["bf16", "fp32"])
+@pytest.mark.parametrize("M,d,B", [(1, 64, 1), (333, 1152, 2), (64, 64, 2)])
+def test_ln_modulate(S, dtype, M, d, B):
+    rng = np.random.default_rng(M + d)
+    x = (rng.standard_normal((M, d)) * 3 + 1).astype(np.float32)
+    mod = rng.standard_normal((B, 6, d)).astype(np.float32)
+    tx = torch.from_numpy(x).cuda()
+    tm = torch.from_numpy(mod).cuda()
+    y = torch.zeros(M, d, device="cuda", dtype=torch.bfloat16 if dtype == 0 else torch.float32)
+    S.k_ln_modulate(dtype, tx, y, M, d, B, tm[0, 0], tm[0, 1], 6 * d)
+    torch.cuda.synchronize()
+    b = np.arange(M) % B
+    ref = OD.layernorm(x.astype(np.float64)) * (1 + mod[b, 1]) + mod[b, 0]
+    assert _rel(y.float().cpu().numpy(), ref) < (1e-2 if dtype == 0 else 1e-5)
+
+
+def test_bad_shapes_rejected(S):
+    A = torch.zeros(128, 100, device="cuda", dtype=torch.bfloat16)
+    W = torch.zeros(64, 100, device="cuda", dtype=torch.bfloat16)
+    out = torch.zeros(128, 64, device="cuda")
+    with pytest.raises(S.StadiError) as e:
+        S.k_gemm(0, A, W, 128, 64, 100, S.EPI_F32, out=out, ldo=64, B=1)   # K % 64 != 0
+    assert e.value.status == 1
+    q = torch.zeros(128, 40, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(S.StadiError):
+        S.k_attention(0, q, q, q, 128, 64, 1, 1, 40)                      # hd 40 unsupported

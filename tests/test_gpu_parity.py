@@ -1,0 +1,173 @@
+"""End-to-end parity (GPU): STADI runs through the C ABI (stadi_run, local
+mode = all ranks of the plan hosted on one GPU, exchange by device copies)
+against the fp64 oracle (oracle/stadi.py) on the same seeded inputs.
+
+North-star tolerances (BASELINE.json): max-abs-rel <= 1e-4 for the fp32 debug
+build, <= 2e-2 for bf16; max-abs-rel = max|x - x_ref| / max|x_ref| on the final
+latent (R23).  In bf16 mode the oracle consumes the same bf16-rounded weights
+(R22).
+"""
+import numpy as np
+import pytest
+
+from oracle import planner as OP
+from oracle import stadi as OR
+from synth import configs, gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {0: 2e-2, 1: 1e-4}
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2509_04719_b200 import stadi
+    return stadi
+
+
+_cache = {}
+
+
+def _inputs(name, **kw):
+    key = (name, tuple(sorted(kw.items())))
+    if key not in _cache:
+        cfg = configs.model(name, **kw)
+        _cache[key] = (cfg, gen.weights(cfg), gen.noise(cfg), gen.cond(cfg))
+    return _cache[key]
+
+
+def _oracle(cfg, W, x, c, plan, dtype):
+    key = ("oracle", cfg["name"], cfg["depth"], cfg["latent_h"], dtype, repr(plan))
+    if key not in _cache:
+        _cache[key] = OR.run(cfg, gen.weights_bf16(W) if dtype == 0 else W, x, c, plan)
+    return _cache[key]
+
+
+def _gpu_run(S, name, cfg, W, x, c, speed, mb, mw, dtype, flags=0, device_ptrs=False,
+             forced=None):
+    desc = S.model_desc(name, dtype, depth=cfg["depth"], latent_h=cfg["latent_h"],
+                        latent_w=cfg["latent_w"])
+    ctx = S.Context(desc, n_local=len(speed))
+    try:
+        ctx.load_weights([W[n] for n, _, _ in configs.manifest(cfg)])
+        p = S.plan(speed, mb, mw, cfg["latent_h"] // cfg["patch"], cfg["patch"], flags=flags,
+                   forced_units=forced)
+        if device_ptrs:
+            noise = torch.from_numpy(x).cuda()
+            out = torch.zeros_like(noise)
+            st = ctx.run(p, noise, c, out)
+            got = out.cpu().numpy()
+        else:
+            out = np.zeros_like(x)
+            st = ctx.run(p, x, c, out)
+            got = out
+        return got.astype(np.float64), p, st
+    finally:
+        ctx.close()
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+@pytest.mark.parametrize("dtype", [1, 0], ids=["fp32", "bf16"])
+def test_c1_tiny_two_ranks(S, dtype):
+    """BASELINE config C1: tiny DiT, speeds [1.0, 0.5], T=10, 2 warmup."""
+    cfg, W, x, c = _inputs("tiny_dit")
+    speed = [1 << 20, 1 << 19]
+    plan = OR.plan_for(cfg, speed, 10, 2)
+    ref = _oracle(cfg, W, x, c, plan, dtype)
+    got, p, st = _gpu_run(S, "tiny_dit", cfg, W, x, c, speed, 10, 2, dtype)
+    assert p.to_dict()["steps"] == [10, 6] and p.to_dict()["units"] == [4, 4]
+    assert np.all(np.isfinite(got))
+    err = _rel(got, ref)
+    print(f"C1 dtype={dtype} max-abs-rel={err:.3e} launches={st.kernel_launches}")
+    assert err <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [1, 0], ids=["fp32", "bf16"])
+@pytest.mark.parametrize("speed,flags", [
+    ([1], 0),                                   # single GPU == sequential DDIM
+    ([3, 2, 1], OP.NO_TA | OP.NO_SA),           # uniform patch parallelism (DistriFusion)
+    ([100, 60, 100, 10], 0),                    # tier 1 / tier 2 / excluded GPU
+    ([5, 4, 3], OP.SIZER_INTERVAL),
+])
+def test_tiny_protocol_variants(S, dtype, speed, flags):
+    cfg, W, x, c = _inputs("tiny_dit")
+    plan = OR.plan_for(cfg, speed, 10, 2, flags=flags)
+    ref = _oracle(cfg, W, x, c, plan, dtype)
+    got, _, _ = _gpu_run(S, "tiny_dit", cfg, W, x, c, speed, 10, 2, dtype, flags=flags,
+                         device_ptrs=True)
+    assert _rel(got, ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [1, 0], ids=["fp32", "bf16"])
+def test_c2_dit_xl2_depth_reduced(S, dtype):
+    """C2 shapes (d 1152, 16 heads, 32x32 latent, CFG 4.0, 50 steps, 2 GPUs,
+    one at 40% occupancy -> v = 0.6), depth reduced to 2 blocks for the oracle."""
+    cfg, W, x, c = _inputs("dit_xl2", depth=2)
+    speed = [65536, 39322]
+    plan = OR.plan_for(cfg, speed, 50, 4)
+    ref = _oracle(cfg, W, x, c, plan, dtype)
+    got, p, _ = _gpu_run(S, "dit_xl2", cfg, W, x, c, speed, 50, 4, dtype)
+    assert p.to_dict()["steps"] == [50, 27]
+    err = _rel(got, ref)
+    print(f"C2(depth2) dtype={dtype} max-abs-rel={err:.3e}")
+    assert err <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [1, 0], ids=["fp32", "bf16"])
+def test_c5_pixart_reduced(S, dtype):
+    """C5 shapes (PixArt-alpha: d 1152, 16 heads, cross-attention to 120x4096
+    text, adaLN-single, CFG 4.5, 20 steps), depth 2 and a 32x40 latent for the
+    oracle; 2 GPUs, the second at 50% occupancy."""
+    cfg, W, x, c = _inputs("pixart_alpha", depth=2, latent_h=32, latent_w=40)
+    speed = [1 << 16, 1 << 15]
+    plan = OR.plan_for(cfg, speed, 20, 4)
+    ref = _oracle(cfg, W, x, c, plan, dtype)
+    got, p, _ = _gpu_run(S, "pixart_alpha", cfg, W, x, c, speed, 20, 4, dtype)
+    err = _rel(got, ref)
+    print(f"C5(reduced) dtype={dtype} max-abs-rel={err:.3e}")
+    assert err <= TOL[dtype]
+
+
+def test_deterministic_and_step_api(S):
+    """stadi_run twice gives identical bits; begin + denoise_step* + gather
+    equals stadi_run."""
+    cfg, W, x, c = _inputs("tiny_dit")
+    a, _, _ = _gpu_run(S, "tiny_dit", cfg, W, x, c, [2, 1], 10, 2, 0)
+    b, _, _ = _gpu_run(S, "tiny_dit", cfg, W, x, c, [2, 1], 10, 2, 0)
+    assert np.array_equal(a, b)
+    desc = S.model_desc("tiny_dit", 0)
+    ctx = S.Context(desc, n_local=2)
+    try:
+        ctx.load_weights([W[n] for n, _, _ in configs.manifest(cfg)])
+        p = S.plan([2, 1], 10, 2, 8, 2)
+        ctx.set_plan(p)
+        ctx.begin(x, c)
+        n = ctx.num_steps()
+        assert n == 10
+        for i in range(n):
+            ctx.denoise_step(i)
+        out = np.zeros_like(x)
+        ctx.gather(out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.astype(np.float64), a)
+    finally:
+        ctx.close()
+
+
+def test_profile_warmup_and_emulator(S):
+    cfg, W, x, c = _inputs("dit_xl2", depth=2)
+    ctx = S.Context(S.model_desc("dit_xl2", 0, depth=2), n_local=2)
+    try:
+        ctx.load_weights([W[n] for n, _, _ in configs.manifest(cfg)])
+        ms, sp = ctx.profile_warmup(3, 2)
+        assert all(m > 0 for m in ms) and max(sp) == 1 << 20 and min(sp) > (1 << 19)
+        ctx.emulator_start(50)
+        ms2, _ = ctx.profile_warmup(3, 2)
+        ctx.emulator_stop()
+        assert min(ms2) > min(ms) * 0.9      # fewer SMs cannot be faster
+    finally:
+        ctx.close()
