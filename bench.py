@@ -1,0 +1,428 @@
+"""bench.py — per-image latency / images/s of STADI on N B200s vs uniform patch
+parallelism built from the same kernels (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c5|c2] [--occupancy half50|zero|<p0,p1,...>]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+
+A "step" is one whole STADI request (SURVEY §8(a) a1..a9 minus the one-off
+profiling): begin (per-request conditioning) -> every denoising step of the
+rank's schedule (patch-local DiT forward with stale K/V exchange + Eq. 3
+sampler) -> final latent all-gather.  One step = one image, so
+``value`` = images/s of the whole job and ``ms_per_step`` = per-image latency.
+
+Workload: BASELINE configs[4] = C5, the PixArt-alpha-shaped DiT
+at 2048^2 (256x256x4 latent, 16384 tokens, d 1152, 16 heads, depth 28, T5 text
+120x4096, CFG 4.5), 20 DDIM steps, M_warmup 4, a = 3/4, b = 1/4; the 1/2/4/8
+GPU scaling sweep with 50% emulated occupancy on the upper half of the GPUs
+(0% at N = 1).  Random-init weights and seeded synthetic inputs (synth/).
+
+JSON keys beyond the base contract: ``uniform_pp`` (the same-kernel uniform
+patch-parallel baseline, NO_TA|NO_SA plan, timed the same way), ``roofline``
+(dominant kernel = self-attention, CUDA events around every launch inside the
+timed region), ``cpu_baseline`` (the fp64 oracle on a bounded sample,
+extrapolated by FLOP count), ``e2e`` (stadi_run with pinned HOST buffers),
+``clocks`` (nvidia-smi sampled during the timed region), ``gpu_launches``.
+
+The oracle (oracle/) is executed only by the cpu_baseline leg and by
+``--impl reference``; the timed path is libstadi.so through its C ABI.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from synth import configs, gen  # noqa: E402
+
+WORKLOADS = {
+    "c5": dict(model="pixart_alpha", m_base=20, m_warmup=4, name=(
+        "C5 PixArt-alpha-shaped DiT 2048^2 (256x256x4 latent, 16384 tokens, d1152 h16 "
+        "depth28, T5 120x4096, CFG 4.5), 20 DDIM steps, M_warmup 4")),
+    "c2": dict(model="dit_xl2", m_base=50, m_warmup=4, name=(
+        "C2 DiT-XL/2-shaped 256^2 (32x32x4 latent, 256 tokens, d1152 h16 depth28, "
+        "class cond, CFG 4.0), 50 DDIM steps, M_warmup 4")),
+}
+PAPER_CONTEXT = ("paper: up to 45% lower latency than patch parallelism (SDXL 1024^2, "
+                 "M_base=100, 2x RTX 4090 over PCIe, occupancy [0,60]%; Table III / L11)")
+
+
+# --------------------------------------------------------------------- helpers
+def dit_flops(cfg, n_q, n_kv, B):
+    """Algorithmic FLOPs of one DiT block on n_q own tokens against n_kv keys
+    (2 per multiply-add): qkv 3d^2 + proj d^2 + fc1/fc2 8d^2 (+ xq/xproj 2d^2
+    for text presets), self-attention 4 n_q n_kv d, cross-attention 4 n_q L d."""
+    d = cfg["hidden"]
+    text = cfg["cond"] == "text"
+    lin = 2.0 * n_q * B * d * d * (12 + (2 if text else 0))
+    att = 4.0 * n_q * n_kv * d * B
+    xatt = 4.0 * n_q * cfg.get("text_len", 0) * d * B if text else 0.0
+    return lin + att + xatt
+
+
+def image_flops(cfg, m_base):
+    hp, wp = configs.tokens_hw(cfg)
+    n = hp * wp
+    B = configs.batch(cfg)
+    return m_base * cfg["depth"] * dit_flops(cfg, n, n, B)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return dict(tflops=float(j["bf16_tflops_sustained"]), tflops_burst=float(j["bf16_tflops"]),
+                    hbm=float(j["hbm_gbs"]), src="measured (MEASURED_PEAKS.json)")
+    except Exception:
+        return dict(tflops=1590.0, tflops_burst=1590.0, hbm=6650.0,
+                    src="fallback (B200_PROFILING.md)")
+
+
+def occupancy_list(spec, n):
+    if spec == "zero":
+        return [0] * n
+    if spec == "half50":
+        return [0] * n if n == 1 else [0 if r < n // 2 else 50 for r in range(n)]
+    v = [int(x) for x in spec.split(",")]
+    assert len(v) == n, "occupancy list must have one entry per GPU"
+    return v
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, v in zip(names, r[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(k)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- oracle legs
+def oracle_sample(cfg, rows_lat, seconds_hint=None):
+    """Run the fp64 oracle (as it stands) on a bounded sample: the full-width
+    latent cut to `rows_lat` rows, depth 1, ONE sequential DDIM step.  Returns
+    (seconds, sample FLOPs, threads)."""
+    from oracle import stadi as OR
+    scfg = configs.model(cfg["name"], depth=1, latent_h=rows_lat)
+    W = gen.weights(scfg)
+    x = gen.noise(scfg)
+    c = gen.cond(scfg)
+    hp, wp = configs.tokens_hw(scfg)
+    n = hp * wp
+    fl = dit_flops(scfg, n, n, configs.batch(scfg))
+    t0 = time.perf_counter()
+    OR.sequential(scfg, W, x, c, 1)
+    dt = time.perf_counter() - t0
+    return dt, fl, _blas_threads()
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        th = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(th) if th else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, wl, target_s=15.0):
+    """Oracle throughput on a bounded sample, extrapolated per image by FLOPs."""
+    rows = 32 if cfg["latent_h"] >= 32 else cfg["latent_h"]
+    total_t, total_f, reps, th = 0.0, 0.0, 0, 1
+    while total_t < target_s and reps < 20:
+        dt, fl, th = oracle_sample(cfg, rows)
+        total_t += dt
+        total_f += fl
+        reps += 1
+    rate = total_f / total_t                              # fp64 FLOP/s on the host
+    ms_img = image_flops(cfg, wl["m_base"]) / rate * 1e3
+    return {"value": 1e3 / ms_img, "unit": "images/s", "ms_per_image": ms_img, "cores": th,
+            "kind": "oracle",
+            "sample": (f"{reps} x oracle.stadi.sequential on a {rows}x{cfg['latent_w']} latent, "
+                       f"depth 1, 1 DDIM step ({total_t:.1f} s, {total_f / 1e9:.0f} GFLOP fp64); "
+                       f"per-image latency extrapolated by FLOP count to the full workload "
+                       f"({image_flops(cfg, wl['m_base']) / 1e12:.0f} TFLOP/image)")}
+
+
+def run_reference(args, cfg, wl, rank, world):
+    """--impl reference: the oracle, as it stands, on this host's cores."""
+    if rank != 0:
+        return
+    rows = 32 if cfg["latent_h"] >= 32 else cfg["latent_h"]
+    for _ in range(args.warmup):
+        oracle_sample(cfg, rows)
+    ts, fls, th = [], [], 1
+    for _ in range(args.steps):
+        dt, fl, th = oracle_sample(cfg, rows)
+        ts.append(dt)
+        fls.append(fl)
+    rate = sum(fls) / sum(ts)
+    ms_img = image_flops(cfg, wl["m_base"]) / rate * 1e3
+    val = 1e3 / ms_img
+    sample = (f"each step = oracle.stadi.sequential on a {rows}x{cfg['latent_w']} latent, depth 1, "
+              f"1 DDIM step ({np.mean(ts):.2f} s); per-image latency extrapolated by FLOP count")
+    out = {"impl": "reference", "metric": args.metric, "value": val, "unit": "images/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_img,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": wl["name"], "n_gpus": world},
+           "cpu_baseline": {"value": val, "unit": "images/s", "cores": th, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": val, "unit": "images/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--occupancy", default="half50")
+    ap.add_argument("--no-uniform", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.metric = "per-image latency ms & images/s at 1/2/4/8 B200 vs uniform patch-par"
+    assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    wl = WORKLOADS[args.workload]
+    cfg = configs.model(wl["model"])
+
+    if args.impl == "reference":
+        run_reference(args, cfg, wl, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2509_04719_b200 import stadi as S
+
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- context (NCCL communicator of the library, id through torch.distributed)
+    nid = None
+    if world > 1:
+        obj = [S.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    desc = S.model_desc(wl["model"], S.DTYPE_BF16)
+    ctx = S.Context(desc, rank=rank, world=world, device=local, nccl_id=nid)
+    W = gen.weights(cfg)
+    ctx.load_weights([W[n] for n, _, _ in configs.manifest(cfg)])
+    del W
+    x = gen.noise(cfg)
+    c = gen.cond(cfg)
+    p = cfg["patch"]
+    p_total = cfg["latent_h"] // p
+
+    # ---- a9 occupancy emulation, a1 profiling, a2/a3 plans
+    occ = occupancy_list(args.occupancy, world)
+    if occ[rank]:
+        ctx.emulator_start(occ[rank])
+    barrier()
+    ms_prof, speed = ctx.profile_warmup(3, world)
+    plan = S.plan(speed, wl["m_base"], wl["m_warmup"], p_total, p)
+    uplan = S.plan(speed, wl["m_base"], wl["m_warmup"], p_total, p, flags=S.NO_TA | S.NO_SA)
+
+    noise_dev = torch.from_numpy(x).cuda()
+    text_dev = None
+    cond = dict(c)
+    if "text" in c:  # conditioning resident in HBM for the device-timed legs
+        text_dev = torch.from_numpy(c["text"]).cuda()
+        cond = {"text": text_dev}
+    out_dev = torch.empty_like(noise_dev)
+    stream = torch.cuda.current_stream()
+
+    def timed(pl, noise, out, cnd, k, w, ktime=False):
+        for _ in range(w):
+            ctx.run(pl, noise, cnd, out, stream=stream)
+        torch.cuda.synchronize()
+        l0 = S.launch_count()
+        if ktime:
+            ctx.kernel_timing(True)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            ctx.run(pl, noise, cnd, out, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        launches = S.launch_count() - l0
+        return max_over_ranks(ms), launches
+
+    # ---- STADI, device-resident inputs (value), with live kernel timing
+    with ClockSampler(local) as clk:
+        ms, launches = timed(plan, noise_dev, out_dev, cond, args.steps, args.warmup, ktime=True)
+    kst = {k: ctx.kernel_stats(k) for k in S.KCLASS}
+    ctx.kernel_timing(False)
+    ms_img = ms / args.steps
+    value = 1e3 / ms_img
+
+    # ---- uniform patch parallelism, same kernels (NO_TA | NO_SA)
+    uni = None
+    if not args.no_uniform:
+        ums, _ = timed(uplan, noise_dev, out_dev, cond, args.steps, args.warmup)
+        u_img = ums / args.steps
+        uni = {"value": 1e3 / u_img, "ms_per_image": u_img, "plan": _plan_json(uplan),
+               "stadi_latency_reduction": 1.0 - ms_img / u_img}
+
+    # ---- e2e: through the C ABI with pinned HOST buffers (H2D + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        noise_h = torch.from_numpy(x).pin_memory()
+        out_h = torch.empty_like(noise_h).pin_memory()
+        cond_h = dict(c)
+        if "text" in c:
+            cond_h = {"text": torch.from_numpy(c["text"]).pin_memory()}
+        ems, _ = timed(plan, noise_h, out_h, cond_h, args.steps, 1)
+        h2d = x.nbytes + (c["text"].nbytes if "text" in c else c["labels"].nbytes)
+        e2e = {"value": 1e3 / (ems / args.steps), "unit": "images/s",
+               "ms_per_image": ems / args.steps, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(x.nbytes)}
+
+    if occ[rank]:
+        ctx.emulator_stop()
+
+    # ---- roofline of the dominant kernel (self-attention)
+    peaks = load_peaks()
+    n_att, ms_att, fl_att, _ = kst["attn"]
+    step_kernel_ms = sum(v[1] for v in kst.values())
+    roof = None
+    if n_att:
+        avg_ms = ms_att / n_att
+        ach = fl_att / n_att / (avg_ms * 1e-3) / 1e12
+        roof = {"kernel": "tc_attn_kernel (own Q x full stale K/V, tcgen05/TMEM)", "bound": "tensor",
+                "achieved": ach, "peak": peaks["tflops"], "unit": "TFLOP/s",
+                "frac": ach / peaks["tflops"], "traffic": _traffic("attn"),
+                "peak_src": peaks["src"] + ", bf16 dense sustained",
+                "flops_per_launch": fl_att / n_att, "avg_launch_ms": avg_ms,
+                "launches": n_att, "share_of_kernel_time": ms_att / max(step_kernel_ms, 1e-9)}
+    kernels = {k: {"launches": v[0], "ms": v[1],
+                   "tflops": (v[2] / (v[1] * 1e-3) / 1e12) if v[1] and v[2] else None,
+                   "gbs": (v[3] / (v[1] * 1e-3) / 1e9) if v[1] and v[3] else None}
+               for k, v in kst.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, wl)
+
+    if rank == 0:
+        res = {
+            "metric": args.metric, "value": value, "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_img,
+            "latency_ms": ms_img, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded noise / T5-shaped text, random-init weights)",
+            "config": {"workload": wl["name"], "n_gpus": world, "occupancy_pct": occ,
+                       "speed_q20": [int(s) for s in speed], "profile_ms": ms_prof,
+                       "plan": _plan_json(plan),
+                       "l2": "inputs larger than L2: 8.5 GB K/V slots + 1.3 GB bf16 weights "
+                             "streamed per image (126 MB L2)",
+                       "parallelism": f"stadi-patch{world}"},
+            "uniform_pp": uni, "e2e": e2e, "roofline": roof, "kernels": kernels,
+            "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(launches),
+            "context": PAPER_CONTEXT,
+        }
+        print(json.dumps(res), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _plan_json(p):
+    d = p.to_dict()
+    return {k: d[k] for k in ("tier", "steps", "units", "rows", "n_exchange_rounds")}
+
+
+def _traffic(kernel):
+    """DRAM bytes per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

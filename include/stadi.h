@@ -238,6 +238,26 @@ stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, const float *no
 stadi_status stadi_emulator_start(stadi_ctx *ctx, uint32_t occupancy_pct);
 stadi_status stadi_emulator_stop(stadi_ctx *ctx);
 
+/* Per-class kernel timing (measurement).  When enabled, every
+ * launch of a timed class is bracketed by two CUDA events recorded on the
+ * stream the kernel is launched on; stadi_kernel_stats synchronises the
+ * device, folds the events in and returns, for the class, the number of
+ * launches, their summed device time in ms and their summed ALGORITHMIC work
+ * (flops: 2 per multiply-add of the layer's definition, attention = QK^T + PV;
+ * bytes: the kernel's compulsory HBM reads + writes).  Enabling (or
+ * re-enabling) resets the totals.  EINVAL for an unknown class. */
+enum {
+  STADI_KCLASS_GEMM = 0,     /* every tcgen05 / SIMT linear layer              */
+  STADI_KCLASS_ATTN = 1,     /* self-attention, own Q x full (stale) K/V       */
+  STADI_KCLASS_XATTN = 2,    /* cross-attention to the text tokens             */
+  STADI_KCLASS_NORM = 3,     /* LayerNorm + adaLN modulate                     */
+  STADI_KCLASS_SAMPLER = 4,  /* CFG + unpatchify + Eq. 3 update                */
+  STADI_KCLASS_COUNT = 5
+};
+stadi_status stadi_kernel_timing(stadi_ctx *ctx, int32_t enable);
+stadi_status stadi_kernel_stats(stadi_ctx *ctx, int32_t kclass, uint64_t *launches, double *ms,
+                                double *flops, double *bytes);
+
 /* ncclGetUniqueId through the library's NCCL (dlopen'ed; ENCCL if absent). */
 stadi_status stadi_nccl_unique_id(uint8_t out[128]);
 

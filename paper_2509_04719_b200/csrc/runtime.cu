@@ -129,7 +129,9 @@ struct stadi_ctx {
   void *csilu = nullptr;
   int *labels_dev = nullptr;
   size_t cond_cap_nt = 0;
+  int tfreq_nt = 0;
   void *text_T = nullptr, *y1 = nullptr, *y = nullptr;
+  float *text_f = nullptr;
   std::vector<void *> kv_text;
   double abar[1000];
 
@@ -146,6 +148,17 @@ struct stadi_ctx {
   int *emu_flag_dev = nullptr;
   cudaStream_t emu_stream = nullptr;
   int emu_ctas = 0;
+
+  // per-class kernel timing (stadi_kernel_timing): CUDA events recorded on the
+  // launching stream around every launch of the class
+  struct KClass {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    size_t used = 0;
+    uint64_t launches = 0;
+    double ms = 0, flops = 0, bytes = 0;
+  };
+  bool ktime = false;
+  KClass kt[STADI_KCLASS_COUNT];
 };
 
 namespace {
@@ -230,28 +243,78 @@ void ddim_coeffs(const double *ab, int t, int t_prev, float *A, float *Bc) {
   *Bc = (float)(-si2 * std::expm1(h));
 }
 
+// ---------------------------------------------------------------- kernel timing
+// Wrap one launch of class `cls` in a pair of CUDA events on its stream when
+// timing is enabled; `flops` / `bytes` are the launch's ALGORITHMIC work
+// (DESIGN.md §6), accumulated beside the measured time.
+template <typename F>
+cudaError_t timed(stadi_ctx *ctx, int cls, double flops, double bytes, cudaStream_t s, F &&f) {
+  if (!ctx->ktime) return f();
+  auto &k = ctx->kt[cls];
+  if (k.used == k.ev.size()) {
+    cudaEvent_t a, b;
+    cudaError_t e = cudaEventCreate(&a);
+    if (e != cudaSuccess) return e;
+    e = cudaEventCreate(&b);
+    if (e != cudaSuccess) return e;
+    k.ev.push_back({a, b});
+  }
+  auto &pr = k.ev[k.used++];
+  cudaError_t e = cudaEventRecord(pr.first, s);
+  if (e != cudaSuccess) return e;
+  e = f();
+  if (e != cudaSuccess) return e;
+  k.launches += 1;
+  k.flops += flops;
+  k.bytes += bytes;
+  return cudaEventRecord(pr.second, s);
+}
+// Fold the recorded event pairs into the per-class totals (caller synchronised).
+cudaError_t collect_timing(stadi_ctx *ctx) {
+  for (auto &k : ctx->kt) {
+    for (size_t i = 0; i < k.used; ++i) {
+      float ms = 0.f;
+      cudaError_t e = cudaEventElapsedTime(&ms, k.ev[i].first, k.ev[i].second);
+      if (e != cudaSuccess) return e;
+      k.ms += ms;
+    }
+    k.used = 0;
+  }
+  return cudaSuccess;
+}
+
 // ---------------------------------------------------------------- kernel dispatch
 cudaError_t gemm(stadi_ctx *ctx, const void *A, const void *W, int M, int N, int K, int epi,
                  const EpiParams &ep, cudaStream_t s) {
-  if (ctx->dtype == STADI_DTYPE_BF16)
-    return tc_gemm_bf16((const bf16 *)A, (const bf16 *)W, M, N, K, epi, ep,
-                        std::max(1, ctx->num_sms - ctx->emu_ctas), s);
-  return simt_gemm<float>((const float *)A, (const float *)W, M, N, K, epi, ep, s);
+  return timed(ctx, STADI_KCLASS_GEMM, 2.0 * M * N * K, 0.0, s, [&] {
+    if (ctx->dtype == STADI_DTYPE_BF16)
+      return tc_gemm_bf16((const bf16 *)A, (const bf16 *)W, M, N, K, epi, ep,
+                          std::max(1, ctx->num_sms - ctx->emu_ctas), s);
+    return simt_gemm<float>((const float *)A, (const float *)W, M, N, K, epi, ep, s);
+  });
 }
-cudaError_t attention(stadi_ctx *ctx, const void *q, const void *kv, void *o, int Nq, int Nkv,
-                      cudaStream_t s) {
+cudaError_t attention(stadi_ctx *ctx, int cls, const void *q, const void *kv, void *o, int Nq,
+                      int Nkv, cudaStream_t s) {
   const Dims &m = ctx->dm;
-  if (ctx->dtype == STADI_DTYPE_BF16)
-    return tc_attention_bf16((const bf16 *)q, (const bf16 *)kv, (bf16 *)o, Nq, Nkv, m.B, m.H,
-                             m.hd, s);
-  return simt_attention<float>((const float *)q, (const float *)kv, (float *)o, Nq, Nkv, m.B,
-                               m.H, m.hd, s);
+  const double flops = 4.0 * Nq * Nkv * m.hd * m.B * m.H;  // QK^T + PV, 2 flops per MAC
+  return timed(ctx, cls, flops, 0.0, s, [&] {
+    if (ctx->dtype == STADI_DTYPE_BF16)
+      return tc_attention_bf16((const bf16 *)q, (const bf16 *)kv, (bf16 *)o, Nq, Nkv, m.B, m.H,
+                               m.hd, s);
+    return simt_attention<float>((const float *)q, (const float *)kv, (float *)o, Nq, Nkv, m.B,
+                                 m.H, m.hd, s);
+  });
 }
 cudaError_t lnmod(stadi_ctx *ctx, const float *x, void *y, int M, const float *shift,
                   const float *scale, int bs, int do_norm, cudaStream_t s) {
-  if (ctx->dtype == STADI_DTYPE_BF16)
-    return ln_modulate<bf16>(x, (bf16 *)y, M, ctx->dm.d, ctx->dm.B, shift, scale, bs, do_norm, s);
-  return ln_modulate<float>(x, (float *)y, M, ctx->dm.d, ctx->dm.B, shift, scale, bs, do_norm, s);
+  const double bytes = (double)M * ctx->dm.d * (4 + ctx->esz);  // fp32 in, T out
+  return timed(ctx, STADI_KCLASS_NORM, 0.0, bytes, s, [&] {
+    if (ctx->dtype == STADI_DTYPE_BF16)
+      return ln_modulate<bf16>(x, (bf16 *)y, M, ctx->dm.d, ctx->dm.B, shift, scale, bs, do_norm,
+                               s);
+    return ln_modulate<float>(x, (float *)y, M, ctx->dm.d, ctx->dm.B, shift, scale, bs, do_norm,
+                              s);
+  });
 }
 
 int widx(stadi_ctx *ctx, const std::string &name) {
@@ -411,6 +474,11 @@ extern "C" void stadi_destroy(stadi_ctx *ctx) {
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
   if (ctx->emu_stream) cudaStreamDestroy(ctx->emu_stream);
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
+  for (auto &k : ctx->kt)
+    for (auto &pr : k.ev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
   if (ctx->emu_flag_host) cudaFreeHost(ctx->emu_flag_host);
   cudaGetLastError();
   delete ctx;
@@ -623,10 +691,12 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
     CK(cudaMalloc(&ctx->tfreq, (size_t)nt * 256 * 4));
     CK(cudaMalloc(&ctx->csilu, (size_t)nt * B * d * ctx->esz));
     ctx->cond_cap_nt = nt;
+    ctx->tfreq_nt = 0;
   }
   ctx->n_t = nt;
-  {
-    // sinusoidal timestep features on the host in fp64 (DiT TimestepEmbedder)
+  if (ctx->tfreq_nt != nt) {
+    // sinusoidal timestep features of the fast grid, fp64 on the host (DiT
+    // TimestepEmbedder); depends only on M_base, uploaded once per plan size
     std::vector<float> tf((size_t)nt * 256);
     const int ratio = 1000 / nt;
     for (int i = 0; i < nt; ++i) {
@@ -637,8 +707,8 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
         tf[(size_t)i * 256 + 128 + k] = (float)std::sin(t * f);
       }
     }
-    CK(cudaMemcpyAsync(ctx->tfreq, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));  // tf is a host temporary
+    CK(cudaMemcpy(ctx->tfreq, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice));
+    ctx->tfreq_nt = nt;
   }
   EpiParams ep{};
   ep.B = 1;
@@ -695,20 +765,17 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
       ctx->kv_text.assign(m.depth, nullptr);
       for (auto &p : ctx->kv_text) CK(dalloc(ctx, &p, Mt * 2 * d * ctx->esz));
     }
-    // host reorder [B, L, D] -> [L, B, D] (token-major, batch innermost)
-    std::vector<float> tx((size_t)Mt * Dt);
+    // [B, L, D] -> [L, B, D] (token-major, batch innermost) by strided copies;
+    // text may be a host or a device pointer (cudaMemcpyDefault)
+    if (!ctx->text_f) CK(dalloc(ctx, &ctx->text_f, Mt * Dt * 4));
     for (int b = 0; b < B; ++b)
-      for (int j = 0; j < L; ++j)
-        std::memcpy(&tx[((size_t)j * B + b) * Dt], cond->text + ((size_t)b * L + j) * Dt, Dt * 4);
-    float *tx_dev = nullptr;
-    CK(cudaMalloc(&tx_dev, tx.size() * 4));
-    CK(cudaMemcpyAsync(tx_dev, tx.data(), tx.size() * 4, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpy2DAsync(ctx->text_f + (size_t)b * Dt, (size_t)B * Dt * 4,
+                           cond->text + (size_t)b * L * Dt, (size_t)Dt * 4, (size_t)Dt * 4, L,
+                           cudaMemcpyDefault, s));
     if (ctx->dtype == STADI_DTYPE_BF16)
-      CK(cast_f32<bf16>(tx_dev, (bf16 *)ctx->text_T, (long)tx.size(), s));
+      CK(cast_f32<bf16>(ctx->text_f, (bf16 *)ctx->text_T, (long)(Mt * Dt), s));
     else
-      CK(cudaMemcpyAsync(ctx->text_T, tx_dev, tx.size() * 4, cudaMemcpyDeviceToDevice, s));
-    CK(cudaStreamSynchronize(s));
-    cudaFree(tx_dev);
+      CK(cudaMemcpyAsync(ctx->text_T, ctx->text_f, Mt * Dt * 4, cudaMemcpyDeviceToDevice, s));
     ep.bias = WF(ctx, "caption.b1");
     ep.out = ctx->y1;
     ep.ldo = (int)d;
@@ -841,7 +908,8 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
       Rank &r = ctx->ranks[P.li];
       const int M = r.n_tok * B;
       const float *mb = ctx->mod + ((int64_t)P.st.m * B * m.depth + l) * 6 * d;
-      CK(attention(ctx, r.q, r.kv[l * 2 + (P.st.read_ver & 1)], r.o, r.n_tok, ntok_full, s));
+      CK(attention(ctx, STADI_KCLASS_ATTN, r.q, r.kv[l * 2 + (P.st.read_ver & 1)], r.o, r.n_tok,
+                    ntok_full, s));
       EpiParams ep{};
       ep.B = B;
       ep.bias = WF(ctx, pre + "proj.b");
@@ -858,7 +926,7 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
         eq.out = r.q;
         eq.ldo = (int)d;
         CK(gemm(ctx, r.xmod, WT(ctx, pre + "xq.w"), M, (int)d, (int)d, EPI_STORE, eq, s));
-        CK(attention(ctx, r.q, ctx->kv_text[l], r.o, r.n_tok, m.txt_len, s));
+        CK(attention(ctx, STADI_KCLASS_XATTN, r.q, ctx->kv_text[l], r.o, r.n_tok, m.txt_len, s));
         EpiParams er{};
         er.B = B;
         er.bias = WF(ctx, pre + "xproj.b");
@@ -896,8 +964,11 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
     CK(gemm(ctx, r.xmod, ctx->final_w, M, ctx->fin_ld, (int)d, EPI_F32, ef, s));
     float A, Bc;
     ddim_coeffs(ctx->abar, P.st.t, P.st.t_prev, &A, &Bc);
-    CK(sampler_update(r.x_band, r.eps_raw, r.rows, m.lat_w, m.c_in, m.p, m.c_out, ctx->fin_ld, B,
-                      m.guidance, A, Bc, s));
+    const double sb = (double)r.rows * m.lat_w * m.c_in * 8 + (double)M * ctx->fin_ld * 4;
+    CK(timed(ctx, STADI_KCLASS_SAMPLER, 0.0, sb, s, [&] {
+      return sampler_update(r.x_band, r.eps_raw, r.rows, m.lat_w, m.c_in, m.p, m.c_out,
+                            ctx->fin_ld, B, m.guidance, A, Bc, s);
+    }));
   }
   return STADI_OK;
 }
@@ -972,6 +1043,7 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
   CK(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  CK(collect_timing(ctx));
   if (stats) {
     stats->ms_total = ms;
     stats->ms_exchange_wait = 0;
@@ -1082,5 +1154,35 @@ extern "C" stadi_status stadi_emulator_stop(stadi_ctx *ctx) {
   *ctx->emu_flag_host = 1;
   CK(cudaStreamSynchronize(ctx->emu_stream));
   ctx->emu_ctas = 0;
+  return STADI_OK;
+}
+
+// ---------------------------------------------------------------- kernel timing (d)
+extern "C" stadi_status stadi_kernel_timing(stadi_ctx *ctx, int32_t enable) {
+  ALIVE();
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  for (auto &k : ctx->kt) {
+    k.used = 0;
+    k.launches = 0;
+    k.ms = k.flops = k.bytes = 0;
+  }
+  ctx->ktime = enable != 0;
+  return STADI_OK;
+}
+
+extern "C" stadi_status stadi_kernel_stats(stadi_ctx *ctx, int32_t kclass, uint64_t *launches,
+                                           double *ms, double *flops, double *bytes) {
+  ALIVE();
+  if (kclass < 0 || kclass >= STADI_KCLASS_COUNT)
+    return ctx_fail(ctx, STADI_EINVAL, "unknown kernel class %d", kclass);
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  CK(collect_timing(ctx));
+  const auto &k = ctx->kt[kclass];
+  if (launches) *launches = k.launches;
+  if (ms) *ms = k.ms;
+  if (flops) *flops = k.flops;
+  if (bytes) *bytes = k.bytes;
   return STADI_OK;
 }

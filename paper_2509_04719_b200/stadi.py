@@ -24,6 +24,7 @@ VER_NONE = -1
 PRESET = {"tiny_dit": 0, "dit_xl2": 1, "pixart_alpha": 2}
 DTYPE_BF16, DTYPE_FP32_DEBUG = 0, 1
 EPI_STORE, EPI_GELU, EPI_GATED_RES, EPI_RES, EPI_QKV, EPI_F32 = range(6)
+KCLASS = {"gemm": 0, "attn": 1, "xattn": 2, "norm": 3, "sampler": 4}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE",
           6: "EUNSUPPORTED"}
 
@@ -104,6 +105,7 @@ EXPORTS = [
     "stadi_load_weights", "stadi_profile_warmup", "stadi_set_plan", "stadi_begin",
     "stadi_num_steps", "stadi_denoise_step", "stadi_gather", "stadi_run",
     "stadi_emulator_start", "stadi_emulator_stop", "stadi_nccl_unique_id",
+    "stadi_kernel_timing", "stadi_kernel_stats",
     "stadi_k_gemm", "stadi_k_attention", "stadi_k_ln_modulate", "stadi_k_launch_count",
 ]
 
@@ -138,6 +140,10 @@ def _load():
         "stadi_emulator_start": (C.c_int, [vp, C.c_uint32]),
         "stadi_emulator_stop": (C.c_int, [vp]),
         "stadi_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+        "stadi_kernel_timing": (C.c_int, [vp, C.c_int32]),
+        "stadi_kernel_stats": (C.c_int, [vp, C.c_int32, C.POINTER(C.c_uint64),
+                                         C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]),
         "stadi_k_gemm": (C.c_int, [C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                    C.POINTER(KEpi), vp]),
         "stadi_k_attention": (C.c_int, [C.c_int32, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32,
@@ -319,6 +325,17 @@ class Context:
 
     def emulator_stop(self):
         self._c(lib.stadi_emulator_stop(self.h))
+
+    def kernel_timing(self, enable=True):
+        self._c(lib.stadi_kernel_timing(self.h, 1 if enable else 0))
+
+    def kernel_stats(self, kclass):
+        """(launches, ms, algorithmic flops, algorithmic bytes) of a kernel class."""
+        n, ms, fl, by = C.c_uint64(), C.c_double(), C.c_double(), C.c_double()
+        k = KCLASS[kclass] if isinstance(kclass, str) else kclass
+        self._c(lib.stadi_kernel_stats(self.h, k, C.byref(n), C.byref(ms), C.byref(fl),
+                                       C.byref(by)))
+        return n.value, ms.value, fl.value, by.value
 
 
 # ---------------------------------------------------------------- kernel-level
