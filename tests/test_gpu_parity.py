@@ -13,6 +13,7 @@ import pytest
 from oracle import planner as OP
 from oracle import stadi as OR
 from synth import configs, gen
+import refcache
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -38,10 +39,13 @@ def _inputs(name, **kw):
 
 
 def _oracle(cfg, W, x, c, plan, dtype):
-    key = ("oracle", cfg["name"], cfg["depth"], cfg["latent_h"], dtype, repr(plan))
-    if key not in _cache:
-        _cache[key] = OR.run(cfg, gen.weights_bf16(W) if dtype == 0 else W, x, c, plan)
-    return _cache[key]
+    """fp64 oracle STADI run (bf16-rounded weights in bf16 mode, R22), from the
+    committed oracle-only cache when present (tests/refcache.py)."""
+    key = dict(kind="stadi_run", cfg=cfg, dtype=dtype, plan=plan)
+
+    def compute():
+        return OR.run(cfg, gen.weights_bf16(W) if dtype == 0 else W, x, c, plan)
+    return refcache.cached(key, compute)
 
 
 def _gpu_run(S, name, cfg, W, x, c, speed, mb, mw, dtype, flags=0, device_ptrs=False,
@@ -67,6 +71,32 @@ def _gpu_run(S, name, cfg, W, x, c, speed, mb, mw, dtype, flags=0, device_ptrs=F
         ctx.close()
 
 
+PROTO_CASES = [
+    ([1], 0),                                   # single GPU == sequential DDIM
+    ([3, 2, 1], OP.NO_TA | OP.NO_SA),           # uniform patch parallelism (DistriFusion)
+    ([100, 60, 100, 10], 0),                    # tier 1 / tier 2 / excluded GPU
+    ([5, 4, 3], OP.SIZER_INTERVAL),
+]
+C2_SPEED = [65536, 39322]                       # 40% occupancy -> v = 0.6
+C5_SPEED = [1 << 16, 1 << 15]                   # 50% occupancy -> v = 0.5
+C2_KW = dict(depth=2)
+C5_KW = dict(depth=2, latent_h=32, latent_w=40)
+
+
+def oracle_cases():
+    """Every (cfg, W, x, c, plan, dtype) the parity tests hand to _oracle
+    (used by tests/golden/make_oracle_refs.py)."""
+    for dtype in (1, 0):
+        cfg, W, x, c = _inputs("tiny_dit")
+        yield cfg, W, x, c, OR.plan_for(cfg, [1 << 20, 1 << 19], 10, 2), dtype
+        for speed, flags in PROTO_CASES:
+            yield cfg, W, x, c, OR.plan_for(cfg, speed, 10, 2, flags=flags), dtype
+        cfg, W, x, c = _inputs("dit_xl2", **C2_KW)
+        yield cfg, W, x, c, OR.plan_for(cfg, C2_SPEED, 50, 4), dtype
+        cfg, W, x, c = _inputs("pixart_alpha", **C5_KW)
+        yield cfg, W, x, c, OR.plan_for(cfg, C5_SPEED, 20, 4), dtype
+
+
 def _rel(a, b):
     return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
 
@@ -87,12 +117,7 @@ def test_c1_tiny_two_ranks(S, dtype):
 
 
 @pytest.mark.parametrize("dtype", [1, 0], ids=["fp32", "bf16"])
-@pytest.mark.parametrize("speed,flags", [
-    ([1], 0),                                   # single GPU == sequential DDIM
-    ([3, 2, 1], OP.NO_TA | OP.NO_SA),           # uniform patch parallelism (DistriFusion)
-    ([100, 60, 100, 10], 0),                    # tier 1 / tier 2 / excluded GPU
-    ([5, 4, 3], OP.SIZER_INTERVAL),
-])
+@pytest.mark.parametrize("speed,flags", PROTO_CASES)
 def test_tiny_protocol_variants(S, dtype, speed, flags):
     cfg, W, x, c = _inputs("tiny_dit")
     plan = OR.plan_for(cfg, speed, 10, 2, flags=flags)
@@ -106,8 +131,8 @@ def test_tiny_protocol_variants(S, dtype, speed, flags):
 def test_c2_dit_xl2_depth_reduced(S, dtype):
     """C2 shapes (d 1152, 16 heads, 32x32 latent, CFG 4.0, 50 steps, 2 GPUs,
     one at 40% occupancy -> v = 0.6), depth reduced to 2 blocks for the oracle."""
-    cfg, W, x, c = _inputs("dit_xl2", depth=2)
-    speed = [65536, 39322]
+    cfg, W, x, c = _inputs("dit_xl2", **C2_KW)
+    speed = C2_SPEED
     plan = OR.plan_for(cfg, speed, 50, 4)
     ref = _oracle(cfg, W, x, c, plan, dtype)
     got, p, _ = _gpu_run(S, "dit_xl2", cfg, W, x, c, speed, 50, 4, dtype)
@@ -122,8 +147,8 @@ def test_c5_pixart_reduced(S, dtype):
     """C5 shapes (PixArt-alpha: d 1152, 16 heads, cross-attention to 120x4096
     text, adaLN-single, CFG 4.5, 20 steps), depth 2 and a 32x40 latent for the
     oracle; 2 GPUs, the second at 50% occupancy."""
-    cfg, W, x, c = _inputs("pixart_alpha", depth=2, latent_h=32, latent_w=40)
-    speed = [1 << 16, 1 << 15]
+    cfg, W, x, c = _inputs("pixart_alpha", **C5_KW)
+    speed = C5_SPEED
     plan = OR.plan_for(cfg, speed, 20, 4)
     ref = _oracle(cfg, W, x, c, plan, dtype)
     got, p, _ = _gpu_run(S, "pixart_alpha", cfg, W, x, c, speed, 20, 4, dtype)
