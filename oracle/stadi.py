@@ -26,7 +26,7 @@ Protocol (SURVEY §8(c) O5/O6 and readings R9-R17):
 """
 from __future__ import annotations
 
-from . import diffusion, dit, planner, schedule
+from . import diffusion, dit, planner, schedule, unet
 
 
 def _group_phases(plan):
@@ -43,6 +43,8 @@ def run(cfg, weights, x_T, cond, plan, return_trace=False):
 
     Returns the final latent [H, W, C] (float64) assembled from the bands.
     """
+    if cfg["family"] == "unet":
+        return run_unet(cfg, weights, x_T, cond, plan, return_trace)
     model = dit.DiT(cfg, weights)
     abar = diffusion.alpha_bar("linear" if cfg["schedule"] == "linear" else "scaled_linear")
     B = dit.batch_of(cfg)
@@ -89,6 +91,74 @@ def run(cfg, weights, x_T, cond, plan, return_trace=False):
     return (out, trace) if return_trace else out
 
 
+def _assemble(kind, r, inc, own, stale):
+    """Answer one exchange request of rank r: own payload
+    fresh, every other included rank's payload of the read version (`stale`:
+    rank -> payload).  Ranks are in row order top to bottom (R8)."""
+    import numpy as np
+    if kind == "kv":
+        ks = [own[0] if j == r else stale[j][0] for j in inc]
+        vs = [own[1] if j == r else stale[j][1] for j in inc]
+        return np.concatenate(ks, axis=1), np.concatenate(vs, axis=1)
+    if kind == "halo":
+        i = inc.index(r)
+        above = stale[inc[i - 1]][1] if i > 0 else np.zeros_like(own[0])       # its last row
+        below = stale[inc[i + 1]][0] if i + 1 < len(inc) else np.zeros_like(own[1])
+        return above, below
+    if kind == "gn":
+        tot = [a.copy() for a in own]
+        for j in inc:
+            if j != r:
+                for t, a in zip(tot, stale[j]):
+                    t += a
+        return tuple(tot)
+    raise ValueError(kind)
+
+
+def run_unet(cfg, weights, x_T, cond, plan, return_trace=False):
+    """Algorithm 1 for the U-Net family: every rank's band forward is a
+    generator (oracle/unet.py) that yields at each exchange site; ranks of a
+    phase advance in lock-step site by site: all publish (pub_ver), then all
+    read (read_ver; fresh when read_ver == pub_ver, R9)."""
+    import numpy as np
+    model = unet.UNet(cfg, weights)
+    abar = diffusion.alpha_bar(cfg["schedule"])
+    inc = [r for r in range(plan["n_gpus"]) if plan["tier"][r] > 0]
+    band = {r: x_T[plan["row_begin"][r]:plan["row_begin"][r] + plan["rows"][r]].astype("float64")
+            for r in inc}
+    store = {}                                   # (version, site, rank) -> payload
+    trace = []
+    for phase in _group_phases(plan):
+        gens = {r: model.band_forward(band[r], st.t, cond) for r, st in phase}
+        steps = {r: st for r, st in phase}
+        reqs = {r: next(g) for r, g in gens.items()}
+        eps = {}
+        site = 0
+        while reqs:
+            kinds = {k for k, _ in reqs.values()}
+            assert len(kinds) == 1, "ranks out of lock-step"
+            for r, (kind, pay) in reqs.items():          # everyone publishes first
+                if steps[r].pub_ver != schedule.NONE:
+                    store[(steps[r].pub_ver, site, r)] = pay
+            nxt = {}
+            for r, (kind, pay) in reqs.items():          # then reads read_ver
+                rv = steps[r].read_ver
+                stale = {j: store[(rv, site, j)] for j in inc if j != r}
+                try:
+                    nxt[r] = gens[r].send(_assemble(kind, r, inc, pay, stale))
+                except StopIteration as e:
+                    eps[r] = e.value
+            reqs = nxt
+            site += 1
+        for r, st in phase:                      # eps on own band + Eq. 3 on own rows
+            band[r] = diffusion.ddim_step(abar, band[r], unet.guided_eps(cfg, eps[r]),
+                                          st.t, st.t_prev)
+            if return_trace:
+                trace.append((st.m, r, st.kind, band[r].copy()))
+    out = np.concatenate([band[r] for r in inc], axis=0)   # final synchronous all-gather
+    return (out, trace) if return_trace else out
+
+
 def _cat(xs):
     import numpy as np
     return np.concatenate(xs, axis=1)
@@ -97,6 +167,16 @@ def _cat(xs):
 def sequential(cfg, weights, x_T, cond, m_base):
     """Non-distributed DDIM with M_base steps on the fast grid (the "Origin"
     method of Table II)."""
+    if cfg["family"] == "unet":
+        model = unet.UNet(cfg, weights)
+        abar = diffusion.alpha_bar(cfg["schedule"])
+        x = x_T.astype("float64")
+        grid = schedule.fast_grid(m_base)
+        for m, t in enumerate(grid):
+            t_prev = grid[m + 1] if m + 1 < m_base else schedule.FINAL
+            eps = unet.guided_eps(cfg, model.forward_full(x, t, cond))
+            x = diffusion.ddim_step(abar, x, eps, t, t_prev)
+        return x
     model = dit.DiT(cfg, weights)
     abar = diffusion.alpha_bar("linear" if cfg["schedule"] == "linear" else "scaled_linear")
     y = model.caption(cond)
@@ -110,7 +190,9 @@ def sequential(cfg, weights, x_T, cond, m_base):
 
 
 def plan_for(cfg, speed, m_base, m_warmup, flags=0, forced_units=None):
-    """Planner call with the DiT unit (R6: one unit = one token row = p latent rows)."""
-    p = cfg["patch"]
-    return planner.plan(speed, m_base, m_warmup, cfg["latent_h"] // p, p,
+    """Planner call with the model's unit (R6: one unit = one row of the coarsest
+    feature map: p latent rows for a DiT, 2^(levels-1) for a U-Net)."""
+    from synth.configs import rows_per_unit
+    u = rows_per_unit(cfg)
+    return planner.plan(speed, m_base, m_warmup, cfg["latent_h"] // u, u,
                         flags=flags, forced_units=forced_units)

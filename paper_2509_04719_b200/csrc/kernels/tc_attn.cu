@@ -1,21 +1,29 @@
 // tcgen05 flash attention for sm_100a: a rank's own queries against the
 // full-image K/V assembled in an exchange slot (own rows fresh, other ranks'
 // rows stale) — SURVEY §2.6 K3, PAPER.md L80/L171 (DistriFusion-style patch
-// parallelism with stale activations).
+// parallelism with stale activations); also the cross-attention to the text
+// tokens.
 //
-// One CTA = one (128-query tile, head h, batch b).  Warp roles:
-//   warp 0      TMA: Q once; K and V tiles of 128 keys into a 3-stage ring
-//               (head dim split into a 128B-swizzled 64-wide part and a
-//               32B-swizzled 16-wide remainder; TMA zero-fills hd..hd_pad)
-//   warp 1      MMA issuer: S_j = Q K_j^T (M=128, N=128, K=hd_pad) into one of
-//               two TMEM S buffers; O_j = P_j V_j (M=128, N=hd_pad) into one of
-//               two TMEM O buffers (V is the MN-major B operand)
-//   warps 2-5   softmax: one query row per thread — running max / sum in
-//               fp32 (exp2), P_j as bf16 into 128B-swizzled smem, then the
-//               lagged correction O_acc = O_acc * 2^(m_ref - m_j) + O_j in
-//               registers, normalise and store.
-// S_{j+1} is computed while the softmax warps work on S_j; PV_j overlaps
-// softmax_{j+1}.
+// One CTA = NQT (1 or 2) query tiles of 128 rows of one (head h, batch b).
+// Warp roles (FA4-style ping-pong):
+//   warp 0        TMA: the Q tiles once; K and V tiles of 128 keys into a
+//                 multi-stage ring.  The head dim is split into chunks of
+//                 64 (128B swizzle), 32 (64B) and 16 (32B) columns; TMA
+//                 zero-fills hd..hd_pad and rows past Nq / Nkv.
+//   warp 1        MMA issuer (one thread): S_g = Q_g K_j^T (SS form, M128 x
+//                 N128) into TMEM, then O_g += P_g V_j with P_g read from TMEM
+//                 (TS form; P overwrites the first 64 columns of S_g as packed
+//                 bf16).  Order per key tile j: PV_0(j), S_0(j+1), PV_1(j),
+//                 S_1(j+1) — while softmax group 0 works on S_0(j+1) the
+//                 tensor core runs PV_1(j) and S_1(j+1), and vice versa.
+//   warps 4..    softmax group g (4 warps, one query row per thread = TMEM
+//                 lane): S row -> registers (all loads in flight, one wait),
+//                 row max, LAZY rescale (O and l are rescaled in TMEM only
+//                 when the running max grows by more than 2^8; otherwise the
+//                 stale max is kept — exact, the same max scales P, l and O),
+//                 P = 2^(s*scale - m) packed to bf16 into TMEM, row sum in fp32.
+//                 Epilogue: O / l -> bf16 global.
+// O accumulates in TMEM across all key tiles: no per-tile correction pass.
 #include <cuda.h>
 
 #include "../kernels.h"
@@ -27,9 +35,9 @@ bool make_tmap(CUtensorMap *m, const void *base, int rank, const uint64_t *dims,
 
 namespace {
 
-constexpr int AQ = 128;   // query rows per CTA
+constexpr int AQ = 128;   // query rows per tile
 constexpr int AK = 128;   // keys per tile
-constexpr int KST = 3;    // K/V pipeline stages
+constexpr float RESCALE_THRESHOLD = 8.f;  // log2 units: keep a stale max up to 2^8
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -37,62 +45,96 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-template <int MAIN, int REM>  // MAIN in {0,64}, REM in {0,16}: hd_pad = MAIN + REM
+// Head-dim chunking: N64 chunks of 64, then optionally one of 32, one of 16.
+template <int N64, int N32, int N16, int NQT_>
 struct AttnCfg {
-  static constexpr int HDP = MAIN + REM;
-  static constexpr int MAIN_BYTES = MAIN * 2 * 128;   // 128 rows x MAIN bf16
-  static constexpr int REM_BYTES = REM * 2 * 128;
-  static constexpr int TILE = MAIN_BYTES + REM_BYTES;  // one Q/K/V tile
-  static constexpr int P_BYTES = AQ * AK * 2;          // 32 KB
-  // layout: Q | K[KST] | V[KST] | P[2] | barriers
-  static constexpr int OFF_K = TILE;
-  static constexpr int OFF_V = OFF_K + KST * TILE;
-  static constexpr int OFF_P = OFF_V + KST * TILE;
-  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+  static constexpr int NQT = NQT_;
+  static constexpr int HDP = 64 * N64 + 32 * N32 + 16 * N16;
+  static constexpr int NCH = N64 + N32 + N16;
+  static constexpr int TILE = AQ * HDP * 2;  // one Q / K / V tile (128 rows), bytes
+  __host__ __device__ static constexpr int cw(int c) {  // chunk width
+    return c < N64 ? 64 : (c < N64 + N32 ? 32 : 16);
+  }
+  __host__ __device__ static constexpr int ccol(int c) {  // first head-dim column
+    return c < N64 ? 64 * c : (c < N64 + N32 ? 64 * N64 : 64 * N64 + 32 * N32);
+  }
+  __host__ __device__ static constexpr int coff(int c) { return AQ * ccol(c) * 2; }  // bytes
+  __host__ __device__ static constexpr uint32_t cswz(int c) {
+    return cw(c) == 64 ? SWZ_128B : (cw(c) == 32 ? SWZ_64B : SWZ_32B);
+  }
+  static constexpr int STAGES =
+      (200 * 1024 - NQT * TILE) / (2 * TILE) > 4 ? 4 : (200 * 1024 - NQT * TILE) / (2 * TILE);
+  static constexpr int OFF_K = NQT * TILE;
+  static constexpr int OFF_V = OFF_K + STAGES * TILE;
+  static constexpr int OFF_BAR = OFF_V + STAGES * TILE;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  // TMEM columns: S buffers at 0 / 128, O buffers at 256 / 384
-  __host__ __device__ static constexpr uint32_t s_col(int i) { return i ? 128u : 0u; }
-  __host__ __device__ static constexpr uint32_t o_col(int i) { return i ? 384u : 256u; }
+  static constexpr int THREADS = 128 + 128 * NQT;
+  // TMEM columns: S_g at 128 g, O_g at 256 + 128 g (HDP <= 128 when NQT == 2)
+  __host__ __device__ static constexpr uint32_t s_col(int g) { return 128u * g; }
+  __host__ __device__ static constexpr uint32_t o_col(int g) {
+    return NQT == 2 ? 256u + 128u * g : 128u;
+  }
+  static_assert(NQT == 1 || HDP <= 128, "two query tiles need HDP <= 128");
+  static_assert(NQT == 2 || HDP <= 384, "HDP too large");
+  static_assert(STAGES >= 2, "smem");
 };
 
-template <int MAIN, int REM>
-__global__ void __launch_bounds__(192, 1)
-    tc_attn_kernel(const __grid_constant__ CUtensorMap tq_main,
-                   const __grid_constant__ CUtensorMap tq_rem,
-                   const __grid_constant__ CUtensorMap tkv_main,
-                   const __grid_constant__ CUtensorMap tkv_rem, bf16 *__restrict__ out, int Nq,
-                   int Nkv, int B, int H, int hd, float scale_log2) {
-  using C = AttnCfg<MAIN, REM>;
+// Load columns [c0, c0 + 16 * n) of this lane's TMEM row into v (fp32).
+template <int N>
+__device__ __forceinline__ void tmem_row_load(uint32_t taddr, float *v) {
+  static_assert(N % 16 == 0, "");
+  uint32_t *r = reinterpret_cast<uint32_t *>(v);
+#pragma unroll
+  for (int c = 0; c + 32 <= N; c += 32) tmem_ld32_nowait(taddr + c, r + c);
+  if constexpr (N % 32) tmem_ld16_nowait(taddr + (N - 16), r + (N - 16));
+  tmem_ld_wait();
+}
+template <int N>
+__device__ __forceinline__ void tmem_row_store(uint32_t taddr, const float *v) {
+  const uint32_t *r = reinterpret_cast<const uint32_t *>(v);
+#pragma unroll
+  for (int c = 0; c + 32 <= N; c += 32) tmem_st32(taddr + c, r + c);
+  if constexpr (N % 32) tmem_st16(taddr + (N - 16), r + (N - 16));
+}
+
+template <int N64, int N32, int N16, int NQT>
+__global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
+    tc_attn_kernel(const __grid_constant__ CUtensorMap tq64, const __grid_constant__ CUtensorMap tq32,
+                   const __grid_constant__ CUtensorMap tq16, const __grid_constant__ CUtensorMap tk64,
+                   const __grid_constant__ CUtensorMap tk32, const __grid_constant__ CUtensorMap tk16,
+                   bf16 *__restrict__ out, int Nq, int Nkv, int B, int H, int hd, float scale_log2) {
+  using C = AttnCfg<N64, N32, N16, NQT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
   uint8_t *sQ = smem;
   uint8_t *sK = smem + C::OFF_K;
   uint8_t *sV = smem + C::OFF_V;
-  uint8_t *sP = smem + C::OFF_P;
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
   uint64_t *q_full = bar;
-  uint64_t *k_full = bar + 1, *k_empty = k_full + KST;
-  uint64_t *v_full = k_empty + KST, *v_empty = v_full + KST;
-  uint64_t *s_full = v_empty + KST, *p_full = s_full + 2, *o_full = p_full + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_full + 2);
+  uint64_t *k_full = bar + 1, *k_empty = k_full + C::STAGES;
+  uint64_t *v_full = k_empty + C::STAGES, *v_empty = v_full + C::STAGES;
+  uint64_t *s_full = v_empty + C::STAGES;  // [NQT]
+  uint64_t *p_full = s_full + 2;           // [NQT]
+  uint64_t *o_done = p_full + 2;           // [NQT]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_done + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int q0 = blockIdx.x * AQ, h = blockIdx.y, b = blockIdx.z;
+  const int q0 = blockIdx.x * (AQ * NQT), h = blockIdx.y, b = blockIdx.z;
   const int n_kv = (Nkv + AK - 1) / AK;
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < KST; ++s) {
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&o_full[i], 1);
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&s_full[g], 1);
+      mbar_init(&p_full[g], 128);
+      mbar_init(&o_done[g], 1);
     }
     fence_mbar_init();
   }
@@ -102,29 +144,35 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // TMA of one 128-row tile of every head-dim chunk (c0: first row coordinate)
+  auto load_tile = [&](const CUtensorMap *m64, const CUtensorMap *m32, const CUtensorMap *m16,
+                       uint8_t *dst, uint64_t *br, int zb, int row) {
+#pragma unroll
+    for (int c = 0; c < C::NCH; ++c) {
+      const CUtensorMap *m = C::cw(c) == 64 ? m64 : (C::cw(c) == 32 ? m32 : m16);
+      tma_load_4d(m, dst + C::coff(c), br, C::ccol(c), h, zb, row);
+    }
+  };
+
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------ TMA producer
-      if (MAIN) tma_prefetch(&tq_main), tma_prefetch(&tkv_main);
-      if (REM) tma_prefetch(&tq_rem), tma_prefetch(&tkv_rem);
-      mbar_expect_tx(q_full, C::TILE);
-      if (MAIN) tma_load_4d(&tq_main, sQ, q_full, 0, h, b, q0);
-      if (REM) tma_load_4d(&tq_rem, sQ + C::MAIN_BYTES, q_full, MAIN, h, b, q0);
+      if (N64) tma_prefetch(&tq64), tma_prefetch(&tk64);
+      if (N32) tma_prefetch(&tq32), tma_prefetch(&tk32);
+      if (N16) tma_prefetch(&tq16), tma_prefetch(&tk16);
+      mbar_expect_tx(q_full, NQT * C::TILE);
+#pragma unroll
+      for (int g = 0; g < NQT; ++g)
+        load_tile(&tq64, &tq32, &tq16, sQ + g * C::TILE, q_full, b, q0 + g * AQ);
       int s = 0;
       uint32_t ph = 0;
       for (int j = 0; j < n_kv; ++j) {
         mbar_wait(&k_empty[s], ph ^ 1);
         mbar_expect_tx(&k_full[s], C::TILE);
-        if (MAIN) tma_load_4d(&tkv_main, sK + s * C::TILE, &k_full[s], 0, h, 2 * b, j * AK);
-        if (REM)
-          tma_load_4d(&tkv_rem, sK + s * C::TILE + C::MAIN_BYTES, &k_full[s], MAIN, h, 2 * b,
-                      j * AK);
+        load_tile(&tk64, &tk32, &tk16, sK + s * C::TILE, &k_full[s], 2 * b, j * AK);
         mbar_wait(&v_empty[s], ph ^ 1);
         mbar_expect_tx(&v_full[s], C::TILE);
-        if (MAIN) tma_load_4d(&tkv_main, sV + s * C::TILE, &v_full[s], 0, h, 2 * b + 1, j * AK);
-        if (REM)
-          tma_load_4d(&tkv_rem, sV + s * C::TILE + C::MAIN_BYTES, &v_full[s], MAIN, h, 2 * b + 1,
-                      j * AK);
-        if (++s == KST) {
+        load_tile(&tk64, &tk32, &tk16, sV + s * C::TILE, &v_full[s], 2 * b + 1, j * AK);
+        if (++s == C::STAGES) {
           s = 0;
           ph ^= 1;
         }
@@ -133,22 +181,32 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------ MMA issuer
       constexpr uint32_t id_s = umma_idesc_bf16(128, AK, 0, 0);
-      constexpr uint32_t id_pv_main = umma_idesc_bf16(128, MAIN > 0 ? MAIN : 64, 0, 1);
-      constexpr uint32_t id_pv_rem = umma_idesc_bf16(128, REM > 0 ? REM : 16, 0, 1);
-      const uint32_t q_addr = smem_u32(sQ);
-      auto issue_s = [&](int j, int st) {
-        const uint32_t dt = tmem + C::s_col(j & 1);
-        const uint32_t k_addr = smem_u32(sK + st * C::TILE);
+      auto issue_s = [&](int g, int st) {
+        const uint32_t dt = tmem + C::s_col(g);
+        const uint32_t qa = smem_u32(sQ + g * C::TILE), ka = smem_u32(sK + st * C::TILE);
         int kk = 0;
-        if (MAIN) {
 #pragma unroll
-          for (int k = 0; k < MAIN / 16; ++k, ++kk)
-            umma_bf16(dt, umma_desc(q_addr + k * 32, 16, 1024, SWZ_128B),
-                      umma_desc(k_addr + k * 32, 16, 1024, SWZ_128B), id_s, kk != 0);
+        for (int c = 0; c < C::NCH; ++c) {
+          const uint32_t rb = C::cw(c) * 2, sbo = 8 * rb;
+#pragma unroll
+          for (int k = 0; k < C::cw(c) / 16; ++k, ++kk)
+            umma_bf16(dt, umma_desc(qa + C::coff(c) + k * 32, 16, sbo, C::cswz(c)),
+                      umma_desc(ka + C::coff(c) + k * 32, 16, sbo, C::cswz(c)), id_s, kk != 0);
         }
-        if (REM) {
-          umma_bf16(dt, umma_desc(q_addr + C::MAIN_BYTES, 16, 256, SWZ_32B),
-                    umma_desc(k_addr + C::MAIN_BYTES, 16, 256, SWZ_32B), id_s, kk != 0);
+      };
+      auto issue_pv = [&](int g, int st, int j) {
+        const uint32_t pa = tmem + C::s_col(g);   // P: 64 columns of packed bf16
+        const uint32_t va = smem_u32(sV + st * C::TILE);
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c) {
+          const uint32_t rb = C::cw(c) * 2;
+          const uint32_t idp = umma_idesc_bf16(128, C::cw(c), 0, 1);
+          const uint32_t dt = tmem + C::o_col(g) + C::ccol(c);
+#pragma unroll
+          for (int k = 0; k < AK / 16; ++k)
+            umma_bf16_ts(dt, pa + k * 8,
+                         umma_desc(va + C::coff(c) + k * 16 * rb, AQ * rb, 8 * rb, C::cswz(c)),
+                         idp, (j | k) != 0);
         }
       };
       mbar_wait(q_full, 0);
@@ -156,149 +214,139 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t kph = 0, vph = 0;
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
-      issue_s(0, 0);
-      umma_commit(&s_full[0]);
+#pragma unroll
+      for (int g = 0; g < NQT; ++g) {
+        issue_s(g, 0);
+        umma_commit(&s_full[g]);
+      }
       umma_commit(&k_empty[0]);
-      ks = 1 % KST;
+      ks = 1 % C::STAGES;
       kph = (ks == 0);
       for (int j = 0; j < n_kv; ++j) {
-        if (j + 1 < n_kv) {
-          mbar_wait(&k_full[ks], kph);
+        mbar_wait(&v_full[vs], vph);
+        const bool more = j + 1 < n_kv;
+#pragma unroll
+        for (int g = 0; g < NQT; ++g) {
+          mbar_wait(&p_full[g], j & 1);
           tc_fence_after();
-          issue_s(j + 1, ks);
-          umma_commit(&s_full[(j + 1) & 1]);
+          issue_pv(g, vs, j);
+          umma_commit(&o_done[g]);
+          if (more) {
+            if (g == 0) {
+              mbar_wait(&k_full[ks], kph);
+              tc_fence_after();
+            }
+            issue_s(g, ks);
+            umma_commit(&s_full[g]);
+          }
+        }
+        umma_commit(&v_empty[vs]);
+        if (++vs == C::STAGES) {
+          vs = 0;
+          vph ^= 1;
+        }
+        if (more) {
           umma_commit(&k_empty[ks]);
-          if (++ks == KST) {
+          if (++ks == C::STAGES) {
             ks = 0;
             kph ^= 1;
           }
         }
-        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
-        mbar_wait(&v_full[vs], vph);
-        tc_fence_after();
-        const uint32_t p_addr = smem_u32(sP + (j & 1) * C::P_BYTES);
-        const uint32_t v_addr = smem_u32(sV + vs * C::TILE);
-        const uint32_t dt = tmem + C::o_col(j & 1);
-#pragma unroll
-        for (int k = 0; k < AK / 16; ++k) {
-          const uint64_t ad =
-              umma_desc(p_addr + (k >> 2) * (AQ * 128) + (k & 3) * 32, 16, 1024, SWZ_128B);
-          if (MAIN)
-            umma_bf16(dt, ad, umma_desc(v_addr + k * 16 * 128, 128 * 128, 1024, SWZ_128B),
-                      id_pv_main, k != 0);
-          if (REM)
-            umma_bf16(dt + MAIN, ad,
-                      umma_desc(v_addr + C::MAIN_BYTES + k * 16 * 32, 128 * 32, 256, SWZ_32B),
-                      id_pv_rem, k != 0);
-        }
-        umma_commit(&o_full[j & 1]);
-        umma_commit(&v_empty[vs]);
-        if (++vs == KST) {
-          vs = 0;
-          vph ^= 1;
-        }
       }
     }
-  } else {  // ------------------------------------------------ softmax warps 2..5
+  } else if (warp >= 4) {  // ------------------------------------ softmax groups
+    const int g = (warp - 4) / 4;
     const int qd = warp & 3;
     const int r = qd * 32 + lane;  // query row within the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    float m = -INFINITY, l = 0.f;
-    float m_hist[2] = {0.f, 0.f};
-    float m_ref = 0.f;
-    float oacc[C::HDP];
-#pragma unroll
-    for (int c = 0; c < C::HDP; ++c) oacc[c] = 0.f;
-    bool have_ref = false;
-
-    auto correction = [&](int i) {
-      mbar_wait(&o_full[i & 1], (i >> 1) & 1);
-      tc_fence_after();
-      const uint32_t ot = tmem + lane_off + C::o_col(i & 1);
-      const float mi = m_hist[i & 1];
-      const float sc = have_ref ? ex2(m_ref - mi) : 0.f;
-      float v[32];
-#pragma unroll
-      for (int c0 = 0; c0 + 32 <= C::HDP; c0 += 32) {
-        tmem_ld32(ot + c0, v);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) oacc[c0 + c] = oacc[c0 + c] * sc + v[c];
-      }
-      if constexpr (C::HDP % 32) {
-        constexpr int c0 = C::HDP - 16;
-        tmem_ld16(ot + c0, v);
-#pragma unroll
-        for (int c = 0; c < 16; ++c) oacc[c0 + c] = oacc[c0 + c] * sc + v[c];
-      }
-      m_ref = mi;
-      have_ref = true;
-      tc_fence_before();
-    };
-
+    const uint32_t st_addr = tmem + lane_off + C::s_col(g);
+    const uint32_t o_addr = tmem + lane_off + C::o_col(g);
+    float m_run = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&s_full[g], j & 1);
       tc_fence_after();
-      const uint32_t st = tmem + lane_off + C::s_col(j & 1);
+      float v[AK];
+      tmem_row_load<AK>(st_addr, v);
       const int valid = Nkv - j * AK;  // columns >= valid are padding
-      float v[32];
       float mt = -INFINITY;
+      if (valid >= AK) {
 #pragma unroll
-      for (int c0 = 0; c0 < AK; c0 += 32) {  // pass 1: row max
-        tmem_ld32(st + c0, v);
+        for (int c = 0; c < AK; ++c) mt = fmaxf(mt, v[c]);
+      } else {
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (c0 + c < valid) mt = fmaxf(mt, v[c]);
+        for (int c = 0; c < AK; ++c)
+          if (c < valid) mt = fmaxf(mt, v[c]);
       }
-      const float m_new = fmaxf(m, mt * scale_log2);
-      const float alpha = ex2(m - m_new);  // m = -inf on the first tile -> 0
-      float rs = 0.f;
-      uint8_t *prow = sP + (j & 1) * C::P_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
+      mt *= scale_log2;
+      // lazy rescale: move the reference max only when it grows by > 2^8
+      float factor = 1.f;
+      const bool grow = mt > m_run + RESCALE_THRESHOLD;
+      if (grow) {
+        factor = ex2(m_run - mt);  // 0 on the first tile (m_run = -inf)
+        m_run = mt;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {
+        // O_g holds PV(j-1) once o_done completes its j-th phase; rescale in
+        // 16-column pieces to keep the register footprint small
+        mbar_wait(&o_done[g], (j - 1) & 1);
+        tc_fence_after();
 #pragma unroll
-      for (int c0 = 0; c0 < AK; c0 += 32) {  // pass 2: p = 2^(s - m), bf16 into swizzled smem
-        tmem_ld32(st + c0, v);
+        for (int c = 0; c < C::HDP; c += 16) {
+          float o[16];
+          tmem_row_load<16>(o_addr + c, o);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] *= factor;
+          tmem_row_store<16>(o_addr + c, o);
+        }
+      }
+      l *= factor;
+      float rs = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < AK; c0 += 32) {  // P = 2^(s - m) as packed bf16 over S
         uint32_t pk[16];
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
-          const float p0 = (c0 + c < valid) ? ex2(v[c] * scale_log2 - m_new) : 0.f;
-          const float p1 = (c0 + c + 1 < valid) ? ex2(v[c + 1] * scale_log2 - m_new) : 0.f;
+          const float p0 = (c0 + c < valid) ? ex2(fmaf(v[c0 + c], scale_log2, -m_run)) : 0.f;
+          const float p1 =
+              (c0 + c + 1 < valid) ? ex2(fmaf(v[c0 + c + 1], scale_log2, -m_run)) : 0.f;
           rs += p0 + p1;
           __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
           pk[c / 2] = *reinterpret_cast<uint32_t *>(&t2);
         }
-        const int atom = c0 >> 6;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {  // four 16-byte chunks of 8 keys
-          const int chunk = ((c0 & 63) >> 3) + u;
-          uint4 w = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-          *reinterpret_cast<uint4 *>(prow + atom * (AQ * 128) + ((chunk ^ (r & 7)) << 4)) = w;
-        }
+        tmem_st16(st_addr + c0 / 2, pk);
       }
-      l = l * alpha + rs;
-      m = m_new;
-      m_hist[j & 1] = m_new;
-      fence_proxy_async_smem();
+      l += rs;
+      tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&p_full[j & 1]);
-      if (j >= 1) correction(j - 1);
+      mbar_arrive(&p_full[g]);
     }
-    correction(n_kv - 1);
-    // normalise + store (rows beyond Nq are padding)
-    const int qrow = q0 + r;
+    // epilogue: O / l (rows beyond Nq are padding)
+    mbar_wait(&o_done[g], (n_kv - 1) & 1);
+    tc_fence_after();
+    float o[C::HDP];
+    tmem_row_load<C::HDP>(o_addr, o);
+    const int qrow = q0 + g * AQ + r;
     if (qrow < Nq) {
       const float inv = 1.f / l;
       const int d = H * hd;
-      bf16 *o = out + ((long)qrow * B + b) * d + h * hd;
+      bf16 *dst = out + ((long)qrow * B + b) * d + h * hd;
+      if ((hd & 7) == 0) {
 #pragma unroll
-      for (int c = 0; c < C::HDP; c += 8) {
-        if (c < hd) {
-          __nv_bfloat162 a0 = __floats2bfloat162_rn(oacc[c] * inv, oacc[c + 1] * inv);
-          __nv_bfloat162 a1 = __floats2bfloat162_rn(oacc[c + 2] * inv, oacc[c + 3] * inv);
-          __nv_bfloat162 a2 = __floats2bfloat162_rn(oacc[c + 4] * inv, oacc[c + 5] * inv);
-          __nv_bfloat162 a3 = __floats2bfloat162_rn(oacc[c + 6] * inv, oacc[c + 7] * inv);
-          uint4 w = make_uint4(*reinterpret_cast<uint32_t *>(&a0), *reinterpret_cast<uint32_t *>(&a1),
-                               *reinterpret_cast<uint32_t *>(&a2), *reinterpret_cast<uint32_t *>(&a3));
-          *reinterpret_cast<uint4 *>(o + c) = w;
+        for (int c = 0; c < C::HDP; c += 8) {
+          if (c < hd) {
+            __nv_bfloat162 a0 = __floats2bfloat162_rn(o[c] * inv, o[c + 1] * inv);
+            __nv_bfloat162 a1 = __floats2bfloat162_rn(o[c + 2] * inv, o[c + 3] * inv);
+            __nv_bfloat162 a2 = __floats2bfloat162_rn(o[c + 4] * inv, o[c + 5] * inv);
+            __nv_bfloat162 a3 = __floats2bfloat162_rn(o[c + 6] * inv, o[c + 7] * inv);
+            *reinterpret_cast<uint4 *>(dst + c) =
+                make_uint4(*reinterpret_cast<uint32_t *>(&a0), *reinterpret_cast<uint32_t *>(&a1),
+                           *reinterpret_cast<uint32_t *>(&a2), *reinterpret_cast<uint32_t *>(&a3));
+          }
         }
+      } else {
+#pragma unroll
+        for (int c = 0; c < C::HDP; ++c)
+          if (c < hd) dst[c] = __float2bfloat16_rn(o[c] * inv);
       }
     }
   }
@@ -310,55 +358,63 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-template <int MAIN, int REM>
+template <int N64, int N32, int N16, int NQT>
 cudaError_t launch_attn(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B, int H,
                         int hd, cudaStream_t s) {
-  using C = AttnCfg<MAIN, REM>;
+  using C = AttnCfg<N64, N32, N16, NQT>;
   const int d = H * hd;
-  CUtensorMap tq_main{}, tq_rem{}, tkv_main{}, tkv_rem{};
+  if (d % 8) return cudaErrorInvalidValue;  // TMA: 16-byte row strides
+  CUtensorMap tm[6] = {};
   const uint64_t dq[4] = {(uint64_t)hd, (uint64_t)H, (uint64_t)B, (uint64_t)Nq};
   const uint64_t sq[3] = {(uint64_t)hd * 2, (uint64_t)d * 2, (uint64_t)B * d * 2};
   const uint64_t dk[4] = {(uint64_t)hd, (uint64_t)H, (uint64_t)2 * B, (uint64_t)Nkv};
   const uint64_t sk[3] = {(uint64_t)hd * 2, (uint64_t)d * 2, (uint64_t)2 * B * d * 2};
-  const uint32_t bmain[4] = {64, 1, 1, 128}, brem[4] = {16, 1, 1, 128};
+  const int widths[3] = {64, 32, 16};
+  const int present[3] = {N64, N32, N16};
+  const CUtensorMapSwizzle swz[3] = {CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_SWIZZLE_64B,
+                                     CU_TENSOR_MAP_SWIZZLE_32B};
   bool ok = true;
-  if (MAIN) {
-    ok &= make_tmap(&tq_main, q, 4, dq, sq, bmain, CU_TENSOR_MAP_SWIZZLE_128B);
-    ok &= make_tmap(&tkv_main, kv, 4, dk, sk, bmain, CU_TENSOR_MAP_SWIZZLE_128B);
-  }
-  if (REM) {
-    ok &= make_tmap(&tq_rem, q, 4, dq, sq, brem, CU_TENSOR_MAP_SWIZZLE_32B);
-    ok &= make_tmap(&tkv_rem, kv, 4, dk, sk, brem, CU_TENSOR_MAP_SWIZZLE_32B);
+  for (int i = 0; i < 3; ++i) {
+    if (!present[i]) continue;
+    const uint32_t box[4] = {(uint32_t)widths[i], 1, 1, 128};
+    ok &= make_tmap(&tm[i], q, 4, dq, sq, box, swz[i]);
+    ok &= make_tmap(&tm[3 + i], kv, 4, dk, sk, box, swz[i]);
   }
   if (!ok) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_attn_kernel<MAIN, REM>,
+    cudaError_t e = cudaFuncSetAttribute(tc_attn_kernel<N64, N32, N16, NQT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((Nq + AQ - 1) / AQ, H, B);
+  dim3 grid((Nq + AQ * NQT - 1) / (AQ * NQT), H, B);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-  tc_attn_kernel<MAIN, REM><<<grid, 192, C::SMEM, s>>>(tq_main, tq_rem, tkv_main, tkv_rem, o, Nq,
-                                                       Nkv, B, H, hd, scale_log2);
+  tc_attn_kernel<N64, N32, N16, NQT><<<grid, C::THREADS, C::SMEM, s>>>(
+      tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], o, Nq, Nkv, B, H, hd, scale_log2);
   ++g_launches;
   return cudaGetLastError();
 }
 
 }  // namespace
 
-bool tc_attention_supported(int hd) { return hd == 16 || hd == 64 || hd == 72 || hd == 80; }
+// Supported head dims (padded to hd_pad): 16 (16), 40 (48 = 32 + 16), 64 (64),
+// 72 / 80 (80 = 64 + 16), 160 (160 = 64 + 64 + 32, one query tile per CTA).
+bool tc_attention_supported(int hd) {
+  return hd == 16 || hd == 40 || hd == 64 || hd == 72 || hd == 80 || hd == 160;
+}
 
 cudaError_t tc_attention_bf16(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B,
                               int H, int hd, cudaStream_t s) {
   if (Nq <= 0) return cudaSuccess;
   if (Nkv <= 0) return cudaErrorInvalidValue;
   switch (hd) {
-    case 16: return launch_attn<0, 16>(q, kv, o, Nq, Nkv, B, H, hd, s);
-    case 64: return launch_attn<64, 0>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 16: return launch_attn<0, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 40: return launch_attn<0, 1, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 64: return launch_attn<1, 0, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 72:
-    case 80: return launch_attn<64, 16>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 80: return launch_attn<1, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 160: return launch_attn<2, 1, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -293,9 +293,14 @@ class Context:
             keep.append(la)
             lp = la.ctypes.data_as(C.POINTER(C.c_int32))
         if text is not None:
-            ta = np.ascontiguousarray(text, dtype=np.float32)
-            keep.append(ta)
-            tp = ta.ctypes.data_as(C.POINTER(C.c_float))
+            if hasattr(text, "data_ptr"):   # torch tensor (host, pinned or device)
+                assert text.is_contiguous() and str(text.dtype) == "torch.float32"
+                keep.append(text)
+                tp = C.cast(C.c_void_p(text.data_ptr()), C.POINTER(C.c_float))
+            else:
+                ta = np.ascontiguousarray(text, dtype=np.float32)
+                keep.append(ta)
+                tp = ta.ctypes.data_as(C.POINTER(C.c_float))
         return Cond(lp, tp), keep
 
     def begin(self, noise, cond, stream=None):

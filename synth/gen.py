@@ -15,25 +15,37 @@ def _rng(seed: int) -> np.random.Generator:
 
 
 def weights(cfg: dict, seed: int = configs.SEED_WEIGHTS) -> dict[str, np.ndarray]:
-    """Random-init weights in manifest order (float32, C-contiguous)."""
+    """Random-init weights in manifest order (float32, C-contiguous).
+
+    fan_in = the input features of a linear / 1x1 conv ([out, in]) or
+    in_channels * 9 of a 3x3 conv ([out, in, 3, 3]).  The residual-branch
+    scaling uses the number of residual blocks: depth (DiT) or the number of
+    'wo' tensors / 2 (U-Net: ResBlock conv2 + attention / FF outputs)."""
     rng = _rng(seed)
-    depth = cfg["depth"]
+    man = configs.manifest(cfg)
+    if cfg["family"] == "unet":
+        nblk = max(1, sum(1 for _, _, k in man if k == "wo") // 2)
+    else:
+        nblk = cfg["depth"]
     out: dict[str, np.ndarray] = {}
-    for name, shape, kind in configs.manifest(cfg):
+    for name, shape, kind in man:
         a = rng.standard_normal(shape, dtype=np.float32)
+        fan_in = int(np.prod(shape[1:])) if len(shape) > 1 else 1
         if kind == "w":
-            a *= np.float32(1.0 / np.sqrt(shape[1]))
+            a *= np.float32(1.0 / np.sqrt(fan_in))
         elif kind == "wo":
-            a *= np.float32(1.0 / np.sqrt(shape[1]) / np.sqrt(2.0 * depth))
+            a *= np.float32(1.0 / np.sqrt(fan_in) / np.sqrt(2.0 * nblk))
         elif kind == "b":
             a *= np.float32(0.02)
+        elif kind == "g":
+            a = np.float32(1.0) + a * np.float32(0.02)
         elif kind == "emb":
             a *= np.float32(0.5)
         elif kind == "table":
             a *= np.float32(1.0 / np.sqrt(cfg["hidden"]))
         else:  # pragma: no cover
             raise ValueError(kind)
-        out[name] = np.ascontiguousarray(a)
+        out[name] = np.ascontiguousarray(a, dtype=np.float32)
     return out
 
 
@@ -48,14 +60,19 @@ def cond(cfg: dict, seed: int = configs.SEED_COND) -> dict:
 
     class-conditional: labels [B] (null class = num_classes for the uncond row).
     text-conditional:  text [B, L_txt, D_txt] float32 ~ N(0,1) (R21: synthetic
-    T5-shaped embeddings; row 0 plays the null caption).
+    T5 / CLIP-shaped embeddings; row 0 plays the null caption); SDXL adds
+    pooled [B, 1280] ~ N(0,1) and the micro-conditioning time_ids [B, 6].
     """
     B = configs.batch(cfg)
     if cfg["cond"] == "class":
         lab = [cfg["class_label"]] if B == 1 else [cfg["num_classes"], cfg["class_label"]]
         return {"labels": np.asarray(lab, dtype=np.int32)}
-    t = _rng(seed).standard_normal((B, cfg["text_len"], cfg["text_dim"]), dtype=np.float32)
-    return {"text": t}
+    rng = _rng(seed)
+    out = {"text": rng.standard_normal((B, cfg["text_len"], cfg["text_dim"]), dtype=np.float32)}
+    if cfg.get("add_embed"):
+        out["pooled"] = rng.standard_normal((B, cfg["pooled_dim"]), dtype=np.float32)
+        out["time_ids"] = np.tile(np.asarray(cfg["time_ids"], dtype=np.float32), (B, 1))
+    return out
 
 
 def bf16_round(a: np.ndarray) -> np.ndarray:

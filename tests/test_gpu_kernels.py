@@ -112,6 +112,10 @@ def test_gemm_gated_residual_and_qkv(S, dtype):
 ATTN_CASES = [  # Nq, Nkv, B, H, hd
     (1, 64, 1, 4, 16), (32, 64, 1, 4, 16), (200, 1000, 2, 3, 64), (128, 256, 2, 2, 72),
     (300, 777, 2, 2, 72), (128, 120, 2, 16, 72), (256, 384, 1, 1, 80), (1000, 2048, 2, 2, 72),
+    (300, 1024, 2, 8, 40), (129, 77, 2, 8, 40),    # SD-1.5 level 0 self / cross (hd 40)
+    (64, 256, 2, 8, 160), (200, 77, 2, 8, 160),    # SD-1.5 level 2 (hd 160, one Q tile/CTA)
+    (500, 1500, 2, 10, 64), (255, 77, 2, 10, 64),  # SDXL level 1 self / cross (hd 64)
+    (257, 129, 1, 1, 16),
 ]
 
 
@@ -134,6 +138,69 @@ def test_attention(S, dtype, Nq, Nkv, B, H, hd):
                        nkv[:, :, 1].transpose(1, 0, 2), H).transpose(1, 0, 2)
     assert np.all(np.isfinite(got))
     assert _rel(got, ref) < (1e-2 if dtype == 0 else 1e-5)
+
+
+@pytest.mark.parametrize("hd", [72, 64, 40, 160])
+def test_attention_growing_max(S, hd):
+    """Keys whose logits grow tile after tile (and a late spike): exercises the
+    lazy rescaling of O / l in TMEM (running max moves by > 2^8 several times)."""
+    rng = np.random.default_rng(hd)
+    Nq, Nkv, B, H = 256, 1200, 1, 2
+    d = H * hd
+    q = rng.standard_normal((Nq, B, d)).astype(np.float32)
+    kv = rng.standard_normal((Nkv, B, 2, d)).astype(np.float32) * 0.3
+    ramp = np.linspace(0.2, 6.0, Nkv).astype(np.float32)
+    kv[:, :, 0] *= ramp[:, None, None]
+    kv[1100, :, 0] *= 4.0
+    tq, nq = _bf(q)
+    tkv, nkv = _bf(kv)
+    o = torch.full((Nq * B, d), float("nan"), device="cuda", dtype=torch.bfloat16)
+    S.k_attention(0, tq, tkv, o, Nq, Nkv, B, H, hd)
+    torch.cuda.synchronize()
+    got = o.float().cpu().numpy().reshape(Nq, B, d)
+    ref = OD.attention(nq.transpose(1, 0, 2), nkv[:, :, 0].transpose(1, 0, 2),
+                       nkv[:, :, 1].transpose(1, 0, 2), H).transpose(1, 0, 2)
+    assert np.all(np.isfinite(got))
+    assert _rel(got, ref) < 1e-2
+
+
+def test_attention_full_size_sampled(S):
+    """C5 at N = 1, the launch bench.py times: Nq = Nkv = 16384 tokens, B 2,
+    16 heads, hd 72.  The oracle evaluates 48 sampled query rows (every head,
+    both batch rows) against the full K/V."""
+    Nq = Nkv = 16384
+    B, H, hd = 2, 16, 72
+    d = H * hd
+    g = torch.Generator(device="cuda").manual_seed(7)
+    tq = torch.randn(Nq * B, d, device="cuda", generator=g).to(torch.bfloat16)
+    tkv = torch.randn(Nkv * B * 2, d, device="cuda", generator=g).to(torch.bfloat16)
+    o = torch.empty(Nq * B, d, device="cuda", dtype=torch.bfloat16)
+    S.k_attention(0, tq, tkv, o, Nq, Nkv, B, H, hd)
+    torch.cuda.synchronize()
+    rows = np.random.default_rng(1).choice(Nq, 48, replace=False)
+    nq = tq.float().cpu().numpy().astype(np.float64).reshape(Nq, B, d)[rows]
+    nkv = tkv.float().cpu().numpy().astype(np.float64).reshape(Nkv, B, 2, d)
+    got = o.float().cpu().numpy().reshape(Nq, B, d)[rows]
+    ref = OD.attention(nq.transpose(1, 0, 2), nkv[:, :, 0].transpose(1, 0, 2),
+                       nkv[:, :, 1].transpose(1, 0, 2), H).transpose(1, 0, 2)
+    assert _rel(got, ref) < 1e-2
+
+
+def test_gemm_full_size_sampled(S):
+    """C5 QKV GEMM at N = 1: M = 16384 tokens x B 2, N = 3456, K = 1152; sampled rows."""
+    M, N, K = 32768, 3456, 1152
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g) * 0.1
+    out = torch.empty(M, N, device="cuda")
+    S.k_gemm(0, A, W, M, N, K, S.EPI_F32, bias=bias, out=out, ldo=N, B=1)
+    torch.cuda.synchronize()
+    rows = np.random.default_rng(2).choice(M, 64, replace=False)
+    nA = A.float().cpu().numpy().astype(np.float64)[rows]
+    ref = OD.linear(nA, W.float().cpu().numpy().astype(np.float64),
+                    bias.cpu().numpy().astype(np.float64))
+    assert _rel(out.cpu().numpy()[rows], ref) < 1e-5 * 50
 
 
 @pytest.mark.parametrize("dtype", [0, 1], ids=["bf16", "fp32"])
@@ -159,6 +226,6 @@ def test_bad_shapes_rejected(S):
     with pytest.raises(S.StadiError) as e:
         S.k_gemm(0, A, W, 128, 64, 100, S.EPI_F32, out=out, ldo=64, B=1)   # K % 64 != 0
     assert e.value.status == 1
-    q = torch.zeros(128, 40, device="cuda", dtype=torch.bfloat16)
+    q = torch.zeros(128, 48, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(S.StadiError):
-        S.k_attention(0, q, q, q, 128, 64, 1, 1, 40)                      # hd 40 unsupported
+        S.k_attention(0, q, q, q, 128, 64, 1, 1, 48)                      # hd 48 unsupported
