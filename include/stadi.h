@@ -147,7 +147,10 @@ stadi_status stadi_schedule(const stadi_plan_t *plan, uint32_t rank,
 enum {
   STADI_PRESET_TINY_DIT = 0,   /* C1: d 64, 4 heads, depth 2, 16x16x4 latent    */
   STADI_PRESET_DIT_XL2 = 1,    /* C2: DiT-XL/2 shapes, 32x32x4 latent, CFG 4.0  */
-  STADI_PRESET_PIXART_ALPHA = 2/* C5: PixArt-alpha shapes, 256x256x4, CFG 4.5   */
+  STADI_PRESET_PIXART_ALPHA = 2,/* C5: PixArt-alpha shapes, 256x256x4, CFG 4.5  */
+  STADI_PRESET_SD15 = 3,       /* C3: SD-1.5 U-Net shapes, 64x64x4, CFG 7.5      */
+  STADI_PRESET_SDXL = 4,       /* C4: SDXL U-Net shapes, 128x128x4, CFG 5.0      */
+  STADI_PRESET_TINY_UNET = 5   /* 2-level U-Net for fast parity tests            */
 };
 enum { STADI_DTYPE_BF16 = 0, STADI_DTYPE_FP32_DEBUG = 1 };
 enum { STADI_SAMPLER_DDIM = 0, STADI_SAMPLER_DDPM = 1 /* NEXT: EUNSUPPORTED */ };
@@ -158,7 +161,8 @@ typedef struct {
                               fp32 residual + latent; FP32_DEBUG: SIMT fp32 (no
                               TF32) kernels for the <=1e-4 parity build         */
   int32_t sampler;         /* STADI_SAMPLER_DDIM                                 */
-  int32_t depth;           /* 0 = preset depth, >0 overrides (reduced variants)  */
+  int32_t depth;           /* 0 = preset depth; >0: DiT blocks, or the cap on every
+                              U-Net transformer depth (reduced parity variants)  */
   int32_t latent_h, latent_w; /* 0 = preset resolution                           */
 } stadi_model_desc;
 
@@ -181,8 +185,13 @@ typedef struct {
 } stadi_dist_desc;
 
 typedef struct {
-  const int32_t *labels;     /* [B] class labels (class presets; B=2: null first) */
-  const float *text;         /* [B, L_txt, D_txt] host fp32 (text presets)        */
+  const int32_t *labels;     /* [B] class labels (class presets; B=2: null first)  */
+  const float *text;         /* [B, L_txt, D_txt] fp32, host or device (text presets;
+                                B=2: the null caption first)                        */
+  const float *pooled;       /* [B, 1280] fp32 pooled text embedding (SDXL), host or
+                                device; NULL for other presets                      */
+  const float *time_ids;     /* [B, 6] host fp32 SDXL micro-conditioning, or NULL =
+                                the preset's (1024, 1024, 0, 0, 1024, 1024)         */
 } stadi_cond;
 
 typedef struct {

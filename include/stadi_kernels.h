@@ -25,7 +25,11 @@ enum {
   STADI_EPI_RES = 3,        /* res[f32] += acc + bias                             */
   STADI_EPI_QKV = 4,        /* cols < d: q[T]; cols >= d: K/V rows of the exchange
                                slot(s) kv_a / kv_b at row kv_row0 + row            */
-  STADI_EPI_F32 = 5         /* out[f32] = acc + bias                              */
+  STADI_EPI_F32 = 5,        /* out[f32] = acc + bias                              */
+  STADI_EPI_CONV = 6,       /* out[f32] = acc + bias (+ gate[row % B][col]: the per-
+                               batch time-embedding term) (+ res[row][col])      */
+  STADI_EPI_GEGLU = 7       /* W rows interleaved (a_0, g_0, a_1, g_1, ...):
+                               out[T][row][k] = a_k * gelu_erf(g_k), N/2 columns  */
 };
 
 typedef struct {

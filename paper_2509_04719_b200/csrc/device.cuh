@@ -24,6 +24,9 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
 }
 __device__ __forceinline__ float silu(float x) { return x / (1.f + expf(-x)); }
+__device__ __forceinline__ float gelu_erf(float x) {
+  return 0.5f * x * (1.f + erff(x * 0.7071067811865476f));
+}
 
 // ----------------------------------------------------------------- GEMM epilogues
 // Shared by the SIMT (fp32 debug) and the tcgen05 GEMM so both paths compute
@@ -35,6 +38,8 @@ enum EpiKind : int {
   EPI_RES = 3,        // res[f32] += acc + bias
   EPI_QKV = 4,        // cols [0,d): q ; [d,3d): K/V into exchange slot(s)
   EPI_F32 = 5,        // outf[f32] = acc + bias
+  EPI_CONV = 6,       // outf[f32] = acc + bias (+ gate[row % B][col]) (+ res[row][col])
+  EPI_GEGLU = 7,      // out[T][col/2 + j] = v[2j] * gelu_erf(v[2j+1])  (interleaved a|g)
 };
 
 struct EpiParams {
@@ -78,6 +83,22 @@ __device__ __forceinline__ void epi_apply(const EpiParams &p, int row, int col, 
 #pragma unroll 8
       for (int i = 0; i < n; ++i) r[i] += v[i];
     }
+  } else if constexpr (EPI == EPI_CONV) {
+    float *o = reinterpret_cast<float *>(p.out) + (long)row * p.ldo + col;
+    const float *g = p.gate ? p.gate + (row % p.B) * p.gate_bstride + col : nullptr;
+    const float *r = p.res ? p.res + (long)row * p.ldr + col : nullptr;
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) {
+      float a = v[i];
+      if (g) a += __ldg(g + i);
+      if (r) a += r[i];
+      o[i] = a;
+    }
+  } else if constexpr (EPI == EPI_GEGLU) {
+    // n is even and col even: pairs (a_k, g_k) -> one output column k = col/2 + j
+    T *o = reinterpret_cast<T *>(p.out) + (long)row * p.ldo + col / 2;
+#pragma unroll 8
+    for (int j = 0; j < n / 2; ++j) o[j] = from_f<T>(v[2 * j] * gelu_erf(v[2 * j + 1]));
   } else if constexpr (EPI == EPI_QKV) {
     // n consecutive columns never straddle the q / kv boundary (d % n == 0).
     if (col < p.d) {

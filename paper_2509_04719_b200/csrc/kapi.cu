@@ -17,7 +17,7 @@ stadi_status cu(cudaError_t e, const char *what) {
 extern "C" stadi_status stadi_k_gemm(int32_t dtype, const void *A, const void *W, int32_t M,
                                      int32_t N, int32_t K, int32_t epi, const stadi_k_epi *e,
                                      void *stream) {
-  if (!A || !W || !e || M < 0 || N <= 0 || K <= 0 || epi < 0 || epi > 5)
+  if (!A || !W || !e || M < 0 || N <= 0 || K <= 0 || epi < 0 || epi > 7)
     return fail(nullptr, STADI_EINVAL, "stadi_k_gemm: bad argument");
   EpiParams ep{};
   ep.bias = e->bias;

@@ -32,9 +32,12 @@ bool tc_attention_supported(int hd);
 
 // ---- elementwise / normalisation -------------------------------------------
 // y[row] = LN(x[row]) * (1 + scale[b]) + shift[b]   (b = row % B); do_norm = 0: y = x
+// eps: 1e-6 (DiT, no affine) or 1e-5 (U-Net LayerNorm with affine: scale = w - 1,
+// shift = b, mod_bstride = 0).
 template <typename T>
 cudaError_t ln_modulate(const float *x, T *y, int M, int d, int B, const float *shift,
-                        const float *scale, int mod_bstride, int do_norm, cudaStream_t s);
+                        const float *scale, int mod_bstride, int do_norm, cudaStream_t s,
+                        float eps = 1e-6f);
 // Patchify a latent band + Linear(p*p*C -> d) + bias + positional embedding,
 // written for every batch row: x_res[(i*B+b), :].
 cudaError_t patch_embed(const float *x_band, int rows, int W, int C, int p, const float *w,
@@ -57,6 +60,27 @@ cudaError_t cast_f32(const float *x, T *y, long n, cudaStream_t s);
 cudaError_t pixart_mods(const float *t0, const float *temb, const float *sst_all,
                         const float *final_sst, int n_t, int B, int depth, int d, float *mod,
                         float *fmod, cudaStream_t s);
+
+// ---- U-Net band kernels (unet_ops.cu): X = [h, W, B, C] fp32 token-major,
+// P = [h+2, W+2, B, C] halo-padded conv input (see unet_ops.cu) --------------
+// GroupNorm partial sums of the band: out[b][g][{S1, S2}] (fp64, zeroed first).
+cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, cudaStream_t s);
+// GroupNorm with the statistics summed over G rank segments [G][B][32][2]
+// (stats == null: plain cast), optional SiLU, pad = write into P's interior.
+template <typename T>
+cudaError_t gn_apply(const float *x, int h, int W, int B, int C, const double *stats, int G,
+                     double n_total, const float *gamma, const float *beta, float eps, int act,
+                     int pad, T *out, cudaStream_t s);
+// latent band [h, W, Cl] -> P (B copies; halo rows untouched)
+template <typename T>
+cudaError_t latent_pad(const float *x, int h, int W, int Cl, int B, T *out, cudaStream_t s);
+// 3x3 conv im2col from P: mode 0 stride 1, 1 stride 2, 2 nearest-x2 upsample.
+// A [(oy*Wo + ox)*B + b][Kp], column (ky*3 + kx)*C + c, zero beyond 9C.
+template <typename T>
+cudaError_t im2col(const T *P, int hin, int Win, int B, int C, int mode, int Kp, T *A,
+                   cudaStream_t s);
+cudaError_t concat_channels(const float *a, int Ca, const float *b, int Cb, long M, float *out,
+                            cudaStream_t s);
 
 // ---- occupancy emulator ---------------------------------
 cudaError_t emulator_launch(int n_ctas, volatile int *stop_flag, cudaStream_t s);

@@ -50,9 +50,14 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const T *__restrict__ A,
   for (int i = 0; i < 4; ++i) {
     const int row = m0 + ty * 4 + i;
     if (row >= M) continue;
+    const int col0 = n0 + tx * 4;
+    if (col0 + 3 < N) {  // 4 consecutive columns (GEGLU pairs stay together)
+      epi_apply<T, EPI>(ep, row, col0, acc[i], 4);
+      continue;
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int col = n0 + tx * 4 + j;
+      const int col = col0 + j;
       if (col >= N) continue;
       float v = acc[i][j];
       epi_apply<T, EPI>(ep, row, col, &v, 1);
@@ -75,6 +80,11 @@ cudaError_t simt_gemm(const T *A, const T *W, int M, int N, int K, int epi, cons
     case EPI_RES: simt_gemm_kernel<T, EPI_RES><<<grid, 256, 0, s>>>(A, W, M, N, K, ep); break;
     case EPI_QKV: simt_gemm_kernel<T, EPI_QKV><<<grid, 256, 0, s>>>(A, W, M, N, K, ep); break;
     case EPI_F32: simt_gemm_kernel<T, EPI_F32><<<grid, 256, 0, s>>>(A, W, M, N, K, ep); break;
+    case EPI_CONV: simt_gemm_kernel<T, EPI_CONV><<<grid, 256, 0, s>>>(A, W, M, N, K, ep); break;
+    case EPI_GEGLU:
+      if (N % 4) return cudaErrorInvalidValue;
+      simt_gemm_kernel<T, EPI_GEGLU><<<grid, 256, 0, s>>>(A, W, M, N, K, ep);
+      break;
     default: return cudaErrorInvalidValue;
   }
   ++g_launches;
@@ -175,7 +185,7 @@ __global__ void __launch_bounds__(256) ln_mod_kernel(const float *__restrict__ x
                                                      int M, int d, int B,
                                                      const float *__restrict__ shift,
                                                      const float *__restrict__ scale, int bs,
-                                                     int do_norm) {
+                                                     int do_norm, float eps) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long row = (long)blockIdx.x * 8 + warp;
   if (row >= M) return;
@@ -217,7 +227,7 @@ __global__ void __launch_bounds__(256) ln_mod_kernel(const float *__restrict__ x
     }
   }
   for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
-  const float rstd = rsqrtf(q / d + 1e-6f);
+  const float rstd = rsqrtf(q / d + eps);
   const int b = (int)(row % B);
   const float *sh = shift + (long)b * bs, *sc = scale + (long)b * bs;
 #pragma unroll
@@ -237,17 +247,19 @@ __global__ void __launch_bounds__(256) ln_mod_kernel(const float *__restrict__ x
 
 template <typename T>
 cudaError_t ln_modulate(const float *x, T *y, int M, int d, int B, const float *shift,
-                        const float *scale, int mod_bstride, int do_norm, cudaStream_t s) {
+                        const float *scale, int mod_bstride, int do_norm, cudaStream_t s,
+                        float eps) {
   if (d % 4 || d / 4 > 32 * LN_MAXV) return cudaErrorInvalidValue;
   if (M <= 0) return cudaSuccess;
-  ln_mod_kernel<T><<<(M + 7) / 8, 256, 0, s>>>(x, y, M, d, B, shift, scale, mod_bstride, do_norm);
+  ln_mod_kernel<T><<<(M + 7) / 8, 256, 0, s>>>(x, y, M, d, B, shift, scale, mod_bstride, do_norm,
+                                               eps);
   ++g_launches;
   return cudaGetLastError();
 }
 template cudaError_t ln_modulate<float>(const float *, float *, int, int, int, const float *,
-                                        const float *, int, int, cudaStream_t);
+                                        const float *, int, int, cudaStream_t, float);
 template cudaError_t ln_modulate<bf16>(const float *, bf16 *, int, int, int, const float *,
-                                       const float *, int, int, cudaStream_t);
+                                       const float *, int, int, cudaStream_t, float);
 
 // ------------------------------------------------------------------ patch embedding
 namespace {

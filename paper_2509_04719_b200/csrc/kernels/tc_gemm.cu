@@ -28,15 +28,78 @@ namespace {
 
 constexpr int GBM = 128, GBK = 64;
 
+constexpr int EPI_LD = 33;                       // staging row stride (floats, bank-free)
+constexpr int EPI_SMEM = 4 * 32 * EPI_LD * 4;    // 4 epilogue warps x 32 x 32 fp32
+
 template <int BN>
 struct GemmCfg {
   static constexpr int A_BYTES = GBM * GBK * 2;              // 16 KB
   static constexpr int B_BYTES = BN * GBK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+  static constexpr int STAGES = (196 * 1024) / STAGE > 8 ? 8 : (196 * 1024) / STAGE;
   static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE + EPI_SMEM + 1024 /*align*/ + 256 /*barriers*/;
 };
+
+// Epilogue of two adjacent columns (col even) of one row, vectorised stores.
+template <int EPI>
+__device__ __forceinline__ void epi_pair(const EpiParams &p, int row, int col, float v0, float v1) {
+  if (p.bias) {
+    const float2 b = *reinterpret_cast<const float2 *>(p.bias + col);
+    v0 += b.x;
+    v1 += b.y;
+  }
+  if constexpr (EPI == EPI_STORE || EPI == EPI_GELU) {
+    if (EPI == EPI_GELU) {
+      v0 = gelu_tanh(v0);
+      v1 = gelu_tanh(v1);
+    }
+    *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<bf16 *>(p.out) + (long)row * p.ldo +
+                                        col) = __floats2bfloat162_rn(v0, v1);
+  } else if constexpr (EPI == EPI_F32 || EPI == EPI_CONV) {
+    if constexpr (EPI == EPI_CONV) {
+      if (p.gate) {
+        const float2 g = *reinterpret_cast<const float2 *>(p.gate + (row % p.B) * p.gate_bstride +
+                                                           col);
+        v0 += g.x;
+        v1 += g.y;
+      }
+      if (p.res) {
+        const float2 r = *reinterpret_cast<const float2 *>(p.res + (long)row * p.ldr + col);
+        v0 += r.x;
+        v1 += r.y;
+      }
+    }
+    *reinterpret_cast<float2 *>(reinterpret_cast<float *>(p.out) + (long)row * p.ldo + col) =
+        make_float2(v0, v1);
+  } else if constexpr (EPI == EPI_GATED_RES || EPI == EPI_RES) {
+    float2 *r = reinterpret_cast<float2 *>(p.res + (long)row * p.ldr + col);
+    float2 a = *r;
+    if constexpr (EPI == EPI_GATED_RES) {
+      const float2 g =
+          *reinterpret_cast<const float2 *>(p.gate + (row % p.B) * p.gate_bstride + col);
+      a.x += g.x * v0;
+      a.y += g.y * v1;
+    } else {
+      a.x += v0;
+      a.y += v1;
+    }
+    *r = a;
+  } else if constexpr (EPI == EPI_GEGLU) {
+    reinterpret_cast<bf16 *>(p.out)[(long)row * p.ldo + col / 2] =
+        __float2bfloat16_rn(v0 * gelu_erf(v1));
+  } else if constexpr (EPI == EPI_QKV) {
+    const __nv_bfloat162 t = __floats2bfloat162_rn(v0, v1);
+    if (col < p.d) {
+      *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<bf16 *>(p.q) + (long)row * p.d + col) =
+          t;
+    } else {
+      const long off = (p.kv_row0 + row) * 2L * p.d + (col - p.d);
+      *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<bf16 *>(p.kv_a) + off) = t;
+      if (p.kv_b) *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<bf16 *>(p.kv_b) + off) = t;
+    }
+  }
+}
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(192, 1)
@@ -48,7 +111,8 @@ __global__ void __launch_bounds__(192, 1)
                                               ~uintptr_t(1023));
   uint8_t *sA = smem;
   uint8_t *sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE);
+  float *stg_all = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE + EPI_SMEM);
   uint64_t *full = bars, *empty = bars + C::STAGES;
   uint64_t *tfull = bars + 2 * C::STAGES, *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
@@ -136,17 +200,33 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int row = mb * GBM + qd * 32 + lane;
+      const int row0 = mb * GBM + qd * 32;
       const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + acc * BN;
+      float *stg = stg_all + (warp - 2) * 32 * EPI_LD;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
+        // TMEM -> registers (lane = row) -> smem, then coalesced: lanes cover
+        // 16 column pairs of two rows per step
         float v[32];
         tmem_ld32(tbase + c0, v);
-        if (row < M) epi_apply<bf16, EPI>(ep, row, nb * BN + c0, v, 32);
+        if (c0 + 32 >= BN) {  // accumulator fully read: release it to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) stg[lane * EPI_LD + i] = v[i];
+        __syncwarp();
+        const int cc = 2 * (lane & 15);
+#pragma unroll 4
+        for (int it = 0; it < 16; ++it) {
+          const int r = 2 * it + (lane >> 4);
+          if (row0 + r < M)
+            epi_pair<EPI>(ep, row0 + r, nb * BN + c0 + cc, stg[r * EPI_LD + cc],
+                          stg[r * EPI_LD + cc + 1]);
+        }
+        __syncwarp();
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   tc_fence_before();
@@ -234,6 +314,8 @@ cudaError_t dispatch_epi(const bf16 *A, const bf16 *W, int M, int N, int K, int 
     case EPI_RES: return launch_gemm<BN, EPI_RES>(A, W, M, N, K, ep, max_ctas, s);
     case EPI_QKV: return launch_gemm<BN, EPI_QKV>(A, W, M, N, K, ep, max_ctas, s);
     case EPI_F32: return launch_gemm<BN, EPI_F32>(A, W, M, N, K, ep, max_ctas, s);
+    case EPI_CONV: return launch_gemm<BN, EPI_CONV>(A, W, M, N, K, ep, max_ctas, s);
+    case EPI_GEGLU: return launch_gemm<BN, EPI_GEGLU>(A, W, M, N, K, ep, max_ctas, s);
   }
   return cudaErrorInvalidValue;
 }

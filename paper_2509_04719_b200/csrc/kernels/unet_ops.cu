@@ -1,0 +1,287 @@
+// HBM-bound kernels of the patch-parallel U-Net:
+// GroupNorm partial statistics of a band (the payload of a GN exchange site,
+// PAPER.md L80 "stale activations"), GroupNorm apply (+SiLU) into
+// the halo-padded conv-input buffer, im2col of a 3x3 conv (stride 1, stride 2,
+// nearest-x2 upsample), channel concat of the skip path and the latent -> padded
+// conv_in input.
+//
+// Activation layout (token-major, batch innermost, as the DiT path):
+//   X [h, W, B, C] fp32: element ((y * W + x) * B + b) * C + c
+//   P [h + 2, W + 2, B, C] bf16, the conv input with one halo row above / below
+//     (filled by the exchange or zero at the image edge) and one zero column
+//     left / right: element (((y + 1) * (W + 2) + x + 1) * B + b) * C + c.
+#include "../kernels.h"
+
+namespace stadi {
+
+namespace {
+
+constexpr int GN_G = 32;
+
+// ------------------------------------------------------------- GN partials
+// out[b][g][0] += sum x, out[b][g][1] += sum x^2 over the band (fp32 per
+// thread over a row chunk, fp64 atomics across chunks).  One block = a chunk of
+// rows; thread t owns float4 channel vectors t, t + 256, ...
+__global__ void __launch_bounds__(256) gn_partials_kernel(const float *__restrict__ x, long M,
+                                                          int B, int C, int rows_per_block,
+                                                          double *__restrict__ out) {
+  extern __shared__ float sm[];  // [2 stats][B][C]
+  const int nvec = C / 4;
+  const long r0 = (long)blockIdx.x * rows_per_block;
+  const long r1 = min(M, r0 + rows_per_block);
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    float s1[2][4] = {}, s2[2][4] = {};
+    for (long r = r0; r < r1; ++r) {
+      const float4 a = reinterpret_cast<const float4 *>(x + r * C)[v];
+      const int b = (int)(r % B) & 1;
+      s1[b][0] += a.x; s1[b][1] += a.y; s1[b][2] += a.z; s1[b][3] += a.w;
+      s2[b][0] += a.x * a.x; s2[b][1] += a.y * a.y; s2[b][2] += a.z * a.z; s2[b][3] += a.w * a.w;
+    }
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        sm[(0 * B + b) * C + 4 * v + i] = s1[b][i];
+        sm[(1 * B + b) * C + 4 * v + i] = s2[b][i];
+      }
+  }
+  __syncthreads();
+  const int cg = C / GN_G;
+  for (int j = threadIdx.x; j < 2 * B * GN_G; j += blockDim.x) {
+    const int st = j / (B * GN_G), b = (j / GN_G) % B, g = j % GN_G;
+    float acc = 0.f;
+    for (int c = 0; c < cg; ++c) acc += sm[(st * B + b) * C + g * cg + c];
+    atomicAdd(out + ((long)b * GN_G + g) * 2 + st, (double)acc);
+  }
+}
+
+// ------------------------------------------------------------- GN apply
+// y = (x - mean) * rstd * gamma + beta (+ SiLU), mean / var from the sum over the
+// G rank segments of the statistics (own fresh + others stale); stats == null:
+// plain cast.  pad: write into the halo-padded buffer (interior + zero columns).
+template <typename T>
+__global__ void __launch_bounds__(256) gn_apply_kernel(
+    const float *__restrict__ x, int h, int W, int B, int C, const double *__restrict__ stats,
+    int G, double n_total, const float *__restrict__ gamma, const float *__restrict__ beta,
+    float eps, int act, int pad, T *__restrict__ out) {
+  __shared__ float mu[2 * GN_G], rs[2 * GN_G];
+  if (stats) {
+    for (int j = threadIdx.x; j < B * GN_G; j += blockDim.x) {
+      double s1 = 0, s2 = 0;
+      for (int q = 0; q < G; ++q) {
+        s1 += stats[((long)q * B * GN_G + j) * 2 + 0];
+        s2 += stats[((long)q * B * GN_G + j) * 2 + 1];
+      }
+      const double m = s1 / n_total;
+      const double var = fmax(s2 / n_total - m * m, 0.0);  // R17 clamp
+      mu[j] = (float)m;
+      rs[j] = (float)(1.0 / sqrt(var + (double)eps));
+    }
+  }
+  __syncthreads();
+  const int nvec = C / 4, cg = C / GN_G;
+  const long total = (long)h * W * B * nvec;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int v = (int)(i % nvec);
+    const long row = i / nvec;  // (y * W + x) * B + b
+    const int b = (int)(row % B);
+    float4 a = reinterpret_cast<const float4 *>(x + row * C)[v];
+    float e[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = 4 * v + k;
+      float y = e[k];
+      if (stats) {
+        const int j = b * GN_G + c / cg;
+        y = (y - mu[j]) * rs[j] * gamma[c] + beta[c];
+      }
+      if (act) y = silu(y);
+      e[k] = y;
+    }
+    long orow = row;
+    if (pad) {
+      const long pix = row / B;
+      const int yy = (int)(pix / W), xx = (int)(pix % W);
+      orow = (((long)(yy + 1) * (W + 2) + xx + 1) * B + b);
+    }
+    T *o = out + orow * C + 4 * v;
+    o[0] = from_f<T>(e[0]); o[1] = from_f<T>(e[1]); o[2] = from_f<T>(e[2]); o[3] = from_f<T>(e[3]);
+    if (pad) {  // zero the left / right border columns of this row
+      const long pix = row / B;
+      const int yy = (int)(pix / W), xx = (int)(pix % W);
+      if (xx == 0 || xx == W - 1) {
+        const long brow = (((long)(yy + 1) * (W + 2) + (xx == 0 ? 0 : W + 1)) * B + b);
+        T *z = out + brow * C + 4 * v;
+        z[0] = z[1] = z[2] = z[3] = from_f<T>(0.f);
+      }
+    }
+  }
+}
+
+// latent band x [h, W, Cl] fp32 -> padded conv_in input [h+2, W+2, B, Cl] (B copies)
+template <typename T>
+__global__ void latent_pad_kernel(const float *__restrict__ x, int h, int W, int Cl, int B,
+                                  T *__restrict__ out) {
+  const long total = (long)(h + 2) * (W + 2) * B * Cl;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Cl);
+    const long pix = i / Cl / B;
+    const int yy = (int)(pix / (W + 2)), xx = (int)(pix % (W + 2));
+    if (yy == 0 || yy == h + 1) continue;  // halo rows belong to the exchange
+    float v = 0.f;
+    if (xx >= 1 && xx <= W) v = x[((long)(yy - 1) * W + (xx - 1)) * Cl + c];
+    out[i] = from_f<T>(v);
+  }
+}
+
+// ------------------------------------------------------------- im2col
+// A[((oy * Wo + ox) * B + b)][(ky * 3 + kx) * C + c] from the padded input
+// (mode 0: stride 1; 1: stride 2; 2: nearest-x2 upsample of the input).
+// Columns >= 9C up to Kp are zero.  V = elements per thread (8 if C % 8 == 0).
+template <typename T, int V>
+__global__ void __launch_bounds__(256) im2col_kernel(const T *__restrict__ P, int hin, int Win,
+                                                     int B, int C, int mode, int ho, int wo,
+                                                     int Kp, T *__restrict__ A) {
+  const int kv = Kp / V;  // vectors per A row
+  const long total = (long)ho * wo * B * kv;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int k0 = (int)(i % kv) * V;
+    const long row = i / kv;
+    const int b = (int)(row % B);
+    const long pix = row / B;
+    const int oy = (int)(pix / wo), ox = (int)(pix % wo);
+    T *dst = A + row * Kp + k0;
+    const int tap = k0 / C, c = k0 % C;
+    bool zero = tap >= 9;
+    long src = 0;
+    if (!zero) {
+      const int ky = tap / 3, kx = tap % 3;
+      int py, px;
+      if (mode == 0) {
+        py = oy + ky;
+        px = ox + kx;
+      } else if (mode == 1) {
+        py = 2 * oy + ky;
+        px = 2 * ox + kx;
+      } else {
+        const int Y = oy + ky, X = ox + kx;  // hi-res padded coordinates
+        if (X == 0 || X == 2 * Win + 1) {
+          zero = true;
+          py = px = 0;
+        } else {
+          py = Y == 0 ? 0 : (Y == 2 * hin + 1 ? hin + 1 : 1 + (Y - 1) / 2);
+          px = 1 + (X - 1) / 2;
+        }
+      }
+      src = (((long)py * (Win + 2) + px) * B + b) * C + c;
+    }
+    if constexpr (V == 8) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (!zero) v = *reinterpret_cast<const uint4 *>(P + src);
+      *reinterpret_cast<uint4 *>(dst) = v;
+    } else {
+      dst[0] = zero ? from_f<T>(0.f) : P[src];
+    }
+  }
+}
+
+// ------------------------------------------------------------- concat
+__global__ void concat_kernel(const float *__restrict__ a, int Ca, const float *__restrict__ b,
+                              int Cb, long M, float *__restrict__ out) {
+  const int C = Ca + Cb;
+  const long total = M * (C / 4);
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int v = (int)(i % (C / 4));
+    const long r = i / (C / 4);
+    const int c = 4 * v;
+    float4 x = c < Ca ? reinterpret_cast<const float4 *>(a + r * Ca)[v]
+                      : reinterpret_cast<const float4 *>(b + r * Cb)[(c - Ca) / 4];
+    reinterpret_cast<float4 *>(out + r * C)[v] = x;
+  }
+}
+
+inline unsigned grid_for(long work, int per_block = 256) {
+  long g = (work + per_block - 1) / per_block;
+  return (unsigned)std::min<long>(std::max<long>(g, 1), 148L * 16);
+}
+
+}  // namespace
+
+cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, cudaStream_t s) {
+  if (C % (4 * GN_G) && C % 4) return cudaErrorInvalidValue;
+  if (B > 2 || C % 4 || C % GN_G) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(out, 0, (size_t)B * GN_G * 2 * sizeof(double), s);
+  if (e != cudaSuccess || M == 0) return e;
+  const int blocks = (int)std::min<long>(296, M);
+  int rpb = (int)((M + blocks - 1) / blocks);
+  const int nb = (int)((M + rpb - 1) / rpb);
+  const size_t smem = (size_t)2 * B * C * sizeof(float);
+  gn_partials_kernel<<<nb, 256, smem, s>>>(x, M, B, C, rpb, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t gn_apply(const float *x, int h, int W, int B, int C, const double *stats, int G,
+                     double n_total, const float *gamma, const float *beta, float eps, int act,
+                     int pad, T *out, cudaStream_t s) {
+  if (C % 4 || (stats && C % GN_G) || B > 2) return cudaErrorInvalidValue;
+  const long work = (long)h * W * B * (C / 4);
+  if (work == 0) return cudaSuccess;
+  gn_apply_kernel<T><<<grid_for(work), 256, 0, s>>>(x, h, W, B, C, stats, G, n_total, gamma,
+                                                    beta, eps, act, pad, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+template cudaError_t gn_apply<bf16>(const float *, int, int, int, int, const double *, int,
+                                    double, const float *, const float *, float, int, int, bf16 *,
+                                    cudaStream_t);
+template cudaError_t gn_apply<float>(const float *, int, int, int, int, const double *, int,
+                                     double, const float *, const float *, float, int, int,
+                                     float *, cudaStream_t);
+
+template <typename T>
+cudaError_t latent_pad(const float *x, int h, int W, int Cl, int B, T *out, cudaStream_t s) {
+  const long work = (long)(h + 2) * (W + 2) * B * Cl;
+  latent_pad_kernel<T><<<grid_for(work), 256, 0, s>>>(x, h, W, Cl, B, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+template cudaError_t latent_pad<bf16>(const float *, int, int, int, int, bf16 *, cudaStream_t);
+template cudaError_t latent_pad<float>(const float *, int, int, int, int, float *, cudaStream_t);
+
+template <typename T>
+cudaError_t im2col(const T *P, int hin, int Win, int B, int C, int mode, int Kp, T *A,
+                   cudaStream_t s) {
+  const int ho = mode == 1 ? hin / 2 : (mode == 2 ? 2 * hin : hin);
+  const int wo = mode == 1 ? Win / 2 : (mode == 2 ? 2 * Win : Win);
+  if (Kp < 9 * C) return cudaErrorInvalidValue;
+  if (C % 8 == 0 && Kp % 8 == 0 && sizeof(T) == 2) {
+    const long work = (long)ho * wo * B * (Kp / 8);
+    im2col_kernel<T, 8><<<grid_for(work), 256, 0, s>>>(P, hin, Win, B, C, mode, ho, wo, Kp, A);
+  } else {
+    const long work = (long)ho * wo * B * Kp;
+    im2col_kernel<T, 1><<<grid_for(work), 256, 0, s>>>(P, hin, Win, B, C, mode, ho, wo, Kp, A);
+  }
+  ++g_launches;
+  return cudaGetLastError();
+}
+template cudaError_t im2col<bf16>(const bf16 *, int, int, int, int, int, int, bf16 *,
+                                  cudaStream_t);
+template cudaError_t im2col<float>(const float *, int, int, int, int, int, int, float *,
+                                   cudaStream_t);
+
+cudaError_t concat_channels(const float *a, int Ca, const float *b, int Cb, long M, float *out,
+                            cudaStream_t s) {
+  if (Ca % 4 || Cb % 4) return cudaErrorInvalidValue;
+  const long work = M * ((Ca + Cb) / 4);
+  if (work == 0) return cudaSuccess;
+  concat_kernel<<<grid_for(work), 256, 0, s>>>(a, Ca, b, Cb, M, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace stadi

@@ -22,8 +22,11 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -88,6 +91,8 @@ struct Part {  // one (hosted rank, schedule entry) executed in a program step
   int li;      // index into ctx->ranks
   stadi_step_t st;
 };
+
+struct UNetState;  // unet_exec.cuh
 
 }  // namespace
 
@@ -159,6 +164,9 @@ struct stadi_ctx {
   };
   bool ktime = false;
   KClass kt[STADI_KCLASS_COUNT];
+
+  // U-Net family executor state (weights, programs, exchange sites)
+  std::unique_ptr<UNetState> un;
 };
 
 namespace {
@@ -196,6 +204,12 @@ stadi_status ctx_fail(stadi_ctx *c, stadi_status st, const char *fmt, ...) {
     if (!ctx) return ctx_fail(nullptr, STADI_EINVAL, "NULL context");                  \
     if (ctx->poisoned) return ctx_fail(ctx, STADI_ESTATE, "context poisoned: %s",      \
                                        ctx->err.c_str());                              \
+  } while (0)
+
+#define ST(call)                          \
+  do {                                    \
+    stadi_status s_ = (call);             \
+    if (s_ != STADI_OK) return s_;        \
   } while (0)
 
 template <typename P>
@@ -325,7 +339,28 @@ int widx(stadi_ctx *ctx, const std::string &name) {
 void *WT(stadi_ctx *ctx, const std::string &n) { return ctx->wT[widx(ctx, n)]; }
 float *WF(stadi_ctx *ctx, const std::string &n) { return ctx->wf[widx(ctx, n)]; }
 
+// Attention with an explicit head count (U-Net levels: d = C, hd = C / H).
+cudaError_t attention_h(stadi_ctx *ctx, int cls, const void *q, const void *kv, void *o, int Nq,
+                        int Nkv, int H, int C, cudaStream_t s) {
+  const int B = ctx->dm.B, hd = C / H;
+  const double flops = 4.0 * Nq * Nkv * hd * B * H;
+  return timed(ctx, cls, flops, 0.0, s, [&] {
+    if (ctx->dtype == STADI_DTYPE_BF16)
+      return tc_attention_bf16((const bf16 *)q, (const bf16 *)kv, (bf16 *)o, Nq, Nkv, B, H, hd,
+                               s);
+    return simt_attention<float>((const float *)q, (const float *)kv, (float *)o, Nq, Nkv, B, H,
+                                 hd, s);
+  });
+}
+
+}  // namespace
+
+#include "unet_exec.cuh"
+
+namespace {
+
 void free_plan_buffers(stadi_ctx *ctx) {
+  unet_free_plan(ctx);
   for (auto &r : ctx->ranks) {
     cudaFree(r.x_band); cudaFree(r.x_res); cudaFree(r.xmod); cudaFree(r.q); cudaFree(r.o);
     cudaFree(r.h1); cudaFree(r.eps_raw);
@@ -401,9 +436,16 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
   if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || dist->n_local < 1 ||
       (dist->world > 1 && dist->n_local != 1) || dist->world * dist->n_local > STADI_MAX_GPUS)
     return fail(nullptr, STADI_EINVAL, "bad dist desc (n_local > 1 requires world == 1)");
-  if (model->dtype == STADI_DTYPE_BF16 && !tc_attention_supported(dm.hd))
-    return fail(nullptr, STADI_EUNSUPPORTED, "head dim %d not supported by the tcgen05 kernel",
-                dm.hd);
+  if (model->dtype == STADI_DTYPE_BF16) {
+    if (!dm.unet && !tc_attention_supported(dm.hd))
+      return fail(nullptr, STADI_EUNSUPPORTED, "head dim %d not supported by the tcgen05 kernel",
+                  dm.hd);
+    for (int l = 0; dm.unet && l < dm.levels(); ++l)
+      if ((dm.tdepth[l] || (l == dm.levels() - 1 && dm.mid_depth)) &&
+          !tc_attention_supported(dm.ch[l] / dm.heads[l]))
+        return fail(nullptr, STADI_EUNSUPPORTED, "head dim %d not supported by the tcgen05 kernel",
+                    dm.ch[l] / dm.heads[l]);
+  }
   auto ctx = std::make_unique<stadi_ctx>();
   ctx->dm = dm;
   ctx->dtype = model->dtype;
@@ -533,6 +575,12 @@ extern "C" stadi_status stadi_load_weights(stadi_ctx *ctx, uint32_t n_tensors,
   if (ctx->weights_loaded) return ctx_fail(ctx, STADI_ESTATE, "weights already loaded");
   const Dims &m = ctx->dm;
   const bool bf = ctx->dtype == STADI_DTYPE_BF16;
+  if (m.unet) {
+    ST(unet_load_weights(ctx, host));
+    CK(cudaDeviceSynchronize());
+    ctx->weights_loaded = true;
+    return STADI_OK;
+  }
   ctx->wT.assign(n_tensors, nullptr);
   ctx->wf.assign(n_tensors, nullptr);
   for (uint32_t i = 0; i < n_tensors; ++i) {
@@ -583,10 +631,12 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
   const Dims &m = ctx->dm;
   if ((int)plan->n_gpus != ctx->G)
     return ctx_fail(ctx, STADI_EINVAL, "plan has %u GPUs, group has %d", plan->n_gpus, ctx->G);
-  if ((int64_t)plan->p_total * plan->rows_per_unit != m.lat_h || plan->rows_per_unit % m.p)
+  const uint32_t unit = m.unet ? (1u << (m.levels() - 1)) : (uint32_t)m.p;
+  if ((int64_t)plan->p_total * plan->rows_per_unit != m.lat_h || plan->rows_per_unit % unit)
     return ctx_fail(ctx, STADI_EINVAL,
-                    "plan covers %u x %u rows; latent has %d rows (unit must be a multiple of p)",
-                    plan->p_total, plan->rows_per_unit, m.lat_h);
+                    "plan covers %u x %u rows; latent has %d rows (unit must be a multiple of "
+                    "%u rows, R6)",
+                    plan->p_total, plan->rows_per_unit, m.lat_h, unit);
   if (plan->m_base > 1000) return ctx_fail(ctx, STADI_EINVAL, "M_base > 1000");
   CK(cudaSetDevice(ctx->device));
   CK(cudaDeviceSynchronize());
@@ -610,6 +660,10 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     stadi_schedule(plan, g, r.sched.data(), n, &n);
     const int64_t M = (int64_t)r.n_tok * m.B;
     CK(cudaMalloc(&r.x_band, std::max<int64_t>(16, (int64_t)r.rows * m.lat_w * m.c_in * 4)));
+    if (m.unet) {  // the U-Net program owns its buffers (unet_set_plan)
+      ctx->ranks.push_back(std::move(r));
+      continue;
+    }
     CK(cudaMalloc(&r.x_res, std::max<int64_t>(16, M * m.d * 4)));
     CK(cudaMalloc(&r.xmod, std::max<int64_t>(16, M * m.d * ctx->esz)));
     CK(cudaMalloc(&r.q, std::max<int64_t>(16, M * m.d * ctx->esz)));
@@ -652,6 +706,7 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     ctx->ev_used.assign(m.depth * 2, 0);
     for (auto &e : ctx->ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  if (m.unet) ST(unet_set_plan(ctx));
   ctx->has_plan = true;
   return STADI_OK;
 }
@@ -679,7 +734,7 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
   const int nt = (int)ctx->plan.m_base;
   const int64_t d = m.d;
   const int B = m.B;
-  if (ctx->cond_cap_nt < (size_t)nt) {
+  if (!m.unet && ctx->cond_cap_nt < (size_t)nt) {
     // (re)allocate per-request conditioning buffers
     for (void *p : {(void *)ctx->mod, (void *)ctx->fmod, (void *)ctx->temb, (void *)ctx->tmp_f,
                     (void *)ctx->tfreq, ctx->csilu})
@@ -694,6 +749,12 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
     ctx->tfreq_nt = 0;
   }
   ctx->n_t = nt;
+  if (m.unet) {
+    ST(unet_begin(ctx, cond, s));
+    ctx->begun = true;
+    ctx->exch_bytes = 0;
+    return STADI_OK;
+  }
   if (ctx->tfreq_nt != nt) {
     // sinusoidal timestep features of the fast grid, fp64 on the host (DiT
     // TimestepEmbedder); depends only on M_base, uploaded once per plan size
@@ -860,15 +921,11 @@ stadi_status wait_version(stadi_ctx *ctx, int l, int ver, cudaStream_t s) {
   return STADI_OK;
 }
 
-#define ST(call)                          \
-  do {                                    \
-    stadi_status s_ = (call);             \
-    if (s_ != STADI_OK) return s_;        \
-  } while (0)
 
 // One program step: patch-local forward of every part in layer lock-step,
 // exchange at every attention site, then the Eq. 3 update of each band.
 stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStream_t s) {
+  if (ctx->dm.unet) return unet_run_phase(ctx, phase, s);
   const Dims &m = ctx->dm;
   const int64_t d = m.d;
   const int B = m.B;
@@ -1070,8 +1127,8 @@ extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, d
   pp.m_base = 10;
   pp.m_warmup = 10;
   pp.a_num = 3; pp.a_den = 4; pp.b_num = 1; pp.b_den = 4;
-  pp.rows_per_unit = m.p;
-  pp.p_total = m.lat_h / m.p;
+  pp.rows_per_unit = m.unet ? (1u << (m.levels() - 1)) : (uint32_t)m.p;
+  pp.p_total = m.lat_h / pp.rows_per_unit;
   pp.flags = STADI_NO_TA | STADI_NO_SA;
   if ((int)pp.p_total < ctx->G) return ctx_fail(ctx, STADI_EINVAL, "latent too small for group");
   stadi_plan_t probe;
@@ -1080,11 +1137,15 @@ extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, d
   ST(stadi_set_plan(ctx, &probe));
   std::vector<float> zeros((size_t)m.lat_h * m.lat_w * m.c_in, 0.f);
   std::vector<int32_t> labels(m.B, 0);
-  std::vector<float> text;
-  stadi_cond cond{labels.data(), nullptr};
+  std::vector<float> text, pooled;
+  stadi_cond cond{labels.data(), nullptr, nullptr, nullptr};
   if (m.text) {
     text.assign((size_t)m.B * m.txt_len * m.txt_dim, 0.f);
     cond.text = text.data();
+  }
+  if (m.add_embed) {
+    pooled.assign((size_t)m.B * m.pooled_dim, 0.f);
+    cond.pooled = pooled.data();
   }
   cudaStream_t s = nullptr;
   ST(stadi_begin(ctx, zeros.data(), &cond, s));

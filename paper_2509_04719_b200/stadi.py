@@ -21,9 +21,9 @@ NO_TA, NO_SA, SIZER_INTERVAL, FORCE_UNITS = 1, 2, 4, 8
 STEP_WARMUP, STEP_UNIFORM, STEP_FAST_EVEN, STEP_FAST_ODD, STEP_SLOW = range(5)
 T_FINAL = -1
 VER_NONE = -1
-PRESET = {"tiny_dit": 0, "dit_xl2": 1, "pixart_alpha": 2}
+PRESET = {"tiny_dit": 0, "dit_xl2": 1, "pixart_alpha": 2, "sd15": 3, "sdxl": 4, "tiny_unet": 5}
 DTYPE_BF16, DTYPE_FP32_DEBUG = 0, 1
-EPI_STORE, EPI_GELU, EPI_GATED_RES, EPI_RES, EPI_QKV, EPI_F32 = range(6)
+EPI_STORE, EPI_GELU, EPI_GATED_RES, EPI_RES, EPI_QKV, EPI_F32, EPI_CONV, EPI_GEGLU = range(8)
 KCLASS = {"gemm": 0, "attn": 1, "xattn": 2, "norm": 3, "sampler": 4}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE",
           6: "EUNSUPPORTED"}
@@ -82,7 +82,8 @@ class DistDesc(C.Structure):
 
 
 class Cond(C.Structure):
-    _fields_ = [("labels", C.POINTER(C.c_int32)), ("text", C.POINTER(C.c_float))]
+    _fields_ = [("labels", C.POINTER(C.c_int32)), ("text", C.POINTER(C.c_float)),
+                ("pooled", C.POINTER(C.c_float)), ("time_ids", C.POINTER(C.c_float))]
 
 
 class RunStats(C.Structure):
@@ -284,24 +285,29 @@ class Context:
 
     @staticmethod
     def _cond(cond):
-        labels = cond.get("labels")
-        text = cond.get("text")
         keep = []
-        lp = tp = None
+
+        def fptr(x):
+            if x is None:
+                return None
+            if hasattr(x, "data_ptr"):   # torch tensor (host, pinned or device)
+                assert x.is_contiguous() and str(x.dtype) == "torch.float32"
+                keep.append(x)
+                return C.cast(C.c_void_p(x.data_ptr()), C.POINTER(C.c_float))
+            a = np.ascontiguousarray(x, dtype=np.float32)
+            keep.append(a)
+            return a.ctypes.data_as(C.POINTER(C.c_float))
+
+        lp = None
+        labels = cond.get("labels")
         if labels is not None:
             la = np.ascontiguousarray(labels, dtype=np.int32)
             keep.append(la)
             lp = la.ctypes.data_as(C.POINTER(C.c_int32))
-        if text is not None:
-            if hasattr(text, "data_ptr"):   # torch tensor (host, pinned or device)
-                assert text.is_contiguous() and str(text.dtype) == "torch.float32"
-                keep.append(text)
-                tp = C.cast(C.c_void_p(text.data_ptr()), C.POINTER(C.c_float))
-            else:
-                ta = np.ascontiguousarray(text, dtype=np.float32)
-                keep.append(ta)
-                tp = ta.ctypes.data_as(C.POINTER(C.c_float))
-        return Cond(lp, tp), keep
+        tid = cond.get("time_ids")
+        if tid is not None and hasattr(tid, "cpu"):
+            tid = tid.cpu().numpy()
+        return Cond(lp, fptr(cond.get("text")), fptr(cond.get("pooled")), fptr(tid)), keep
 
     def begin(self, noise, cond, stream=None):
         c, keep = self._cond(cond)

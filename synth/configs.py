@@ -34,10 +34,10 @@ MODELS = {
     ),
     # tiny U-Net for fast oracle pins / parity (2 levels, SDXL-style add embedding)
     "tiny_unet": dict(
-        family="unet", cond="text", channels=[32, 64], tdepth=[0, 1], mid_depth=1,
+        family="unet", cond="text", channels=[64, 128], tdepth=[0, 1], mid_depth=1,
         heads=None, head_dim=16, layers_per_block=1, c_in=4, c_out=4,
-        latent_h=16, latent_w=16, text_len=8, text_dim=32, add_embed=True,
-        pooled_dim=32, time_ids=[64, 64, 0, 0, 64, 64], guidance=5.0,
+        latent_h=16, latent_w=16, text_len=8, text_dim=64, add_embed=True,
+        pooled_dim=64, time_ids=[64, 64, 0, 0, 64, 64], guidance=5.0,
         schedule="scaled_linear",
     ),
     # C3: SD-1.5 shaped U-Net, 512^2 image -> 64x64 latent, CLIP-L text 77x768

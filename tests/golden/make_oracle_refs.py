@@ -15,10 +15,12 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 os.environ["STADI_WRITE_REFS"] = "1"
 
 import test_gpu_parity as T  # noqa: E402
+import test_gpu_unet as TU  # noqa: E402
 
 if __name__ == "__main__":
-    for case in T.oracle_cases():
-        t0 = time.time()
-        T._oracle(*case)
-        print(f"{case[0]['name']} depth={case[0]['depth']} plan={case[4]['steps']} "
-              f"dtype={case[5]} {time.time() - t0:.1f}s", flush=True)
+    for mod in (T, TU):
+        for case in mod.oracle_cases():
+            t0 = time.time()
+            mod._oracle(*case)
+            print(f"{case[0]['name']} depth={case[0].get('depth')} plan={case[4]['steps']} "
+                  f"rows={case[4]['rows']} dtype={case[5]} {time.time() - t0:.1f}s", flush=True)

@@ -102,11 +102,14 @@ def test_schedule_bit_exact(S):
             assert S.schedule(p, r) == want
 
 
-@pytest.mark.parametrize("name,kw", [("tiny_dit", {}), ("dit_xl2", {}), ("pixart_alpha", {}),
-                                     ("dit_xl2", dict(depth=2)), ("pixart_alpha", dict(depth=3))])
-def test_weight_manifest_matches_synth(S, name, kw):
+@pytest.mark.parametrize("name,kw,depth", [
+    ("tiny_dit", {}, 0), ("dit_xl2", {}, 0), ("pixart_alpha", {}, 0),
+    ("dit_xl2", dict(depth=2), 2), ("pixart_alpha", dict(depth=3), 3),
+    ("tiny_unet", {}, 0), ("sd15", {}, 0), ("sdxl", {}, 0),
+    ("sdxl", dict(tdepth=[0, 1, 1], mid_depth=1), 1), ("sd15", dict(latent_h=32), 0)])
+def test_weight_manifest_matches_synth(S, name, kw, depth):
     cfg = configs.model(name, **kw)
-    desc = S.model_desc(name, depth=kw.get("depth", 0))
+    desc = S.model_desc(name, depth=depth)
     got = S.weight_manifest(desc)
     want = [(n, int(__import__("numpy").prod(shape))) for n, shape, _ in configs.manifest(cfg)]
     assert got == want
