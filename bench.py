@@ -241,9 +241,15 @@ def main():
     ap.add_argument("--no-uniform", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ncu", action="store_true",
+                    help="profiling pass under ncu: 1 untimed request after profiling, no "
+                         "uniform / e2e / cpu legs (its numbers are never bench values)")
     args = ap.parse_args()
+    if args.ncu:
+        args.warmup, args.steps = 0, 1
+        args.no_uniform = args.no_e2e = args.no_cpu_baseline = True
     args.metric = "per-image latency ms & images/s at 1/2/4/8 B200 vs uniform patch-par"
-    assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
+    assert args.warmup >= 3 or args.impl == "reference" or args.ncu, "W >= 3 warm-up steps"
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
