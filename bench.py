@@ -53,6 +53,12 @@ WORKLOADS = {
     "c2": dict(model="dit_xl2", m_base=50, m_warmup=4, name=(
         "C2 DiT-XL/2-shaped 256^2 (32x32x4 latent, 256 tokens, d1152 h16 depth28, "
         "class cond, CFG 4.0), 50 DDIM steps, M_warmup 4")),
+    "c3": dict(model="sd15", m_base=50, m_warmup=4, name=(
+        "C3 SD-1.5-shaped U-Net 512^2 (64x64x4 latent, channels 320/640/1280/1280, 8 heads, "
+        "text 77x768, CFG 7.5), 50 DDIM steps, M_warmup 4")),
+    "c4": dict(model="sdxl", m_base=50, m_warmup=4, name=(
+        "C4 SDXL-shaped U-Net 1024^2 (128x128x4 latent, channels 320/640/1280, transformer "
+        "depth 0/2/10, text 77x2048 + pooled, CFG 5.0), 50 DDIM steps, M_warmup 4")),
 }
 PAPER_CONTEXT = ("paper: up to 45% lower latency than patch parallelism (SDXL 1024^2, "
                  "M_base=100, 2x RTX 4090 over PCIe, occupancy [0,60]%; Table III / L11)")
@@ -71,7 +77,55 @@ def dit_flops(cfg, n_q, n_kv, B):
     return lin + att + xatt
 
 
+def unet_flops(cfg, rows):
+    """Algorithmic FLOPs of one U-Net forward (B = 2) on the full-width latent cut
+    to `rows` rows, attention over the same tokens: conv 2*9*Cin*Cout per output
+    pixel, linear 2*K*N per token, attention 4*n_q*n_kv*C, cross 4*n_q*L*C."""
+    B = configs.batch(cfg)
+    W0, L = cfg["latent_w"], len(cfg["channels"])
+    f = 0.0
+
+    def conv(h, w, cin, cout):
+        return 2.0 * 9 * cin * cout * h * w * B
+
+    def res(h, w, cin, cout):
+        return conv(h, w, cin, cout) + conv(h, w, cout, cout) + \
+            (2.0 * cin * cout * h * w * B if cin != cout else 0.0)
+
+    def tr(h, w, c, depth):
+        n = h * w
+        per = 2.0 * n * B * c * c * (4 + 2 + 8 + 4) + 4.0 * n * n * c * B + \
+            4.0 * n * cfg["text_len"] * c * B
+        return 2.0 * 2 * n * B * c * c + depth * per
+
+    lv = configs.unet_levels(cfg)
+    f += conv(rows, W0, cfg["c_in"], cfg["channels"][0])
+    prev = cfg["channels"][0]
+    for i, (c, att, depth, _) in enumerate(lv):
+        h, w = rows >> i, W0 >> i
+        for j in range(cfg["layers_per_block"]):
+            f += res(h, w, prev if j == 0 else c, c) + (tr(h, w, c, depth) if att else 0.0)
+        if i < L - 1:
+            f += conv(h // 2, w // 2, c, c)
+        prev = c
+    h, w = rows >> (L - 1), W0 >> (L - 1)
+    cm = cfg["channels"][-1]
+    f += 2 * res(h, w, cm, cm) + tr(h, w, cm, cfg["mid_depth"])
+    for i, io in enumerate(configs.unet_up_io(cfg)):
+        l = L - 1 - i
+        c, att, depth, _ = lv[l]
+        h, w = rows >> l, W0 >> l
+        for rin, sk, oc in io:
+            f += res(h, w, rin + sk, oc) + (tr(h, w, oc, depth) if att else 0.0)
+        if i < L - 1:
+            f += conv(2 * h, 2 * w, c, c)
+    f += conv(rows, W0, cfg["channels"][0], cfg["c_out"])
+    return f
+
+
 def image_flops(cfg, m_base):
+    if cfg["family"] == "unet":
+        return m_base * unet_flops(cfg, cfg["latent_h"])
     hp, wp = configs.tokens_hw(cfg)
     n = hp * wp
     B = configs.batch(cfg)
@@ -160,17 +214,28 @@ def oracle_sample(cfg, rows_lat, seconds_hint=None):
     latent cut to `rows_lat` rows, depth 1, ONE sequential DDIM step.  Returns
     (seconds, sample FLOPs, threads)."""
     from oracle import stadi as OR
-    scfg = configs.model(cfg["name"], depth=1, latent_h=rows_lat)
+    if cfg["family"] == "unet":
+        scfg = configs.model(cfg["name"], latent_h=rows_lat)
+        fl = unet_flops(scfg, rows_lat)
+    else:
+        scfg = configs.model(cfg["name"], depth=1, latent_h=rows_lat)
+        hp, wp = configs.tokens_hw(scfg)
+        n = hp * wp
+        fl = dit_flops(scfg, n, n, configs.batch(scfg))
     W = gen.weights(scfg)
     x = gen.noise(scfg)
     c = gen.cond(scfg)
-    hp, wp = configs.tokens_hw(scfg)
-    n = hp * wp
-    fl = dit_flops(scfg, n, n, configs.batch(scfg))
     t0 = time.perf_counter()
     OR.sequential(scfg, W, x, c, 1)
     dt = time.perf_counter() - t0
     return dt, fl, _blas_threads()
+
+
+def _sample_rows(cfg):
+    """Latent rows of the bounded oracle sample: the smallest legal band."""
+    if cfg["family"] == "unet":
+        return configs.rows_per_unit(cfg)
+    return 32 if cfg["latent_h"] >= 32 else cfg["latent_h"]
 
 
 def _blas_threads():
@@ -184,7 +249,7 @@ def _blas_threads():
 
 def cpu_baseline(cfg, wl, target_s=15.0):
     """Oracle throughput on a bounded sample, extrapolated per image by FLOPs."""
-    rows = 32 if cfg["latent_h"] >= 32 else cfg["latent_h"]
+    rows = _sample_rows(cfg)
     total_t, total_f, reps, th = 0.0, 0.0, 0, 1
     while total_t < target_s and reps < 20:
         dt, fl, th = oracle_sample(cfg, rows)
@@ -196,7 +261,8 @@ def cpu_baseline(cfg, wl, target_s=15.0):
     return {"value": 1e3 / ms_img, "unit": "images/s", "ms_per_image": ms_img, "cores": th,
             "kind": "oracle",
             "sample": (f"{reps} x oracle.stadi.sequential on a {rows}x{cfg['latent_w']} latent, "
-                       f"depth 1, 1 DDIM step ({total_t:.1f} s, {total_f / 1e9:.0f} GFLOP fp64); "
+                       f"{'full depth' if cfg['family'] == 'unet' else 'depth 1'}, 1 DDIM step "
+                       f"({total_t:.1f} s, {total_f / 1e9:.0f} GFLOP fp64); "
                        f"per-image latency extrapolated by FLOP count to the full workload "
                        f"({image_flops(cfg, wl['m_base']) / 1e12:.0f} TFLOP/image)")}
 
@@ -205,7 +271,7 @@ def run_reference(args, cfg, wl, rank, world):
     """--impl reference: the oracle, as it stands, on this host's cores."""
     if rank != 0:
         return
-    rows = 32 if cfg["latent_h"] >= 32 else cfg["latent_h"]
+    rows = _sample_rows(cfg)
     for _ in range(args.warmup):
         oracle_sample(cfg, rows)
     ts, fls, th = [], [], 1
@@ -295,7 +361,7 @@ def main():
     del W
     x = gen.noise(cfg)
     c = gen.cond(cfg)
-    p = cfg["patch"]
+    p = configs.rows_per_unit(cfg)          # R6: latent rows per planner unit
     p_total = cfg["latent_h"] // p
 
     # ---- a9 occupancy emulation, a1 profiling, a2/a3 plans
@@ -311,8 +377,7 @@ def main():
     text_dev = None
     cond = dict(c)
     if "text" in c:  # conditioning resident in HBM for the device-timed legs
-        text_dev = torch.from_numpy(c["text"]).cuda()
-        cond = {"text": text_dev}
+        cond = {k: (torch.from_numpy(v).cuda() if k != "time_ids" else v) for k, v in c.items()}
     out_dev = torch.empty_like(noise_dev)
     stream = torch.cuda.current_stream()
 
@@ -359,9 +424,10 @@ def main():
         out_h = torch.empty_like(noise_h).pin_memory()
         cond_h = dict(c)
         if "text" in c:
-            cond_h = {"text": torch.from_numpy(c["text"]).pin_memory()}
+            cond_h = {k: (torch.from_numpy(v).pin_memory() if k != "time_ids" else v)
+                      for k, v in c.items()}
         ems, _ = timed(plan, noise_h, out_h, cond_h, args.steps, 1)
-        h2d = x.nbytes + (c["text"].nbytes if "text" in c else c["labels"].nbytes)
+        h2d = x.nbytes + sum(v.nbytes for v in c.values())
         e2e = {"value": 1e3 / (ems / args.steps), "unit": "images/s",
                "ms_per_image": ems / args.steps, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(x.nbytes)}
@@ -369,20 +435,24 @@ def main():
     if occ[rank]:
         ctx.emulator_stop()
 
-    # ---- roofline of the dominant kernel (self-attention)
+    # ---- roofline of the dominant kernel class (largest share of kernel time)
     peaks = load_peaks()
-    n_att, ms_att, fl_att, _ = kst["attn"]
+    names = {"attn": "tc_attn_kernel (own Q x full stale K/V, tcgen05/TMEM, TMA)",
+             "gemm": "tc_gemm_kernel (tcgen05/TMEM + TMA; linear layers and im2col convs)",
+             "xattn": "tc_attn_kernel (cross-attention to the text tokens)"}
     step_kernel_ms = sum(v[1] for v in kst.values())
+    dom = max(("attn", "gemm", "xattn"), key=lambda k: kst[k][1])
+    n_k, ms_k, fl_k, _ = kst[dom]
     roof = None
-    if n_att:
-        avg_ms = ms_att / n_att
-        ach = fl_att / n_att / (avg_ms * 1e-3) / 1e12
-        roof = {"kernel": "tc_attn_kernel (own Q x full stale K/V, tcgen05/TMEM)", "bound": "tensor",
-                "achieved": ach, "peak": peaks["tflops"], "unit": "TFLOP/s",
-                "frac": ach / peaks["tflops"], "traffic": _traffic("attn"),
+    if n_k:
+        avg_ms = ms_k / n_k
+        ach = fl_k / n_k / (avg_ms * 1e-3) / 1e12
+        roof = {"kernel": names[dom], "class": dom, "bound": "tensor", "achieved": ach,
+                "peak": peaks["tflops"], "unit": "TFLOP/s", "frac": ach / peaks["tflops"],
+                "traffic": _traffic(dom),
                 "peak_src": peaks["src"] + ", bf16 dense sustained",
-                "flops_per_launch": fl_att / n_att, "avg_launch_ms": avg_ms,
-                "launches": n_att, "share_of_kernel_time": ms_att / max(step_kernel_ms, 1e-9)}
+                "flops_per_launch": fl_k / n_k, "avg_launch_ms": avg_ms, "launches": n_k,
+                "share_of_kernel_time": ms_k / max(step_kernel_ms, 1e-9)}
     kernels = {k: {"launches": v[0], "ms": v[1],
                    "tflops": (v[2] / (v[1] * 1e-3) / 1e12) if v[1] and v[2] else None,
                    "gbs": (v[3] / (v[1] * 1e-3) / 1e9) if v[1] and v[3] else None}
@@ -402,8 +472,8 @@ def main():
             "config": {"workload": wl["name"], "n_gpus": world, "occupancy_pct": occ,
                        "speed_q20": [int(s) for s in speed], "profile_ms": ms_prof,
                        "plan": _plan_json(plan),
-                       "l2": "inputs larger than L2: 8.5 GB K/V slots + 1.3 GB bf16 weights "
-                             "streamed per image (126 MB L2)",
+                       "l2": "inputs larger than L2: the K/V slots + bf16 weights streamed per "
+                             "image exceed the 126 MB L2 (C5: 8.5 GB + 1.3 GB)",
                        "parallelism": f"stadi-patch{world}"},
             "uniform_pp": uni, "e2e": e2e, "roofline": roof, "kernels": kernels,
             "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(launches),

@@ -63,6 +63,16 @@ stadi_status stadi_k_ln_modulate(int32_t dtype, const float *x, void *y, int32_t
                                  int32_t B, const float *shift, const float *scale,
                                  int32_t bstride, void *stream);
 
+/* 3x3 convolution (pad 1) of the halo-padded input P [h+2, W+2, B, C] (T; row 0 /
+ * h+1 are the halo rows, columns 0 / W+1 zero) with Wt [N, Kp] (T, column
+ * (ky*3 + kx)*C + c, Kp = 9C rounded up to 64): out[f32] [(oy*Wo + ox)*B + b][N]
+ * = conv + bias.  mode 0 stride 1, 1 stride 2, 2 nearest-x2 upsample of P.
+ * implicit = 1 (BF16, mode 0, C % 64 == 0): the implicit-GEMM tcgen05 kernel (A
+ * tiles TMA-loaded from P); otherwise im2col + GEMM. */
+stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void *Wt, int32_t h, int32_t W,
+                             int32_t B, int32_t C, int32_t N, int32_t mode, int32_t implicit,
+                             const float *bias, float *out, void *stream);
+
 /* Number of kernels launched by this process so far. */
 uint64_t stadi_k_launch_count(void);
 

@@ -77,3 +77,46 @@ extern "C" stadi_status stadi_k_ln_modulate(int32_t dtype, const float *x, void 
 }
 
 extern "C" uint64_t stadi_k_launch_count(void) { return g_launches; }
+
+extern "C" stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void *Wt, int32_t h,
+                                        int32_t W, int32_t B, int32_t C, int32_t N, int32_t mode,
+                                        int32_t implicit, const float *bias, float *out,
+                                        void *stream) {
+  if (!P || !Wt || !out || h <= 0 || W <= 0 || B <= 0 || C <= 0 || N <= 0 || mode < 0 ||
+      mode > 2)
+    return fail(nullptr, STADI_EINVAL, "stadi_k_conv3x3: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int ho = mode == 1 ? h / 2 : (mode == 2 ? 2 * h : h);
+  const int wo = mode == 1 ? W / 2 : (mode == 2 ? 2 * W : W);
+  const int M = ho * wo * B, kp = (9 * C + 63) / 64 * 64;
+  EpiParams ep{};
+  ep.B = B;
+  ep.bias = bias;
+  ep.out = out;
+  ep.ldo = N;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dtype == STADI_DTYPE_BF16 && implicit) {
+    if (mode != 0) return fail(nullptr, STADI_EINVAL, "implicit conv: stride 1 only");
+    return cu(tc_conv3x3_bf16((const bf16 *)P, (const bf16 *)Wt, h, W, B, C, N, EPI_CONV, ep, sms,
+                              s),
+              "tc_conv3x3_bf16");
+  }
+  const size_t esz = dtype == STADI_DTYPE_BF16 ? 2 : 4;
+  void *A = nullptr;
+  cudaError_t e = cudaMallocAsync(&A, (size_t)M * kp * esz, s);
+  if (e != cudaSuccess) return cu(e, "cudaMallocAsync");
+  if (dtype == STADI_DTYPE_BF16) {
+    e = im2col<bf16>((const bf16 *)P, h, W, B, C, mode, kp, (bf16 *)A, s);
+    if (e == cudaSuccess) e = tc_gemm_bf16((const bf16 *)A, (const bf16 *)Wt, M, N, kp, EPI_CONV,
+                                           ep, sms, s);
+  } else {
+    e = im2col<float>((const float *)P, h, W, B, C, mode, kp, (float *)A, s);
+    if (e == cudaSuccess) e = simt_gemm<float>((const float *)A, (const float *)Wt, M, N, kp,
+                                               EPI_CONV, ep, s);
+  }
+  cudaFreeAsync(A, s);
+  return cu(e, "conv3x3");
+}
+

@@ -20,6 +20,10 @@ cudaError_t simt_gemm(const T *A, const T *W, int M, int N, int K, int epi, cons
 // N % 64 == 0.  max_ctas bounds the grid (SMs not pinned by the emulator).
 cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
                          const EpiParams &ep, int max_ctas, cudaStream_t s);
+// Implicit-GEMM 3x3 conv, stride 1, from the halo-padded input P [h+2, W+2, B, C]
+// (C % 64 == 0, W*B a divisor or multiple of 128); epi EPI_CONV or EPI_F32.
+cudaError_t tc_conv3x3_bf16(const bf16 *P, const bf16 *Wt, int h, int W, int B, int C, int N,
+                            int epi, const EpiParams &ep, int max_ctas, cudaStream_t s);
 
 // ---- attention  o = softmax(q k^T / sqrt(hd)) v  per (batch b, head h) ------
 // q, o: [Nq * B, H*hd] (row = token*B + b);  kv: [Nkv, B, 2, H*hd] (K then V).

@@ -18,6 +18,8 @@
 //    epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cuda.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "../kernels.h"
@@ -101,10 +103,24 @@ __device__ __forceinline__ void epi_pair(const EpiParams &p, int row, int col, f
   }
 }
 
-template <int BN, int EPI>
+// MC = 2: CTA pairs (a 2-CTA cluster) work on vertically adjacent 128-row tiles
+// of the same BN columns; each CTA TMA-loads its own A tile and HALF of the W
+// tile, multicast into both CTAs' smem, so the L2 -> SM traffic per MMA drops
+// from (128 + BN) to (128 + BN / 2) rows.  Each MMA commit frees the stage in
+// both CTAs (empty barriers count 2).
+// Implicit 3x3 convolution (AM == 1): the A operand is not materialised; for
+// K block kb = (tap, 64-channel chunk) the producer TMA-loads the 128 output
+// rows' input pixels shifted by the tap straight from the halo-padded NHWC
+// buffer P [h+2, W+2, B, C] with a 3-D box (64 ch, min(W B, 128) pixel-batch
+// rows, 128 / (W B) image rows): exactly the K-major 128B-swizzled A tile.
+struct ConvGeo {
+  int W, B, C;  // band width, batch, input channels (C % 64 == 0)
+};
+
+template <int BN, int EPI, int MC, int AM>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   int M, int N, int K, EpiParams ep) {
+                   int M, int N, int K, EpiParams ep, ConvGeo cg) {
   using C = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -119,15 +135,22 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_n = N / BN, tiles_m = (M + GBM - 1) / GBM;
-  const int n_tiles = tiles_m * tiles_n;
   const int nkb = K / GBK;
+  // tile walk: MC tiles (one per cluster CTA) per work item, N fastest
+  const int crank = MC == 2 ? (int)cluster_ctarank() : 0;
+  const int n_items = ((tiles_m + MC - 1) / MC) * tiles_n;
+  const int item0 = blockIdx.x / MC, item_step = gridDim.x / MC;
+  auto tile_of = [&](int item, int *mb, int *nb) {
+    *mb = (item / tiles_n) * MC + crank;
+    *nb = item % tiles_n;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -138,6 +161,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  if (MC == 2) cluster_sync();  // partner's barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -145,13 +169,25 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {  // ---------------- TMA producer
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int mb = tile / tiles_n, nb = tile % tiles_n;
+      for (int item = item0; item < n_items; item += item_step) {
+        int mb, nb;
+        tile_of(item, &mb, &nb);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], C::STAGE);
-          tma_load_2d(&tmA, sA + s * C::A_BYTES, &full[s], kb * GBK, mb * GBM);
-          tma_load_2d(&tmB, sB + s * C::B_BYTES, &full[s], kb * GBK, nb * BN);
+          if constexpr (AM == 1) {
+            const int cpb = cg.C / GBK, tap = kb / cpb, c0 = (kb % cpb) * GBK;
+            const int p0 = mb * (GBM / cg.B);  // first output pixel of the tile
+            tma_load_3d(&tmA, sA + s * C::A_BYTES, &full[s], c0,
+                        (p0 % cg.W + tap % 3) * cg.B, p0 / cg.W + tap / 3);
+          } else {
+            tma_load_2d(&tmA, sA + s * C::A_BYTES, &full[s], kb * GBK, mb * GBM);
+          }
+          if constexpr (MC == 2)
+            tma_load_2d_mc(&tmB, sB + s * C::B_BYTES + crank * (C::B_BYTES / 2), &full[s],
+                           kb * GBK, nb * BN + crank * (BN / 2), (uint16_t)0x3);
+          else
+            tma_load_2d(&tmB, sB + s * C::B_BYTES, &full[s], kb * GBK, nb * BN);
           if (++s == C::STAGES) {
             s = 0;
             ph ^= 1;
@@ -165,7 +201,7 @@ __global__ void __launch_bounds__(192, 1)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      for (int item = item0; item < n_items; item += item_step, ++it) {
         const int acc = it & 1;
         const uint32_t aph = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
@@ -182,7 +218,8 @@ __global__ void __launch_bounds__(192, 1)
             const uint64_t bd = umma_desc(b0 + k * 32, 16, 1024, SWZ_128B);
             umma_bf16(dtm, ad, bd, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty[s]);
+          if constexpr (MC == 2) umma_commit_mc(&empty[s], (uint16_t)0x3);
+          else umma_commit(&empty[s]);
           if (++s == C::STAGES) {
             s = 0;
             ph ^= 1;
@@ -194,8 +231,9 @@ __global__ void __launch_bounds__(192, 1)
   } else {  // ---------------------------- epilogue warps 2..5
     const int qd = warp & 3;  // TMEM lane quarter this warp may access
     int it = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
-      const int mb = tile / tiles_n, nb = tile % tiles_n;
+    for (int item = item0; item < n_items; item += item_step, ++it) {
+      int mb, nb;
+      tile_of(item, &mb, &nb);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
@@ -231,6 +269,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (MC == 2) cluster_sync();  // no CTA leaves while its partner may still signal it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
@@ -278,60 +317,96 @@ bool make_tmap(CUtensorMap *m, const void *base, int rank, const uint64_t *dims,
 }
 
 namespace {
-template <int BN, int EPI>
+template <int BN, int EPI, int MC, int AM>
 cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const EpiParams &ep,
-                        int max_ctas, cudaStream_t s) {
+                        int max_ctas, const ConvGeo &cg, int conv_h, cudaStream_t s) {
   using C = GemmCfg<BN>;
   CUtensorMap ta, tb;
-  const uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
-  const uint32_t ba[2] = {GBK, GBM};
+  bool ok;
+  if constexpr (AM == 1) {  // P [h+2, (W+2) B, C]
+    const int wb = cg.W * cg.B;
+    const uint64_t da[3] = {(uint64_t)cg.C, (uint64_t)(cg.W + 2) * cg.B, (uint64_t)conv_h + 2};
+    const uint64_t sa[2] = {(uint64_t)cg.C * 2, (uint64_t)(cg.W + 2) * cg.B * cg.C * 2};
+    const uint32_t ba[3] = {GBK, (uint32_t)std::min(wb, GBM), (uint32_t)std::max(1, GBM / wb)};
+    ok = make_tmap(&ta, A, 3, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else {
+    const uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
+    const uint32_t ba[2] = {GBK, GBM};
+    ok = make_tmap(&ta, A, 2, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
   const uint64_t db[2] = {(uint64_t)K, (uint64_t)N}, sb[1] = {(uint64_t)K * 2};
-  const uint32_t bb[2] = {GBK, (uint32_t)BN};
-  if (!make_tmap(&ta, A, 2, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_tmap(&tb, W, 2, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B))
+  const uint32_t bb[2] = {GBK, (uint32_t)(BN / MC)};
+  if (!ok || !make_tmap(&tb, W, 2, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   static bool attr_set = false;  // per template instance
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, EPI>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, EPI, MC, AM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((M + GBM - 1) / GBM) * (N / BN);
-  const int grid = tiles < max_ctas ? tiles : max_ctas;
-  tc_gemm_kernel<BN, EPI><<<grid, 192, C::SMEM, s>>>(ta, tb, M, N, K, ep);
+  const int items = ((M + GBM - 1) / GBM + MC - 1) / MC * (N / BN);
+  int grid = std::min(items * MC, max_ctas / MC * MC);
+  if (grid < MC) grid = MC;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = MC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, EPI, MC, AM>, ta, tb, M, N, K, ep,
+                                     cg);
   ++g_launches;
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-template <int BN>
+template <int BN, int MC>
 cudaError_t dispatch_epi(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
                          const EpiParams &ep, int max_ctas, cudaStream_t s) {
+  const ConvGeo g{0, 0, 0};
   switch (epi) {
-    case EPI_STORE: return launch_gemm<BN, EPI_STORE>(A, W, M, N, K, ep, max_ctas, s);
-    case EPI_GELU: return launch_gemm<BN, EPI_GELU>(A, W, M, N, K, ep, max_ctas, s);
-    case EPI_GATED_RES: return launch_gemm<BN, EPI_GATED_RES>(A, W, M, N, K, ep, max_ctas, s);
-    case EPI_RES: return launch_gemm<BN, EPI_RES>(A, W, M, N, K, ep, max_ctas, s);
-    case EPI_QKV: return launch_gemm<BN, EPI_QKV>(A, W, M, N, K, ep, max_ctas, s);
-    case EPI_F32: return launch_gemm<BN, EPI_F32>(A, W, M, N, K, ep, max_ctas, s);
-    case EPI_CONV: return launch_gemm<BN, EPI_CONV>(A, W, M, N, K, ep, max_ctas, s);
-    case EPI_GEGLU: return launch_gemm<BN, EPI_GEGLU>(A, W, M, N, K, ep, max_ctas, s);
+    case EPI_STORE: return launch_gemm<BN, EPI_STORE, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
+    case EPI_GELU: return launch_gemm<BN, EPI_GELU, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
+    case EPI_GATED_RES:
+      return launch_gemm<BN, EPI_GATED_RES, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
+    case EPI_RES: return launch_gemm<BN, EPI_RES, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
+    case EPI_QKV: return launch_gemm<BN, EPI_QKV, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
+    case EPI_F32: return launch_gemm<BN, EPI_F32, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
+    case EPI_CONV: return launch_gemm<BN, EPI_CONV, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
+    case EPI_GEGLU: return launch_gemm<BN, EPI_GEGLU, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
   }
+  return cudaErrorInvalidValue;
+}
+template <int BN>
+cudaError_t dispatch_mc(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
+                        const EpiParams &ep, int max_ctas, int mc, cudaStream_t s) {
+  if (mc == 2) return dispatch_epi<BN, 2>(A, W, M, N, K, epi, ep, max_ctas, s);
+  return dispatch_epi<BN, 1>(A, W, M, N, K, epi, ep, max_ctas, s);
+}
+template <int BN, int MC>
+cudaError_t dispatch_conv(const bf16 *P, const bf16 *W, int h, const ConvGeo &g, int N, int epi,
+                          const EpiParams &ep, int max_ctas, cudaStream_t s) {
+  const int M = h * g.W * g.B, K = 9 * g.C;
+  if (epi == EPI_CONV)
+    return launch_gemm<BN, EPI_CONV, MC, 1>(P, W, M, N, K, ep, max_ctas, g, h, s);
+  if (epi == EPI_F32)
+    return launch_gemm<BN, EPI_F32, MC, 1>(P, W, M, N, K, ep, max_ctas, g, h, s);
   return cudaErrorInvalidValue;
 }
 }  // namespace
 
-cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
-                         const EpiParams &ep, int max_ctas, cudaStream_t s) {
-  if (M <= 0) return cudaSuccess;
-  if (K % GBK || N % 64 || max_ctas < 1) return cudaErrorInvalidValue;
-  if (reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(W) % 16)
-    return cudaErrorInvalidValue;
-  // Pick the N tile that minimises (waves x tile width), preferring wider tiles.
+// N tile that minimises (waves x tile width), preferring wider tiles.
+int pick_bn(int tm, int N, int max_ctas) {
   const int cands[4] = {256, 192, 128, 64};
   int best = 64;
   long best_cost = -1;
-  const int tm = (M + GBM - 1) / GBM;
   for (int bn : cands) {
     if (N % bn) continue;
     const long tiles = (long)tm * (N / bn);
@@ -342,12 +417,59 @@ cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int 
       best = bn;
     }
   }
+  return best;
+}
+
+// STADI_GEMM_MC=0 in the environment forces single-CTA tiles (A/B comparisons).
+bool gemm_mc_disabled() {
+  static const int v = [] {
+    const char *e = getenv("STADI_GEMM_MC");
+    return (e && e[0] == '0') ? 1 : 0;
+  }();
+  return v != 0;
+}
+
+cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
+                         const EpiParams &ep, int max_ctas, cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  if (K % GBK || N % 64 || max_ctas < 1) return cudaErrorInvalidValue;
+  if (reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(W) % 16)
+    return cudaErrorInvalidValue;
+  const int tm = (M + GBM - 1) / GBM;
+  const int best = pick_bn(tm, N, max_ctas);
+  // CTA pairs with a multicast W tile once there are enough row tiles to pair
+  const int mc = (tm >= 4 && max_ctas >= 2 && !gemm_mc_disabled()) ? 2 : 1;
   switch (best) {
-    case 256: return dispatch_epi<256>(A, W, M, N, K, epi, ep, max_ctas, s);
-    case 192: return dispatch_epi<192>(A, W, M, N, K, epi, ep, max_ctas, s);
-    case 128: return dispatch_epi<128>(A, W, M, N, K, epi, ep, max_ctas, s);
-    default: return dispatch_epi<64>(A, W, M, N, K, epi, ep, max_ctas, s);
+    case 256: return dispatch_mc<256>(A, W, M, N, K, epi, ep, max_ctas, mc, s);
+    case 192: return dispatch_mc<192>(A, W, M, N, K, epi, ep, max_ctas, mc, s);
+    case 128: return dispatch_mc<128>(A, W, M, N, K, epi, ep, max_ctas, mc, s);
+    default: return dispatch_mc<64>(A, W, M, N, K, epi, ep, max_ctas, mc, s);
   }
+}
+
+// Implicit-GEMM 3x3 conv (stride 1): out = epi(conv(P) . W^T) with P the
+// halo-padded input [h+2, W+2, B, C] and W [N, 9C] (column (ky*3 + kx)*C + c).
+cudaError_t tc_conv3x3_bf16(const bf16 *P, const bf16 *Wt, int h, int W, int B, int C, int N,
+                            int epi, const EpiParams &ep, int max_ctas, cudaStream_t s) {
+  if (h <= 0) return cudaSuccess;
+  const int wb = W * B;
+  if (C % GBK || N % 64 || max_ctas < 1 || (wb % GBM && GBM % wb)) return cudaErrorInvalidValue;
+  const ConvGeo g{W, B, C};
+  const int M = h * wb, tm = (M + GBM - 1) / GBM;
+  const int best = pick_bn(tm, N, max_ctas);
+  const int mc = (tm >= 4 && max_ctas >= 2 && !gemm_mc_disabled()) ? 2 : 1;
+#define STADI_CONV_CASE(BNV)                                                          \
+  case BNV:                                                                           \
+    return mc == 2 ? dispatch_conv<BNV, 2>(P, Wt, h, g, N, epi, ep, max_ctas, s)      \
+                   : dispatch_conv<BNV, 1>(P, Wt, h, g, N, epi, ep, max_ctas, s);
+  switch (best) {
+    STADI_CONV_CASE(256)
+    STADI_CONV_CASE(192)
+    STADI_CONV_CASE(128)
+    default: return mc == 2 ? dispatch_conv<64, 2>(P, Wt, h, g, N, epi, ep, max_ctas, s)
+                            : dispatch_conv<64, 1>(P, Wt, h, g, N, epi, ep, max_ctas, s);
+  }
+#undef STADI_CONV_CASE
 }
 
 }  // namespace stadi

@@ -66,6 +66,15 @@ struct UNetState {
 
 inline int64_t rup64(int64_t a) { return (a + 63) / 64 * 64; }
 
+// STADI_CONV_IMPLICIT=0 forces the im2col path (A/B comparisons).
+bool conv_implicit_disabled() {
+  static const int v = [] {
+    const char *e = getenv("STADI_CONV_IMPLICIT");
+    return (e && e[0] == '0') ? 1 : 0;
+  }();
+  return v != 0;
+}
+
 // ------------------------------------------------------------------ weights
 __global__ void temb_combine_kernel(const float *temb, const float *aug, int nt, int B, int td,
                                     float *out) {  // out[m*B + b] = temb[m] + aug[b]
@@ -415,8 +424,11 @@ struct UBuilder {
     const int64_t Mo = (int64_t)rows(lo) * width(lo) * B;
     const int64_t kp = rup64(9 * C);
     const int ncols = ldo ? ldo : cout;
+    const int wb = W * B;
+    const bool implicit = ctx->dtype == STADI_DTYPE_BF16 && mode == 0 && C % 64 == 0 &&
+                          (wb % 128 == 0 || 128 % wb == 0) && !conv_implicit_disabled();
     need(UB_PAD, (size_t)(h + 2) * (W + 2) * B * C * esz);
-    need(UB_COL, (size_t)(Mo * kp) * esz);
+    if (!implicit) need(UB_COL, (size_t)(Mo * kp) * esz);
     need(out, (size_t)(Mo * ncols) * 4);
     auto D = P(UB_PAD), A = P(UB_COL), O = P(out);
     std::function<void *()> Rs = res >= 0 ? P(res) : std::function<void *()>();
@@ -468,10 +480,6 @@ struct UBuilder {
                          (size_t)B * C * ctx->esz, s));
       CK(cudaMemsetAsync((char *)D() + ((size_t)(h + 1) * (W + 2) + W + 1) * B * C * ctx->esz,
                          0, (size_t)B * C * ctx->esz, s));
-      if (ctx->dtype == STADI_DTYPE_BF16)
-        CK(im2col<bf16>((const bf16 *)D(), h, W, B, C, mode, (int)kp, (bf16 *)A(), s));
-      else
-        CK(im2col<float>((const float *)D(), h, W, B, C, mode, (int)kp, (float *)A(), s));
       EpiParams ep{};
       ep.B = B;
       ep.bias = bias;
@@ -485,6 +493,17 @@ struct UBuilder {
         ep.gate = U->temb_all + (int64_t)st.m * B * U->temb_total + toff;
         ep.gate_bstride = U->temb_total;
       }
+      if (implicit) {  // tcgen05 implicit GEMM straight from the padded input
+        CK(timed(ctx, STADI_KCLASS_GEMM, 2.0 * Mo * ncols * kp, 0.0, s, [&] {
+          return tc_conv3x3_bf16((const bf16 *)D(), (const bf16 *)wt, h, W, B, C, ncols, epi, ep,
+                                 std::max(1, ctx->num_sms - ctx->emu_ctas), s);
+        }));
+        return STADI_OK;
+      }
+      if (ctx->dtype == STADI_DTYPE_BF16)
+        CK(im2col<bf16>((const bf16 *)D(), h, W, B, C, mode, (int)kp, (bf16 *)A(), s));
+      else
+        CK(im2col<float>((const float *)D(), h, W, B, C, mode, (int)kp, (float *)A(), s));
       CK(gemm(ctx, A(), wt, (int)Mo, ncols, (int)kp, epi, ep, s));
       return STADI_OK;
     });

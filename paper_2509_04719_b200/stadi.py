@@ -107,7 +107,8 @@ EXPORTS = [
     "stadi_num_steps", "stadi_denoise_step", "stadi_gather", "stadi_run",
     "stadi_emulator_start", "stadi_emulator_stop", "stadi_nccl_unique_id",
     "stadi_kernel_timing", "stadi_kernel_stats",
-    "stadi_k_gemm", "stadi_k_attention", "stadi_k_ln_modulate", "stadi_k_launch_count",
+    "stadi_k_gemm", "stadi_k_attention", "stadi_k_ln_modulate", "stadi_k_conv3x3",
+    "stadi_k_launch_count",
 ]
 
 
@@ -151,6 +152,8 @@ def _load():
                                         C.c_int32, C.c_int32, vp]),
         "stadi_k_ln_modulate": (C.c_int, [C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp,
                                           vp, C.c_int32, vp]),
+        "stadi_k_conv3x3": (C.c_int, [C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]),
         "stadi_k_launch_count": (C.c_uint64, []),
     }
     for name, (res, args) in sig.items():
@@ -365,6 +368,11 @@ def k_attention(dtype, q, kv, o, Nq, Nkv, B, H, hd, stream=None):
 def k_ln_modulate(dtype, x, y, M, d, B, shift, scale, bstride, stream=None):
     _check(lib.stadi_k_ln_modulate(dtype, ptr(x), ptr(y), M, d, B, ptr(shift), ptr(scale),
                                    bstride, stream_ptr(stream)))
+
+
+def k_conv3x3(dtype, P, Wt, h, W, B, C_, N, mode, implicit, bias, out, stream=None):
+    _check(lib.stadi_k_conv3x3(dtype, ptr(P), ptr(Wt), h, W, B, C_, N, mode, implicit, ptr(bias),
+                               ptr(out), stream_ptr(stream)))
 
 
 def launch_count() -> int:

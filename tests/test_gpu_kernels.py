@@ -229,3 +229,49 @@ def test_bad_shapes_rejected(S):
     q = torch.zeros(128, 48, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(S.StadiError):
         S.k_attention(0, q, q, q, 128, 64, 1, 1, 48)                      # hd 48 unsupported
+
+
+CONV_CASES = [  # h, W, B, C, N, mode, implicit
+    (4, 64, 2, 64, 64, 0, 1), (3, 32, 2, 128, 192, 0, 1), (5, 16, 2, 64, 128, 0, 1),
+    (2, 128, 2, 320, 320, 0, 1), (7, 8, 2, 64, 64, 0, 1), (1, 64, 1, 64, 256, 0, 1),
+    (4, 16, 2, 64, 128, 1, 0), (3, 8, 2, 64, 64, 2, 0), (6, 12, 2, 4, 64, 0, 0),
+]
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["bf16", "fp32"])
+@pytest.mark.parametrize("h,W,B,C,N,mode,implicit", CONV_CASES)
+def test_conv3x3(S, dtype, h, W, B, C, N, mode, implicit):
+    """3x3 conv from the halo-padded token-major buffer vs the oracle's conv
+    (oracle/unet.py conv3x3_valid on the same padded, upsampled input)."""
+    from oracle import unet as OU
+    rng = np.random.default_rng(h * 100 + W + C + mode)
+    P = rng.standard_normal((h + 2, W + 2, B, C)).astype(np.float32)
+    P[:, 0] = 0
+    P[:, -1] = 0
+    w = (rng.standard_normal((N, C, 3, 3)) / np.sqrt(9 * C)).astype(np.float32)
+    bias = (rng.standard_normal(N) * 0.1).astype(np.float32)
+    kp = (9 * C + 63) // 64 * 64
+    wt = np.zeros((N, kp), np.float32)
+    wt[:, :9 * C] = w.transpose(0, 2, 3, 1).reshape(N, 9 * C)
+    mk = _bf if dtype == 0 else _f32
+    tP, nP = mk(P)
+    tW, nW = mk(wt)
+    nw = nW[:, :9 * C].reshape(N, 3, 3, C).transpose(0, 3, 1, 2)
+    tb = torch.from_numpy(bias).cuda()
+    ho = h // 2 if mode == 1 else (2 * h if mode == 2 else h)
+    wo = W // 2 if mode == 1 else (2 * W if mode == 2 else W)
+    out = torch.full((ho * wo * B, N), float("nan"), device="cuda")
+    S.k_conv3x3(dtype, tP, tW, h, W, B, C, N, mode, implicit if dtype == 0 else 0, tb, out)
+    torch.cuda.synchronize()
+    x = nP.transpose(2, 0, 1, 3)                       # [B, h+2, W+2, C]
+    if mode == 2:   # nearest x2 of the interior, halo rows stay pre-upsample rows
+        inner = x[:, 1:-1, 1:-1].repeat(2, axis=1).repeat(2, axis=2)
+        top = x[:, :1, 1:-1].repeat(2, axis=2)
+        bot = x[:, -1:, 1:-1].repeat(2, axis=2)
+        x = OU.pad_cols(np.concatenate([top, inner, bot], axis=1))
+    if mode == 1:
+        x = x[:, :-1]
+    ref = OU.conv3x3_valid(x, nw, bias.astype(np.float64), 2 if mode == 1 else 1)
+    got = out.cpu().numpy().reshape(ho, wo, B, N).transpose(2, 0, 1, 3)
+    assert np.all(np.isfinite(got))
+    assert _rel(got, ref) < (1e-2 if dtype == 0 else 1e-5)
