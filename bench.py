@@ -334,7 +334,11 @@ def main():
     assert torch.cuda.is_available(), "bench.py needs a CUDA device"
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # control plane only (barriers, the ncclUniqueId broadcast, max-over-ranks):
+        # gloo on the host, because ProcessGroupNCCL's barrier synchronises the whole
+        # device, which never returns while an occupancy-emulator kernel is resident.
+        # The data path is the library's own NCCL communicator over NVLink.
+        dist.init_process_group("gloo")
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
 
     def barrier():
@@ -344,7 +348,7 @@ def main():
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -381,21 +385,28 @@ def main():
     out_dev = torch.empty_like(noise_dev)
     stream = torch.cuda.current_stream()
 
+    # NOTE: stream synchronisation, not torch.cuda.synchronize(): on the ranks with
+    # emulated occupancy a persistent spin kernel stays resident on the device for
+    # the whole run, so a device-wide sync would never return.  Every kernel of a
+    # request runs on `stream` (and the library's comm stream, which joins it).
+    def sync():
+        stream.synchronize()
+
     def timed(pl, noise, out, cnd, k, w, ktime=False):
         for _ in range(w):
             ctx.run(pl, noise, cnd, out, stream=stream)
-        torch.cuda.synchronize()
+        sync()
         l0 = S.launch_count()
         if ktime:
             ctx.kernel_timing(True)
         barrier()
-        torch.cuda.synchronize()
+        sync()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(k):
             ctx.run(pl, noise, cnd, out, stream=stream)
         e1.record(stream)
-        torch.cuda.synchronize()
+        sync()
         barrier()
         ms = e0.elapsed_time(e1)
         launches = S.launch_count() - l0

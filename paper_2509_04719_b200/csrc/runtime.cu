@@ -142,6 +142,9 @@ struct stadi_ctx {
 
   // streams / NCCL
   cudaStream_t comm = nullptr;
+  cudaStream_t astream = nullptr;      // stream-ordered plan / request allocations
+  cudaStream_t last_stream = nullptr;  // last stream denoise_step / run enqueued on
+  bool last_stream_set = false;
   ncclComm_t world_comm = nullptr, sub_comm = nullptr;
   std::vector<cudaEvent_t> ev_done;  // [depth*2] exchange completion per (site, parity)
   std::vector<char> ev_used;
@@ -211,6 +214,32 @@ stadi_status ctx_fail(stadi_ctx *c, stadi_status st, const char *fmt, ...) {
     stadi_status s_ = (call);             \
     if (s_ != STADI_OK) return s_;        \
   } while (0)
+
+// Plan- and request-lifetime device memory is stream-ordered (cudaMallocAsync /
+// cudaFreeAsync on the context's allocation stream): re-planning never implies a
+// device-wide synchronisation.  That matters because the occupancy emulator
+// (a9) keeps a persistent kernel resident — cudaFree / cudaDeviceSynchronize
+// would wait for it forever.
+template <typename P>
+cudaError_t pmalloc(stadi_ctx *ctx, P **p, size_t bytes) {
+  void *q = nullptr;
+  cudaError_t e = cudaMallocAsync(&q, bytes ? bytes : 16, ctx->astream);
+  *p = reinterpret_cast<P *>(q);
+  return e;
+}
+inline void pfree(stadi_ctx *ctx, void *p) {
+  if (p) cudaFreeAsync(p, ctx->astream);
+}
+// Wait for everything this context enqueued (its streams and the caller's last
+// stream) without a device-wide synchronisation.
+cudaError_t quiesce(stadi_ctx *ctx) {
+  cudaError_t e = cudaSuccess;
+  if (ctx->last_stream_set) e = cudaStreamSynchronize(ctx->last_stream);
+  if (e == cudaSuccess && ctx->comm) e = cudaStreamSynchronize(ctx->comm);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  if (e == cudaSuccess && ctx->astream) e = cudaStreamSynchronize(ctx->astream);
+  return e;
+}
 
 template <typename P>
 cudaError_t dalloc(stadi_ctx *ctx, P **p, size_t bytes) {
@@ -362,9 +391,9 @@ namespace {
 void free_plan_buffers(stadi_ctx *ctx) {
   unet_free_plan(ctx);
   for (auto &r : ctx->ranks) {
-    cudaFree(r.x_band); cudaFree(r.x_res); cudaFree(r.xmod); cudaFree(r.q); cudaFree(r.o);
-    cudaFree(r.h1); cudaFree(r.eps_raw);
-    for (void *p : r.kv) cudaFree(p);
+    for (void *p : {(void *)r.x_band, (void *)r.x_res, r.xmod, r.q, r.o, r.h1, (void *)r.eps_raw})
+      pfree(ctx, p);
+    for (void *p : r.kv) pfree(ctx, p);
   }
   ctx->ranks.clear();
   ctx->program.clear();
@@ -466,6 +495,7 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
     int lo, hi;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi));
+    CK(cudaStreamCreateWithFlags(&ctx->astream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
     // positional embedding of the full token grid, fp64 on the host (pins the
     // values to 1 ulp of fp32), [sin(c w), cos(c w), sin(r w), cos(r w)]
@@ -514,6 +544,7 @@ extern "C" void stadi_destroy(stadi_ctx *ctx) {
   for (float *p : ctx->wf) cudaFree(p);
   if (ctx->world_comm && nccl().CommDestroy) nccl().CommDestroy(ctx->world_comm);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
+  if (ctx->astream) cudaStreamDestroy(ctx->astream);
   if (ctx->emu_stream) cudaStreamDestroy(ctx->emu_stream);
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
   for (auto &k : ctx->kt)
@@ -577,7 +608,7 @@ extern "C" stadi_status stadi_load_weights(stadi_ctx *ctx, uint32_t n_tensors,
   const bool bf = ctx->dtype == STADI_DTYPE_BF16;
   if (m.unet) {
     ST(unet_load_weights(ctx, host));
-    CK(cudaDeviceSynchronize());
+    CK(cudaStreamSynchronize(0));
     ctx->weights_loaded = true;
     return STADI_OK;
   }
@@ -619,7 +650,7 @@ extern "C" stadi_status stadi_load_weights(stadi_ctx *ctx, uint32_t n_tensors,
   CK(dalloc(ctx, &ctx->final_b, ctx->fin_ld * 4));
   CK(cudaMemset(ctx->final_b, 0, ctx->fin_ld * 4));
   CK(cudaMemcpy(ctx->final_b, WF(ctx, "final.linear.b"), nf * 4, cudaMemcpyDeviceToDevice));
-  CK(cudaDeviceSynchronize());
+  CK(cudaStreamSynchronize(0));
   ctx->weights_loaded = true;
   return STADI_OK;
 }
@@ -639,7 +670,7 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
                     plan->p_total, plan->rows_per_unit, m.lat_h, unit);
   if (plan->m_base > 1000) return ctx_fail(ctx, STADI_EINVAL, "M_base > 1000");
   CK(cudaSetDevice(ctx->device));
-  CK(cudaDeviceSynchronize());
+  CK(quiesce(ctx));
   free_plan_buffers(ctx);
   ctx->plan = *plan;
   const int g0 = ctx->rank * ctx->n_local;
@@ -659,22 +690,24 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     r.sched.resize(n);
     stadi_schedule(plan, g, r.sched.data(), n, &n);
     const int64_t M = (int64_t)r.n_tok * m.B;
-    CK(cudaMalloc(&r.x_band, std::max<int64_t>(16, (int64_t)r.rows * m.lat_w * m.c_in * 4)));
+    CK(pmalloc(ctx, &r.x_band, std::max<int64_t>(16, (int64_t)r.rows * m.lat_w * m.c_in * 4)));
     if (m.unet) {  // the U-Net program owns its buffers (unet_set_plan)
       ctx->ranks.push_back(std::move(r));
       continue;
     }
-    CK(cudaMalloc(&r.x_res, std::max<int64_t>(16, M * m.d * 4)));
-    CK(cudaMalloc(&r.xmod, std::max<int64_t>(16, M * m.d * ctx->esz)));
-    CK(cudaMalloc(&r.q, std::max<int64_t>(16, M * m.d * ctx->esz)));
-    CK(cudaMalloc(&r.o, std::max<int64_t>(16, M * m.d * ctx->esz)));
-    CK(cudaMalloc(&r.h1, std::max<int64_t>(16, M * 4 * m.d * ctx->esz)));
-    CK(cudaMalloc(&r.eps_raw, std::max<int64_t>(16, M * ctx->fin_ld * 4)));
+    CK(pmalloc(ctx, &r.x_res, std::max<int64_t>(16, M * m.d * 4)));
+    CK(pmalloc(ctx, &r.xmod, std::max<int64_t>(16, M * m.d * ctx->esz)));
+    CK(pmalloc(ctx, &r.q, std::max<int64_t>(16, M * m.d * ctx->esz)));
+    CK(pmalloc(ctx, &r.o, std::max<int64_t>(16, M * m.d * ctx->esz)));
+    CK(pmalloc(ctx, &r.h1, std::max<int64_t>(16, M * 4 * m.d * ctx->esz)));
+    CK(pmalloc(ctx, &r.eps_raw, std::max<int64_t>(16, M * ctx->fin_ld * 4)));
     r.kv.assign(m.depth * 2, nullptr);
+    CK(cudaStreamSynchronize(ctx->astream));
     for (auto &p : r.kv) {
-      CK(cudaMalloc(&p, slot_elems(m) * ctx->esz));
-      CK(cudaMemset(p, 0, slot_elems(m) * ctx->esz));
+      CK(pmalloc(ctx, &p, slot_elems(m) * ctx->esz));
+      CK(cudaMemsetAsync(p, 0, slot_elems(m) * ctx->esz, ctx->astream));
     }
+    CK(cudaStreamSynchronize(ctx->astream));
     ctx->ranks.push_back(std::move(r));
   }
   // program
@@ -736,15 +769,17 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
   const int B = m.B;
   if (!m.unet && ctx->cond_cap_nt < (size_t)nt) {
     // (re)allocate per-request conditioning buffers
+    CK(quiesce(ctx));
     for (void *p : {(void *)ctx->mod, (void *)ctx->fmod, (void *)ctx->temb, (void *)ctx->tmp_f,
                     (void *)ctx->tfreq, ctx->csilu})
-      cudaFree(p);
-    CK(cudaMalloc(&ctx->mod, (size_t)nt * B * m.depth * 6 * d * 4));
-    CK(cudaMalloc(&ctx->fmod, (size_t)nt * B * 2 * d * 4));
-    CK(cudaMalloc(&ctx->temb, (size_t)nt * d * 4));
-    CK(cudaMalloc(&ctx->tmp_f, (size_t)nt * 6 * d * 4));
-    CK(cudaMalloc(&ctx->tfreq, (size_t)nt * 256 * 4));
-    CK(cudaMalloc(&ctx->csilu, (size_t)nt * B * d * ctx->esz));
+      pfree(ctx, p);
+    CK(pmalloc(ctx, &ctx->mod, (size_t)nt * B * m.depth * 6 * d * 4));
+    CK(pmalloc(ctx, &ctx->fmod, (size_t)nt * B * 2 * d * 4));
+    CK(pmalloc(ctx, &ctx->temb, (size_t)nt * d * 4));
+    CK(pmalloc(ctx, &ctx->tmp_f, (size_t)nt * 6 * d * 4));
+    CK(pmalloc(ctx, &ctx->tfreq, (size_t)nt * 256 * 4));
+    CK(pmalloc(ctx, &ctx->csilu, (size_t)nt * B * d * ctx->esz));
+    CK(cudaStreamSynchronize(ctx->astream));
     ctx->cond_cap_nt = nt;
     ctx->tfreq_nt = 0;
   }
@@ -1034,6 +1069,8 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
 
 extern "C" stadi_status stadi_denoise_step(stadi_ctx *ctx, uint32_t step, void *stream) {
   ALIVE();
+  ctx->last_stream = (cudaStream_t)stream;
+  ctx->last_stream_set = true;
   if (!ctx->begun) return ctx_fail(ctx, STADI_ESTATE, "stadi_denoise_step before stadi_begin");
   if (step >= ctx->program.size()) return ctx_fail(ctx, STADI_EINVAL, "step out of range");
   CK(cudaSetDevice(ctx->device));
@@ -1086,6 +1123,8 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
   if (!ctx->has_plan || std::memcmp(plan, &ctx->plan, sizeof(stadi_plan_t)) != 0)
     ST(stadi_set_plan(ctx, plan));
   cudaStream_t s = (cudaStream_t)stream;
+  ctx->last_stream = s;
+  ctx->last_stream_set = true;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -1176,13 +1215,14 @@ extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, d
     for (size_t li = 0; li < ctx->ranks.size(); ++li) all[ctx->ranks[li].g] = ms_local[li];
   } else {
     double *dsend = nullptr, *drecv = nullptr;
-    CK(cudaMalloc(&dsend, 8));
-    CK(cudaMalloc(&drecv, 8 * ctx->G));
+    CK(pmalloc(ctx, &dsend, 8));
+    CK(pmalloc(ctx, &drecv, 8 * ctx->G));
+    CK(cudaStreamSynchronize(ctx->astream));
     CK(cudaMemcpy(dsend, ms_local.data(), 8, cudaMemcpyHostToDevice));
     CKN(nccl().AllGather(dsend, drecv, 1, ncclFloat64, ctx->world_comm, s));
     CK(cudaMemcpy(all.data(), drecv, 8 * ctx->G, cudaMemcpyDeviceToHost));
-    cudaFree(dsend);
-    cudaFree(drecv);
+    pfree(ctx, dsend);
+    pfree(ctx, drecv);
   }
   double mn = all[0];
   for (double x : all) mn = std::min(mn, x);
@@ -1222,7 +1262,7 @@ extern "C" stadi_status stadi_emulator_stop(stadi_ctx *ctx) {
 extern "C" stadi_status stadi_kernel_timing(stadi_ctx *ctx, int32_t enable) {
   ALIVE();
   CK(cudaSetDevice(ctx->device));
-  CK(cudaDeviceSynchronize());
+  CK(quiesce(ctx));
   for (auto &k : ctx->kt) {
     k.used = 0;
     k.launches = 0;
@@ -1238,7 +1278,7 @@ extern "C" stadi_status stadi_kernel_stats(stadi_ctx *ctx, int32_t kclass, uint6
   if (kclass < 0 || kclass >= STADI_KCLASS_COUNT)
     return ctx_fail(ctx, STADI_EINVAL, "unknown kernel class %d", kclass);
   CK(cudaSetDevice(ctx->device));
-  CK(cudaDeviceSynchronize());
+  CK(quiesce(ctx));
   CK(collect_timing(ctx));
   const auto &k = ctx->kt[kclass];
   if (launches) *launches = k.launches;

@@ -112,8 +112,8 @@ cudaError_t upload_gemm(stadi_ctx *ctx, const std::vector<float> &h, void **dst)
     bf16 *t = nullptr;
     e = dalloc(ctx, &t, h.size() * 2);
     if (e == cudaSuccess) e = cast_f32<bf16>(f, t, (long)h.size(), 0);
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    cudaFree(f);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    cudaFreeAsync(f, 0);
     *dst = t;
     return e;
   }
@@ -444,16 +444,18 @@ struct UBuilder {
       USite &S = ctx->un->sites[sid];
       const int pos = inc_pos(ctx->un.get(), ctx->ranks[me].g);
       if (st.pub_ver != st.read_ver) ST(u_wait(ctx, S, st.read_ver, s));
+      if (st.pub_ver < 0) return STADI_OK;
+      // own boundary rows -> own segment of the publish slot (the consumer reads
+      // only the neighbours' rows, so the read slot needs no own copy).  The last
+      // send from this parity (version pub - 2) completed before the read wait of
+      // the previous round (or of the previous fresh step).
       const size_t rb = (size_t)rowe * ctx->esz;
       const char *first = (const char *)D() + ((size_t)1 * (W + 2) + 1) * B * C * ctx->esz;
       const char *last = (const char *)D() + ((size_t)h * (W + 2) + 1) * B * C * ctx->esz;
-      for (int par : {st.read_ver & 1, st.pub_ver & 1}) {
-        if (par == (st.pub_ver & 1) && (st.pub_ver < 0 || st.pub_ver == st.read_ver)) continue;
-        char *sg = (char *)S.slot[me][par] + pos * S.seg_bytes;
-        CK(cudaMemcpyAsync(sg, first, rb, cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(sg + rb, last, rb, cudaMemcpyDeviceToDevice, s));
-      }
-      if (st.pub_ver >= 0) ST(u_publish(ctx, S, me, st.pub_ver, s));
+      char *sg = (char *)S.slot[me][st.pub_ver & 1] + pos * S.seg_bytes;
+      CK(cudaMemcpyAsync(sg, first, rb, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(sg + rb, last, rb, cudaMemcpyDeviceToDevice, s));
+      ST(u_publish(ctx, S, me, st.pub_ver, s));
       return STADI_OK;
     });
     op([=](const stadi_step_t &st, cudaStream_t s) -> stadi_status {  // consume + conv
@@ -786,11 +788,11 @@ void unet_free_plan(stadi_ctx *ctx) {
   UNetState *U = ctx->un.get();
   if (!U) return;
   for (auto &R : U->ranks)
-    for (void *p : R.buf) cudaFree(p);
+    for (void *p : R.buf) pfree(ctx, p);
   for (auto &S : U->sites) {
     for (auto &pr : S.slot) {
-      cudaFree(pr[0]);
-      cudaFree(pr[1]);
+      pfree(ctx, pr[0]);
+      pfree(ctx, pr[1]);
     }
     for (auto e : S.ev)
       if (e) cudaEventDestroy(e);
@@ -814,8 +816,8 @@ stadi_status unet_set_plan(stadi_ctx *ctx) {
   for (auto &R : U->ranks)
     for (size_t i = 0; i < R.size.size(); ++i)
       if (R.size[i]) {
-        CK(cudaMalloc(&R.buf[i], R.size[i]));
-        CK(cudaMemset(R.buf[i], 0, R.size[i]));
+        CK(pmalloc(ctx, &R.buf[i], R.size[i]));
+        CK(cudaMemsetAsync(R.buf[i], 0, R.size[i], ctx->astream));
       }
   const int n_inc = (int)U->inc.size();
   for (auto &S : U->sites) {
@@ -825,12 +827,13 @@ stadi_status unet_set_plan(stadi_ctx *ctx) {
     S.slot.assign(ctx->ranks.size(), {nullptr, nullptr});
     for (auto &pr : S.slot)
       for (int par = 0; par < 2; ++par) {
-        CK(cudaMalloc(&pr[par], std::max<int64_t>(bytes, 16)));
-        CK(cudaMemset(pr[par], 0, std::max<int64_t>(bytes, 16)));
+        CK(pmalloc(ctx, &pr[par], std::max<int64_t>(bytes, 16)));
+        CK(cudaMemsetAsync(pr[par], 0, std::max<int64_t>(bytes, 16), ctx->astream));
       }
     if (ctx->world > 1)
       for (auto &e : S.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  CK(cudaStreamSynchronize(ctx->astream));
   return STADI_OK;
 }
 
@@ -845,15 +848,17 @@ stadi_status unet_begin(stadi_ctx *ctx, const stadi_cond *cond, cudaStream_t s) 
   if (m.add_embed && !cond->pooled)
     return ctx_fail(ctx, STADI_EINVAL, "conditioning missing (pooled text embedding)");
   if (U->cap_nt < nt) {
+    CK(quiesce(ctx));
     for (void *p : {(void *)U->tfeat, (void *)U->t1, (void *)U->temb, (void *)U->tembB,
                     (void *)U->temb_all, U->tsilu})
-      cudaFree(p);
-    CK(cudaMalloc(&U->tfeat, (size_t)nt * C0 * 4));
-    CK(cudaMalloc(&U->t1, (size_t)nt * td * 4));
-    CK(cudaMalloc(&U->temb, (size_t)nt * td * 4));
-    CK(cudaMalloc(&U->tembB, (size_t)nt * B * td * 4));
-    CK(cudaMalloc(&U->tsilu, (size_t)nt * B * td * ctx->esz));
-    CK(cudaMalloc(&U->temb_all, (size_t)nt * B * U->temb_total * 4));
+      pfree(ctx, p);
+    CK(pmalloc(ctx, &U->tfeat, (size_t)nt * C0 * 4));
+    CK(pmalloc(ctx, &U->t1, (size_t)nt * td * 4));
+    CK(pmalloc(ctx, &U->temb, (size_t)nt * td * 4));
+    CK(pmalloc(ctx, &U->tembB, (size_t)nt * B * td * 4));
+    CK(pmalloc(ctx, &U->tsilu, (size_t)nt * B * td * ctx->esz));
+    CK(pmalloc(ctx, &U->temb_all, (size_t)nt * B * U->temb_total * 4));
+    CK(cudaStreamSynchronize(ctx->astream));
     U->cap_nt = nt;
     ctx->tfreq_nt = 0;
   }
