@@ -16,7 +16,8 @@
 //                 bf16).  Order per key tile j: PV_0(j), S_0(j+1), PV_1(j),
 //                 S_1(j+1) — while softmax group 0 works on S_0(j+1) the
 //                 tensor core runs PV_1(j) and S_1(j+1), and vice versa.
-//   warps 4..    softmax group g (4 warps, one query row per thread = TMEM
+//   warps 2..    softmax group g (warps 2+4g .. 5+4g; warp w owns TMEM lanes
+//                 32 (w % 4) .. +31, so each group covers all 128; one query row per thread = TMEM
 //                 lane): S row -> registers (all loads in flight, one wait),
 //                 row max, LAZY rescale (O and l are rescaled in TMEM only
 //                 when the running max grows by more than 2^8; otherwise the
@@ -25,6 +26,8 @@
 //                 Epilogue: O / l -> bf16 global.
 // O accumulates in TMEM across all key tiles: no per-tile correction pass.
 #include <cuda.h>
+
+#include <cstdlib>
 
 #include "../kernels.h"
 
@@ -44,6 +47,55 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Blackwell 3-input max (FMNMX3) and packed fp32x2 FMA / add (FFMA2 / FADD2)
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t pack_f32x2(float a, float b) {
+  uint64_t u;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(u) : "f"(a), "f"(b));
+  return u;
+}
+__device__ __forceinline__ void unpack_f32x2(uint64_t u, float &a, float &b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(u));
+}
+__device__ __forceinline__ uint64_t ffma_f32x2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t add_f32x2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for a pair on the FMA / ALU pipes instead of MUFU (FA4's trick to relieve
+// the 16 op/clk/SM exp unit): n = rint(x) via the 1.5 * 2^23 magic add,
+// f = x - n in [-0.5, 0.5], 2^f by a degree-3 fit (max rel. err 7.5e-5, far
+// below the bf16 rounding of P), 2^n added into the exponent field.  x is
+// clamped at -125 (2^-125 instead of 0: negligible against a row sum >= 1).
+__device__ __forceinline__ void ex2_poly_x2(uint64_t xx, float &p0, float &p1) {
+  float x0, x1;
+  unpack_f32x2(xx, x0, x1);
+  xx = pack_f32x2(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+  const float MAGIC = 12582912.f;
+  const uint64_t t = add_f32x2(xx, pack_f32x2(MAGIC, MAGIC));
+  const uint64_t nf = add_f32x2(t, pack_f32x2(-MAGIC, -MAGIC));
+  const uint64_t f = ffma_f32x2(nf, pack_f32x2(-1.f, -1.f), xx);
+  uint64_t q = ffma_f32x2(f, pack_f32x2(0.05517161168f, 0.05517161168f),
+                          pack_f32x2(0.24261117048f, 0.24261117048f));
+  q = ffma_f32x2(q, f, pack_f32x2(0.69326100063f, 0.69326100063f));
+  q = ffma_f32x2(q, f, pack_f32x2(0.99992807098f, 0.99992807098f));
+  float q0, q1, t0, t1;
+  unpack_f32x2(q, q0, q1);
+  unpack_f32x2(t, t0, t1);
+  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
+}
+// Of every 8 column pairs, POLY (a kernel template parameter) use the
+// polynomial exp2, the rest MUFU ex2.
 
 // Head-dim chunking: N64 chunks of 64, then optionally one of 32, one of 16.
 template <int N64, int N32, int N16, int NQT_>
@@ -68,7 +120,7 @@ struct AttnCfg {
   static constexpr int OFF_V = OFF_K + STAGES * TILE;
   static constexpr int OFF_BAR = OFF_V + STAGES * TILE;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int THREADS = 128 + 128 * NQT;
+  static constexpr int THREADS = 64 + 128 * NQT;
   // TMEM columns: S_g at 128 g, O_g at 256 + 128 g (HDP <= 128 when NQT == 2)
   __host__ __device__ static constexpr uint32_t s_col(int g) { return 128u * g; }
   __host__ __device__ static constexpr uint32_t o_col(int g) {
@@ -97,7 +149,7 @@ __device__ __forceinline__ void tmem_row_store(uint32_t taddr, const float *v) {
   if constexpr (N % 32) tmem_st16(taddr + (N - 16), r + (N - 16));
 }
 
-template <int N64, int N32, int N16, int NQT>
+template <int N64, int N32, int N16, int NQT, int POLY>
 __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
     tc_attn_kernel(const __grid_constant__ CUtensorMap tq64, const __grid_constant__ CUtensorMap tq32,
                    const __grid_constant__ CUtensorMap tq16, const __grid_constant__ CUtensorMap tk64,
@@ -254,8 +306,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         }
       }
     }
-  } else if (warp >= 4) {  // ------------------------------------ softmax groups
-    const int g = (warp - 4) / 4;
+  } else {  // ------------------------------------------------------ softmax groups
+    const int g = (warp - 2) / 4;
     const int qd = warp & 3;
     const int r = qd * 32 + lane;  // query row within the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
@@ -265,17 +317,29 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(&s_full[g], j & 1);
       tc_fence_after();
-      float v[AK];
-      tmem_row_load<AK>(st_addr, v);
-      const int valid = Nkv - j * AK;  // columns >= valid are padding
+      const int valid = Nkv - j * AK;  // columns >= valid are padding (last tile only)
+      // pass 1: row max, 64 columns in flight, four independent FMNMX3 chains
       float mt = -INFINITY;
-      if (valid >= AK) {
 #pragma unroll
-        for (int c = 0; c < AK; ++c) mt = fmaxf(mt, v[c]);
-      } else {
+      for (int h = 0; h < AK; h += 64) {
+        float v[64];
+        tmem_ld32_nowait(st_addr + h, reinterpret_cast<uint32_t *>(v));
+        tmem_ld32_nowait(st_addr + h + 32, reinterpret_cast<uint32_t *>(v) + 32);
+        tmem_ld_wait();
+        if (valid < AK) {
 #pragma unroll
-        for (int c = 0; c < AK; ++c)
-          if (c < valid) mt = fmaxf(mt, v[c]);
+          for (int c = 0; c < 64; ++c)
+            if (h + c >= valid) v[c] = -INFINITY;
+        }
+        float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 64; c += 8) {
+          a0 = fmax3(a0, v[c], v[c + 1]);
+          a1 = fmax3(a1, v[c + 2], v[c + 3]);
+          a2 = fmax3(a2, v[c + 4], v[c + 5]);
+          a3 = fmax3(a3, v[c + 6], v[c + 7]);
+        }
+        mt = fmax3(mt, fmaxf(a0, a1), fmaxf(a2, a3));
       }
       mt *= scale_log2;
       // lazy rescale: move the reference max only when it grows by > 2^8
@@ -300,22 +364,48 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         }
       }
       l *= factor;
-      float rs = 0.f;
+      // P = 2^(s * scale - m): packed FFMA2, MUFU ex2, FADD2 row sums in four
+      // independent pairs, bf16x2 packs stored over S in TMEM
+      const uint64_t sc2 = pack_f32x2(scale_log2, scale_log2), nm2 = pack_f32x2(-m_run, -m_run);
+      uint64_t acc[4] = {0, 0, 0, 0};
+      // pass 2: S re-read from TMEM 32 columns at a time (TMEM reads are cheap;
+      // keeps the register footprint low); P overwrites S columns already consumed
 #pragma unroll
-      for (int c0 = 0; c0 < AK; c0 += 32) {  // P = 2^(s - m) as packed bf16 over S
+      for (int c0 = 0; c0 < AK; c0 += 32) {
+        float v[32];
+        tmem_ld32_nowait(st_addr + c0, reinterpret_cast<uint32_t *>(v));
+        tmem_ld_wait();
+        if (valid < AK) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (c0 + c >= valid) v[c] = -INFINITY;
+        }
         uint32_t pk[16];
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
-          const float p0 = (c0 + c < valid) ? ex2(fmaf(v[c0 + c], scale_log2, -m_run)) : 0.f;
-          const float p1 =
-              (c0 + c + 1 < valid) ? ex2(fmaf(v[c0 + c + 1], scale_log2, -m_run)) : 0.f;
-          rs += p0 + p1;
+          const uint64_t xx = ffma_f32x2(pack_f32x2(v[c], v[c + 1]), sc2, nm2);
+          float p0, p1;
+          if ((c / 2) % 8 < POLY) {
+            ex2_poly_x2(xx, p0, p1);
+          } else {
+            float x0, x1;
+            unpack_f32x2(xx, x0, x1);
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          const uint64_t pp = pack_f32x2(p0, p1);
+          acc[(c / 2) & 3] = add_f32x2(acc[(c / 2) & 3], pp);
           __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
           pk[c / 2] = *reinterpret_cast<uint32_t *>(&t2);
         }
         tmem_st16(st_addr + c0 / 2, pk);
       }
-      l += rs;
+      {
+        const uint64_t t = add_f32x2(add_f32x2(acc[0], acc[1]), add_f32x2(acc[2], acc[3]));
+        float r0, r1;
+        unpack_f32x2(t, r0, r1);
+        l += r0 + r1;
+      }
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[g]);
@@ -358,8 +448,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
   }
 }
 
-template <int N64, int N32, int N16, int NQT>
-cudaError_t launch_attn(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B, int H,
+template <int N64, int N32, int N16, int NQT, int POLY>
+cudaError_t launch_attn_p(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B, int H,
                         int hd, cudaStream_t s) {
   using C = AttnCfg<N64, N32, N16, NQT>;
   const int d = H * hd;
@@ -383,17 +473,39 @@ cudaError_t launch_attn(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv,
   if (!ok) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_attn_kernel<N64, N32, N16, NQT>,
+    cudaError_t e = cudaFuncSetAttribute(tc_attn_kernel<N64, N32, N16, NQT, POLY>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   dim3 grid((Nq + AQ * NQT - 1) / (AQ * NQT), H, B);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-  tc_attn_kernel<N64, N32, N16, NQT><<<grid, C::THREADS, C::SMEM, s>>>(
+  tc_attn_kernel<N64, N32, N16, NQT, POLY><<<grid, C::THREADS, C::SMEM, s>>>(
       tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], o, Nq, Nkv, B, H, hd, scale_log2);
   ++g_launches;
   return cudaGetLastError();
+}
+
+// STADI_ATTN_POLY=k (0..4): k of every 8 column pairs take the polynomial exp2
+// (default 3); for A/B measurements of the MUFU / FMA balance.
+int attn_poly() {
+  static const int v = [] {
+    const char *e = getenv("STADI_ATTN_POLY");
+    const int k = e ? atoi(e) : 3;
+    return k < 0 ? 0 : (k > 4 ? 4 : k);
+  }();
+  return v;
+}
+template <int N64, int N32, int N16, int NQT>
+cudaError_t launch_attn(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B, int H,
+                        int hd, cudaStream_t s) {
+  switch (attn_poly()) {
+    case 0: return launch_attn_p<N64, N32, N16, NQT, 0>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 1: return launch_attn_p<N64, N32, N16, NQT, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 2: return launch_attn_p<N64, N32, N16, NQT, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 4: return launch_attn_p<N64, N32, N16, NQT, 4>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    default: return launch_attn_p<N64, N32, N16, NQT, 3>(q, kv, o, Nq, Nkv, B, H, hd, s);
+  }
 }
 
 }  // namespace

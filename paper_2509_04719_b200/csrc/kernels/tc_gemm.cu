@@ -44,49 +44,69 @@ struct GemmCfg {
 };
 
 // Epilogue of two adjacent columns (col even) of one row, vectorised stores.
+// Split in two so a warp can issue the global reads of all its rows first (the
+// residual of RES / GATED_RES / CONV is read-modify-write in HBM: issuing the 16
+// loads of a chunk back to back hides their latency behind each other).
+struct EpiIn {
+  float2 r;  // residual (the only operand streamed from HBM)
+};
 template <int EPI>
-__device__ __forceinline__ void epi_pair(const EpiParams &p, int row, int col, float v0, float v1) {
-  if (p.bias) {
-    const float2 b = *reinterpret_cast<const float2 *>(p.bias + col);
-    v0 += b.x;
-    v1 += b.y;
+__device__ __forceinline__ EpiIn epi_load(const EpiParams &p, int row, int col) {
+  EpiIn in;
+  in.r = make_float2(0.f, 0.f);
+  if constexpr (EPI == EPI_GATED_RES || EPI == EPI_RES || EPI == EPI_CONV) {
+    if (p.res) in.r = *reinterpret_cast<const float2 *>(p.res + (long)row * p.ldr + col);
   }
+  return in;
+}
+// Per-chunk constants of a lane's column pair: bias and the B (<= 2) gate rows,
+// loaded once per 32-column chunk instead of once per row.
+struct EpiCol {
+  float2 b, g[2];
+};
+template <int EPI>
+__device__ __forceinline__ EpiCol epi_col(const EpiParams &p, int col) {
+  EpiCol c;
+  c.b = p.bias ? *reinterpret_cast<const float2 *>(p.bias + col) : make_float2(0.f, 0.f);
+  c.g[0] = c.g[1] = make_float2(0.f, 0.f);
+  if constexpr (EPI == EPI_GATED_RES || EPI == EPI_CONV) {
+    if (p.gate)
+      for (int b = 0; b < p.B && b < 2; ++b)
+        c.g[b] = *reinterpret_cast<const float2 *>(p.gate + b * p.gate_bstride + col);
+  }
+  return c;
+}
+__device__ __forceinline__ float gelu_tanh_fast(float x) {  // MUFU.TANH
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+  return 0.5f * x * (1.f + t);
+}
+template <int EPI>
+__device__ __forceinline__ void epi_finish(const EpiParams &p, int row, int col, float v0,
+                                           float v1, const EpiIn &in, const EpiCol &cc) {
+  v0 += cc.b.x;
+  v1 += cc.b.y;
+  const float2 g = cc.g[(row % p.B) & 1];
   if constexpr (EPI == EPI_STORE || EPI == EPI_GELU) {
     if (EPI == EPI_GELU) {
-      v0 = gelu_tanh(v0);
-      v1 = gelu_tanh(v1);
+      v0 = gelu_tanh_fast(v0);
+      v1 = gelu_tanh_fast(v1);
     }
     *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<bf16 *>(p.out) + (long)row * p.ldo +
                                         col) = __floats2bfloat162_rn(v0, v1);
   } else if constexpr (EPI == EPI_F32 || EPI == EPI_CONV) {
     if constexpr (EPI == EPI_CONV) {
-      if (p.gate) {
-        const float2 g = *reinterpret_cast<const float2 *>(p.gate + (row % p.B) * p.gate_bstride +
-                                                           col);
-        v0 += g.x;
-        v1 += g.y;
-      }
-      if (p.res) {
-        const float2 r = *reinterpret_cast<const float2 *>(p.res + (long)row * p.ldr + col);
-        v0 += r.x;
-        v1 += r.y;
-      }
+      v0 += g.x + in.r.x;
+      v1 += g.y + in.r.y;
     }
     *reinterpret_cast<float2 *>(reinterpret_cast<float *>(p.out) + (long)row * p.ldo + col) =
         make_float2(v0, v1);
-  } else if constexpr (EPI == EPI_GATED_RES || EPI == EPI_RES) {
-    float2 *r = reinterpret_cast<float2 *>(p.res + (long)row * p.ldr + col);
-    float2 a = *r;
-    if constexpr (EPI == EPI_GATED_RES) {
-      const float2 g =
-          *reinterpret_cast<const float2 *>(p.gate + (row % p.B) * p.gate_bstride + col);
-      a.x += g.x * v0;
-      a.y += g.y * v1;
-    } else {
-      a.x += v0;
-      a.y += v1;
-    }
-    *r = a;
+  } else if constexpr (EPI == EPI_GATED_RES) {
+    *reinterpret_cast<float2 *>(p.res + (long)row * p.ldr + col) =
+        make_float2(in.r.x + g.x * v0, in.r.y + g.y * v1);
+  } else if constexpr (EPI == EPI_RES) {
+    *reinterpret_cast<float2 *>(p.res + (long)row * p.ldr + col) =
+        make_float2(in.r.x + v0, in.r.y + v1);
   } else if constexpr (EPI == EPI_GEGLU) {
     reinterpret_cast<bf16 *>(p.out)[(long)row * p.ldo + col / 2] =
         __float2bfloat16_rn(v0 * gelu_erf(v1));
@@ -103,11 +123,6 @@ __device__ __forceinline__ void epi_pair(const EpiParams &p, int row, int col, f
   }
 }
 
-// MC = 2: CTA pairs (a 2-CTA cluster) work on vertically adjacent 128-row tiles
-// of the same BN columns; each CTA TMA-loads its own A tile and HALF of the W
-// tile, multicast into both CTAs' smem, so the L2 -> SM traffic per MMA drops
-// from (128 + BN) to (128 + BN / 2) rows.  Each MMA commit frees the stage in
-// both CTAs (empty barriers count 2).
 // Implicit 3x3 convolution (AM == 1): the A operand is not materialised; for
 // K block kb = (tap, 64-channel chunk) the producer TMA-loads the 128 output
 // rows' input pixels shifted by the tap straight from the halo-padded NHWC
@@ -255,13 +270,20 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) stg[lane * EPI_LD + i] = v[i];
         __syncwarp();
-        const int cc = 2 * (lane & 15);
-#pragma unroll 4
+        const int cc = 2 * (lane & 15), col = nb * BN + c0 + cc;
+        const EpiCol ecol = epi_col<EPI>(ep, col);
+        EpiIn in[16];
+#pragma unroll
+        for (int it = 0; it < 16; ++it) {  // all global reads of the chunk in flight
+          const int row = row0 + 2 * it + (lane >> 4);
+          if (row < M) in[it] = epi_load<EPI>(ep, row, col);
+        }
+#pragma unroll
         for (int it = 0; it < 16; ++it) {
           const int r = 2 * it + (lane >> 4);
           if (row0 + r < M)
-            epi_pair<EPI>(ep, row0 + r, nb * BN + c0 + cc, stg[r * EPI_LD + cc],
-                          stg[r * EPI_LD + cc + 1]);
+            epi_finish<EPI>(ep, row0 + r, col, stg[r * EPI_LD + cc], stg[r * EPI_LD + cc + 1],
+                            in[it], ecol);
         }
         __syncwarp();
       }

@@ -1,0 +1,64 @@
+"""Kernel micro-bench (CUDA events, warm, inputs > L2): C5-shaped attention and
+GEMMs through the kernel-level C ABI.  Prints TFLOP/s per case."""
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2509_04719_b200 import stadi as S  # noqa: E402
+
+
+def timeit(fn, reps=10):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def attn(Nq, Nkv, B, H, hd):
+    d = H * hd
+    q = torch.randn(Nq * B, d, device="cuda").to(torch.bfloat16)
+    kv = torch.randn(Nkv * B * 2, d, device="cuda").to(torch.bfloat16)
+    o = torch.empty(Nq * B, d, device="cuda", dtype=torch.bfloat16)
+    ms = timeit(lambda: S.k_attention(0, q, kv, o, Nq, Nkv, B, H, hd))
+    fl = 4.0 * Nq * Nkv * hd * B * H
+    print(f"attn Nq={Nq} Nkv={Nkv} B={B} H={H} hd={hd}: {ms:.3f} ms  {fl / ms / 1e9:.0f} TFLOP/s")
+
+
+def gemm(M, N, K, epi):
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    bias = torch.zeros(N, device="cuda")
+    kw = dict(bias=bias, B=2)
+    if epi in (S.EPI_STORE, S.EPI_GELU):
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        kw.update(out=out, ldo=N)
+    elif epi in (S.EPI_RES, S.EPI_GATED_RES):
+        res = torch.zeros(M, N, device="cuda")
+        gate = torch.ones(2, N, device="cuda")
+        kw.update(res=res, ldr=N, gate=gate, gate_bstride=N)
+    else:
+        out = torch.empty(M, N, device="cuda")
+        kw.update(out=out, ldo=N)
+    ms = timeit(lambda: S.k_gemm(0, A, W, M, N, K, epi, **kw))
+    print(f"gemm M={M} N={N} K={K} epi={epi}: {ms:.3f} ms  {2.0 * M * N * K / ms / 1e9:.0f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    attn(16384, 16384, 2, 16, 72)
+    attn(8192, 16384, 2, 16, 72)
+    attn(4096, 4096, 2, 10, 64)
+    attn(4096, 4096, 2, 8, 40)
+    for M, N, K, e in [(32768, 3456, 1152, S.EPI_QKV if False else S.EPI_STORE),
+                       (32768, 1152, 1152, S.EPI_GATED_RES), (32768, 1152, 1152, S.EPI_RES),
+                       (32768, 4608, 1152, S.EPI_GELU), (32768, 1152, 4608, S.EPI_GATED_RES),
+                       (8192, 8192, 8192, S.EPI_STORE), (32768, 3456, 1152, S.EPI_F32)]:
+        gemm(M, N, K, e)
