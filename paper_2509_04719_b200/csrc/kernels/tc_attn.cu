@@ -119,8 +119,14 @@ struct AttnCfg {
   static constexpr int OFF_K = NQT * TILE;
   static constexpr int OFF_V = OFF_K + STAGES * TILE;
   static constexpr int OFF_BAR = OFF_V + STAGES * TILE;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int THREADS = 64 + 128 * NQT;
+  // SPLIT threads share a query row (each owns AK / SPLIT key columns); they
+  // exchange partial row maxima / sums through RED [2 parities][2 groups][SPLIT][128]
+  static constexpr int SPLIT = 2;
+  static constexpr int CW = AK / SPLIT;
+  static constexpr int OFF_RED = OFF_BAR + 256;
+  static constexpr int RED_BYTES = 2 * 2 * SPLIT * 128 * 4;
+  static constexpr int SMEM = OFF_RED + RED_BYTES + 1024;
+  static constexpr int THREADS = 64 + 128 * SPLIT * NQT;
   // TMEM columns: S_g at 128 g, O_g at 256 + 128 g (HDP <= 128 when NQT == 2)
   __host__ __device__ static constexpr uint32_t s_col(int g) { return 128u * g; }
   __host__ __device__ static constexpr uint32_t o_col(int g) {
@@ -129,6 +135,7 @@ struct AttnCfg {
   static_assert(NQT == 1 || HDP <= 128, "two query tiles need HDP <= 128");
   static_assert(NQT == 2 || HDP <= 384, "HDP too large");
   static_assert(STAGES >= 2, "smem");
+  static_assert(SMEM <= 227 * 1024, "smem");
 };
 
 // Load columns [c0, c0 + 16 * n) of this lane's TMEM row into v (fp32).
@@ -169,7 +176,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
   uint64_t *s_full = v_empty + C::STAGES;  // [NQT]
   uint64_t *p_full = s_full + 2;           // [NQT]
   uint64_t *o_done = p_full + 2;           // [NQT]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_done + 2);
+  uint64_t *tok = o_done + 2;              // [2] softmax ping-pong tokens
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tok + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q0 = blockIdx.x * (AQ * NQT), h = blockIdx.y, b = blockIdx.z;
@@ -185,8 +193,9 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&s_full[g], 1);
-      mbar_init(&p_full[g], 128);
+      mbar_init(&p_full[g], 128 * C::SPLIT);
       mbar_init(&o_done[g], 1);
+      mbar_init(&tok[g], 128 * C::SPLIT);
     }
     fence_mbar_init();
   }
@@ -307,39 +316,62 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
       }
     }
   } else {  // ------------------------------------------------------ softmax groups
-    const int g = (warp - 2) / 4;
+    // warp w >= 2: group g, column half hf; TMEM lane quarter w % 4 (each group's
+    // 4 * SPLIT warps cover all 128 rows SPLIT times)
+    constexpr int SPLIT = C::SPLIT, CW = C::CW;
+    const int sw = warp - 2;
+    const int g = sw / (4 * SPLIT), hf = (sw % (4 * SPLIT)) / 4;
     const int qd = warp & 3;
     const int r = qd * 32 + lane;  // query row within the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const uint32_t st_addr = tmem + lane_off + C::s_col(g);
     const uint32_t o_addr = tmem + lane_off + C::o_col(g);
+    const int colb = hf * CW;  // first key column of this thread
+    float *red = reinterpret_cast<float *>(smem + C::OFF_RED);
+    auto red_at = [&](int par, int half) -> float & {
+      return red[((par * 2 + g) * SPLIT + half) * 128 + r];
+    };
+    auto group_sync = [&] {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(128 * SPLIT) : "memory");
+    };
     float m_run = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(&s_full[g], j & 1);
+      // ping-pong: the two groups' softmax phases are mutually exclusive (they share
+      // the SM's MUFU / issue slots), so one group's exp work overlaps the other
+      // group's PV + S MMAs instead of both groups stalling on the tensor core
+      if constexpr (NQT == 2) {
+        if (g == 1) mbar_wait(&tok[1], j & 1);
+        else if (j > 0) mbar_wait(&tok[0], (j - 1) & 1);
+      }
       tc_fence_after();
       const int valid = Nkv - j * AK;  // columns >= valid are padding (last tile only)
-      // pass 1: row max, 64 columns in flight, four independent FMNMX3 chains
-      float mt = -INFINITY;
+      float v[CW];
 #pragma unroll
-      for (int h = 0; h < AK; h += 64) {
-        float v[64];
-        tmem_ld32_nowait(st_addr + h, reinterpret_cast<uint32_t *>(v));
-        tmem_ld32_nowait(st_addr + h + 32, reinterpret_cast<uint32_t *>(v) + 32);
-        tmem_ld_wait();
-        if (valid < AK) {
+      for (int c = 0; c < CW; c += 32)
+        tmem_ld32_nowait(st_addr + colb + c, reinterpret_cast<uint32_t *>(v) + c);
+      tmem_ld_wait();
+      if (valid < AK) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c)
-            if (h + c >= valid) v[c] = -INFINITY;
-        }
-        float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
+        for (int c = 0; c < CW; ++c)
+          if (colb + c >= valid) v[c] = -INFINITY;
+      }
+      // row max: four independent FMNMX3 chains over my columns, then the pair's
+      float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 64; c += 8) {
-          a0 = fmax3(a0, v[c], v[c + 1]);
-          a1 = fmax3(a1, v[c + 2], v[c + 3]);
-          a2 = fmax3(a2, v[c + 4], v[c + 5]);
-          a3 = fmax3(a3, v[c + 6], v[c + 7]);
-        }
-        mt = fmax3(mt, fmaxf(a0, a1), fmaxf(a2, a3));
+      for (int c = 0; c < CW; c += 8) {
+        a0 = fmax3(a0, v[c], v[c + 1]);
+        a1 = fmax3(a1, v[c + 2], v[c + 3]);
+        a2 = fmax3(a2, v[c + 4], v[c + 5]);
+        a3 = fmax3(a3, v[c + 6], v[c + 7]);
+      }
+      float mt = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+      if constexpr (SPLIT == 2) {
+        // also orders my S reads before the partner's P stores (P of the upper
+        // half overwrites S columns of the lower half)
+        red_at(j & 1, hf) = mt;
+        group_sync();
+        mt = fmaxf(red_at(j & 1, 0), red_at(j & 1, 1));
       }
       mt *= scale_log2;
       // lazy rescale: move the reference max only when it grows by > 2^8
@@ -350,12 +382,13 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         m_run = mt;
       }
       if (j > 0 && __any_sync(0xffffffffu, grow)) {
-        // O_g holds PV(j-1) once o_done completes its j-th phase; rescale in
-        // 16-column pieces to keep the register footprint small
+        // O_g holds PV(j-1) once o_done completes its j-th phase; the pair
+        // rescales interleaved 16-column pieces
         mbar_wait(&o_done[g], (j - 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < C::HDP; c += 16) {
+          if ((c / 16) % SPLIT != hf) continue;
           float o[16];
           tmem_row_load<16>(o_addr + c, o);
 #pragma unroll
@@ -364,26 +397,16 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         }
       }
       l *= factor;
-      // P = 2^(s * scale - m): packed FFMA2, MUFU ex2, FADD2 row sums in four
-      // independent pairs, bf16x2 packs stored over S in TMEM
+      // P = 2^(s * scale - m): packed FFMA2, MUFU ex2 (or the polynomial), FADD2
+      // row sums in four independent pairs, bf16x2 packs stored over S in TMEM
       const uint64_t sc2 = pack_f32x2(scale_log2, scale_log2), nm2 = pack_f32x2(-m_run, -m_run);
       uint64_t acc[4] = {0, 0, 0, 0};
-      // pass 2: S re-read from TMEM 32 columns at a time (TMEM reads are cheap;
-      // keeps the register footprint low); P overwrites S columns already consumed
 #pragma unroll
-      for (int c0 = 0; c0 < AK; c0 += 32) {
-        float v[32];
-        tmem_ld32_nowait(st_addr + c0, reinterpret_cast<uint32_t *>(v));
-        tmem_ld_wait();
-        if (valid < AK) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (c0 + c >= valid) v[c] = -INFINITY;
-        }
+      for (int c0 = 0; c0 < CW; c0 += 32) {
         uint32_t pk[16];
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
-          const uint64_t xx = ffma_f32x2(pack_f32x2(v[c], v[c + 1]), sc2, nm2);
+          const uint64_t xx = ffma_f32x2(pack_f32x2(v[c0 + c], v[c0 + c + 1]), sc2, nm2);
           float p0, p1;
           if ((c / 2) % 8 < POLY) {
             ex2_poly_x2(xx, p0, p1);
@@ -398,7 +421,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
           __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
           pk[c / 2] = *reinterpret_cast<uint32_t *>(&t2);
         }
-        tmem_st16(st_addr + c0 / 2, pk);
+        tmem_st16(st_addr + (colb + c0) / 2, pk);
       }
       {
         const uint64_t t = add_f32x2(add_f32x2(acc[0], acc[1]), add_f32x2(acc[2], acc[3]));
@@ -409,34 +432,46 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[g]);
+      if constexpr (NQT == 2) mbar_arrive(&tok[1 - g]);  // hand the exp units over
     }
-    // epilogue: O / l (rows beyond Nq are padding)
+    // epilogue: O / l; the pair combines its partial row sums, then each thread
+    // stores its interleaved 16-column pieces (rows beyond Nq are padding)
+    if constexpr (SPLIT == 2) {
+      group_sync();  // every thread is past its last tile's max exchange
+      red_at(0, hf) = l;
+      group_sync();
+      l = red_at(0, 0) + red_at(0, 1);
+    }
     mbar_wait(&o_done[g], (n_kv - 1) & 1);
     tc_fence_after();
-    float o[C::HDP];
-    tmem_row_load<C::HDP>(o_addr, o);
     const int qrow = q0 + g * AQ + r;
-    if (qrow < Nq) {
-      const float inv = 1.f / l;
-      const int d = H * hd;
-      bf16 *dst = out + ((long)qrow * B + b) * d + h * hd;
-      if ((hd & 7) == 0) {
+    const float inv = 1.f / l;
+    const int d = H * hd;
+    bf16 *dst = out + ((long)qrow * B + b) * d + h * hd;
 #pragma unroll
-        for (int c = 0; c < C::HDP; c += 8) {
-          if (c < hd) {
-            __nv_bfloat162 a0 = __floats2bfloat162_rn(o[c] * inv, o[c + 1] * inv);
-            __nv_bfloat162 a1 = __floats2bfloat162_rn(o[c + 2] * inv, o[c + 3] * inv);
-            __nv_bfloat162 a2 = __floats2bfloat162_rn(o[c + 4] * inv, o[c + 5] * inv);
-            __nv_bfloat162 a3 = __floats2bfloat162_rn(o[c + 6] * inv, o[c + 7] * inv);
-            *reinterpret_cast<uint4 *>(dst + c) =
-                make_uint4(*reinterpret_cast<uint32_t *>(&a0), *reinterpret_cast<uint32_t *>(&a1),
-                           *reinterpret_cast<uint32_t *>(&a2), *reinterpret_cast<uint32_t *>(&a3));
+    for (int c = 0; c < C::HDP; c += 16) {
+      if ((c / 16) % SPLIT != hf) continue;
+      float o[16];
+      tmem_row_load<16>(o_addr + c, o);
+      if (qrow < Nq) {
+        if ((hd & 7) == 0) {
+#pragma unroll
+          for (int e = 0; e < 16; e += 8) {
+            if (c + e < hd) {
+              __nv_bfloat162 b0 = __floats2bfloat162_rn(o[e] * inv, o[e + 1] * inv);
+              __nv_bfloat162 b1 = __floats2bfloat162_rn(o[e + 2] * inv, o[e + 3] * inv);
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(o[e + 4] * inv, o[e + 5] * inv);
+              __nv_bfloat162 b3 = __floats2bfloat162_rn(o[e + 6] * inv, o[e + 7] * inv);
+              *reinterpret_cast<uint4 *>(dst + c + e) =
+                  make_uint4(*reinterpret_cast<uint32_t *>(&b0), *reinterpret_cast<uint32_t *>(&b1),
+                             *reinterpret_cast<uint32_t *>(&b2), *reinterpret_cast<uint32_t *>(&b3));
+            }
           }
-        }
-      } else {
+        } else {
 #pragma unroll
-        for (int c = 0; c < C::HDP; ++c)
-          if (c < hd) dst[c] = __float2bfloat16_rn(o[c] * inv);
+          for (int e = 0; e < 16; ++e)
+            if (c + e < hd) dst[c + e] = __float2bfloat16_rn(o[e] * inv);
+        }
       }
     }
   }
@@ -487,11 +522,12 @@ cudaError_t launch_attn_p(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nk
 }
 
 // STADI_ATTN_POLY=k (0..4): k of every 8 column pairs take the polynomial exp2
-// (default 3); for A/B measurements of the MUFU / FMA balance.
+// (default 0: measured on B200 the exp units are not the bound of this kernel);
+// for A/B measurements of the MUFU / FMA balance.
 int attn_poly() {
   static const int v = [] {
     const char *e = getenv("STADI_ATTN_POLY");
-    const int k = e ? atoi(e) : 3;
+    const int k = e ? atoi(e) : 0;
     return k < 0 ? 0 : (k > 4 ? 4 : k);
   }();
   return v;

@@ -52,7 +52,14 @@ def gemm(M, N, K, epi):
     print(f"gemm M={M} N={N} K={K} epi={epi}: {ms:.3f} ms  {2.0 * M * N * K / ms / 1e9:.0f} TFLOP/s")
 
 
-if __name__ == "__main__":
+def attn_sweep():
+    for hd, H in ((64, 18), (72, 16), (80, 16), (40, 16), (16, 16)):
+        attn(16384, 16384, 2, H, hd)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "sweep":
+    attn_sweep()
+elif __name__ == "__main__":
     attn(16384, 16384, 2, 16, 72)
     attn(8192, 16384, 2, 16, 72)
     attn(4096, 4096, 2, 10, 64)
