@@ -114,8 +114,15 @@ struct AttnCfg {
   __host__ __device__ static constexpr uint32_t cswz(int c) {
     return cw(c) == 64 ? SWZ_128B : (cw(c) == 32 ? SWZ_64B : SWZ_32B);
   }
+  // one query tile with HDP <= 128 fits 256 TMEM columns (S 128 + O 128): two CTAs
+  // share an SM (independent MMA / softmax chains), with a 2-stage K/V ring each
+  static constexpr bool TWO_CTAS = NQT == 1 && HDP <= 128;
+  static constexpr int TMEM_COLS = TWO_CTAS ? 256 : 512;
+  static constexpr int MIN_BLOCKS = TWO_CTAS ? 2 : 1;
   static constexpr int STAGES =
-      (200 * 1024 - NQT * TILE) / (2 * TILE) > 4 ? 4 : (200 * 1024 - NQT * TILE) / (2 * TILE);
+      TWO_CTAS ? 2
+               : ((200 * 1024 - NQT * TILE) / (2 * TILE) > 4 ? 4
+                                                              : (200 * 1024 - NQT * TILE) / (2 * TILE));
   static constexpr int OFF_K = NQT * TILE;
   static constexpr int OFF_V = OFF_K + STAGES * TILE;
   static constexpr int OFF_BAR = OFF_V + STAGES * TILE;
@@ -157,7 +164,8 @@ __device__ __forceinline__ void tmem_row_store(uint32_t taddr, const float *v) {
 }
 
 template <int N64, int N32, int N16, int NQT, int POLY>
-__global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
+__global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
+                                  AttnCfg<N64, N32, N16, NQT>::MIN_BLOCKS)
     tc_attn_kernel(const __grid_constant__ CUtensorMap tq64, const __grid_constant__ CUtensorMap tq32,
                    const __grid_constant__ CUtensorMap tq16, const __grid_constant__ CUtensorMap tk64,
                    const __grid_constant__ CUtensorMap tk32, const __grid_constant__ CUtensorMap tk16,
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -479,7 +487,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
 
@@ -546,6 +554,15 @@ cudaError_t launch_attn(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv,
 
 }  // namespace
 
+// STADI_ATTN_NQT=1: one query tile per CTA, two CTAs per SM (A/B experiments).
+int attn_nqt() {
+  static const int v = [] {
+    const char *e = getenv("STADI_ATTN_NQT");
+    return (e && e[0] == '1') ? 1 : 2;
+  }();
+  return v;
+}
+
 // Supported head dims (padded to hd_pad): 16 (16), 40 (48 = 32 + 16), 64 (64),
 // 72 / 80 (80 = 64 + 16), 160 (160 = 64 + 64 + 32, one query tile per CTA).
 bool tc_attention_supported(int hd) {
@@ -559,9 +576,13 @@ cudaError_t tc_attention_bf16(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, in
   switch (hd) {
     case 16: return launch_attn<0, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 40: return launch_attn<0, 1, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
-    case 64: return launch_attn<1, 0, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 64:
+      return attn_nqt() == 1 ? launch_attn<1, 0, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s)
+                             : launch_attn<1, 0, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 72:
-    case 80: return launch_attn<1, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 80:
+      return attn_nqt() == 1 ? launch_attn<1, 0, 1, 1>(q, kv, o, Nq, Nkv, B, H, hd, s)
+                             : launch_attn<1, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 160: return launch_attn<2, 1, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
   }
   return cudaErrorInvalidValue;

@@ -62,17 +62,18 @@ __device__ __forceinline__ EpiIn epi_load(const EpiParams &p, int row, int col) 
 // Per-chunk constants of a lane's column pair: bias and the B (<= 2) gate rows,
 // loaded once per 32-column chunk instead of once per row.
 struct EpiCol {
-  float2 b, g[2];
+  float2 b, g0, g1;  // bias; gate rows of batch 0 / 1 (no dynamic indexing: registers)
 };
 template <int EPI>
 __device__ __forceinline__ EpiCol epi_col(const EpiParams &p, int col) {
   EpiCol c;
   c.b = p.bias ? *reinterpret_cast<const float2 *>(p.bias + col) : make_float2(0.f, 0.f);
-  c.g[0] = c.g[1] = make_float2(0.f, 0.f);
+  c.g0 = c.g1 = make_float2(0.f, 0.f);
   if constexpr (EPI == EPI_GATED_RES || EPI == EPI_CONV) {
-    if (p.gate)
-      for (int b = 0; b < p.B && b < 2; ++b)
-        c.g[b] = *reinterpret_cast<const float2 *>(p.gate + b * p.gate_bstride + col);
+    if (p.gate) {
+      c.g0 = *reinterpret_cast<const float2 *>(p.gate + col);
+      c.g1 = p.B > 1 ? *reinterpret_cast<const float2 *>(p.gate + p.gate_bstride + col) : c.g0;
+    }
   }
   return c;
 }
@@ -86,7 +87,7 @@ __device__ __forceinline__ void epi_finish(const EpiParams &p, int row, int col,
                                            float v1, const EpiIn &in, const EpiCol &cc) {
   v0 += cc.b.x;
   v1 += cc.b.y;
-  const float2 g = cc.g[(row % p.B) & 1];
+  const float2 g = (row % p.B) ? cc.g1 : cc.g0;
   if constexpr (EPI == EPI_STORE || EPI == EPI_GELU) {
     if (EPI == EPI_GELU) {
       v0 = gelu_tanh_fast(v0);

@@ -1093,7 +1093,11 @@ extern "C" stadi_status stadi_gather(stadi_ctx *ctx, float *out_full, void *stre
                          dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     return STADI_OK;
   }
-  // NCCL: every rank (excluded ones too) receives every band (world communicator)
+  // NCCL: every rank (excluded ones too) receives every band (world communicator).
+  // The exchange collectives run on the comm stream, possibly on the same
+  // communicator: join it first so no two streams drive one communicator at once.
+  CK(cudaEventRecord(ctx->ev_ready, ctx->comm));
+  CK(cudaStreamWaitEvent(s, ctx->ev_ready, 0));
   float *full = nullptr;
   CK(cudaMallocAsync(&full, (size_t)m.lat_h * row_elems * 4, s));
   if (!ctx->ranks.empty())
