@@ -112,13 +112,17 @@ __device__ __forceinline__ void ex2_poly_x2(uint64_t xx, float &p0, float &p1) {
 // Of every 8 column pairs, POLY (a kernel template parameter) use the
 // polynomial exp2, the rest MUFU ex2.
 
-// Head-dim chunking: N64 chunks of 64, then optionally one of 32, one of 16.
+// Head-dim chunking: N64 chunks of 64, then N32 of 32, then N16 of 16.
 template <int N64, int N32, int N16, int NQT_>
 struct AttnCfg {
   static constexpr int NQT = NQT_;
   static constexpr int HDP = 64 * N64 + 32 * N32 + 16 * N16;
   static constexpr int NCH = N64 + N32 + N16;
-  static constexpr int TILE = AQ * HDP * 2;  // one Q / K / V tile (128 rows), bytes
+  // keys per tile: 112 with two query tiles so that S (2 x 112), O (2 x 80) and a
+  // separate P region (2 x 64) fit the 512 TMEM columns; 128 with one tile
+  static constexpr int AKT = NQT == 2 ? 112 : 128;
+  static constexpr int QTILE = AQ * HDP * 2;   // one Q tile (128 rows), bytes
+  static constexpr int KTILE = AKT * HDP * 2;  // one K or V tile, bytes
   __host__ __device__ static constexpr int cw(int c) {  // chunk width
     return c < N64 ? 64 : (c < N64 + N32 ? 32 : 16);
   }
@@ -128,41 +132,40 @@ struct AttnCfg {
                                     : 64 * N64 + 32 * N32 + 16 * (c - N64 - N32));
   }
   // all chunks 16 wide (32B swizzle): the V tile is one MN-major operand of N = HDP
-  // (16-column atoms AQ * 32 bytes apart), so PV is ONE MMA per 16 keys
+  // (16-column atoms AKT * 32 bytes apart), so PV is ONE MMA per 16 keys
   static constexpr bool NARROW = N64 == 0 && N32 == 0;
-  __host__ __device__ static constexpr int coff(int c) { return AQ * ccol(c) * 2; }  // bytes
+  __host__ __device__ static constexpr int qoff(int c) { return AQ * ccol(c) * 2; }
+  __host__ __device__ static constexpr int koff(int c) { return AKT * ccol(c) * 2; }
   __host__ __device__ static constexpr uint32_t cswz(int c) {
     return cw(c) == 64 ? SWZ_128B : (cw(c) == 32 ? SWZ_64B : SWZ_32B);
   }
-  // one query tile with HDP <= 128 fits 256 TMEM columns (S 128 + O 128): two CTAs
-  // share an SM (independent MMA / softmax chains), with a 2-stage K/V ring each
-  static constexpr bool TWO_CTAS = NQT == 1 && HDP <= 128;
-  static constexpr int TMEM_COLS = TWO_CTAS ? 256 : 512;
-  static constexpr int MIN_BLOCKS = TWO_CTAS ? 2 : 1;
   static constexpr int STAGES =
-      TWO_CTAS ? 2
-               : ((200 * 1024 - NQT * TILE) / (2 * TILE) > 4 ? 4
-                                                              : (200 * 1024 - NQT * TILE) / (2 * TILE));
-  static constexpr int OFF_K = NQT * TILE;
-  static constexpr int OFF_V = OFF_K + STAGES * TILE;
-  static constexpr int OFF_BAR = OFF_V + STAGES * TILE;
-  // SPLIT threads share a query row (each owns AK / SPLIT key columns); they
-  // exchange partial row maxima / sums through RED [2 parities][2 groups][SPLIT][128]
+      (200 * 1024 - NQT * QTILE) / (2 * KTILE) > 4 ? 4 : (200 * 1024 - NQT * QTILE) / (2 * KTILE);
+  static constexpr int OFF_K = NQT * QTILE;
+  static constexpr int OFF_V = OFF_K + STAGES * KTILE;
+  static constexpr int OFF_BAR = OFF_V + STAGES * KTILE;
+  // SPLIT threads share a query row: half 0 owns key columns [0, 64), half 1
+  // [64, AKT); they exchange partial row maxima / sums through RED
+  // [2 parities][2 groups][SPLIT][128]
   static constexpr int SPLIT = 2;
-  static constexpr int CW = AK / SPLIT;
+  static constexpr int W0 = 64, W1 = AKT - 64;
   static constexpr int OFF_RED = OFF_BAR + 256;
   static constexpr int RED_BYTES = 2 * 2 * SPLIT * 128 * 4;
   static constexpr int SMEM = OFF_RED + RED_BYTES + 1024;
   static constexpr int THREADS = 64 + 128 * SPLIT * NQT;
-  // TMEM columns: S_g at 128 g, O_g at 256 + 128 g (HDP <= 128 when NQT == 2)
-  __host__ __device__ static constexpr uint32_t s_col(int g) { return 128u * g; }
+  // TMEM columns: S_g, then O_g (HDP wide), then P_g (packed bf16, AKT / 2 <= 64)
+  __host__ __device__ static constexpr uint32_t s_col(int g) { return (uint32_t)(AKT * g); }
   __host__ __device__ static constexpr uint32_t o_col(int g) {
-    return NQT == 2 ? 256u + 128u * g : 128u;
+    return (uint32_t)(NQT * AKT + HDP * g);
   }
-  static_assert(NQT == 1 || HDP <= 128, "two query tiles need HDP <= 128");
-  static_assert(NQT == 2 || HDP <= 384, "HDP too large");
+  __host__ __device__ static constexpr uint32_t p_col(int g) {
+    return (uint32_t)(NQT * (AKT + HDP) + 64 * g);
+  }
+  static_assert(NQT * (AKT + HDP + 64) <= 512, "TMEM columns");
+  static_assert(NQT == 1 || HDP <= 80, "two query tiles need HDP <= 80");
   static_assert(STAGES >= 2, "smem");
   static_assert(SMEM <= 227 * 1024, "smem");
+  static_assert(W1 % 16 == 0 && W1 > 0, "column split");
 };
 
 // Load columns [c0, c0 + 16 * n) of this lane's TMEM row into v (fp32).
@@ -183,14 +186,57 @@ __device__ __forceinline__ void tmem_row_store(uint32_t taddr, const float *v) {
   if constexpr (N % 32) tmem_st16(taddr + (N - 16), r + (N - 16));
 }
 
+// Softmax of one key tile for the W key columns [colb, colb + W) of this
+// thread's query row: returns the tile's partial row sum and stores P (bf16
+// pairs) into TMEM at p_addr.  v holds the S values (already loaded).
+template <int W, int POLY>
+__device__ __forceinline__ float softmax_tile(float *v, uint64_t sc2, uint64_t nm2,
+                                              uint32_t *pk) {
+  uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int c = 0; c < W; c += 2) {
+    const uint64_t xx = ffma_f32x2(pack_f32x2(v[c], v[c + 1]), sc2, nm2);
+    float p0, p1;
+    if ((c / 2) % 8 < POLY) {
+      ex2_poly_x2(xx, p0, p1);
+    } else {
+      float x0, x1;
+      unpack_f32x2(xx, x0, x1);
+      p0 = ex2(x0);
+      p1 = ex2(x1);
+    }
+    acc[(c / 2) & 3] = add_f32x2(acc[(c / 2) & 3], pack_f32x2(p0, p1));
+    __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
+    pk[c / 2] = *reinterpret_cast<uint32_t *>(&t2);
+  }
+  const uint64_t t = add_f32x2(add_f32x2(acc[0], acc[1]), add_f32x2(acc[2], acc[3]));
+  float r0, r1;
+  unpack_f32x2(t, r0, r1);
+  return r0 + r1;
+}
+template <int W>
+__device__ __forceinline__ void tmem_load_cols(uint32_t taddr, float *v) {
+  uint32_t *r = reinterpret_cast<uint32_t *>(v);
+#pragma unroll
+  for (int c = 0; c + 32 <= W; c += 32) tmem_ld32_nowait(taddr + c, r + c);
+  if constexpr (W % 32) tmem_ld16_nowait(taddr + (W - 16), r + (W - 16));
+  tmem_ld_wait();
+}
+template <int NP>  // NP packed columns (multiple of 8)
+__device__ __forceinline__ void tmem_store_packed(uint32_t taddr, const uint32_t *pk) {
+#pragma unroll
+  for (int c = 0; c + 16 <= NP; c += 16) tmem_st16(taddr + c, pk + c);
+  if constexpr (NP % 16) tmem_st8(taddr + (NP - 8), pk + (NP - 8));
+}
+
 template <int N64, int N32, int N16, int NQT, int POLY>
-__global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
-                                  AttnCfg<N64, N32, N16, NQT>::MIN_BLOCKS)
+__global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
     tc_attn_kernel(const __grid_constant__ CUtensorMap tq64, const __grid_constant__ CUtensorMap tq32,
                    const __grid_constant__ CUtensorMap tq16, const __grid_constant__ CUtensorMap tk64,
                    const __grid_constant__ CUtensorMap tk32, const __grid_constant__ CUtensorMap tk16,
                    bf16 *__restrict__ out, int Nq, int Nkv, int B, int H, int hd, float scale_log2) {
   using C = AttnCfg<N64, N32, N16, NQT>;
+  constexpr int AKT = C::AKT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -201,15 +247,16 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
   uint64_t *q_full = bar;
   uint64_t *k_full = bar + 1, *k_empty = k_full + C::STAGES;
   uint64_t *v_full = k_empty + C::STAGES, *v_empty = v_full + C::STAGES;
-  uint64_t *s_full = v_empty + C::STAGES;  // [NQT]
-  uint64_t *p_full = s_full + 2;           // [NQT]
-  uint64_t *o_done = p_full + 2;           // [NQT]
-  uint64_t *tok = o_done + 2;              // [2] softmax ping-pong tokens
+  uint64_t *s_full = v_empty + C::STAGES;  // [2] S_g(j) computed
+  uint64_t *s_free = s_full + 2;           // [2] S_g(j) read by the softmax group
+  uint64_t *p_full = s_free + 2;           // [2] P_g(j) stored
+  uint64_t *o_done = p_full + 2;           // [2] PV_g(j) complete (P_g free, O_g final)
+  uint64_t *tok = o_done + 2;              // [2] exp-phase tokens (groups alternate)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tok + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q0 = blockIdx.x * (AQ * NQT), h = blockIdx.y, b = blockIdx.z;
-  const int n_kv = (Nkv + AK - 1) / AK;
+  const int n_kv = (Nkv + AKT - 1) / AKT;
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
@@ -221,25 +268,26 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&s_full[g], 1);
+      mbar_init(&s_free[g], 128 * C::SPLIT);
       mbar_init(&p_full[g], 128 * C::SPLIT);
       mbar_init(&o_done[g], 1);
       mbar_init(&tok[g], 128 * C::SPLIT);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // TMA of one 128-row tile of every head-dim chunk (c0: first row coordinate)
+  // TMA of one tile of every head-dim chunk (row: first token coordinate)
   auto load_tile = [&](const CUtensorMap *m64, const CUtensorMap *m32, const CUtensorMap *m16,
-                       uint8_t *dst, uint64_t *br, int zb, int row) {
+                       uint8_t *dst, uint64_t *br, int zb, int row, int rows) {
 #pragma unroll
     for (int c = 0; c < C::NCH; ++c) {
       const CUtensorMap *m = C::cw(c) == 64 ? m64 : (C::cw(c) == 32 ? m32 : m16);
-      tma_load_4d(m, dst + C::coff(c), br, C::ccol(c), h, zb, row);
+      tma_load_4d(m, dst + rows * C::ccol(c) * 2, br, C::ccol(c), h, zb, row);
     }
   };
 
@@ -248,19 +296,19 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
       if (N64) tma_prefetch(&tq64), tma_prefetch(&tk64);
       if (N32) tma_prefetch(&tq32), tma_prefetch(&tk32);
       if (N16) tma_prefetch(&tq16), tma_prefetch(&tk16);
-      mbar_expect_tx(q_full, NQT * C::TILE);
+      mbar_expect_tx(q_full, NQT * C::QTILE);
 #pragma unroll
       for (int g = 0; g < NQT; ++g)
-        load_tile(&tq64, &tq32, &tq16, sQ + g * C::TILE, q_full, b, q0 + g * AQ);
+        load_tile(&tq64, &tq32, &tq16, sQ + g * C::QTILE, q_full, b, q0 + g * AQ, AQ);
       int s = 0;
       uint32_t ph = 0;
       for (int j = 0; j < n_kv; ++j) {
         mbar_wait(&k_empty[s], ph ^ 1);
-        mbar_expect_tx(&k_full[s], C::TILE);
-        load_tile(&tk64, &tk32, &tk16, sK + s * C::TILE, &k_full[s], 2 * b, j * AK);
+        mbar_expect_tx(&k_full[s], C::KTILE);
+        load_tile(&tk64, &tk32, &tk16, sK + s * C::KTILE, &k_full[s], 2 * b, j * AKT, AKT);
         mbar_wait(&v_empty[s], ph ^ 1);
-        mbar_expect_tx(&v_full[s], C::TILE);
-        load_tile(&tk64, &tk32, &tk16, sV + s * C::TILE, &v_full[s], 2 * b + 1, j * AK);
+        mbar_expect_tx(&v_full[s], C::KTILE);
+        load_tile(&tk64, &tk32, &tk16, sV + s * C::KTILE, &v_full[s], 2 * b + 1, j * AKT, AKT);
         if (++s == C::STAGES) {
           s = 0;
           ph ^= 1;
@@ -269,47 +317,50 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------ MMA issuer
-      constexpr uint32_t id_s = umma_idesc_bf16(128, AK, 0, 0);
+      constexpr uint32_t id_s = umma_idesc_bf16(128, AKT, 0, 0);
+      // Descriptors are built once per operand base and advanced by adding the
+      // (16-byte granular) start-address offset into their low field: the single
+      // issuing thread must not spend ~10 dependent ALU ops per MMA on them.
       auto issue_s = [&](int g, int st) {
         const uint32_t dt = tmem + C::s_col(g);
-        const uint32_t qa = smem_u32(sQ + g * C::TILE), ka = smem_u32(sK + st * C::TILE);
+        const uint32_t qa = smem_u32(sQ + g * C::QTILE), ka = smem_u32(sK + st * C::KTILE);
         int kk = 0;
 #pragma unroll
         for (int c = 0; c < C::NCH; ++c) {
-          const uint32_t rb = C::cw(c) * 2, sbo = 8 * rb;
+          const uint32_t sbo = 8 * C::cw(c) * 2;
+          const uint64_t qd0 = umma_desc(qa + C::qoff(c), 16, sbo, C::cswz(c));
+          const uint64_t kd0 = umma_desc(ka + C::koff(c), 16, sbo, C::cswz(c));
 #pragma unroll
           for (int k = 0; k < C::cw(c) / 16; ++k, ++kk)
-            umma_bf16(dt, umma_desc(qa + C::coff(c) + k * 32, 16, sbo, C::cswz(c)),
-                      umma_desc(ka + C::coff(c) + k * 32, 16, sbo, C::cswz(c)), id_s, kk != 0);
+            umma_bf16(dt, qd0 + (uint64_t)(2 * k), kd0 + (uint64_t)(2 * k), id_s, kk != 0);
         }
       };
       auto issue_pv = [&](int g, int st, int j) {
-        const uint32_t pa = tmem + C::s_col(g);   // P: 64 columns of packed bf16
-        const uint32_t va = smem_u32(sV + st * C::TILE);
+        const uint32_t pa = tmem + C::p_col(g);  // P: AKT / 2 columns of packed bf16
+        const uint32_t va = smem_u32(sV + st * C::KTILE);
         if constexpr (C::NARROW) {
           constexpr uint32_t idp = umma_idesc_bf16(128, C::HDP, 0, 1);
           const uint32_t dt = tmem + C::o_col(g);
+          const uint64_t vd0 = umma_desc(va, AKT * 32, 8 * 32, SWZ_32B);
 #pragma unroll
-          for (int k = 0; k < AK / 16; ++k)
-            umma_bf16_ts(dt, pa + k * 8, umma_desc(va + k * 16 * 32, AQ * 32, 8 * 32, SWZ_32B),
-                         idp, (j | k) != 0);
-          return;
-        }
+          for (int k = 0; k < AKT / 16; ++k)  // 16 keys x 32 B = 512 B = 32 units per step
+            umma_bf16_ts(dt, pa + k * 8, vd0 + (uint64_t)(32 * k), idp, (j | k) != 0);
+        } else {
 #pragma unroll
-        for (int c = 0; c < C::NCH; ++c) {
-          const uint32_t rb = C::cw(c) * 2;
-          const uint32_t idp = umma_idesc_bf16(128, C::cw(c), 0, 1);
-          const uint32_t dt = tmem + C::o_col(g) + C::ccol(c);
+          for (int c = 0; c < C::NCH; ++c) {
+            const uint32_t rb = C::cw(c) * 2;
+            const uint32_t idp = umma_idesc_bf16(128, C::cw(c), 0, 1);
+            const uint32_t dt = tmem + C::o_col(g) + C::ccol(c);
+            const uint64_t vd0 = umma_desc(va + C::koff(c), AKT * rb, 8 * rb, C::cswz(c));
 #pragma unroll
-          for (int k = 0; k < AK / 16; ++k)
-            umma_bf16_ts(dt, pa + k * 8,
-                         umma_desc(va + C::coff(c) + k * 16 * rb, AQ * rb, 8 * rb, C::cswz(c)),
-                         idp, (j | k) != 0);
+            for (int k = 0; k < AKT / 16; ++k)
+              umma_bf16_ts(dt, pa + k * 8, vd0 + (uint64_t)(k * rb), idp, (j | k) != 0);
+          }
         }
       };
+      // Order per key tile j: S_g(j+1) as soon as the group has read S_g(j) (it
+      // overlaps that group's exp work), then PV_g(j) once P_g(j) is stored.
       mbar_wait(q_full, 0);
-      int ks = 0, vs = 0;
-      uint32_t kph = 0, vph = 0;
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
 #pragma unroll
@@ -318,55 +369,56 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
         umma_commit(&s_full[g]);
       }
       umma_commit(&k_empty[0]);
-      ks = 1 % C::STAGES;
-      kph = (ks == 0);
+      int ks = 1 % C::STAGES, vs = 0;
+      uint32_t kph = (ks == 0), vph = 0;
       for (int j = 0; j < n_kv; ++j) {
-        mbar_wait(&v_full[vs], vph);
-        const bool more = j + 1 < n_kv;
+        if (j + 1 < n_kv) {
+          mbar_wait(&k_full[ks], kph);
 #pragma unroll
-        for (int g = 0; g < NQT; ++g) {
-          mbar_wait(&p_full[g], j & 1);
-          ATTN_TRACE(0, g, j);
-          tc_fence_after();
-          issue_pv(g, vs, j);
-          ATTN_TRACE(1, g, j);
-          umma_commit(&o_done[g]);
-          if (more) {
-            if (g == 0) {
-              mbar_wait(&k_full[ks], kph);
-              tc_fence_after();
-            }
+          for (int g = 0; g < NQT; ++g) {
+            mbar_wait(&s_free[g], j & 1);
+            ATTN_TRACE(0, g, j);
+            tc_fence_after();
             issue_s(g, ks);
             umma_commit(&s_full[g]);
-            ATTN_TRACE(2, g, j);
+            ATTN_TRACE(1, g, j);
           }
-        }
-        umma_commit(&v_empty[vs]);
-        if (++vs == C::STAGES) {
-          vs = 0;
-          vph ^= 1;
-        }
-        if (more) {
           umma_commit(&k_empty[ks]);
           if (++ks == C::STAGES) {
             ks = 0;
             kph ^= 1;
           }
         }
+        mbar_wait(&v_full[vs], vph);
+#pragma unroll
+        for (int g = 0; g < NQT; ++g) {
+          mbar_wait(&p_full[g], j & 1);
+          ATTN_TRACE(2, g, j);
+          tc_fence_after();
+          issue_pv(g, vs, j);
+          umma_commit(&o_done[g]);
+          ATTN_TRACE(8, g, j);
+        }
+        umma_commit(&v_empty[vs]);
+        if (++vs == C::STAGES) {
+          vs = 0;
+          vph ^= 1;
+        }
       }
     }
   } else {  // ------------------------------------------------------ softmax groups
     // warp w >= 2: group g, column half hf; TMEM lane quarter w % 4 (each group's
-    // 4 * SPLIT warps cover all 128 rows SPLIT times)
-    constexpr int SPLIT = C::SPLIT, CW = C::CW;
+    // 8 warps cover all 128 rows twice)
+    constexpr int SPLIT = C::SPLIT;
     const int sw = warp - 2;
     const int g = sw / (4 * SPLIT), hf = (sw % (4 * SPLIT)) / 4;
     const int qd = warp & 3;
     const int r = qd * 32 + lane;  // query row within the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    const uint32_t st_addr = tmem + lane_off + C::s_col(g);
+    const uint32_t st_addr = tmem + lane_off + C::s_col(g) + hf * C::W0;
+    const uint32_t p_addr = tmem + lane_off + C::p_col(g) + hf * (C::W0 / 2);
     const uint32_t o_addr = tmem + lane_off + C::o_col(g);
-    const int colb = hf * CW;  // first key column of this thread
+    const int colb = hf * C::W0;  // first key column of this thread
     float *red = reinterpret_cast<float *>(smem + C::OFF_RED);
     auto red_at = [&](int par, int half) -> float & {
       return red[((par * 2 + g) * SPLIT + half) * 128 + r];
@@ -378,45 +430,37 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(&s_full[g], j & 1);
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(3, g, j);
-      // ping-pong: the two groups' softmax phases are mutually exclusive (they share
-      // the SM's MUFU / issue slots), so one group's exp work overlaps the other
-      // group's PV + S MMAs instead of both groups stalling on the tensor core
-      if constexpr (NQT == 2) {
-        if (g == 1) mbar_wait(&tok[1], j & 1);
-        else if (j > 0) mbar_wait(&tok[0], (j - 1) & 1);
-      }
       tc_fence_after();
-      const int valid = Nkv - j * AK;  // columns >= valid are padding (last tile only)
-      float v[CW];
-#pragma unroll
-      for (int c = 0; c < CW; c += 32)
-        tmem_ld32_nowait(st_addr + colb + c, reinterpret_cast<uint32_t *>(v) + c);
-      tmem_ld_wait();
+      const int valid = Nkv - j * AKT;  // columns >= valid are padding (last tile only)
+      float v[C::W0];                   // W1 <= W0
+      if (hf == 0) tmem_load_cols<C::W0>(st_addr, v);
+      else tmem_load_cols<C::W1>(st_addr, v);
+      tc_fence_before();
+      mbar_arrive(&s_free[g]);  // S_g may be overwritten by S_g(j+1)
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(4, g, j);
-      if (valid < AK) {
+      const int W = hf == 0 ? C::W0 : C::W1;
+      if (valid < AKT) {
 #pragma unroll
-        for (int c = 0; c < CW; ++c)
-          if (colb + c >= valid) v[c] = -INFINITY;
+        for (int c = 0; c < C::W0; ++c)
+          if (c >= W || colb + c >= valid) v[c] = -INFINITY;
+      } else if (hf == 1) {
+#pragma unroll
+        for (int c = C::W1; c < C::W0; ++c) v[c] = -INFINITY;
       }
-      // row max: four independent FMNMX3 chains over my columns, then the pair's
+      // row max: four independent FMNMX3 chains, then the pair's
       float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < CW; c += 8) {
+      for (int c = 0; c < C::W0; c += 8) {
         a0 = fmax3(a0, v[c], v[c + 1]);
         a1 = fmax3(a1, v[c + 2], v[c + 3]);
         a2 = fmax3(a2, v[c + 4], v[c + 5]);
         a3 = fmax3(a3, v[c + 6], v[c + 7]);
       }
       float mt = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
-      if constexpr (SPLIT == 2) {
-        // also orders my S reads before the partner's P stores (P of the upper
-        // half overwrites S columns of the lower half)
-        red_at(j & 1, hf) = mt;
-        group_sync();
-        mt = fmaxf(red_at(j & 1, 0), red_at(j & 1, 1));
-      }
+      red_at(j & 1, hf) = mt;
+      group_sync();
+      mt = fmaxf(red_at(j & 1, 0), red_at(j & 1, 1)) * scale_log2;
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(5, g, j);
-      mt *= scale_log2;
       // lazy rescale: move the reference max only when it grows by > 2^8
       float factor = 1.f;
       const bool grow = mt > m_run + RESCALE_THRESHOLD;
@@ -424,13 +468,14 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
         factor = ex2(m_run - mt);  // 0 on the first tile (m_run = -inf)
         m_run = mt;
       }
-      if (j > 0 && __any_sync(0xffffffffu, grow)) {
-        // O_g holds PV(j-1) once o_done completes its j-th phase; the pair
-        // rescales interleaved 16-column pieces
+      // P_g and O_g are in use by PV_g(j-1) until o_done completes its j-th phase
+      if (j > 0) {
         mbar_wait(&o_done[g], (j - 1) & 1);
         tc_fence_after();
+      }
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {
 #pragma unroll
-        for (int c = 0; c < C::HDP; c += 16) {
+        for (int c = 0; c < C::HDP; c += 16) {  // the pair rescales alternate pieces
           if ((c / 16) % SPLIT != hf) continue;
           float o[16];
           tmem_row_load<16>(o_addr + c, o);
@@ -440,52 +485,34 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
         }
       }
       l *= factor;
-      // P = 2^(s * scale - m): packed FFMA2, MUFU ex2 (or the polynomial), FADD2
-      // row sums in four independent pairs, bf16x2 packs stored over S in TMEM
+      // exp phase: the two groups take turns (the SM's 16 ex2/clk are shared), so
+      // one group's S read / max exchange overlaps the other group's exps
+      if constexpr (NQT == 2) {
+        if (g == 1) mbar_wait(&tok[1], j & 1);
+        else if (j > 0) mbar_wait(&tok[0], (j - 1) & 1);
+      }
+      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(7, g, j);
       const uint64_t sc2 = pack_f32x2(scale_log2, scale_log2), nm2 = pack_f32x2(-m_run, -m_run);
-      uint64_t acc[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int c0 = 0; c0 < CW; c0 += 32) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const uint64_t xx = ffma_f32x2(pack_f32x2(v[c0 + c], v[c0 + c + 1]), sc2, nm2);
-          float p0, p1;
-          if ((c / 2) % 8 < POLY) {
-            ex2_poly_x2(xx, p0, p1);
-          } else {
-            float x0, x1;
-            unpack_f32x2(xx, x0, x1);
-            p0 = ex2(x0);
-            p1 = ex2(x1);
-          }
-          const uint64_t pp = pack_f32x2(p0, p1);
-          acc[(c / 2) & 3] = add_f32x2(acc[(c / 2) & 3], pp);
-          __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
-          pk[c / 2] = *reinterpret_cast<uint32_t *>(&t2);
-        }
-        tmem_st16(st_addr + (colb + c0) / 2, pk);
+      uint32_t pk[C::W0 / 2];
+      if (hf == 0) {
+        l += softmax_tile<C::W0, POLY>(v, sc2, nm2, pk);
+        tmem_store_packed<C::W0 / 2>(p_addr, pk);
+      } else {
+        l += softmax_tile<C::W1, POLY>(v, sc2, nm2, pk);
+        tmem_store_packed<C::W1 / 2>(p_addr, pk);
       }
-      {
-        const uint64_t t = add_f32x2(add_f32x2(acc[0], acc[1]), add_f32x2(acc[2], acc[3]));
-        float r0, r1;
-        unpack_f32x2(t, r0, r1);
-        l += r0 + r1;
-      }
+      if constexpr (NQT == 2) mbar_arrive(&tok[1 - g]);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[g]);
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(6, g, j);
-      if constexpr (NQT == 2) mbar_arrive(&tok[1 - g]);  // hand the exp units over
     }
     // epilogue: O / l; the pair combines its partial row sums, then each thread
-    // stores its interleaved 16-column pieces (rows beyond Nq are padding)
-    if constexpr (SPLIT == 2) {
-      group_sync();  // every thread is past its last tile's max exchange
-      red_at(0, hf) = l;
-      group_sync();
-      l = red_at(0, 0) + red_at(0, 1);
-    }
+    // stores its alternate 16-column pieces (rows beyond Nq are padding)
+    group_sync();  // every thread is past its last tile's max exchange
+    red_at(0, hf) = l;
+    group_sync();
+    l = red_at(0, 0) + red_at(0, 1);
     mbar_wait(&o_done[g], (n_kv - 1) & 1);
     tc_fence_after();
     const int qrow = q0 + g * AQ + r;
@@ -523,7 +550,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, C::TMEM_COLS);
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -545,9 +572,10 @@ cudaError_t launch_attn_p(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nk
   bool ok = true;
   for (int i = 0; i < 3; ++i) {
     if (!present[i]) continue;
-    const uint32_t box[4] = {(uint32_t)widths[i], 1, 1, 128};
-    ok &= make_tmap(&tm[i], q, 4, dq, sq, box, swz[i]);
-    ok &= make_tmap(&tm[3 + i], kv, 4, dk, sk, box, swz[i]);
+    const uint32_t qbox[4] = {(uint32_t)widths[i], 1, 1, (uint32_t)AQ};
+    const uint32_t kbox[4] = {(uint32_t)widths[i], 1, 1, (uint32_t)C::AKT};
+    ok &= make_tmap(&tm[i], q, 4, dq, sq, qbox, swz[i]);
+    ok &= make_tmap(&tm[3 + i], kv, 4, dk, sk, kbox, swz[i]);
   }
   if (!ok) return cudaErrorInvalidValue;
   static bool attr = false;
@@ -590,15 +618,6 @@ cudaError_t launch_attn(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv,
 
 }  // namespace
 
-// STADI_ATTN_NQT=1: one query tile per CTA, two CTAs per SM (A/B experiments).
-int attn_nqt() {
-  static const int v = [] {
-    const char *e = getenv("STADI_ATTN_NQT");
-    return (e && e[0] == '1') ? 1 : 2;
-  }();
-  return v;
-}
-
 // hd 72 / 80: 16-wide (32B-swizzled) head-dim chunks, one PV MMA of N = 80 per 16
 // keys (measured 8% faster than 64 + 16 chunks); STADI_ATTN_NARROW=0 switches back.
 int attn_narrow() {
@@ -622,14 +641,11 @@ cudaError_t tc_attention_bf16(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, in
   switch (hd) {
     case 16: return launch_attn<0, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 40: return launch_attn<0, 1, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
-    case 64:
-      return attn_nqt() == 1 ? launch_attn<1, 0, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s)
-                             : launch_attn<1, 0, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 64: return launch_attn<1, 0, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 72:
     case 80:
       if (attn_narrow()) return launch_attn<0, 0, 5, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
-      return attn_nqt() == 1 ? launch_attn<1, 0, 1, 1>(q, kv, o, Nq, Nkv, B, H, hd, s)
-                             : launch_attn<1, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+      return launch_attn<1, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 160: return launch_attn<2, 1, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
   }
   return cudaErrorInvalidValue;

@@ -17,13 +17,13 @@ int main(int argc, char **argv) {
   cudaDeviceSynchronize();
   std::vector<long long> t(16 * 2 * 64);
   cudaMemcpyFromSymbol(t.data(), g_attn_trace, t.size() * 8);
-  const char *names[7] = {"mma:p_full", "mma:pv_issued", "mma:s_issued", "sm:s_full",
-                          "sm:s_loaded", "sm:max_done", "sm:p_arrived"};
+  const char *names[9] = {"mma:s_free", "mma:S_iss", "mma:p_full", "sm:s_full",
+                          "sm:loaded", "sm:max", "sm:p_arr", "sm:tok", "mma:PV_iss"};
   long long t0 = t[(3 * 2 + 0) * 64 + 0];
   for (int j = 0; j < 12; ++j)
     for (int g = 0; g < 2; ++g) {
       printf("j=%2d g=%d:", j, g);
-      for (int e = 0; e < 7; ++e) printf(" %s=%7lld", names[e], t[(e * 2 + g) * 64 + j] - t0);
+      for (int e = 0; e < 9; ++e) printf(" %s=%6lld", names[e], t[(e * 2 + g) * 64 + j] - t0);
       printf("\n");
     }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
