@@ -19,37 +19,47 @@ namespace {
 constexpr int GN_G = 32;
 
 // ------------------------------------------------------------- GN partials
-// out[b][g][0] += sum x, out[b][g][1] += sum x^2 over the band (fp32 per
-// thread over a row chunk, fp64 atomics across chunks).  One block = a chunk of
-// rows; thread t owns float4 channel vectors t, t + 256, ...
+// out[b][g][0] += sum x, out[b][g][1] += sum x^2 over the band.  One block = a
+// chunk of rows; thread t owns float4 channel vector t % nvec of row slots
+// t / nvec (all 256 threads busy when nvec < 256), fp32 per thread, reduced in
+// smem per (b, channel), then per (b, group) with fp64 atomics across blocks.
 __global__ void __launch_bounds__(256) gn_partials_kernel(const float *__restrict__ x, long M,
                                                           int B, int C, int rows_per_block,
                                                           double *__restrict__ out) {
-  extern __shared__ float sm[];  // [2 stats][B][C]
+  extern __shared__ float sm[];  // [2 stats][slots][B][C]
   const int nvec = C / 4;
+  const int slots = nvec >= 256 ? 1 : 256 / nvec;
   const long r0 = (long)blockIdx.x * rows_per_block;
   const long r1 = min(M, r0 + rows_per_block);
-  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-    float s1[2][4] = {}, s2[2][4] = {};
-    for (long r = r0; r < r1; ++r) {
+  for (int t = threadIdx.x; t < (nvec >= 256 ? nvec : slots * nvec); t += blockDim.x) {
+    const int v = t % nvec, slot = t / nvec;
+    float4 s1a = make_float4(0.f, 0.f, 0.f, 0.f), s2a = s1a, s1b = s1a, s2b = s1a;
+    for (long r = r0 + slot; r < r1; r += slots) {
       const float4 a = reinterpret_cast<const float4 *>(x + r * C)[v];
-      const int b = (int)(r % B) & 1;
-      s1[b][0] += a.x; s1[b][1] += a.y; s1[b][2] += a.z; s1[b][3] += a.w;
-      s2[b][0] += a.x * a.x; s2[b][1] += a.y * a.y; s2[b][2] += a.z * a.z; s2[b][3] += a.w * a.w;
-    }
-    for (int b = 0; b < B; ++b)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        sm[(0 * B + b) * C + 4 * v + i] = s1[b][i];
-        sm[(1 * B + b) * C + 4 * v + i] = s2[b][i];
+      if ((r % B) == 0) {
+        s1a.x += a.x; s1a.y += a.y; s1a.z += a.z; s1a.w += a.w;
+        s2a.x += a.x * a.x; s2a.y += a.y * a.y; s2a.z += a.z * a.z; s2a.w += a.w * a.w;
+      } else {
+        s1b.x += a.x; s1b.y += a.y; s1b.z += a.z; s1b.w += a.w;
+        s2b.x += a.x * a.x; s2b.y += a.y * a.y; s2b.z += a.z * a.z; s2b.w += a.w * a.w;
       }
+    }
+    float *p1 = sm + ((0 * slots + slot) * B) * C + 4 * v;
+    float *p2 = sm + ((1 * slots + slot) * B) * C + 4 * v;
+    *reinterpret_cast<float4 *>(p1) = s1a;
+    *reinterpret_cast<float4 *>(p2) = s2a;
+    if (B > 1) {
+      *reinterpret_cast<float4 *>(p1 + C) = s1b;
+      *reinterpret_cast<float4 *>(p2 + C) = s2b;
+    }
   }
   __syncthreads();
   const int cg = C / GN_G;
-  for (int j = threadIdx.x; j < 2 * B * GN_G; j += blockDim.x) {
-    const int st = j / (B * GN_G), b = (j / GN_G) % B, g = j % GN_G;
+  for (int jj = threadIdx.x; jj < 2 * B * GN_G; jj += blockDim.x) {
+    const int st = jj / (B * GN_G), b = (jj / GN_G) % B, g = jj % GN_G;
     float acc = 0.f;
-    for (int c = 0; c < cg; ++c) acc += sm[(st * B + b) * C + g * cg + c];
+    for (int sl = 0; sl < slots; ++sl)
+      for (int c = 0; c < cg; ++c) acc += sm[((st * slots + sl) * B + b) * C + g * cg + c];
     atomicAdd(out + ((long)b * GN_G + g) * 2 + st, (double)acc);
   }
 }
@@ -105,7 +115,13 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(
       orow = (((long)(yy + 1) * (W + 2) + xx + 1) * B + b);
     }
     T *o = out + orow * C + 4 * v;
-    o[0] = from_f<T>(e[0]); o[1] = from_f<T>(e[1]); o[2] = from_f<T>(e[2]); o[3] = from_f<T>(e[3]);
+    if constexpr (sizeof(T) == 2) {  // one 8-byte store of 4 bf16
+      __nv_bfloat162 lo = __floats2bfloat162_rn(e[0], e[1]), hi = __floats2bfloat162_rn(e[2], e[3]);
+      *reinterpret_cast<uint2 *>(o) =
+          make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+    } else {
+      *reinterpret_cast<float4 *>(o) = make_float4(e[0], e[1], e[2], e[3]);
+    }
     if (pad) {  // zero the left / right border columns of this row
       const long pix = row / B;
       const int yy = (int)(pix / W), xx = (int)(pix % W);
@@ -215,10 +231,11 @@ cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, cudaS
   if (B > 2 || C % 4 || C % GN_G) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(out, 0, (size_t)B * GN_G * 2 * sizeof(double), s);
   if (e != cudaSuccess || M == 0) return e;
-  const int blocks = (int)std::min<long>(296, M);
+  const int blocks = (int)std::min<long>(592, M);
   int rpb = (int)((M + blocks - 1) / blocks);
   const int nb = (int)((M + rpb - 1) / rpb);
-  const size_t smem = (size_t)2 * B * C * sizeof(float);
+  const int nvec = C / 4, slots = nvec >= 256 ? 1 : 256 / nvec;
+  const size_t smem = (size_t)2 * slots * B * C * sizeof(float);
   gn_partials_kernel<<<nb, 256, smem, s>>>(x, M, B, C, rpb, out);
   ++g_launches;
   return cudaGetLastError();

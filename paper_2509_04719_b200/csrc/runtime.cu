@@ -165,6 +165,14 @@ struct stadi_ctx {
     uint64_t launches = 0;
     double ms = 0, flops = 0, bytes = 0;
   };
+  // CUDA graphs: one per program step of the installed plan (local mode), captured on
+  // first use on gstream and replayed on the caller's stream.  Dropped with the plan.
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long launches = 0;  // kernels inside (for the launch counter)
+  };
+  std::vector<StepGraph> graphs;
+  cudaStream_t gstream = nullptr;
   bool ktime = false;
   KClass kt[STADI_KCLASS_COUNT];
 
@@ -382,13 +390,22 @@ cudaError_t attention_h(stadi_ctx *ctx, int cls, const void *q, const void *kv, 
   });
 }
 
+void free_graphs(stadi_ctx *ctx);
+
 }  // namespace
 
 #include "unet_exec.cuh"
 
 namespace {
 
+void free_graphs(stadi_ctx *ctx) {
+  for (auto &g : ctx->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  ctx->graphs.clear();
+}
+
 void free_plan_buffers(stadi_ctx *ctx) {
+  free_graphs(ctx);
   unet_free_plan(ctx);
   for (auto &r : ctx->ranks) {
     for (void *p : {(void *)r.x_band, (void *)r.x_res, r.xmod, r.q, r.o, r.h1, (void *)r.eps_raw})
@@ -496,6 +513,7 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi));
     CK(cudaStreamCreateWithFlags(&ctx->astream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
     // positional embedding of the full token grid, fp64 on the host (pins the
     // values to 1 ulp of fp32), [sin(c w), cos(c w), sin(r w), cos(r w)]
@@ -545,6 +563,7 @@ extern "C" void stadi_destroy(stadi_ctx *ctx) {
   if (ctx->world_comm && nccl().CommDestroy) nccl().CommDestroy(ctx->world_comm);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
   if (ctx->astream) cudaStreamDestroy(ctx->astream);
+  if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   if (ctx->emu_stream) cudaStreamDestroy(ctx->emu_stream);
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
   for (auto &k : ctx->kt)
@@ -781,6 +800,7 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
     CK(pmalloc(ctx, &ctx->csilu, (size_t)nt * B * d * ctx->esz));
     CK(cudaStreamSynchronize(ctx->astream));
     ctx->cond_cap_nt = nt;
+    free_graphs(ctx);  // captured steps reference the old conditioning buffers
     ctx->tfreq_nt = 0;
   }
   ctx->n_t = nt;
@@ -1067,6 +1087,48 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
 
 }  // namespace
 
+namespace {
+// STADI_GRAPHS=0 disables the per-step CUDA graphs.
+bool graphs_enabled(stadi_ctx *ctx) {
+  static const int env = [] {
+    const char *e = getenv("STADI_GRAPHS");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  // local mode only (NCCL mode's cross-stream exchange events stay eager), and not
+  // while per-launch kernel timing is on (its events must see every launch)
+  return env && ctx->world == 1 && !ctx->ktime;
+}
+
+// Program step i on stream s: replay its graph, capturing it on first use.
+stadi_status exec_step(stadi_ctx *ctx, uint32_t i, cudaStream_t s) {
+  if (!graphs_enabled(ctx)) return run_phase(ctx, ctx->program[i], s);
+  if (ctx->graphs.size() != ctx->program.size()) ctx->graphs.assign(ctx->program.size(), {});
+  auto &G = ctx->graphs[i];
+  if (!G.exec) {
+    // capture on the context's own stream (the caller's may be the legacy stream)
+    CK(cudaStreamSynchronize(s));
+    const unsigned long long l0 = g_launches;
+    CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
+    const stadi_status st = run_phase(ctx, ctx->program[i], ctx->gstream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(ctx->gstream, &graph);
+    if (st != STADI_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    CK(ec);
+    const cudaError_t ei = cudaGraphInstantiate(&G.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(ei);
+    G.launches = g_launches - l0;
+    g_launches = l0;  // counted when the graph runs
+  }
+  CK(cudaGraphLaunch(G.exec, s));
+  g_launches += G.launches;
+  return STADI_OK;
+}
+}  // namespace
+
 extern "C" stadi_status stadi_denoise_step(stadi_ctx *ctx, uint32_t step, void *stream) {
   ALIVE();
   ctx->last_stream = (cudaStream_t)stream;
@@ -1074,7 +1136,7 @@ extern "C" stadi_status stadi_denoise_step(stadi_ctx *ctx, uint32_t step, void *
   if (!ctx->begun) return ctx_fail(ctx, STADI_ESTATE, "stadi_denoise_step before stadi_begin");
   if (step >= ctx->program.size()) return ctx_fail(ctx, STADI_EINVAL, "step out of range");
   CK(cudaSetDevice(ctx->device));
-  return run_phase(ctx, ctx->program[step], (cudaStream_t)stream);
+  return exec_step(ctx, step, (cudaStream_t)stream);
 }
 
 extern "C" stadi_status stadi_gather(stadi_ctx *ctx, float *out_full, void *stream) {
@@ -1135,7 +1197,7 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
   const unsigned long long l0 = g_launches;
   CK(cudaEventRecord(e0, s));
   ST(stadi_begin(ctx, noise_full, cond, stream));
-  for (uint32_t i = 0; i < ctx->program.size(); ++i) ST(run_phase(ctx, ctx->program[i], s));
+  for (uint32_t i = 0; i < ctx->program.size(); ++i) ST(exec_step(ctx, i, s));
   ST(stadi_gather(ctx, out_full, stream));
   CK(cudaEventRecord(e1, s));
   CK(cudaEventSynchronize(e1));

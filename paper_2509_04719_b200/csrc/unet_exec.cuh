@@ -860,6 +860,7 @@ stadi_status unet_begin(stadi_ctx *ctx, const stadi_cond *cond, cudaStream_t s) 
     CK(pmalloc(ctx, &U->temb_all, (size_t)nt * B * U->temb_total * 4));
     CK(cudaStreamSynchronize(ctx->astream));
     U->cap_nt = nt;
+    free_graphs(ctx);  // captured steps reference the old time-embedding buffers
     ctx->tfreq_nt = 0;
   }
   if (!U->addin) {
