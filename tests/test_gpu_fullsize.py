@@ -1,0 +1,65 @@
+"""Full-size checks (GPU) at BASELINE.json's sizes, in the configuration bench.py
+times (bf16, full depth), where the fp64 oracle cannot run the whole request.
+Properties that hold at any size (PAPER.md L80 / L171):
+
+* fresh exchange == unpatched: with M_warmup = M_base every step exchanges fresh
+  (R9), so the 2-rank band-parallel request equals the 1-rank request up to bf16
+  rounding-order effects (tolerance 2e-2, the north-star bound);
+* the result is bitwise reproducible, and identical with and without the per-step
+  CUDA graphs (kernel timing forces the eager path);
+* outputs are finite and the latent statistics stay sane.
+"""
+import numpy as np
+import pytest
+
+from synth import configs, gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+CASES = [("dit_xl2", 10), ("sdxl", 6), ("sd15", 6), ("pixart_alpha", 4)]
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2509_04719_b200 import stadi
+    return stadi
+
+
+def _ctx(S, name, n_local, W, cfg):
+    ctx = S.Context(S.model_desc(name, S.DTYPE_BF16), n_local=n_local)
+    ctx.load_weights([W[n] for n, _, _ in configs.manifest(cfg)])
+    return ctx
+
+
+@pytest.mark.parametrize("name,steps", CASES)
+def test_fresh_two_band_equals_one_band(S, name, steps):
+    cfg = configs.model(name)
+    W, x, c = gen.weights(cfg), gen.noise(cfg), gen.cond(cfg)
+    u = configs.rows_per_unit(cfg)
+    P = cfg["latent_h"] // u
+    outs = {}
+    for n in (1, 2):
+        ctx = _ctx(S, name, n, W, cfg)
+        try:
+            plan = S.plan([1] * n, steps, steps, P, u)     # M_warmup = M_base: all fresh
+            out = np.zeros_like(x)
+            ctx.run(plan, x, c, out)
+            outs[n] = out.astype(np.float64)
+            if n == 1:   # reproducible, graphs == eager (kernel timing disables graphs)
+                again = np.zeros_like(x)
+                ctx.run(plan, x, c, again)
+                assert np.array_equal(again, out)
+                ctx.kernel_timing(True)
+                eager = np.zeros_like(x)
+                ctx.run(plan, x, c, eager)
+                ctx.kernel_timing(False)
+                assert np.array_equal(eager, out)
+        finally:
+            ctx.close()
+    a, b = outs[1], outs[2]
+    assert np.all(np.isfinite(a)) and np.all(np.isfinite(b))
+    assert 0.01 < np.std(a) < 100
+    err = float(np.max(np.abs(a - b)) / np.max(np.abs(a)))
+    print(f"{name}: fresh 2-band vs 1-band max-abs-rel {err:.3e}")
+    assert err <= 2e-2
