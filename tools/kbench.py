@@ -59,6 +59,11 @@ def attn_sweep():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "sweep":
     attn_sweep()
+elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "attn":
+    attn(16384, 16384, 2, 16, 72)
+    attn(4096, 4096, 2, 10, 64)
+    attn(4096, 4096, 2, 8, 40)
+    attn(1024, 1024, 2, 8, 160)
 elif __name__ == "__main__":
     attn(16384, 16384, 2, 16, 72)
     attn(8192, 16384, 2, 16, 72)
