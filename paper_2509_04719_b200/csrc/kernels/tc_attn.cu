@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
     float m_run[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(&s_full[g], j & 1);
+      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(3, g, j);
       tc_fence_after();
       const int valid = Nkv - j * AKT;
       float v[4 * NR];
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&s_free[g]);
+      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(4, g, j);
       if (valid < AKT) {
 #pragma unroll
         for (int i = 0; i < 4 * NR; ++i)
@@ -454,6 +456,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
         mt[rr] = m * scale_log2;
       }
+      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(5, g, j);
       float factor[2] = {1.f, 1.f};
       bool grow = false;
 #pragma unroll
@@ -468,6 +471,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         mbar_wait(&o_done[g], (j - 1) & 1);
         tc_fence_after();
       }
+      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(9, g, j);
       if (j > 0 && __any_sync(0xffffffffu, grow)) {
         static_assert(NO % 2 == 0, "O rescale in 16-column pieces");
 #pragma unroll
@@ -486,6 +490,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         if (g == 1) mbar_wait(&tok[1], j & 1);
         else if (j > 0) mbar_wait(&tok[0], (j - 1) & 1);
       }
+      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(7, g, j);
       const uint64_t sc2 = pack_f32x2(scale_log2, scale_log2);
       const uint64_t nm2[2] = {pack_f32x2(-m_run[0], -m_run[0]), pack_f32x2(-m_run[1], -m_run[1])};
       uint64_t acc[2][2] = {{0, 0}, {0, 0}};
@@ -522,6 +527,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[g]);
+      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(6, g, j);
     }
     // epilogue: quad-reduce the row sums, O / l -> bf16 (rows past Nq are padding)
 #pragma unroll

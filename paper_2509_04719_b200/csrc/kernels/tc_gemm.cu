@@ -11,7 +11,7 @@
 //  * warp 1: allocates TMEM and issues tcgen05.mma (M=128, N=BN, K=16) from
 //    one elected lane; tcgen05.commit frees smem stages / publishes an
 //    accumulator;
-//  * warps 2-5: epilogue — tcgen05.ld of the fp32 accumulator (each warp owns
+//  * warps 2-9: epilogue — tcgen05.ld of the fp32 accumulator (each warp owns
 //    its 32-lane TMEM quarter), fused bias / GELU / adaLN-gated residual /
 //    K-V-slot scatter, direct global stores;
 //  * the accumulator is double-buffered in TMEM (2 x BN columns) so the
@@ -31,16 +31,25 @@ namespace {
 constexpr int GBM = 128, GBK = 64;
 
 constexpr int EPI_LD = 33;                       // staging row stride (floats, bank-free)
-constexpr int EPI_SMEM = 4 * 32 * EPI_LD * 4;    // 4 epilogue warps x 32 x 32 fp32
+constexpr int EPI_WARPS = 8;                     // two per TMEM lane quarter (column halves)
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int EPI_SMEM = EPI_WARPS * 32 * EPI_LD * 4;  // per warp 32 x 32 fp32 staging
 
-template <int BN>
+// MC: 1 = one CTA per tile; 2 = CTA pair, each CTA its own 128-row tile, the W tile
+// loaded half by each CTA and multicast to both; 3 = CTA pair running ONE
+// M = 256 tcgen05.mma (cta_group::2) issued by the leader: each CTA stages its
+// own 128 A rows and HALF of the W tile, so per-SM shared-memory traffic per
+// MMA is halved.
+template <int BN, int MC = 1>
 struct GemmCfg {
   static constexpr int A_BYTES = GBM * GBK * 2;              // 16 KB
-  static constexpr int B_BYTES = BN * GBK * 2;
+  static constexpr int B_BYTES = (MC == 3 ? BN / 2 : BN) * GBK * 2;  // per CTA
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (196 * 1024) / STAGE > 8 ? 8 : (196 * 1024) / STAGE;
+  static constexpr int RING = 227 * 1024 - EPI_SMEM - 1024 /*align*/ - 256 /*barriers*/;
+  static constexpr int STAGES = RING / STAGE > 8 ? 8 : RING / STAGE;
   static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
   static constexpr int SMEM = STAGES * STAGE + EPI_SMEM + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(SMEM <= 227 * 1024 && STAGES >= 2, "GEMM shared memory");
 };
 
 // Epilogue of two adjacent columns (col even) of one row, vectorised stores.
@@ -134,10 +143,12 @@ struct ConvGeo {
 };
 
 template <int BN, int EPI, int MC, int AM>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, EpiParams ep, ConvGeo cg) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, MC>;
+  constexpr int NCL = MC == 1 ? 1 : 2;  // cluster size
+  constexpr bool PAIR = MC == 3;        // cta_group::2 MMA
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -152,12 +163,12 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_n = N / BN, tiles_m = (M + GBM - 1) / GBM;
   const int nkb = K / GBK;
-  // tile walk: MC tiles (one per cluster CTA) per work item, N fastest
-  const int crank = MC == 2 ? (int)cluster_ctarank() : 0;
-  const int n_items = ((tiles_m + MC - 1) / MC) * tiles_n;
-  const int item0 = blockIdx.x / MC, item_step = gridDim.x / MC;
+  // tile walk: NCL row tiles (one per cluster CTA) per work item, N fastest
+  const int crank = NCL == 2 ? (int)cluster_ctarank() : 0;
+  const int n_items = ((tiles_m + NCL - 1) / NCL) * tiles_n;
+  const int item0 = blockIdx.x / NCL, item_step = gridDim.x / NCL;
   auto tile_of = [&](int item, int *mb, int *nb) {
-    *mb = (item / tiles_n) * MC + crank;
+    *mb = (item / tiles_n) * NCL + crank;
     *nb = item % tiles_n;
   };
 
@@ -166,18 +177,21 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tmB);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MC);
+      mbar_init(&empty[s], MC == 2 ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], (PAIR ? 2 : 1) * EPI_WARPS);  // one arrive per epilogue warp (of the pair)
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_cg2(tmem_slot, C::TMEM_COLS);
+    else tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
-  if (MC == 2) cluster_sync();  // partner's barriers initialised before any multicast
+  if (NCL == 2) cluster_sync();  // partner's barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -190,16 +204,25 @@ __global__ void __launch_bounds__(192, 1)
         tile_of(item, &mb, &nb);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], C::STAGE);
+          if (!PAIR || crank == 0) mbar_expect_tx(&full[s], (PAIR ? 2 : 1) * C::STAGE);
           if constexpr (AM == 1) {
             const int cpb = cg.C / GBK, tap = kb / cpb, c0 = (kb % cpb) * GBK;
             const int p0 = mb * (GBM / cg.B);  // first output pixel of the tile
-            tma_load_3d(&tmA, sA + s * C::A_BYTES, &full[s], c0,
-                        (p0 % cg.W + tap % 3) * cg.B, p0 / cg.W + tap / 3);
+            if constexpr (PAIR)
+              tma_load_3d_cg2(&tmA, sA + s * C::A_BYTES, &full[s], c0,
+                              (p0 % cg.W + tap % 3) * cg.B, p0 / cg.W + tap / 3);
+            else
+              tma_load_3d(&tmA, sA + s * C::A_BYTES, &full[s], c0,
+                          (p0 % cg.W + tap % 3) * cg.B, p0 / cg.W + tap / 3);
+          } else if constexpr (PAIR) {
+            tma_load_2d_cg2(&tmA, sA + s * C::A_BYTES, &full[s], kb * GBK, mb * GBM);
           } else {
             tma_load_2d(&tmA, sA + s * C::A_BYTES, &full[s], kb * GBK, mb * GBM);
           }
-          if constexpr (MC == 2)
+          if constexpr (PAIR)
+            tma_load_2d_cg2(&tmB, sB + s * C::B_BYTES, &full[s], kb * GBK,
+                            nb * BN + crank * (BN / 2));
+          else if constexpr (MC == 2)
             tma_load_2d_mc(&tmB, sB + s * C::B_BYTES + crank * (C::B_BYTES / 2), &full[s],
                            kb * GBK, nb * BN + crank * (BN / 2), (uint16_t)0x3);
           else
@@ -212,8 +235,8 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      constexpr uint32_t idesc = umma_idesc_bf16(GBM, BN, 0, 0);
+    if (lane == 0 && (!PAIR || crank == 0)) {  // ---------------- MMA issuer (pair: leader)
+      constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * GBM : GBM, BN, 0, 0);
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
@@ -232,20 +255,24 @@ __global__ void __launch_bounds__(192, 1)
           for (int k = 0; k < GBK / 16; ++k) {
             const uint64_t ad = umma_desc(a0 + k * 32, 16, 1024, SWZ_128B);
             const uint64_t bd = umma_desc(b0 + k * 32, 16, 1024, SWZ_128B);
-            umma_bf16(dtm, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (PAIR) umma_bf16_cg2(dtm, ad, bd, idesc, (kb | k) != 0);
+            else umma_bf16(dtm, ad, bd, idesc, (kb | k) != 0);
           }
-          if constexpr (MC == 2) umma_commit_mc(&empty[s], (uint16_t)0x3);
+          if constexpr (PAIR) umma_commit_cg2(&empty[s]);
+          else if constexpr (MC == 2) umma_commit_mc(&empty[s], (uint16_t)0x3);
           else umma_commit(&empty[s]);
           if (++s == C::STAGES) {
             s = 0;
             ph ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (PAIR) umma_commit_cg2(&tfull[acc]);
+        else umma_commit(&tfull[acc]);
       }
     }
   } else {  // ---------------------------- epilogue warps 2..5
     const int qd = warp & 3;  // TMEM lane quarter this warp may access
+    const int hcol = (warp - 2) / 4 * (BN / 2);  // first accumulator column of this warp
     int it = 0;
     for (int item = item0; item < n_items; item += item_step, ++it) {
       int mb, nb;
@@ -258,15 +285,18 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + acc * BN;
       float *stg = stg_all + (warp - 2) * 32 * EPI_LD;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = hcol; c0 < hcol + BN / 2; c0 += 32) {
         // TMEM -> registers (lane = row) -> smem, then coalesced: lanes cover
         // 16 column pairs of two rows per step
         float v[32];
         tmem_ld32(tbase + c0, v);
-        if (c0 + 32 >= BN) {  // accumulator fully read: release it to the MMA warp
+        if (c0 + 32 >= hcol + BN / 2) {  // this warp's part read: release it
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if constexpr (PAIR) mbar_arrive_cluster(&tempty[acc], 0);  // the leader's
+            else mbar_arrive(&tempty[acc]);
+          }
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i) stg[lane * EPI_LD + i] = v[i];
@@ -292,10 +322,11 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (MC == 2) cluster_sync();  // no CTA leaves while its partner may still signal it
+  if (NCL == 2) cluster_sync();  // no CTA leaves while its partner may still signal it
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, C::TMEM_COLS);
+    if constexpr (PAIR) tmem_dealloc_cg2(tmem, C::TMEM_COLS);
+    else tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
 
@@ -343,7 +374,8 @@ namespace {
 template <int BN, int EPI, int MC, int AM>
 cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const EpiParams &ep,
                         int max_ctas, const ConvGeo &cg, int conv_h, cudaStream_t s) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, MC>;
+  constexpr int NCL = MC == 1 ? 1 : 2;
   CUtensorMap ta, tb;
   bool ok;
   if constexpr (AM == 1) {  // P [h+2, (W+2) B, C]
@@ -358,7 +390,7 @@ cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const
     ok = make_tmap(&ta, A, 2, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   const uint64_t db[2] = {(uint64_t)K, (uint64_t)N}, sb[1] = {(uint64_t)K * 2};
-  const uint32_t bb[2] = {GBK, (uint32_t)(BN / MC)};
+  const uint32_t bb[2] = {GBK, (uint32_t)(BN / NCL)};
   if (!ok || !make_tmap(&tb, W, 2, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   static bool attr_set = false;  // per template instance
@@ -368,17 +400,17 @@ cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int items = ((M + GBM - 1) / GBM + MC - 1) / MC * (N / BN);
-  int grid = std::min(items * MC, max_ctas / MC * MC);
-  if (grid < MC) grid = MC;
+  const int items = ((M + GBM - 1) / GBM + NCL - 1) / NCL * (N / BN);
+  int grid = std::min(items * NCL, max_ctas / NCL * NCL);
+  if (grid < NCL) grid = NCL;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(192);
+  cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = MC;
+  at[0].val.clusterDim.x = NCL;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
@@ -410,6 +442,7 @@ cudaError_t dispatch_epi(const bf16 *A, const bf16 *W, int M, int N, int K, int 
 template <int BN>
 cudaError_t dispatch_mc(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
                         const EpiParams &ep, int max_ctas, int mc, cudaStream_t s) {
+  if (mc == 3) return dispatch_epi<BN, 3>(A, W, M, N, K, epi, ep, max_ctas, s);
   if (mc == 2) return dispatch_epi<BN, 2>(A, W, M, N, K, epi, ep, max_ctas, s);
   return dispatch_epi<BN, 1>(A, W, M, N, K, epi, ep, max_ctas, s);
 }
@@ -443,13 +476,26 @@ int pick_bn(int tm, int N, int max_ctas) {
   return best;
 }
 
-// STADI_GEMM_MC=0 in the environment forces single-CTA tiles (A/B comparisons).
-bool gemm_mc_disabled() {
+// CTA-pair mode of the GEMMs with >= 4 row tiles (see GemmCfg).  Default (measured
+// on B200, tools/kbench.py gemm): the cta_group::2 M = 256 MMA, except for the
+// fp32 residual read-modify-write epilogues, whose HBM-bound epilogue prefers
+// two independent 128-row tiles with a multicast W tile (C5 out-proj 654 vs 613
+// TFLOP/s; 8192^3 1342 vs 1278 the other way).  STADI_GEMM_MC=0 / 2 / 3 forces
+// single-CTA tiles / multicast pairs / the cta_group::2 MMA (A/B comparisons).
+int gemm_pair_mode() {
   static const int v = [] {
     const char *e = getenv("STADI_GEMM_MC");
-    return (e && e[0] == '0') ? 1 : 0;
+    if (e && e[0] == '0') return 1;
+    if (e && e[0] == '2') return 2;
+    if (e && e[0] == '3') return 3;
+    return 0;
   }();
-  return v != 0;
+  return v;
+}
+int pair_mode_for(int tm, int max_ctas, int epi) {
+  if (tm < 4 || max_ctas < 2) return 1;
+  if (gemm_pair_mode()) return gemm_pair_mode();
+  return (epi == EPI_GATED_RES || epi == EPI_RES) ? 2 : 3;
 }
 
 cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
@@ -460,8 +506,7 @@ cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int 
     return cudaErrorInvalidValue;
   const int tm = (M + GBM - 1) / GBM;
   const int best = pick_bn(tm, N, max_ctas);
-  // CTA pairs with a multicast W tile once there are enough row tiles to pair
-  const int mc = (tm >= 4 && max_ctas >= 2 && !gemm_mc_disabled()) ? 2 : 1;
+  const int mc = pair_mode_for(tm, max_ctas, epi);
   switch (best) {
     case 256: return dispatch_mc<256>(A, W, M, N, K, epi, ep, max_ctas, mc, s);
     case 192: return dispatch_mc<192>(A, W, M, N, K, epi, ep, max_ctas, mc, s);
@@ -480,18 +525,19 @@ cudaError_t tc_conv3x3_bf16(const bf16 *P, const bf16 *Wt, int h, int W, int B, 
   const ConvGeo g{W, B, C};
   const int M = h * wb, tm = (M + GBM - 1) / GBM;
   const int best = pick_bn(tm, N, max_ctas);
-  const int mc = (tm >= 4 && max_ctas >= 2 && !gemm_mc_disabled()) ? 2 : 1;
+  const int mc = pair_mode_for(tm, max_ctas, epi);
 #define STADI_CONV_CASE(BNV)                                                          \
   case BNV:                                                                           \
-    return mc == 2 ? dispatch_conv<BNV, 2>(P, Wt, h, g, N, epi, ep, max_ctas, s)      \
-                   : dispatch_conv<BNV, 1>(P, Wt, h, g, N, epi, ep, max_ctas, s);
+    return mc == 3   ? dispatch_conv<BNV, 3>(P, Wt, h, g, N, epi, ep, max_ctas, s)    \
+           : mc == 2 ? dispatch_conv<BNV, 2>(P, Wt, h, g, N, epi, ep, max_ctas, s)    \
+                     : dispatch_conv<BNV, 1>(P, Wt, h, g, N, epi, ep, max_ctas, s);
   switch (best) {
     STADI_CONV_CASE(256)
     STADI_CONV_CASE(192)
     STADI_CONV_CASE(128)
-    default: return mc == 2 ? dispatch_conv<64, 2>(P, Wt, h, g, N, epi, ep, max_ctas, s)
-                            : dispatch_conv<64, 1>(P, Wt, h, g, N, epi, ep, max_ctas, s);
+    STADI_CONV_CASE(64)
   }
+  return cudaErrorInvalidValue;
 #undef STADI_CONV_CASE
 }
 

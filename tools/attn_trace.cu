@@ -1,5 +1,5 @@
 // Standalone timeline trace of the attention kernel (CTA 0): build on the box with
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DSTADI_ATTN_TRACE \
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -rdc=true -DSTADI_ATTN_TRACE \
 //     -Iinclude -Ipaper_2509_04719_b200/csrc tools/attn_trace.cu \
 //     paper_2509_04719_b200/csrc/kernels/{tc_attn,tc_gemm,simt}.cu -o /tmp/attn_trace
 #include <cstdio>
@@ -17,13 +17,13 @@ int main(int argc, char **argv) {
   cudaDeviceSynchronize();
   std::vector<long long> t(16 * 2 * 64);
   cudaMemcpyFromSymbol(t.data(), g_attn_trace, t.size() * 8);
-  const char *names[9] = {"mma:s_free", "mma:S_iss", "mma:p_full", "sm:s_full",
-                          "sm:loaded", "sm:max", "sm:p_arr", "sm:tok", "mma:PV_iss"};
+  const char *names[10] = {"mma:s_free", "mma:S_iss", "mma:p_full", "sm:s_full",
+                           "sm:loaded", "sm:max", "sm:p_arr", "sm:tok", "mma:PV_iss", "sm:o_done"};
   long long t0 = t[(3 * 2 + 0) * 64 + 0];
-  for (int j = 0; j < 12; ++j)
+  for (int j = 0; j < 16; ++j)
     for (int g = 0; g < 2; ++g) {
       printf("j=%2d g=%d:", j, g);
-      for (int e = 0; e < 9; ++e) printf(" %s=%6lld", names[e], t[(e * 2 + g) * 64 + j] - t0);
+      for (int e = 0; e < 10; ++e) printf(" %s=%6lld", names[e], t[(e * 2 + g) * 64 + j] - t0);
       printf("\n");
     }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));

@@ -59,6 +59,13 @@ def attn_sweep():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "sweep":
     attn_sweep()
+elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "gemm":
+    for M, N, K, e in [(32768, 3456, 1152, S.EPI_STORE), (32768, 1152, 1152, S.EPI_GATED_RES),
+                       (32768, 4608, 1152, S.EPI_GELU), (32768, 1152, 4608, S.EPI_GATED_RES),
+                       (8192, 8192, 8192, S.EPI_STORE), (2048, 1280, 1280, S.EPI_STORE),
+                       (2048, 10240, 1280, S.EPI_STORE), (2048, 1280, 5120, S.EPI_RES),
+                       (8192, 640, 640, S.EPI_STORE), (32768, 320, 2880, S.EPI_F32)]:
+        gemm(M, N, K, e)
 elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "attn":
     attn(16384, 16384, 2, 16, 72)
     attn(4096, 4096, 2, 10, 64)
