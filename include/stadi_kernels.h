@@ -45,6 +45,11 @@ typedef struct {
   void *kv_a, *kv_b;   /* EPI_QKV: slot(s) [N_tok, B, 2, d]; kv_b may be NULL  */
   int64_t kv_row0;
   int32_t d;
+  float *ws;           /* BF16 GEMM split-K workspace (f32, caller-owned device memory,
+                          ws_elems floats) or NULL: with a workspace, GEMMs whose tiles
+                          fill at most half the SMs split K and reduce the partials in a
+                          fixed order (bitwise reproducible)                     */
+  int64_t ws_elems;
 } stadi_k_epi;
 
 /* out = epilogue(A[M,K] . W[N,K]^T).  BF16 path: K % 64 == 0, N % 64 == 0. */

@@ -56,6 +56,8 @@ struct EpiParams {
   void *kv_b;          // optional second slot (publish version), may be nullptr
   long kv_row0;        // first own row of the slot = tok_begin * B
   int d;
+  float *ws;           // tcgen05 GEMM split-K workspace (fp32 partial tiles), or nullptr
+  long ws_elems;
 };
 
 // Apply the epilogue to `n` consecutive columns col..col+n-1 of one row.

@@ -33,6 +33,8 @@ extern "C" stadi_status stadi_k_gemm(int32_t dtype, const void *A, const void *W
   ep.kv_b = e->kv_b;
   ep.kv_row0 = e->kv_row0;
   ep.d = e->d;
+  ep.ws = e->ws;
+  ep.ws_elems = e->ws ? e->ws_elems : 0;
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == STADI_DTYPE_BF16) {
     int dev = 0, sms = 148;
@@ -97,16 +99,31 @@ extern "C" stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // split-K workspace (used when the conv's tiles fill at most half the SMs)
+  float *ws = nullptr;
+  if (dtype == STADI_DTYPE_BF16) {
+    ep.ws_elems = (long)M * N * 16;
+    cudaError_t e = cudaMallocAsync(&ws, (size_t)ep.ws_elems * 4, s);
+    if (e != cudaSuccess) return cu(e, "cudaMallocAsync");
+    ep.ws = ws;
+  }
   if (dtype == STADI_DTYPE_BF16 && implicit) {
-    if (mode != 0) return fail(nullptr, STADI_EINVAL, "implicit conv: stride 1 only");
-    return cu(tc_conv3x3_bf16((const bf16 *)P, (const bf16 *)Wt, h, W, B, C, N, EPI_CONV, ep, sms,
-                              s),
-              "tc_conv3x3_bf16");
+    if (mode != 0) {
+      cudaFreeAsync(ws, s);
+      return fail(nullptr, STADI_EINVAL, "implicit conv: stride 1 only");
+    }
+    cudaError_t e =
+        tc_conv3x3_bf16((const bf16 *)P, (const bf16 *)Wt, h, W, B, C, N, EPI_CONV, ep, sms, s);
+    cudaFreeAsync(ws, s);
+    return cu(e, "tc_conv3x3_bf16");
   }
   const size_t esz = dtype == STADI_DTYPE_BF16 ? 2 : 4;
   void *A = nullptr;
   cudaError_t e = cudaMallocAsync(&A, (size_t)M * kp * esz, s);
-  if (e != cudaSuccess) return cu(e, "cudaMallocAsync");
+  if (e != cudaSuccess) {
+    if (ws) cudaFreeAsync(ws, s);
+    return cu(e, "cudaMallocAsync");
+  }
   if (dtype == STADI_DTYPE_BF16) {
     e = im2col<bf16>((const bf16 *)P, h, W, B, C, mode, kp, (bf16 *)A, s);
     if (e == cudaSuccess) e = tc_gemm_bf16((const bf16 *)A, (const bf16 *)Wt, M, N, kp, EPI_CONV,
@@ -117,6 +134,7 @@ extern "C" stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void
                                                EPI_CONV, ep, s);
   }
   cudaFreeAsync(A, s);
+  if (ws) cudaFreeAsync(ws, s);
   return cu(e, "conv3x3");
 }
 

@@ -145,7 +145,7 @@ struct ConvGeo {
 template <int BN, int EPI, int MC, int AM>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   int M, int N, int K, EpiParams ep, ConvGeo cg) {
+                   int M, int N, int K, EpiParams ep, ConvGeo cg, int ksplit) {
   using C = GemmCfg<BN, MC>;
   constexpr int NCL = MC == 1 ? 1 : 2;  // cluster size
   constexpr bool PAIR = MC == 3;        // cta_group::2 MMA
@@ -165,11 +165,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int nkb = K / GBK;
   // tile walk: NCL row tiles (one per cluster CTA) per work item, N fastest
   const int crank = NCL == 2 ? (int)cluster_ctarank() : 0;
-  const int n_items = ((tiles_m + NCL - 1) / NCL) * tiles_n;
+  // split-K (ksplit > 1): item = (tile, split); split sp accumulates k blocks
+  // [sp nkb / ksplit, (sp + 1) nkb / ksplit) and stores an fp32 partial tile into
+  // ep.ws[sp]; splitk_reduce_kernel sums the partials in split order (deterministic)
+  // and runs the epilogue
+  const int n_items = ((tiles_m + NCL - 1) / NCL) * tiles_n * ksplit;
   const int item0 = blockIdx.x / NCL, item_step = gridDim.x / NCL;
   auto tile_of = [&](int item, int *mb, int *nb) {
-    *mb = (item / tiles_n) * NCL + crank;
-    *nb = item % tiles_n;
+    const int t = item / ksplit;
+    *mb = (t / tiles_n) * NCL + crank;
+    *nb = t % tiles_n;
+  };
+  auto k_range = [&](int item, int *kb0, int *kb1) {
+    const int sp = item % ksplit;
+    *kb0 = (int)((long)sp * nkb / ksplit);
+    *kb1 = (int)((long)(sp + 1) * nkb / ksplit);
   };
 
   if (warp == 0 && lane == 0) {
@@ -200,9 +210,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int item = item0; item < n_items; item += item_step) {
-        int mb, nb;
+        int mb, nb, kb0, kb1;
         tile_of(item, &mb, &nb);
-        for (int kb = 0; kb < nkb; ++kb) {
+        k_range(item, &kb0, &kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           if (!PAIR || crank == 0) mbar_expect_tx(&full[s], (PAIR ? 2 : 1) * C::STAGE);
           if constexpr (AM == 1) {
@@ -246,7 +257,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t dtm = tmem + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
+        int kb0, kb1;
+        k_range(item, &kb0, &kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + s * C::A_BYTES);
@@ -255,8 +268,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < GBK / 16; ++k) {
             const uint64_t ad = umma_desc(a0 + k * 32, 16, 1024, SWZ_128B);
             const uint64_t bd = umma_desc(b0 + k * 32, 16, 1024, SWZ_128B);
-            if constexpr (PAIR) umma_bf16_cg2(dtm, ad, bd, idesc, (kb | k) != 0);
-            else umma_bf16(dtm, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (PAIR) umma_bf16_cg2(dtm, ad, bd, idesc, (kb - kb0) | k);
+            else umma_bf16(dtm, ad, bd, idesc, (kb - kb0) | k);
           }
           if constexpr (PAIR) umma_commit_cg2(&empty[s]);
           else if constexpr (MC == 2) umma_commit_mc(&empty[s], (uint16_t)0x3);
@@ -270,9 +283,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         else umma_commit(&tfull[acc]);
       }
     }
-  } else {  // ---------------------------- epilogue warps 2..5
+  } else {  // ---------------------------- epilogue warps 2..9
     const int qd = warp & 3;  // TMEM lane quarter this warp may access
-    const int hcol = (warp - 2) / 4 * (BN / 2);  // first accumulator column of this warp
+    const int half = (warp - 2) / 4;  // 32-column chunks half, half + 2, ... of the tile
+    constexpr int NCHUNK = BN / 32;
+    static_assert(BN % 32 == 0, "epilogue chunks");
     int it = 0;
     for (int item = item0; item < n_items; item += item_step, ++it) {
       int mb, nb;
@@ -285,12 +300,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + acc * BN;
       float *stg = stg_all + (warp - 2) * 32 * EPI_LD;
 #pragma unroll 1
-      for (int c0 = hcol; c0 < hcol + BN / 2; c0 += 32) {
+      for (int ch = half; ch < NCHUNK; ch += 2) {
+        const int c0 = 32 * ch;
         // TMEM -> registers (lane = row) -> smem, then coalesced: lanes cover
         // 16 column pairs of two rows per step
         float v[32];
         tmem_ld32(tbase + c0, v);
-        if (c0 + 32 >= hcol + BN / 2) {  // this warp's part read: release it
+        if (ch + 2 >= NCHUNK) {  // this warp's chunks read: release the accumulator
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -302,6 +318,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int i = 0; i < 32; ++i) stg[lane * EPI_LD + i] = v[i];
         __syncwarp();
         const int cc = 2 * (lane & 15), col = nb * BN + c0 + cc;
+        if (ksplit > 1) {  // fp32 partial tile of split `item % ksplit`
+          float *wsp = ep.ws + (long)(item % ksplit) * M * N;
+#pragma unroll
+          for (int it = 0; it < 16; ++it) {
+            const int r = 2 * it + (lane >> 4);
+            if (row0 + r < M)
+              *reinterpret_cast<float2 *>(wsp + (long)(row0 + r) * N + col) =
+                  make_float2(stg[r * EPI_LD + cc], stg[r * EPI_LD + cc + 1]);
+          }
+          __syncwarp();
+          continue;
+        }
         const EpiCol ecol = epi_col<EPI>(ep, col);
         EpiIn in[16];
 #pragma unroll
@@ -327,6 +355,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     if constexpr (PAIR) tmem_dealloc_cg2(tmem, C::TMEM_COLS);
     else tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// Split-K epilogue: sum the ksplit fp32 partial tiles in split order (the same
+// order every run: deterministic), then the GEMM epilogue on the column pair.
+template <int EPI>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(int M, int N, int ksplit, EpiParams ep) {
+  const long quads = (long)M * (N / 4);
+  const long plane = (long)M * N;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < quads;
+       i += (long)gridDim.x * blockDim.x) {
+    const int row = (int)(i / (N / 4)), col = 4 * (int)(i % (N / 4));
+    const float *w = ep.ws + (long)row * N + col;
+    float4 a = *reinterpret_cast<const float4 *>(w);
+    for (int sp = 1; sp < ksplit; ++sp) {
+      const float4 b = *reinterpret_cast<const float4 *>(w + sp * plane);
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    const EpiCol c0 = epi_col<EPI>(ep, col), c1 = epi_col<EPI>(ep, col + 2);
+    const EpiIn i0 = epi_load<EPI>(ep, row, col), i1 = epi_load<EPI>(ep, row, col + 2);
+    epi_finish<EPI>(ep, row, col, a.x, a.y, i0, c0);
+    epi_finish<EPI>(ep, row, col + 2, a.z, a.w, i1, c1);
   }
 }
 
@@ -371,9 +424,19 @@ bool make_tmap(CUtensorMap *m, const void *base, int rank, const uint64_t *dims,
 }
 
 namespace {
+constexpr int NCL_OF(int mc) { return mc == 1 ? 1 : 2; }
+// STADI_SPLITK=0 disables split-K (A/B comparisons).
+bool splitk_disabled() {
+  static const int v = [] {
+    const char *e = getenv("STADI_SPLITK");
+    return (e && e[0] == '0') ? 1 : 0;
+  }();
+  return v != 0;
+}
 template <int BN, int EPI, int MC, int AM>
 cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const EpiParams &ep,
-                        int max_ctas, const ConvGeo &cg, int conv_h, cudaStream_t s) {
+                        int max_ctas, const ConvGeo &cg, int conv_h, int ksplit, cudaStream_t s) {
+  if (ksplit > 1 && (!ep.ws || (long)ksplit * M * N > ep.ws_elems)) return cudaErrorInvalidValue;
   using C = GemmCfg<BN, MC>;
   constexpr int NCL = MC == 1 ? 1 : 2;
   CUtensorMap ta, tb;
@@ -400,7 +463,7 @@ cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int items = ((M + GBM - 1) / GBM + NCL - 1) / NCL * (N / BN);
+  const int items = ((M + GBM - 1) / GBM + NCL - 1) / NCL * (N / BN) * ksplit;
   int grid = std::min(items * NCL, max_ctas / NCL * NCL);
   if (grid < NCL) grid = NCL;
   cudaLaunchConfig_t cfg{};
@@ -416,61 +479,87 @@ cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, EPI, MC, AM>, ta, tb, M, N, K, ep,
-                                     cg);
+                                     cg, ksplit);
   ++g_launches;
   if (e != cudaSuccess) return e;
+  if (ksplit > 1) {
+    const long quads = (long)M * (N / 4);
+    const int rb = (int)std::min<long>((quads + 255) / 256, 148L * 8);
+    splitk_reduce_kernel<EPI><<<rb, 256, 0, s>>>(M, N, ksplit, ep);
+    ++g_launches;
+  }
   return cudaGetLastError();
 }
 
 template <int BN, int MC>
 cudaError_t dispatch_epi(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
-                         const EpiParams &ep, int max_ctas, cudaStream_t s) {
+                         const EpiParams &ep, int max_ctas, int ks, cudaStream_t s) {
   const ConvGeo g{0, 0, 0};
   switch (epi) {
-    case EPI_STORE: return launch_gemm<BN, EPI_STORE, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
-    case EPI_GELU: return launch_gemm<BN, EPI_GELU, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
+    case EPI_STORE: return launch_gemm<BN, EPI_STORE, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, ks, s);
+    case EPI_GELU: return launch_gemm<BN, EPI_GELU, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, ks, s);
     case EPI_GATED_RES:
-      return launch_gemm<BN, EPI_GATED_RES, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
-    case EPI_RES: return launch_gemm<BN, EPI_RES, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
-    case EPI_QKV: return launch_gemm<BN, EPI_QKV, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
-    case EPI_F32: return launch_gemm<BN, EPI_F32, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
-    case EPI_CONV: return launch_gemm<BN, EPI_CONV, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
-    case EPI_GEGLU: return launch_gemm<BN, EPI_GEGLU, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, s);
+      return launch_gemm<BN, EPI_GATED_RES, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, ks, s);
+    case EPI_RES: return launch_gemm<BN, EPI_RES, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, ks, s);
+    case EPI_QKV: return launch_gemm<BN, EPI_QKV, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, ks, s);
+    case EPI_F32: return launch_gemm<BN, EPI_F32, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, ks, s);
+    case EPI_CONV: return launch_gemm<BN, EPI_CONV, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, ks, s);
+    case EPI_GEGLU: return launch_gemm<BN, EPI_GEGLU, MC, 0>(A, W, M, N, K, ep, max_ctas, g, 0, ks, s);
   }
   return cudaErrorInvalidValue;
 }
 template <int BN>
 cudaError_t dispatch_mc(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
-                        const EpiParams &ep, int max_ctas, int mc, cudaStream_t s) {
-  if (mc == 3) return dispatch_epi<BN, 3>(A, W, M, N, K, epi, ep, max_ctas, s);
-  if (mc == 2) return dispatch_epi<BN, 2>(A, W, M, N, K, epi, ep, max_ctas, s);
-  return dispatch_epi<BN, 1>(A, W, M, N, K, epi, ep, max_ctas, s);
+                        const EpiParams &ep, int max_ctas, int mc, int ks, cudaStream_t s) {
+  if (mc == 3) return dispatch_epi<BN, 3>(A, W, M, N, K, epi, ep, max_ctas, ks, s);
+  if (mc == 2) return dispatch_epi<BN, 2>(A, W, M, N, K, epi, ep, max_ctas, ks, s);
+  return dispatch_epi<BN, 1>(A, W, M, N, K, epi, ep, max_ctas, ks, s);
 }
 template <int BN, int MC>
 cudaError_t dispatch_conv(const bf16 *P, const bf16 *W, int h, const ConvGeo &g, int N, int epi,
-                          const EpiParams &ep, int max_ctas, cudaStream_t s) {
+                          const EpiParams &ep, int max_ctas, int ks, cudaStream_t s) {
   const int M = h * g.W * g.B, K = 9 * g.C;
   if (epi == EPI_CONV)
-    return launch_gemm<BN, EPI_CONV, MC, 1>(P, W, M, N, K, ep, max_ctas, g, h, s);
+    return launch_gemm<BN, EPI_CONV, MC, 1>(P, W, M, N, K, ep, max_ctas, g, h, ks, s);
   if (epi == EPI_F32)
-    return launch_gemm<BN, EPI_F32, MC, 1>(P, W, M, N, K, ep, max_ctas, g, h, s);
+    return launch_gemm<BN, EPI_F32, MC, 1>(P, W, M, N, K, ep, max_ctas, g, h, ks, s);
   return cudaErrorInvalidValue;
 }
 }  // namespace
 
-// N tile that minimises (waves x tile width), preferring wider tiles.
-int pick_bn(int tm, int N, int max_ctas) {
-  const int cands[4] = {256, 192, 128, 64};
-  int best = 64;
-  long best_cost = -1;
+// Tile width BN and K split of one GEMM from a small cost model of B200 (clocks of
+// one SM): a CTA's 64-deep k block costs max(2 BN MMA clocks (M = 128 rows per
+// CTA), its operand bytes / the per-SM share of the ~6300 B/clk chip L2 limit)
+// (A 16 KB + W BN x 128 B, or half of W when a CTA pair shares it), plus ~1500
+// clocks of fill / epilogue per work item; waves of the persistent grid; split-K
+// adds the fp32 partial round trip through L2/HBM and a reduce launch.
+struct GemmPlan {
+  int bn, ks;
+};
+GemmPlan plan_gemm(int M, int N, int K, int max_ctas, int mc, long ws_elems) {
+  const int tm = (M + GBM - 1) / GBM, nkb = K / GBK;
+  const int ncl = mc == 1 ? 1 : 2;
+  const int tmr = (tm + ncl - 1) / ncl * ncl;
+  const int cands[5] = {256, 192, 160, 128, 64};
+  GemmPlan best{64, 1};
+  double best_t = -1;
   for (int bn : cands) {
     if (N % bn) continue;
-    const long tiles = (long)tm * (N / bn);
-    const long waves = (tiles + max_ctas - 1) / max_ctas;
-    const long cost = waves * (bn + 32);  // +32: per-tile fixed overhead
-    if (best_cost < 0 || cost < best_cost) {
-      best_cost = cost;
-      best = bn;
+    const double wbytes = (mc == 1 ? 128.0 : 64.0) * bn;
+    const double per_kb = std::max(2.0 * bn, (16384.0 + wbytes) / (6300.0 / max_ctas));
+    for (int ks = 1; ks <= 16; ++ks) {
+      if (ks > 1 && (nkb / ks < 8 || (long)ks * M * N > ws_elems || splitk_disabled())) break;
+      const long ctas = (long)tmr * (N / bn) * ks;
+      const long waves = (ctas + max_ctas - 1) / max_ctas;
+      const long per_cta = (ctas + waves - 1) / waves;  // CTAs of a wave, sharing L2
+      const double kb = (double)nkb / ks;
+      const double l2 = kb * (16384.0 + wbytes) * per_cta / 6300.0;
+      double t = waves * std::max(kb * 2.0 * bn + 1500.0, l2 + 1500.0);
+      if (ks > 1) t += (ks + 2.0) * M * N * 4.0 / 3300.0 + 4000.0;
+      if (best_t < 0 || t < best_t * 0.97) {  // prefer the earlier (wider, unsplit) option
+        best_t = t;
+        best = {bn, ks};
+      }
     }
   }
   return best;
@@ -505,13 +594,14 @@ cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int 
   if (reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(W) % 16)
     return cudaErrorInvalidValue;
   const int tm = (M + GBM - 1) / GBM;
-  const int best = pick_bn(tm, N, max_ctas);
   const int mc = pair_mode_for(tm, max_ctas, epi);
-  switch (best) {
-    case 256: return dispatch_mc<256>(A, W, M, N, K, epi, ep, max_ctas, mc, s);
-    case 192: return dispatch_mc<192>(A, W, M, N, K, epi, ep, max_ctas, mc, s);
-    case 128: return dispatch_mc<128>(A, W, M, N, K, epi, ep, max_ctas, mc, s);
-    default: return dispatch_mc<64>(A, W, M, N, K, epi, ep, max_ctas, mc, s);
+  const GemmPlan g = plan_gemm(M, N, K, max_ctas, mc, ep.ws ? ep.ws_elems : 0);
+  switch (g.bn) {
+    case 256: return dispatch_mc<256>(A, W, M, N, K, epi, ep, max_ctas, mc, g.ks, s);
+    case 192: return dispatch_mc<192>(A, W, M, N, K, epi, ep, max_ctas, mc, g.ks, s);
+    case 160: return dispatch_mc<160>(A, W, M, N, K, epi, ep, max_ctas, mc, g.ks, s);
+    case 128: return dispatch_mc<128>(A, W, M, N, K, epi, ep, max_ctas, mc, g.ks, s);
+    default: return dispatch_mc<64>(A, W, M, N, K, epi, ep, max_ctas, mc, g.ks, s);
   }
 }
 
@@ -524,16 +614,18 @@ cudaError_t tc_conv3x3_bf16(const bf16 *P, const bf16 *Wt, int h, int W, int B, 
   if (C % GBK || N % 64 || max_ctas < 1 || (wb % GBM && GBM % wb)) return cudaErrorInvalidValue;
   const ConvGeo g{W, B, C};
   const int M = h * wb, tm = (M + GBM - 1) / GBM;
-  const int best = pick_bn(tm, N, max_ctas);
   const int mc = pair_mode_for(tm, max_ctas, epi);
+  const GemmPlan gp = plan_gemm(M, N, 9 * C, max_ctas, mc, ep.ws ? ep.ws_elems : 0);
+  const int ks = gp.ks;
 #define STADI_CONV_CASE(BNV)                                                          \
   case BNV:                                                                           \
-    return mc == 3   ? dispatch_conv<BNV, 3>(P, Wt, h, g, N, epi, ep, max_ctas, s)    \
-           : mc == 2 ? dispatch_conv<BNV, 2>(P, Wt, h, g, N, epi, ep, max_ctas, s)    \
-                     : dispatch_conv<BNV, 1>(P, Wt, h, g, N, epi, ep, max_ctas, s);
-  switch (best) {
+    return mc == 3   ? dispatch_conv<BNV, 3>(P, Wt, h, g, N, epi, ep, max_ctas, ks, s) \
+           : mc == 2 ? dispatch_conv<BNV, 2>(P, Wt, h, g, N, epi, ep, max_ctas, ks, s) \
+                     : dispatch_conv<BNV, 1>(P, Wt, h, g, N, epi, ep, max_ctas, ks, s);
+  switch (gp.bn) {
     STADI_CONV_CASE(256)
     STADI_CONV_CASE(192)
+    STADI_CONV_CASE(160)
     STADI_CONV_CASE(128)
     STADI_CONV_CASE(64)
   }

@@ -117,6 +117,8 @@ struct stadi_ctx {
   float *final_b = nullptr;  // [fin_ld]
   int fin_ld = 64;
   float *pos_full = nullptr; // [hp*wp, d]
+  float *splitk_ws = nullptr;  // split-K partial tiles of the small tcgen05 GEMMs
+  long splitk_elems = 0;
   std::vector<void *> allocs;
 
   // plan
@@ -338,9 +340,13 @@ cudaError_t collect_timing(stadi_ctx *ctx) {
 cudaError_t gemm(stadi_ctx *ctx, const void *A, const void *W, int M, int N, int K, int epi,
                  const EpiParams &ep, cudaStream_t s) {
   return timed(ctx, STADI_KCLASS_GEMM, 2.0 * M * N * K, 0.0, s, [&] {
-    if (ctx->dtype == STADI_DTYPE_BF16)
-      return tc_gemm_bf16((const bf16 *)A, (const bf16 *)W, M, N, K, epi, ep,
+    if (ctx->dtype == STADI_DTYPE_BF16) {
+      EpiParams e2 = ep;
+      e2.ws = ctx->splitk_ws;
+      e2.ws_elems = ctx->splitk_elems;
+      return tc_gemm_bf16((const bf16 *)A, (const bf16 *)W, M, N, K, epi, e2,
                           std::max(1, ctx->num_sms - ctx->emu_ctas), s);
+    }
     return simt_gemm<float>((const float *)A, (const float *)W, M, N, K, epi, ep, s);
   });
 }
@@ -532,6 +538,11 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
       }
     CK(dalloc(ctx, &ctx->pos_full, pos.size() * 4));
     CK(cudaMemcpy(ctx->pos_full, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice));
+    if (ctx->dtype == STADI_DTYPE_BF16) {
+      // split-K uses at most (#SMs) partial tiles of 128 x 256 fp32: 19 MB on B200
+      ctx->splitk_elems = (long)ctx->num_sms * 128 * 256;
+      CK(dalloc(ctx, &ctx->splitk_ws, (size_t)ctx->splitk_elems * 4));
+    }
     if (dist->world > 1) {
       if (!nccl().ok) return ctx_fail(ctx, STADI_ENCCL, "libnccl.so.2 not loadable");
       if (!dist->nccl_id) return ctx_fail(ctx, STADI_EINVAL, "nccl_id required when world > 1");

@@ -496,6 +496,8 @@ struct UBuilder {
         ep.gate_bstride = U->temb_total;
       }
       if (implicit) {  // tcgen05 implicit GEMM straight from the padded input
+        ep.ws = ctx->splitk_ws;
+        ep.ws_elems = ctx->splitk_elems;
         CK(timed(ctx, STADI_KCLASS_GEMM, 2.0 * Mo * ncols * kp, 0.0, s, [&] {
           return tc_conv3x3_bf16((const bf16 *)D(), (const bf16 *)wt, h, W, B, C, ncols, epi, ep,
                                  std::max(1, ctx->num_sms - ctx->emu_ctas), s);

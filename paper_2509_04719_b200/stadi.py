@@ -97,7 +97,7 @@ class KEpi(C.Structure):
                 ("res", C.c_void_p), ("ldr", C.c_int32), ("gate", C.c_void_p),
                 ("gate_bstride", C.c_int32), ("B", C.c_int32), ("q", C.c_void_p),
                 ("kv_a", C.c_void_p), ("kv_b", C.c_void_p), ("kv_row0", C.c_int64),
-                ("d", C.c_int32)]
+                ("d", C.c_int32), ("ws", C.c_void_p), ("ws_elems", C.c_int64)]
 
 
 EXPORTS = [
@@ -356,7 +356,8 @@ class Context:
 def k_gemm(dtype, A, W, M, N, K, epi, stream=None, **ep):
     e = KEpi()
     for k, v in ep.items():
-        setattr(e, k, ptr(v) if k in ("bias", "out", "res", "gate", "q", "kv_a", "kv_b") else v)
+        setattr(e, k, ptr(v) if k in ("bias", "out", "res", "gate", "q", "kv_a", "kv_b", "ws")
+                else v)
     _check(lib.stadi_k_gemm(dtype, ptr(A), ptr(W), M, N, K, epi, C.byref(e), stream_ptr(stream)))
 
 

@@ -109,6 +109,52 @@ def test_gemm_gated_residual_and_qkv(S, dtype):
         assert np.all(got[:tok0] == 0) and np.all(got[tok0 + ntok:] == 0)
 
 
+SPLITK_SHAPES = [(128, 1280, 11520), (256, 320, 2880), (300, 640, 1280), (64, 256, 4608),
+                 (1000, 192, 2048)]
+
+
+@pytest.mark.parametrize("M,N,K", SPLITK_SHAPES)
+def test_gemm_split_k(S, M, N, K):
+    """With a workspace, GEMMs whose tiles fill <= half the SMs split K: every
+    epilogue kind against the oracle, and bitwise reproducible (fixed-order reduce)."""
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    bias = (rng.standard_normal(N) * 0.1).astype(np.float32)
+    tA, nA = _bf(A)
+    tW, nW = _bf(W)
+    tb = torch.from_numpy(bias).cuda()
+    ws = torch.empty(16 * M * N, device="cuda")
+    wk = dict(ws=ws, ws_elems=ws.numel())
+    ref = OD.linear(nA, nW, bias.astype(np.float64))
+    outs = []
+    for _ in range(2):
+        out = torch.zeros(M, N, device="cuda")
+        S.k_gemm(0, tA, tW, M, N, K, S.EPI_F32, bias=tb, out=out, ldo=N, B=1, **wk)
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy())
+    assert _rel(outs[0], ref) < 1e-5
+    assert np.array_equal(outs[0], outs[1])
+    nosplit = torch.zeros(M, N, device="cuda")
+    S.k_gemm(0, tA, tW, M, N, K, S.EPI_F32, bias=tb, out=nosplit, ldo=N, B=1)
+    torch.cuda.synchronize()
+    # two fp32 summation orders over K <= 11520, each within 1e-5 of the oracle
+    assert _rel(outs[0], nosplit.cpu().numpy().astype(np.float64)) < 3e-5
+    outT = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    S.k_gemm(0, tA, tW, M, N, K, S.EPI_GELU, bias=tb, out=outT, ldo=N, B=1, **wk)
+    torch.cuda.synchronize()
+    assert _rel(outT.float().cpu().numpy(), OD.gelu_tanh(ref)) < 1e-2
+    B = 2
+    gate = rng.standard_normal((B, N)).astype(np.float32)
+    res0 = rng.standard_normal((M, N)).astype(np.float32)
+    res = torch.from_numpy(res0.copy()).cuda()
+    S.k_gemm(0, tA, tW, M, N, K, S.EPI_GATED_RES, bias=tb, res=res, ldr=N,
+             gate=torch.from_numpy(gate).cuda(), gate_bstride=N, B=B, **wk)
+    torch.cuda.synchronize()
+    g = gate[np.arange(M) % B].astype(np.float64)
+    assert _rel(res.cpu().numpy() - res0, g * ref) < 1e-5
+
+
 ATTN_CASES = [  # Nq, Nkv, B, H, hd
     (1, 64, 1, 4, 16), (32, 64, 1, 4, 16), (200, 1000, 2, 3, 64), (128, 256, 2, 2, 72),
     (300, 777, 2, 2, 72), (128, 120, 2, 16, 72), (256, 384, 1, 1, 80), (1000, 2048, 2, 2, 72),

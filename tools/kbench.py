@@ -38,6 +38,9 @@ def gemm(M, N, K, epi):
     W = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
     bias = torch.zeros(N, device="cuda")
     kw = dict(bias=bias, B=2)
+    if os.environ.get("STADI_SPLITK", "1") != "0":  # the runtime's split-K workspace
+        ws = torch.empty(148 * 128 * 256, device="cuda")
+        kw.update(ws=ws, ws_elems=ws.numel())
     if epi in (S.EPI_STORE, S.EPI_GELU):
         out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
         kw.update(out=out, ldo=N)
@@ -64,7 +67,9 @@ elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "gemm":
                        (32768, 4608, 1152, S.EPI_GELU), (32768, 1152, 4608, S.EPI_GATED_RES),
                        (8192, 8192, 8192, S.EPI_STORE), (2048, 1280, 1280, S.EPI_STORE),
                        (2048, 10240, 1280, S.EPI_STORE), (2048, 1280, 5120, S.EPI_RES),
-                       (8192, 640, 640, S.EPI_STORE), (32768, 320, 2880, S.EPI_F32)]:
+                       (8192, 640, 640, S.EPI_STORE), (32768, 320, 2880, S.EPI_F32),
+                       (128, 1280, 11520, S.EPI_F32), (512, 1280, 11520, S.EPI_F32),
+                       (8192, 320, 2880, S.EPI_F32), (256, 1280, 1280, S.EPI_STORE)]:
         gemm(M, N, K, e)
 elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "attn":
     attn(16384, 16384, 2, 16, 72)
