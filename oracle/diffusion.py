@@ -13,6 +13,17 @@ Readings:
        [0.00085, 0.012]; alpha_t = sqrt(alpha_bar_t), sigma_t =
        sqrt(1 - alpha_bar_t); the "final" step lands on alpha_bar_0.
   R20  classifier-free guidance eps = eps_u + w (eps_c - eps_u).
+  R19  DDPM variant (north_star "fused DDIM/DDPM sampler update"; Eq. 2
+       p_theta(x_{t-1}|x_t) = N(mu_theta, Sigma_theta) realised as the
+       eta = 1 member of the DDIM family of ref. [28] (Song et al., Eq. 12),
+       which for consecutive t equals the DDPM ancestral step of ref. [1]):
+         x0_hat    = (x_t - sigma_t eps) / alpha_t
+         sigma_eta = sqrt((1 - abar') / (1 - abar)) sqrt(1 - abar / abar')
+         x'        = alpha' x0_hat + sqrt(1 - abar' - sigma_eta^2) eps
+                     + sigma_eta z,
+       z the full-image N(0, 1) draw of fast-grid index m (an INPUT here:
+       synth/gen.py ddpm_noise); a stride-2 jump uses the same formula
+       with t' = t_{m+2} and z_m.
 """
 from __future__ import annotations
 
@@ -54,6 +65,15 @@ def ddim_step(abar, x, eps, t, t_prev):
     """Eq. 3 (L72)."""
     A, Bc = ddim_coeffs(abar, t, t_prev)
     return A * x + Bc * eps
+
+
+def ddpm_step(abar, x, eps, t, t_prev, z):
+    """R19: eta = 1 step of [28] Eq. 12 from t to t_prev with noise z."""
+    ab = abar[t]
+    ab2 = abar[0] if t_prev < 0 else abar[t_prev]
+    x0 = (x - np.sqrt(1.0 - ab) * eps) / np.sqrt(ab)
+    s_eta = np.sqrt((1.0 - ab2) / (1.0 - ab)) * np.sqrt(1.0 - ab / ab2)
+    return np.sqrt(ab2) * x0 + np.sqrt(1.0 - ab2 - s_eta ** 2) * eps + s_eta * z
 
 
 def cfg_combine(eps_u, eps_c, w):

@@ -38,13 +38,24 @@ def _group_phases(plan):
     return [phases[m] for m in sorted(phases)]
 
 
-def run(cfg, weights, x_T, cond, plan, return_trace=False):
+def _update(abar, x, eps, st, ddpm_z, r0):
+    """Sampler update of one band (rows [r0, r0 + len(x)) of the image): Eq. 3
+    DDIM, or the R19 DDPM step with the band's rows of z_m when ddpm_z (a
+    callable m -> full-image z_m, an input) is given."""
+    if ddpm_z is None:
+        return diffusion.ddim_step(abar, x, eps, st.t, st.t_prev)
+    z = ddpm_z(st.m)[r0:r0 + x.shape[0]]
+    return diffusion.ddpm_step(abar, x, eps, st.t, st.t_prev, z)
+
+
+def run(cfg, weights, x_T, cond, plan, return_trace=False, ddpm_z=None):
     """Execute STADI for one request.  x_T: full noise [H, W, C] (any float).
+    ddpm_z: None (DDIM, Eq. 3) or m -> z_m [H, W, C] (DDPM, R19).
 
     Returns the final latent [H, W, C] (float64) assembled from the bands.
     """
     if cfg["family"] == "unet":
-        return run_unet(cfg, weights, x_T, cond, plan, return_trace)
+        return run_unet(cfg, weights, x_T, cond, plan, return_trace, ddpm_z)
     model = dit.DiT(cfg, weights)
     abar = diffusion.alpha_bar("linear" if cfg["schedule"] == "linear" else "scaled_linear")
     B = dit.batch_of(cfg)
@@ -83,7 +94,7 @@ def run(cfg, weights, x_T, cond, plan, return_trace=False):
         for P in parts:                          # eps on own band + Eq. 3 on own rows
             r, st = P["r"], P["st"]
             eps = dit.guided_eps(cfg, model.final(P["h"], P["fin"], band[r].shape[0]))
-            band[r] = diffusion.ddim_step(abar, band[r], eps, st.t, st.t_prev)
+            band[r] = _update(abar, band[r], eps, st, ddpm_z, plan["row_begin"][r])
             if return_trace:
                 trace.append((st.m, r, st.kind, band[r].copy()))
     import numpy as np
@@ -115,7 +126,7 @@ def _assemble(kind, r, inc, own, stale):
     raise ValueError(kind)
 
 
-def run_unet(cfg, weights, x_T, cond, plan, return_trace=False):
+def run_unet(cfg, weights, x_T, cond, plan, return_trace=False, ddpm_z=None):
     """Algorithm 1 for the U-Net family: every rank's band forward is a
     generator (oracle/unet.py) that yields at each exchange site; ranks of a
     phase advance in lock-step site by site: all publish (pub_ver), then all
@@ -151,8 +162,8 @@ def run_unet(cfg, weights, x_T, cond, plan, return_trace=False):
             reqs = nxt
             site += 1
         for r, st in phase:                      # eps on own band + Eq. 3 on own rows
-            band[r] = diffusion.ddim_step(abar, band[r], unet.guided_eps(cfg, eps[r]),
-                                          st.t, st.t_prev)
+            band[r] = _update(abar, band[r], unet.guided_eps(cfg, eps[r]), st, ddpm_z,
+                              plan["row_begin"][r])
             if return_trace:
                 trace.append((st.m, r, st.kind, band[r].copy()))
     out = np.concatenate([band[r] for r in inc], axis=0)   # final synchronous all-gather
@@ -164,9 +175,15 @@ def _cat(xs):
     return np.concatenate(xs, axis=1)
 
 
-def sequential(cfg, weights, x_T, cond, m_base):
-    """Non-distributed DDIM with M_base steps on the fast grid (the "Origin"
-    method of Table II)."""
+def sequential(cfg, weights, x_T, cond, m_base, ddpm_z=None):
+    """Non-distributed DDIM (or R19 DDPM) with M_base steps on the fast grid
+    (the "Origin" method of Table II)."""
+
+    def upd(abar, x, eps, m, t, t_prev):
+        if ddpm_z is None:
+            return diffusion.ddim_step(abar, x, eps, t, t_prev)
+        return diffusion.ddpm_step(abar, x, eps, t, t_prev, ddpm_z(m))
+
     if cfg["family"] == "unet":
         model = unet.UNet(cfg, weights)
         abar = diffusion.alpha_bar(cfg["schedule"])
@@ -175,7 +192,7 @@ def sequential(cfg, weights, x_T, cond, m_base):
         for m, t in enumerate(grid):
             t_prev = grid[m + 1] if m + 1 < m_base else schedule.FINAL
             eps = unet.guided_eps(cfg, model.forward_full(x, t, cond))
-            x = diffusion.ddim_step(abar, x, eps, t, t_prev)
+            x = upd(abar, x, eps, m, t, t_prev)
         return x
     model = dit.DiT(cfg, weights)
     abar = diffusion.alpha_bar("linear" if cfg["schedule"] == "linear" else "scaled_linear")
@@ -185,7 +202,7 @@ def sequential(cfg, weights, x_T, cond, m_base):
     for m, t in enumerate(grid):
         t_prev = grid[m + 1] if m + 1 < m_base else schedule.FINAL
         eps = dit.guided_eps(cfg, model.forward_full(x, t, cond, y))
-        x = diffusion.ddim_step(abar, x, eps, t, t_prev)
+        x = upd(abar, x, eps, m, t, t_prev)
     return x
 
 

@@ -90,3 +90,37 @@ def bf16_round(a: np.ndarray) -> np.ndarray:
 
 def weights_bf16(w: dict[str, np.ndarray]) -> dict[str, np.ndarray]:
     return {k: bf16_round(v) for k, v in w.items()}
+
+
+# ------------------------------------------------------------------ DDPM noise
+# R19: the DDPM (eta = 1) sampler adds sigma_eta * z_m, z_m a
+# full-image N(0, 1) tensor per fast-grid index m.  Both sides implement the
+# same counter-based generator (the CUDA sampler draws z in-kernel, the oracle
+# receives it from here), so nothing has to be copied per step:
+#   Philox4x64-10 (Salmon et al., SC'11; numpy's np.random.Philox), key =
+#   (seed, m), counter = (e >> 2, 0, 0, 0) for the element with flat index e of
+#   the full [H, W, C] image, 64-bit word = lane e & 3 of that block;
+#   u1 = ((w >> 40) + 1/2) 2^-24, u2 = (((w >> 16) & (2^24 - 1)) + 1/2) 2^-24,
+#   z = sqrt(-2 ln u1) cos(2 pi u2)            (Box-Muller, cosine branch).
+# 24-bit uniforms are exact in fp32, so the device's fp32 transform differs
+# from this fp64 one only by rounding (~1e-7 relative).
+SEED_DDPM = 2024
+_ALL_ONES = (1 << 64) - 1
+
+
+def philox_words(seed: int, m: int, n_words: int) -> np.ndarray:
+    """The first n_words 64-bit outputs of Philox4x64-10 with key (seed, m),
+    counter blocks 0, 1, 2, ... (numpy increments the counter before each
+    block, so it starts from all-ones = -1)."""
+    g = np.random.Philox(counter=[_ALL_ONES] * 4, key=[seed & _ALL_ONES, m & _ALL_ONES])
+    return g.random_raw(n_words)
+
+
+def ddpm_noise(shape, m: int, seed: int = SEED_DDPM) -> np.ndarray:
+    """z_m for fast-grid index m: full-image [H, W, C] float64 ~ N(0, 1)."""
+    n = int(np.prod(shape))
+    w = philox_words(seed, m, n).astype(np.uint64)
+    u1 = ((w >> np.uint64(40)).astype(np.float64) + 0.5) * 2.0 ** -24
+    u2 = (((w >> np.uint64(16)) & np.uint64(0xFFFFFF)).astype(np.float64) + 0.5) * 2.0 ** -24
+    z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+    return z.reshape(shape)
