@@ -153,14 +153,18 @@ enum {
   STADI_PRESET_TINY_UNET = 5   /* 2-level U-Net for fast parity tests            */
 };
 enum { STADI_DTYPE_BF16 = 0, STADI_DTYPE_FP32_DEBUG = 1 };
-enum { STADI_SAMPLER_DDIM = 0, STADI_SAMPLER_DDPM = 1 /* NEXT: EUNSUPPORTED */ };
+/* DDIM: Eq. 3.  DDPM: Eq. 2 (L62) realised as the eta = 1
+ * step of ref. [28] (R19): x' = alpha' x0_hat + sqrt(1 - abar' - s^2) eps + s z_m,
+ * s = sqrt((1 - abar')/(1 - abar)) sqrt(1 - abar/abar'), z_m drawn in the
+ * sampler kernel from the counter-based generator keyed by stadi_cond.ddpm_seed. */
+enum { STADI_SAMPLER_DDIM = 0, STADI_SAMPLER_DDPM = 1 };
 
 typedef struct {
   int32_t preset;          /* STADI_PRESET_*                                     */
   int32_t dtype;           /* BF16: tcgen05 bf16 GEMM/attention, fp32 accumulate,
                               fp32 residual + latent; FP32_DEBUG: SIMT fp32 (no
                               TF32) kernels for the <=1e-4 parity build         */
-  int32_t sampler;         /* STADI_SAMPLER_DDIM                                 */
+  int32_t sampler;         /* STADI_SAMPLER_DDIM | STADI_SAMPLER_DDPM (EINVAL else) */
   int32_t depth;           /* 0 = preset depth; >0: DiT blocks, or the cap on every
                               U-Net transformer depth (reduced parity variants)  */
   int32_t latent_h, latent_w; /* 0 = preset resolution                           */
@@ -192,6 +196,10 @@ typedef struct {
                                 device; NULL for other presets                      */
   const float *time_ids;     /* [B, 6] host fp32 SDXL micro-conditioning, or NULL =
                                 the preset's (1024, 1024, 0, 0, 1024, 1024)         */
+  uint64_t ddpm_seed;        /* STADI_SAMPLER_DDPM: key of the request's noise draws
+                                z_m (R19: Philox4x64-10, key (ddpm_seed, m), counter
+                                = full-image element index / 4, Box-Muller); ignored
+                                by DDIM                                              */
 } stadi_cond;
 
 typedef struct {

@@ -78,6 +78,22 @@ stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void *Wt, int32
                              int32_t B, int32_t C, int32_t N, int32_t mode, int32_t implicit,
                              const float *bias, float *out, void *stream);
 
+/* Fused CFG + unpatchify + sampler update of an fp32 band x [rows, W, C]
+ * (NHWC; Eq. 3, R19 DDPM): eps_raw f32 [tokens * B, ld], token
+ * (row/p)*(W/p) + col/p, column ((row%p)*p + col%p)*c_out + ch; with B == 2
+ * eps = e0 + guidance (e1 - e0) (R20); x = A x + Bc eps + Cz z, z the element's
+ * draw of the R19 generator (key (seed, m), full-image index (row0 + row)*W*C
+ * + ...), skipped when Cz == 0. */
+stadi_status stadi_k_sampler(float *x, const float *eps_raw, int32_t rows, int32_t W, int32_t C,
+                             int32_t p, int32_t c_out, int32_t ld, int32_t B, float guidance,
+                             float A, float Bc, float Cz, uint64_t seed, uint32_t m,
+                             int32_t row0, void *stream);
+
+/* out[i] = z_m element e0 + i of the R19 generator (Philox4x64-10 key (seed, m),
+ * Box-Muller), i < n.  out: f32 device. */
+stadi_status stadi_k_ddpm_noise(float *out, int64_t n, uint64_t seed, uint32_t m, int64_t e0,
+                                void *stream);
+
 /* Number of kernels launched by this process so far. */
 uint64_t stadi_k_launch_count(void);
 

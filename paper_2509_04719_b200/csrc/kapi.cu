@@ -138,3 +138,22 @@ extern "C" stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void
   return cu(e, "conv3x3");
 }
 
+
+extern "C" stadi_status stadi_k_sampler(float *x, const float *eps_raw, int32_t rows, int32_t W,
+                                        int32_t C, int32_t p, int32_t c_out, int32_t ld,
+                                        int32_t B, float guidance, float A, float Bc, float Cz,
+                                        uint64_t seed, uint32_t m, int32_t row0, void *stream) {
+  if (!x || !eps_raw || rows < 0 || W <= 0 || C <= 0 || p <= 0 || rows % p || W % p ||
+      c_out < C || ld < p * p * c_out || (B != 1 && B != 2) || row0 < 0)
+    return fail(nullptr, STADI_EINVAL, "stadi_k_sampler: bad argument");
+  return cu(sampler_update(x, eps_raw, rows, W, C, p, c_out, ld, B, guidance, A, Bc, Cz, seed, m,
+                           row0, (cudaStream_t)stream),
+            "sampler_update");
+}
+
+extern "C" stadi_status stadi_k_ddpm_noise(float *out, int64_t n, uint64_t seed, uint32_t m,
+                                           int64_t e0, void *stream) {
+  if (!out || n < 0 || e0 < 0) return fail(nullptr, STADI_EINVAL, "stadi_k_ddpm_noise: bad argument");
+  return cu(philox_normal_fill(out, (long)n, seed, m, (long)e0, (cudaStream_t)stream),
+            "philox_normal_fill");
+}

@@ -47,11 +47,16 @@ cudaError_t ln_modulate(const float *x, T *y, int M, int d, int B, const float *
 cudaError_t patch_embed(const float *x_band, int rows, int W, int C, int p, const float *w,
                         const float *b, const float *pos_rows, int d, int B, float *x_res,
                         cudaStream_t s);
-// CFG combine + unpatchify + Eq. 3 update of the band:  x = A x + Bc eps.
-// eps_raw row stride = ld (>= p*p*c_out).
+// CFG combine + unpatchify + sampler update of the band:
+//   x = A x + Bc eps (+ Cz z_m when Cz != 0: R19 DDPM, z_m drawn in-kernel by
+//   Philox4x64-10 with key (seed, m) at the element's full-image index, the
+//   band starting at latent row row0).  eps_raw row stride = ld (>= p*p*c_out).
 cudaError_t sampler_update(float *x_band, const float *eps_raw, int rows, int W, int C, int p,
                            int c_out, int ld, int B, float guidance, float A, float Bc,
-                           cudaStream_t s);
+                           float Cz, uint64_t seed, uint32_t m, int row0, cudaStream_t s);
+// z_m elements [e0, e0 + n) of the R19 generator (parity tests).
+cudaError_t philox_normal_fill(float *out, long n, uint64_t seed, uint32_t m, long e0,
+                               cudaStream_t s);
 // Conditioning helpers
 cudaError_t silu_inplace(float *x, long n, cudaStream_t s);
 template <typename T>

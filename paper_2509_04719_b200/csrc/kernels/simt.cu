@@ -287,9 +287,37 @@ __global__ void __launch_bounds__(256) patch_embed_kernel(const float *__restric
   }
 }
 
+// Philox4x64-10 (Salmon et al., SC'11) -- the counter-based generator R19's
+// DDPM noise is defined by (synth/gen.py states the same definition for the
+// oracle side): key (seed, m), counter (e >> 2, 0, 0, 0), word e & 3.
+__device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t m, uint64_t block,
+                                                int lane) {
+  uint64_t c0 = block, c1 = 0, c2 = 0, c3 = 0, k0 = seed, k1 = m;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t lo0 = 0xD2E7470EE14C6C93ull * c0, hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c0);
+    const uint64_t lo1 = 0xCA5A826395121157ull * c2, hi1 = __umul64hi(0xCA5A826395121157ull, c2);
+    c0 = hi1 ^ c1 ^ k0;
+    c1 = lo1;
+    c2 = hi0 ^ c3 ^ k1;
+    c3 = lo0;
+    k0 += 0x9E3779B97F4A7C15ull;
+    k1 += 0xBB67AE8584CAA73Bull;
+  }
+  return lane == 0 ? c0 : lane == 1 ? c1 : lane == 2 ? c2 : c3;
+}
+
+// N(0, 1) by Box-Muller (cosine branch) of two exact 24-bit uniforms.
+__device__ __forceinline__ float philox_normal(uint64_t seed, uint32_t m, uint64_t e) {
+  const uint64_t w = philox_word(seed, m, e >> 2, (int)(e & 3));
+  const float u1 = ((float)(uint32_t)(w >> 40) + 0.5f) * 0x1p-24f;
+  const float u2 = ((float)(uint32_t)((w >> 16) & 0xFFFFFFu) + 0.5f) * 0x1p-24f;
+  return sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+}
+
 __global__ void sampler_kernel(float *__restrict__ xb, const float *__restrict__ eps, int rows,
                                int W, int C, int p, int c_out, int ld, int B, float g, float A,
-                               float Bc) {
+                               float Bc, float Cz, uint64_t seed, uint32_t m, int row0) {
   const long n = (long)rows * W * C;
   const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n) return;
@@ -305,7 +333,15 @@ __global__ void sampler_kernel(float *__restrict__ xb, const float *__restrict__
     const float ec = eps[(tok * B + 1) * ncol + j];
     e = e + g * (ec - e);                                   // CFG (R20)
   }
-  xb[idx] = A * xb[idx] + Bc * e;                           // Eq. 3
+  float x = A * xb[idx] + Bc * e;                           // Eq. 3 (DDIM)
+  if (Cz != 0.f)                                            // R19 DDPM: + sigma_eta z_m
+    x += Cz * philox_normal(seed, m, (uint64_t)row0 * W * C + (uint64_t)idx);
+  xb[idx] = x;
+}
+
+__global__ void philox_normal_kernel(float *out, long n, uint64_t seed, uint32_t m, long e0) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = philox_normal(seed, m, (uint64_t)(e0 + i));
 }
 }  // namespace
 
@@ -322,11 +358,19 @@ cudaError_t patch_embed(const float *x_band, int rows, int W, int C, int p, cons
 
 cudaError_t sampler_update(float *x_band, const float *eps_raw, int rows, int W, int C, int p,
                            int c_out, int ld, int B, float guidance, float A, float Bc,
-                           cudaStream_t s) {
+                           float Cz, uint64_t seed, uint32_t m, int row0, cudaStream_t s) {
   const long n = (long)rows * W * C;
   if (n == 0) return cudaSuccess;
-  sampler_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x_band, eps_raw, rows, W, C, p,
-                                                              c_out, ld, B, guidance, A, Bc);
+  sampler_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+      x_band, eps_raw, rows, W, C, p, c_out, ld, B, guidance, A, Bc, Cz, seed, m, row0);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t philox_normal_fill(float *out, long n, uint64_t seed, uint32_t m, long e0,
+                               cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  philox_normal_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, n, seed, m, e0);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -99,6 +99,8 @@ struct UNetState;  // unet_exec.cuh
 struct stadi_ctx {
   Dims dm;
   int dtype = STADI_DTYPE_BF16;
+  int sampler = STADI_SAMPLER_DDIM;
+  uint64_t ddpm_seed = 0;    // per request (stadi_cond), R19
   int device = 0, rank = 0, world = 1, n_local = 1, G = 1;
   int num_sms = 148;
   std::string err;
@@ -296,6 +298,21 @@ void ddim_coeffs(const double *ab, int t, int t_prev, float *A, float *Bc) {
   *Bc = (float)(-si2 * std::expm1(h));
 }
 
+// R19 DDPM (eta = 1) as x' = A x + Bc eps + Cz z:  with x0 = (x - sigma eps) / alpha,
+// x' = alpha' x0 + sqrt(1 - abar' - s^2) eps + s z, s = sqrt((1-abar')/(1-abar)) sqrt(1 - abar/abar').
+void sampler_coeffs(const stadi_ctx *ctx, int t, int t_prev, float *A, float *Bc, float *Cz) {
+  if (ctx->sampler == STADI_SAMPLER_DDIM) {
+    ddim_coeffs(ctx->abar, t, t_prev, A, Bc);
+    *Cz = 0.f;
+    return;
+  }
+  const double a1 = ctx->abar[t], a2 = t_prev < 0 ? ctx->abar[0] : ctx->abar[t_prev];
+  const double se = std::sqrt((1 - a2) / (1 - a1)) * std::sqrt(1 - a1 / a2);
+  *A = (float)(std::sqrt(a2) / std::sqrt(a1));
+  *Bc = (float)(std::sqrt(1 - a2 - se * se) - std::sqrt(a2) * std::sqrt(1 - a1) / std::sqrt(a1));
+  *Cz = (float)se;
+}
+
 // ---------------------------------------------------------------- kernel timing
 // Wrap one launch of class `cls` in a pair of CUDA events on its stream when
 // timing is enabled; `flops` / `bytes` are the launch's ALGORITHMIC work
@@ -483,8 +500,8 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
   if (!make_dims(*model, dm, e)) return fail(nullptr, STADI_EINVAL, "%s", e.c_str());
   if (model->dtype != STADI_DTYPE_BF16 && model->dtype != STADI_DTYPE_FP32_DEBUG)
     return fail(nullptr, STADI_EINVAL, "bad dtype");
-  if (model->sampler != STADI_SAMPLER_DDIM)
-    return fail(nullptr, STADI_EUNSUPPORTED, "only the DDIM sampler (Eq. 3) is implemented");
+  if (model->sampler != STADI_SAMPLER_DDIM && model->sampler != STADI_SAMPLER_DDPM)
+    return fail(nullptr, STADI_EINVAL, "bad sampler");
   if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || dist->n_local < 1 ||
       (dist->world > 1 && dist->n_local != 1) || dist->world * dist->n_local > STADI_MAX_GPUS)
     return fail(nullptr, STADI_EINVAL, "bad dist desc (n_local > 1 requires world == 1)");
@@ -501,6 +518,7 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
   auto ctx = std::make_unique<stadi_ctx>();
   ctx->dm = dm;
   ctx->dtype = model->dtype;
+  ctx->sampler = model->sampler;
   ctx->esz = model->dtype == STADI_DTYPE_BF16 ? 2 : 4;
   ctx->device = dist->device;
   ctx->rank = dist->rank;
@@ -786,6 +804,7 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
     return ctx_fail(ctx, STADI_EINVAL, "conditioning missing (%s)", m.text ? "text" : "labels");
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(ctx->device));
+  ctx->ddpm_seed = cond->ddpm_seed;
   // noise bands
   const bool dev = is_device_ptr(noise_full);
   const size_t row_bytes = (size_t)m.lat_w * m.c_in * 4;
@@ -1085,12 +1104,13 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
     ef.out = r.eps_raw;
     ef.ldo = ctx->fin_ld;
     CK(gemm(ctx, r.xmod, ctx->final_w, M, ctx->fin_ld, (int)d, EPI_F32, ef, s));
-    float A, Bc;
-    ddim_coeffs(ctx->abar, P.st.t, P.st.t_prev, &A, &Bc);
+    float A, Bc, Cz;
+    sampler_coeffs(ctx, P.st.t, P.st.t_prev, &A, &Bc, &Cz);
     const double sb = (double)r.rows * m.lat_w * m.c_in * 8 + (double)M * ctx->fin_ld * 4;
     CK(timed(ctx, STADI_KCLASS_SAMPLER, 0.0, sb, s, [&] {
       return sampler_update(r.x_band, r.eps_raw, r.rows, m.lat_w, m.c_in, m.p, m.c_out,
-                            ctx->fin_ld, B, m.guidance, A, Bc, s);
+                            ctx->fin_ld, B, m.guidance, A, Bc, Cz, ctx->ddpm_seed, P.st.m,
+                            r.row_begin, s);
     }));
   }
   return STADI_OK;

@@ -768,12 +768,13 @@ struct UBuilder {
       const int h = rows(0), W = width(0);
       op([=](const stadi_step_t &st, cudaStream_t s) -> stadi_status {
         stadi_ctx *ctx = c;
-        float A, Bc;
-        ddim_coeffs(ctx->abar, st.t, st.t_prev, &A, &Bc);
+        float A, Bc, Cz;
+        sampler_coeffs(ctx, st.t, st.t_prev, &A, &Bc, &Cz);
         const double sb = (double)h * W * 4 * 8 + (double)h * W * B * 64 * 4;
         CK(timed(ctx, STADI_KCLASS_SAMPLER, 0.0, sb, s, [&] {
           return sampler_update(ctx->ranks[me].x_band, (const float *)E(), h, W, ctx->dm.c_in, 1,
-                                4, 64, B, ctx->dm.guidance, A, Bc, s);
+                                4, 64, B, ctx->dm.guidance, A, Bc, Cz, ctx->ddpm_seed, st.m,
+                                ctx->ranks[me].row_begin, s);
         }));
         return STADI_OK;
       });

@@ -23,6 +23,7 @@ T_FINAL = -1
 VER_NONE = -1
 PRESET = {"tiny_dit": 0, "dit_xl2": 1, "pixart_alpha": 2, "sd15": 3, "sdxl": 4, "tiny_unet": 5}
 DTYPE_BF16, DTYPE_FP32_DEBUG = 0, 1
+SAMPLER_DDIM, SAMPLER_DDPM = 0, 1
 EPI_STORE, EPI_GELU, EPI_GATED_RES, EPI_RES, EPI_QKV, EPI_F32, EPI_CONV, EPI_GEGLU = range(8)
 KCLASS = {"gemm": 0, "attn": 1, "xattn": 2, "norm": 3, "sampler": 4}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE",
@@ -83,7 +84,8 @@ class DistDesc(C.Structure):
 
 class Cond(C.Structure):
     _fields_ = [("labels", C.POINTER(C.c_int32)), ("text", C.POINTER(C.c_float)),
-                ("pooled", C.POINTER(C.c_float)), ("time_ids", C.POINTER(C.c_float))]
+                ("pooled", C.POINTER(C.c_float)), ("time_ids", C.POINTER(C.c_float)),
+                ("ddpm_seed", C.c_uint64)]
 
 
 class RunStats(C.Structure):
@@ -108,7 +110,7 @@ EXPORTS = [
     "stadi_emulator_start", "stadi_emulator_stop", "stadi_nccl_unique_id",
     "stadi_kernel_timing", "stadi_kernel_stats",
     "stadi_k_gemm", "stadi_k_attention", "stadi_k_ln_modulate", "stadi_k_conv3x3",
-    "stadi_k_launch_count",
+    "stadi_k_sampler", "stadi_k_ddpm_noise", "stadi_k_launch_count",
 ]
 
 
@@ -154,6 +156,11 @@ def _load():
                                           vp, C.c_int32, vp]),
         "stadi_k_conv3x3": (C.c_int, [C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32,
                                       C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]),
+        "stadi_k_sampler": (C.c_int, [vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float,
+                                      C.c_float, C.c_float, C.c_uint64, C.c_uint32, C.c_int32,
+                                      vp]),
+        "stadi_k_ddpm_noise": (C.c_int, [vp, C.c_int64, C.c_uint64, C.c_uint32, C.c_int64, vp]),
         "stadi_k_launch_count": (C.c_uint64, []),
     }
     for name, (res, args) in sig.items():
@@ -217,8 +224,9 @@ def schedule(p: Plan, rank: int):
     return [buf[i].tuple() for i in range(n.value)]
 
 
-def model_desc(preset, dtype=DTYPE_BF16, depth=0, latent_h=0, latent_w=0) -> ModelDesc:
-    return ModelDesc(PRESET[preset] if isinstance(preset, str) else preset, dtype, 0, depth,
+def model_desc(preset, dtype=DTYPE_BF16, depth=0, latent_h=0, latent_w=0,
+               sampler=SAMPLER_DDIM) -> ModelDesc:
+    return ModelDesc(PRESET[preset] if isinstance(preset, str) else preset, dtype, sampler, depth,
                      latent_h, latent_w)
 
 
@@ -310,7 +318,8 @@ class Context:
         tid = cond.get("time_ids")
         if tid is not None and hasattr(tid, "cpu"):
             tid = tid.cpu().numpy()
-        return Cond(lp, fptr(cond.get("text")), fptr(cond.get("pooled")), fptr(tid)), keep
+        return Cond(lp, fptr(cond.get("text")), fptr(cond.get("pooled")), fptr(tid),
+                    int(cond.get("ddpm_seed", 0))), keep
 
     def begin(self, noise, cond, stream=None):
         c, keep = self._cond(cond)
@@ -374,6 +383,16 @@ def k_ln_modulate(dtype, x, y, M, d, B, shift, scale, bstride, stream=None):
 def k_conv3x3(dtype, P, Wt, h, W, B, C_, N, mode, implicit, bias, out, stream=None):
     _check(lib.stadi_k_conv3x3(dtype, ptr(P), ptr(Wt), h, W, B, C_, N, mode, implicit, ptr(bias),
                                ptr(out), stream_ptr(stream)))
+
+
+def k_sampler(x, eps_raw, rows, W, C_, p, c_out, ld, B, guidance, A, Bc, Cz=0.0, seed=0, m=0,
+              row0=0, stream=None):
+    _check(lib.stadi_k_sampler(ptr(x), ptr(eps_raw), rows, W, C_, p, c_out, ld, B, guidance, A,
+                               Bc, Cz, seed, m, row0, stream_ptr(stream)))
+
+
+def k_ddpm_noise(out, n, seed, m, e0=0, stream=None):
+    _check(lib.stadi_k_ddpm_noise(ptr(out), n, seed, m, e0, stream_ptr(stream)))
 
 
 def launch_count() -> int:

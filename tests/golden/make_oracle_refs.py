@@ -16,9 +16,10 @@ os.environ["STADI_WRITE_REFS"] = "1"
 
 import test_gpu_parity as T  # noqa: E402
 import test_gpu_unet as TU  # noqa: E402
+import test_gpu_ddpm as TD  # noqa: E402
 
 if __name__ == "__main__":
-    for mod in (T, TU):
+    for mod in (T, TU, TD):
         for case in mod.oracle_cases():
             t0 = time.time()
             mod._oracle(*case)
