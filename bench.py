@@ -77,11 +77,13 @@ def dit_flops(cfg, n_q, n_kv, B):
     return lin + att + xatt
 
 
-def unet_flops(cfg, rows):
+def unet_flops(cfg, rows, kv_rows=None):
     """Algorithmic FLOPs of one U-Net forward (B = 2) on the full-width latent cut
-    to `rows` rows, attention over the same tokens: conv 2*9*Cin*Cout per output
-    pixel, linear 2*K*N per token, attention 4*n_q*n_kv*C, cross 4*n_q*L*C."""
+    to `rows` rows, attention against kv_rows rows (default: the same tokens):
+    conv 2*9*Cin*Cout per output pixel, linear 2*K*N per token, attention
+    4*n_q*n_kv*C, cross 4*n_q*L*C."""
     B = configs.batch(cfg)
+    kv_rows = rows if kv_rows is None else kv_rows
     W0, L = cfg["latent_w"], len(cfg["channels"])
     f = 0.0
 
@@ -94,7 +96,8 @@ def unet_flops(cfg, rows):
 
     def tr(h, w, c, depth):
         n = h * w
-        per = 2.0 * n * B * c * c * (4 + 2 + 8 + 4) + 4.0 * n * n * c * B + \
+        n_kv = n * kv_rows // max(rows, 1)
+        per = 2.0 * n * B * c * c * (4 + 2 + 8 + 4) + 4.0 * n * n_kv * c * B + \
             4.0 * n * cfg["text_len"] * c * B
         return 2.0 * 2 * n * B * c * c + depth * per
 
@@ -130,6 +133,62 @@ def image_flops(cfg, m_base):
     n = hp * wp
     B = configs.batch(cfg)
     return m_base * cfg["depth"] * dit_flops(cfg, n, n, B)
+
+
+def step_flops(cfg, rows):
+    """Algorithmic FLOPs of one denoising step of a band of `rows` latent rows
+    (own queries x full-image K/V, SURVEY §8(d) 'Method')."""
+    H = cfg["latent_h"]
+    if cfg["family"] == "unet":
+        return unet_flops(cfg, rows, kv_rows=H)
+    hp, wp = configs.tokens_hw(cfg)
+    nq = rows // cfg["patch"] * wp
+    return cfg["depth"] * dit_flops(cfg, nq, hp * wp, configs.batch(cfg))
+
+
+def kv_bytes_per_round(cfg):
+    """Full-image K/V bytes of one exchange round: sum over self-attention sites
+    of 2 (K, V) * B * N_tokens * C * 2 bytes (bf16) (SURVEY §8(d) 'Bytes per round')."""
+    B = configs.batch(cfg)
+    if cfg["family"] != "unet":
+        hp, wp = configs.tokens_hw(cfg)
+        return cfg["depth"] * 2 * B * hp * wp * cfg["hidden"] * 2
+    tot, H, W = 0, cfg["latent_h"], cfg["latent_w"]
+    lv = configs.unet_levels(cfg)
+    for i, (c, att, depth, _) in enumerate(lv):
+        if att:
+            n = (H >> i) * (W >> i)
+            sites = depth * (2 * cfg["layers_per_block"] + 1)   # down + up blocks
+            tot += sites * 2 * B * n * c * 2
+    L = len(lv) - 1
+    tot += cfg["mid_depth"] * 2 * B * (H >> L) * (W >> L) * lv[-1][0] * 2
+    return tot
+
+
+NVLINK_GBS = 900.0   # NVLink 5 per direction per GPU (B200_PROFILING.md / SURVEY App. B)
+
+
+def path_lower_bound(cfg, plan_d, occ, peak_tflops):
+    """SURVEY §8(d) end-to-end lower bound of one image under a plan:
+    LB = max(sum_i W_i / sum_i (1 - rho_i) peak,  max_i inbound_i rounds / BW_NVL,
+             max_i W_i / ((1 - rho_i) peak)),
+    W_i = M_i * step_flops(rows_i) (algorithmic, fewer steps on tier-2 ranks),
+    inbound_i = (1 - rows_i / H) * K/V bytes per round."""
+    H = cfg["latent_h"]
+    inc = [i for i, t in enumerate(plan_d["tier"]) if t > 0]
+    Wi = {i: plan_d["steps"][i] * step_flops(cfg, plan_d["rows"][i]) for i in inc}
+    free = {i: max(1e-6, 1.0 - occ[i] / 100.0) for i in inc}
+    pk = peak_tflops * 1e12
+    t_total = sum(Wi.values()) / (sum(free.values()) * pk)
+    t_rank = max(Wi[i] / (free[i] * pk) for i in inc)
+    kvb = kv_bytes_per_round(cfg) if len(inc) > 1 else 0
+    t_comm = max((1.0 - plan_d["rows"][i] / H) * kvb * plan_d["n_exchange_rounds"]
+                 for i in inc) / (NVLINK_GBS * 1e9)
+    lb = max(t_total, t_rank, t_comm)
+    return {"lb_ms": lb * 1e3, "compute_ms": max(t_total, t_rank) * 1e3, "nvlink_ms": t_comm * 1e3,
+            "flops_per_image": sum(Wi.values()), "kv_bytes_per_round": kvb,
+            "peak_tflops": peak_tflops, "nvlink_gbs": NVLINK_GBS,
+            "bound": "tensor" if max(t_total, t_rank) >= t_comm else "nvlink"}
 
 
 def load_peaks():
@@ -476,6 +535,13 @@ def main():
                    "gbs": (v[3] / (v[1] * 1e-3) / 1e9) if v[1] and v[3] else None}
                for k, v in kst.items()}
 
+    # ---- whole-path roofline: SURVEY §8(d) lower bound of the plan vs measured latency
+    path_roof = path_lower_bound(cfg, plan.to_dict(), occ, peaks["tflops"])
+    path_roof["frac"] = path_roof["lb_ms"] / ms_img
+    if uni is not None:
+        ulb = path_lower_bound(cfg, uplan.to_dict(), occ, peaks["tflops"])
+        uni["path_roofline"] = dict(ulb, frac=ulb["lb_ms"] / uni["ms_per_image"])
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, wl)
@@ -493,7 +559,8 @@ def main():
                        "l2": "inputs larger than L2: the K/V slots + bf16 weights streamed per "
                              "image exceed the 126 MB L2 (C5: 8.5 GB + 1.3 GB)",
                        "parallelism": f"stadi-patch{world}"},
-            "uniform_pp": uni, "e2e": e2e, "roofline": roof, "kernels": kernels,
+            "uniform_pp": uni, "e2e": e2e, "roofline": roof, "path_roofline": path_roof,
+            "kernels": kernels,
             "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(launches),
             "context": PAPER_CONTEXT,
         }
