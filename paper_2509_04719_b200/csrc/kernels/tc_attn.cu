@@ -149,7 +149,7 @@ struct AttnCfg {
   // [2 parities][2 groups][SPLIT][128]
   static constexpr int SPLIT = 2;
   static constexpr int W0 = 64, W1 = AKT - 64;
-  static constexpr int OFF_RED = OFF_BAR + 256;
+  static constexpr int OFF_RED = OFF_BAR + 512;
   static constexpr int RED_BYTES = 2 * 2 * SPLIT * 128 * 4;
   static constexpr int SMEM = OFF_RED + RED_BYTES + 1024;
   static constexpr int THREADS = 64 + 128 * SPLIT * NQT;
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
                    const __grid_constant__ CUtensorMap tq16, const __grid_constant__ CUtensorMap tk64,
                    const __grid_constant__ CUtensorMap tk32, const __grid_constant__ CUtensorMap tk16,
                    bf16 *__restrict__ out, int Nq, int Nkv, int B, int H, int hd, float scale_log2,
-                   int use_tok) {
+                   int flags) {  // bit 0: exp-phase tokens, bit 1: deferred PV wait (QUAD), bit 2: MMA order
   using C = AttnCfg<N64, N32, N16, NQT>;
   constexpr int AKT = C::AKT;
   extern __shared__ uint8_t smem_raw[];
@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
   uint64_t *p_full = s_free + 2;           // [2] P_g(j) stored
   uint64_t *o_done = p_full + 2;           // [2] PV_g(j) complete (P_g free, O_g final)
   uint64_t *tok = o_done + 2;              // [2] exp-phase tokens (groups alternate)
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tok + 2);
+  uint64_t *tok4 = tok + 2;                // [2][4] per-SMSP exp-phase tokens (QUAD)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tok4 + 8);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q0 = blockIdx.x * (AQ * NQT), h = blockIdx.y, b = blockIdx.z;
@@ -269,10 +270,13 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&s_full[g], 1);
-      mbar_init(&s_free[g], 128 * C::SPLIT);
-      mbar_init(&p_full[g], 128 * C::SPLIT);
+      // QUAD: one elected arrival per softmax warp (8 per group); else per thread
+      constexpr int ARR = QUAD ? 4 * C::SPLIT : 128 * C::SPLIT;
+      mbar_init(&s_free[g], ARR);
+      mbar_init(&p_full[g], ARR);
       mbar_init(&o_done[g], 1);
-      mbar_init(&tok[g], 128 * C::SPLIT);
+      mbar_init(&tok[g], ARR);
+      for (int k = 0; k < 4; ++k) mbar_init(&tok4[g * 4 + k], 2);
     }
     fence_mbar_init();
   }
@@ -372,6 +376,62 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
       umma_commit(&k_empty[0]);
       int ks = 1 % C::STAGES, vs = 0;
       uint32_t kph = (ks == 0), vph = 0;
+      if (NQT == 2 && (flags & 4)) {
+        // Event order S_0(j+1), PV_1(j-1), S_1(j+1), PV_0(j): each S is issued as
+        // soon as its group has read the previous S, not queued behind the other
+        // group's PV of the same tile (which waits for that group's whole exp phase).
+        int pvs = 0;  // V slot of tile j-1
+        for (int j = 0; j < n_kv; ++j) {
+          if (j + 1 < n_kv) {
+            mbar_wait(&k_full[ks], kph);
+            mbar_wait(&s_free[0], j & 1);
+            ATTN_TRACE(0, 0, j);
+            tc_fence_after();
+            issue_s(0, ks);
+            umma_commit(&s_full[0]);
+            ATTN_TRACE(1, 0, j);
+          }
+          if (j > 0) {
+            mbar_wait(&p_full[1], (j - 1) & 1);
+            ATTN_TRACE(2, 1, j - 1);
+            tc_fence_after();
+            issue_pv(1, pvs, j - 1);
+            umma_commit(&o_done[1]);
+            umma_commit(&v_empty[pvs]);
+            ATTN_TRACE(8, 1, j - 1);
+          }
+          if (j + 1 < n_kv) {
+            mbar_wait(&s_free[1], j & 1);
+            ATTN_TRACE(0, 1, j);
+            tc_fence_after();
+            issue_s(1, ks);
+            umma_commit(&s_full[1]);
+            umma_commit(&k_empty[ks]);
+            ATTN_TRACE(1, 1, j);
+            if (++ks == C::STAGES) {
+              ks = 0;
+              kph ^= 1;
+            }
+          }
+          mbar_wait(&v_full[vs], vph);
+          mbar_wait(&p_full[0], j & 1);
+          ATTN_TRACE(2, 0, j);
+          tc_fence_after();
+          issue_pv(0, vs, j);
+          umma_commit(&o_done[0]);
+          ATTN_TRACE(8, 0, j);
+          pvs = vs;
+          if (++vs == C::STAGES) {
+            vs = 0;
+            vph ^= 1;
+          }
+        }
+        mbar_wait(&p_full[1], (n_kv - 1) & 1);
+        tc_fence_after();
+        issue_pv(1, pvs, n_kv - 1);
+        umma_commit(&o_done[1]);
+        umma_commit(&v_empty[pvs]);
+      } else {
       for (int j = 0; j < n_kv; ++j) {
         if (j + 1 < n_kv) {
           mbar_wait(&k_full[ks], kph);
@@ -406,6 +466,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
           vph ^= 1;
         }
       }
+      }
     }
   } else if constexpr (QUAD) {  // ------------------------------ softmax groups (quad rows)
     // warp w >= 2: group g = (w - 2) / 8; TMEM lane quarter w % 4, of which the
@@ -435,7 +496,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
       tmem_ld_q256<NR>(s_addr, reinterpret_cast<uint32_t *>(v));
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(&s_free[g]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[g]);
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(4, g, j);
       if (valid < AKT) {
 #pragma unroll
@@ -467,12 +529,17 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
           grow = true;
         }
       }
-      if (j > 0) {
+      // PV_g(j-1) must be complete before O is rescaled or P_g overwritten.  With
+      // `defer` the wait moves to just before the P store unless this warp rescales,
+      // so the PV latency overlaps the token wait and the exp phase.
+      const bool any_grow = __any_sync(0xffffffffu, grow);
+      const bool wait_now = j > 0 && (!(flags & 2) || any_grow);
+      if (wait_now) {
         mbar_wait(&o_done[g], (j - 1) & 1);
         tc_fence_after();
       }
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(9, g, j);
-      if (j > 0 && __any_sync(0xffffffffu, grow)) {
+      if (j > 0 && any_grow) {
         static_assert(NO % 2 == 0, "O rescale in 16-column pieces");
 #pragma unroll
         for (int c = 0; c < NO; c += 2) {  // 16 columns at a time: S values stay live
@@ -486,7 +553,13 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
       }
       l[0] *= factor[0];
       l[1] *= factor[1];
-      if (NQT == 2 && use_tok) {
+      // exp-phase tokens: the two groups take turns on the exp units, per group
+      // (bit 0) or per SM sub-partition (bit 3: the two warps of each group that
+      // share an SMSP's MUFU hand over to the other group's two warps there)
+      if (NQT == 2 && (flags & 8)) {
+        if (g == 1) mbar_wait(&tok4[4 + (warp & 3)], j & 1);
+        else if (j > 0) mbar_wait(&tok4[warp & 3], (j - 1) & 1);
+      } else if (NQT == 2 && (flags & 1)) {
         if (g == 1) mbar_wait(&tok[1], j & 1);
         else if (j > 0) mbar_wait(&tok[0], (j - 1) & 1);
       }
@@ -515,6 +588,12 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
           pk[2 * r + rr] = *reinterpret_cast<uint32_t *>(&t2);
         }
       }
+      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(10, g, j);
+      if (j > 0 && !wait_now) {
+        mbar_wait(&o_done[g], (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(11, g, j);
       tmem_st_q128<NR>(p_addr, pk);
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
@@ -523,10 +602,18 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         unpack_f32x2(acc[rr][1], s2, s3);
         l[rr] += (s0 + s1) + (s2 + s3);
       }
-      if (NQT == 2 && use_tok) mbar_arrive(&tok[1 - g]);
+      if (NQT == 2 && (flags & 8)) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tok4[(1 - g) * 4 + (warp & 3)]);
+      } else if (NQT == 2 && (flags & 1)) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tok[1 - g]);
+      }
       tmem_st_wait();
+      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(12, g, j);
       tc_fence_before();
-      mbar_arrive(&p_full[g]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[g]);
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(6, g, j);
     }
     // epilogue: quad-reduce the row sums, O / l -> bf16 (rows past Nq are padding)
@@ -703,11 +790,18 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
   }
 }
 
-// STADI_ATTN_TOK=0: the two softmax groups' exp phases are not serialised by tokens
-int attn_tok() {
+// STADI_ATTN_TOK=0: the two softmax groups' exp phases are not serialised by tokens;
+// STADI_ATTN_DEFER=0: wait for PV(j-1) before the rescale check, not before the P store;
+// STADI_ATTN_ORDER=1: MMA issue order S_0(j+1), PV_1(j-1), S_1(j+1), PV_0(j) instead of
+// S_0(j+1), S_1(j+1), PV_0(j), PV_1(j) (measured 0.5% slower);
+// STADI_ATTN_TOK4=1: per-SMSP exp-phase tokens
+int attn_flags() {
   static const int v = [] {
-    const char *e = getenv("STADI_ATTN_TOK");
-    return (e && e[0] == '0') ? 0 : 1;
+    const char *e = getenv("STADI_ATTN_TOK"), *d = getenv("STADI_ATTN_DEFER"),
+               *o = getenv("STADI_ATTN_ORDER");
+    const char *t4 = getenv("STADI_ATTN_TOK4");
+    return ((e && e[0] == '0') ? 0 : 1) | ((d && d[0] == '0') ? 0 : 2) |
+           ((o && o[0] == '1') ? 4 : 0) | ((t4 && t4[0] == '1') ? 8 : 0);
   }();
   return v;
 }
@@ -745,7 +839,7 @@ cudaError_t launch_attn_p(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nk
   dim3 grid((Nq + AQ * NQT - 1) / (AQ * NQT), H, B);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
   tc_attn_kernel<N64, N32, N16, NQT, POLY, QUAD><<<grid, C::THREADS, C::SMEM, s>>>(
-      tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], o, Nq, Nkv, B, H, hd, scale_log2, attn_tok());
+      tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], o, Nq, Nkv, B, H, hd, scale_log2, attn_flags());
   ++g_launches;
   return cudaGetLastError();
 }
