@@ -366,6 +366,7 @@ def main():
     ap.add_argument("--no-uniform", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-occ-sweep", action="store_true")
     ap.add_argument("--ncu", action="store_true",
                     help="profiling pass under ncu: 1 untimed request after profiling, no "
                          "uniform / e2e / cpu legs (its numbers are never bench values)")
@@ -429,6 +430,11 @@ def main():
 
     # ---- a9 occupancy emulation, a1 profiling, a2/a3 plans
     occ = occupancy_list(args.occupancy, world)
+    # one untimed probe before the emulator starts: every kernel of the path is
+    # then loaded (CUDA lazy loading of a kernel first launched while the
+    # emulator's resident kernel runs can need a context sync -> deadlock; the
+    # library force-loads the SM-count-dependent tcgen05 variants itself)
+    ctx.profile_warmup(1, world)
     if occ[rank]:
         ctx.emulator_start(occ[rank])
     barrier()
@@ -509,6 +515,38 @@ def main():
     if occ[rank]:
         ctx.emulator_stop()
 
+    # ---- occupancy sweep (N = 1): the single GPU's probe step time under 0/20/40/60%
+    # emulated occupancy (a9 + a1), and the plan the planner makes from those measured
+    # speeds for a 4-GPU job with one GPU at each level.  The per-image latencies of
+    # that job are a PROJECTION (measured per-step ms x rows_i / H x M_i, no exchange
+    # cost), labelled as such -- gpurun provides one GPU.
+    occ_sweep = None
+    if world == 1 and not args.ncu and not args.no_occ_sweep:
+        pcts = [0, 20, 40, 60]
+        pms = []
+        for pct in pcts:
+            if pct:
+                ctx.emulator_start(pct)
+            m_, _ = ctx.profile_warmup(3, 1)
+            if pct:
+                ctx.emulator_stop()
+            pms.append(m_[0])
+        sq = [int(round((1 << 20) * min(pms) / v)) for v in pms]
+        p4 = S.plan(sq, wl["m_base"], wl["m_warmup"], p_total, p).to_dict()
+        u4 = S.plan(sq, wl["m_base"], wl["m_warmup"], p_total, p, flags=S.NO_TA | S.NO_SA).to_dict()
+        H = cfg["latent_h"]
+
+        def proj(pd):
+            return max(pd["steps"][i] * pms[i] * pd["rows"][i] / H
+                       for i in range(4) if pd["tier"][i])
+        ts, tu = proj(p4), proj(u4)
+        occ_sweep = {"occupancy_pct": pcts, "probe_ms_per_step": pms, "speed_q20": sq,
+                     "plan_4gpu": {k: p4[k] for k in ("tier", "steps", "units", "rows")},
+                     "projected_4gpu_ms": {"stadi": ts, "uniform_pp": tu,
+                                           "stadi_latency_reduction": 1.0 - ts / tu},
+                     "note": "probe times measured on this GPU under the emulator; the 4-GPU "
+                             "latencies are a compute-only projection, not a measurement"}
+
     # ---- roofline of the dominant kernel class (largest share of kernel time)
     peaks = load_peaks()
     names = {"attn": "tc_attn_kernel (own Q x full stale K/V, tcgen05/TMEM, TMA)",
@@ -562,6 +600,7 @@ def main():
             "uniform_pp": uni, "e2e": e2e, "roofline": roof, "path_roofline": path_roof,
             "kernels": kernels,
             "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(launches),
+            "occupancy_sweep": occ_sweep,
             "context": PAPER_CONTEXT,
         }
         print(json.dumps(res), flush=True)

@@ -250,8 +250,12 @@ stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, const float *no
                        const stadi_cond *cond, float *out_full, stadi_run_stats *stats,
                        void *stream);
 
-/* Occupancy emulator: pin ceil(pct * SMs / 100) SMs with a
- * persistent spin kernel until stopped (hard self-timeout 900 s). */
+/* Occupancy emulator (R24): take ceil(pct * SMs / 100) SMs,
+ * rounded up to an even count (whole TPCs, so the free SMs still form the CTA
+ * pairs of the cta_group::2 GEMMs), with a resident kernel whose CTAs hold all of
+ * an SM's shared memory, threads and registers and sleep until stopped (hard
+ * self-timeout 900 s).  The context's persistent GEMM grids shrink to the free
+ * SMs.  ESTATE if already running; EINVAL for pct > 95. */
 stadi_status stadi_emulator_start(stadi_ctx *ctx, uint32_t occupancy_pct);
 stadi_status stadi_emulator_stop(stadi_ctx *ctx);
 

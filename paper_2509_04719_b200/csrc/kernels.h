@@ -93,5 +93,12 @@ cudaError_t concat_channels(const float *a, int Ca, const float *b, int Cb, long
 
 // ---- occupancy emulator ---------------------------------
 cudaError_t emulator_launch(int n_ctas, volatile int *stop_flag, cudaStream_t s);
+// Force-load every tcgen05 GEMM / attention kernel instance (lazy loading must
+// not happen while the occupancy emulator's kernel is resident: deadlock).
+cudaError_t tc_gemm_preload();
+cudaError_t tc_attention_preload();
+// SMs the emulator takes for pct% occupancy: ceil(pct * SMs / 100) rounded up to
+// whole TPCs (even).
+int emulator_ctas(int pct, int num_sms);
 
 }  // namespace stadi

@@ -2,6 +2,7 @@
 // no tensor cores, no TF32 — and small conditioning GEMMs),
 // plus the HBM-bound elementwise kernels of the hot path (LN + adaLN modulate,
 // patch embedding, fused CFG + unpatchify + Eq. 3 sampler).
+#include <cstdlib>
 #include <float.h>
 
 #include "../kernels.h"
@@ -471,33 +472,58 @@ template cudaError_t class_cond<bf16>(const float *, const float *, const int *,
 
 // ------------------------------------------------------------------ occupancy emulator
 namespace {
-// One CTA per SM (max shared memory + 1024 threads keep anything else off that
-// SM).  FMA spin until *stop is set or 900 s elapse.
+// Occupancy emulator (reading R24: occupancy = SMs taken away).
+// One CTA per SM whose shared memory keeps everything else off that SM: the
+// opt-in maximum per CTA plus the 1 KB every CTA reserves is the SM's whole
+// 228 KB, so no other CTA (which needs at least its own reserved 1 KB) fits.
+// CTAs are launched in clusters of two, so the emulator takes whole TPCs and the
+// free SMs still pair up for the cta_group::2 GEMMs.
+// Thread 0 sleeps (nanosleep) between polls of the host-mapped stop flag, the
+// other warps wait at a barrier: the emulator holds SMs without issuing work or
+// memory traffic, so the free SMs run at their full speed (an FMA spin with every
+// thread polling host memory made the free SMs 2-5x slower, not 1/(1 - rho)).
 __global__ void __launch_bounds__(1024, 1) emulator_kernel(volatile int *stop) {
   extern __shared__ float pad[];
-  const uint64_t t0 = globaltimer();
-  float a = threadIdx.x * 1e-3f, b = 1.0001f;
-  for (uint32_t it = 0;; ++it) {
-#pragma unroll 16
-    for (int k = 0; k < 256; ++k) a = fmaf(a, b, 1e-7f);
-    if ((it & 63) == 0) {
-      if (*stop) break;
-      if (globaltimer() - t0 > 900000000000ull) break;
-    }
+  if (threadIdx.x == 0) {  // one poller per CTA: 1024 pollers of host memory per SM
+    const uint64_t t0 = globaltimer();  // flooded PCIe and slowed the whole chip
+    while (!*stop && globaltimer() - t0 < 900000000000ull) __nanosleep(20000);
+    pad[0] = 0.f;
   }
-  if (a == 12345.f) pad[threadIdx.x] = a;  // keep the loop alive
+  __syncthreads();  // the other warps wait here without issuing
 }
 }  // namespace
 
+int emulator_ctas(int pct, int num_sms) {  // whole TPCs: an even number of SMs
+  if (pct <= 0) return 0;
+  int n = (int)((pct * (long)num_sms + 99) / 100);
+  n += n & 1;
+  return n > num_sms ? num_sms : n;
+}
+
 cudaError_t emulator_launch(int n_ctas, volatile int *stop_flag, cudaStream_t s) {
   if (n_ctas <= 0) return cudaSuccess;
-  const int smem = 200 * 1024;
+  int dev = 0, smem = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaError_t e =
       cudaFuncSetAttribute(emulator_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  emulator_kernel<<<n_ctas, 1024, smem, s>>>(stop_flag);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)((n_ctas + 1) & ~1));
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  const char *ec = getenv("STADI_EMU_CLUSTER");  // =0: plain launch (A/B)
+  cfg.numAttrs = (ec && ec[0] == '0') ? 0 : 1;
+  e = cudaLaunchKernelEx(&cfg, emulator_kernel, stop_flag);
   ++g_launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace stadi

@@ -139,8 +139,15 @@ struct AttnCfg {
   __host__ __device__ static constexpr uint32_t cswz(int c) {
     return cw(c) == 64 ? SWZ_128B : (cw(c) == 32 ? SWZ_64B : SWZ_32B);
   }
+#ifndef STADI_ATTN_SMEM_KB
+#define STADI_ATTN_SMEM_KB 200
+#endif
+#ifndef STADI_ATTN_MAX_STAGES
+#define STADI_ATTN_MAX_STAGES 4
+#endif
+  static constexpr int STAGES_FIT = (STADI_ATTN_SMEM_KB * 1024 - NQT * QTILE) / (2 * KTILE);
   static constexpr int STAGES =
-      (200 * 1024 - NQT * QTILE) / (2 * KTILE) > 4 ? 4 : (200 * 1024 - NQT * QTILE) / (2 * KTILE);
+      STAGES_FIT > STADI_ATTN_MAX_STAGES ? STADI_ATTN_MAX_STAGES : STAGES_FIT;
   static constexpr int OFF_K = NQT * QTILE;
   static constexpr int OFF_V = OFF_K + STAGES * KTILE;
   static constexpr int OFF_BAR = OFF_V + STAGES * KTILE;
@@ -433,8 +440,10 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         umma_commit(&v_empty[pvs]);
       } else {
       for (int j = 0; j < n_kv; ++j) {
+        ATTN_TRACE(13, 0, j);
         if (j + 1 < n_kv) {
           mbar_wait(&k_full[ks], kph);
+          ATTN_TRACE(14, 0, j);
 #pragma unroll
           for (int g = 0; g < NQT; ++g) {
             mbar_wait(&s_free[g], j & 1);
@@ -450,7 +459,9 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
             kph ^= 1;
           }
         }
+        ATTN_TRACE(13, 1, j);
         mbar_wait(&v_full[vs], vph);
+        ATTN_TRACE(14, 1, j);
 #pragma unroll
         for (int g = 0; g < NQT; ++g) {
           mbar_wait(&p_full[g], j & 1);
@@ -887,6 +898,29 @@ int attn_narrow() {
     return (e && e[0] == '0') ? 0 : 1;
   }();
   return v;
+}
+
+// Force-load every attention kernel instance (see tc_gemm_preload).
+namespace {
+template <int N64, int N32, int N16, int NQT>
+void preload_attn(cudaFuncAttributes *a) {
+  cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 0>);
+  cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 1>);
+  cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 1, 1>);
+  cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 2, 1>);
+  cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 3, 1>);
+  cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 4, 1>);
+}
+}  // namespace
+cudaError_t tc_attention_preload() {
+  cudaFuncAttributes a;
+  preload_attn<0, 0, 1, 2>(&a);
+  preload_attn<0, 1, 1, 2>(&a);
+  preload_attn<1, 0, 0, 2>(&a);
+  preload_attn<0, 0, 5, 2>(&a);
+  preload_attn<1, 0, 1, 2>(&a);
+  preload_attn<2, 1, 0, 1>(&a);
+  return cudaGetLastError();
 }
 
 // Supported head dims (padded to hd_pad): 16 (16), 40 (48 = 32 + 16), 64 (64),

@@ -581,8 +581,21 @@ int gemm_pair_mode() {
   }();
   return v;
 }
+int device_sms() {
+  static const int v = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return v;
+}
 int pair_mode_for(int tm, int max_ctas, int epi) {
-  if (tm < 4 || max_ctas < 2) return 1;
+  // Fewer CTAs than SMs means the occupancy emulator holds the rest: launch
+  // single-CTA tiles (no clusters).  Measured on B200: with 40% of the SMs held,
+  // 2-CTA cluster launches of the C2-shaped GEMMs never got placed (hang), while
+  // cluster-free launches run on the free SMs.
+  if (tm < 4 || max_ctas < 2 || max_ctas < device_sms()) return 1;
   if (gemm_pair_mode()) return gemm_pair_mode();
   return (epi == EPI_GATED_RES || epi == EPI_RES) ? 2 : 3;
 }
@@ -603,6 +616,51 @@ cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int 
     case 128: return dispatch_mc<128>(A, W, M, N, K, epi, ep, max_ctas, mc, g.ks, s);
     default: return dispatch_mc<64>(A, W, M, N, K, epi, ep, max_ctas, mc, g.ks, s);
   }
+}
+
+// Force-load every GEMM kernel instance the dispatch can select (CUDA lazy loading
+// would otherwise load a never-launched variant -- e.g. single-CTA tiles chosen
+// because the occupancy emulator holds SMs -- on first launch, and loading may
+// need a context synchronisation, which never completes while the emulator's
+// resident kernel runs: a deadlock observed on B200 with the C2 shapes).
+namespace {
+template <int BN, int MC>
+void preload_bn_mc(cudaFuncAttributes *a) {
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_STORE, MC, 0>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_GELU, MC, 0>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_GATED_RES, MC, 0>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_RES, MC, 0>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_QKV, MC, 0>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_F32, MC, 0>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_CONV, MC, 0>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_GEGLU, MC, 0>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_CONV, MC, 1>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_F32, MC, 1>);
+}
+template <int BN>
+void preload_bn(cudaFuncAttributes *a) {
+  preload_bn_mc<BN, 1>(a);
+  preload_bn_mc<BN, 2>(a);
+  preload_bn_mc<BN, 3>(a);
+}
+}  // namespace
+
+cudaError_t tc_gemm_preload() {
+  cudaFuncAttributes a;
+  preload_bn<256>(&a);
+  preload_bn<192>(&a);
+  preload_bn<160>(&a);
+  preload_bn<128>(&a);
+  preload_bn<64>(&a);
+  cudaFuncGetAttributes(&a, splitk_reduce_kernel<EPI_STORE>);
+  cudaFuncGetAttributes(&a, splitk_reduce_kernel<EPI_GELU>);
+  cudaFuncGetAttributes(&a, splitk_reduce_kernel<EPI_GATED_RES>);
+  cudaFuncGetAttributes(&a, splitk_reduce_kernel<EPI_RES>);
+  cudaFuncGetAttributes(&a, splitk_reduce_kernel<EPI_QKV>);
+  cudaFuncGetAttributes(&a, splitk_reduce_kernel<EPI_F32>);
+  cudaFuncGetAttributes(&a, splitk_reduce_kernel<EPI_CONV>);
+  cudaFuncGetAttributes(&a, splitk_reduce_kernel<EPI_GEGLU>);
+  return cudaGetLastError();
 }
 
 // Implicit-GEMM 3x3 conv (stride 1): out = epi(conv(P) . W^T) with P the

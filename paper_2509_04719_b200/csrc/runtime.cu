@@ -1339,7 +1339,15 @@ extern "C" stadi_status stadi_emulator_start(stadi_ctx *ctx, uint32_t pct) {
   if (ctx->emu_ctas) return ctx_fail(ctx, STADI_ESTATE, "emulator already running");
   if (pct == 0) return STADI_OK;
   CK(cudaSetDevice(ctx->device));
-  const int n = (int)std::ceil(pct * ctx->num_sms / 100.0);
+  const int n = emulator_ctas((int)pct, ctx->num_sms);
+  // every kernel the context may launch while the emulator is resident must be
+  // loaded now (lazy loading may need a context sync: it would wait for the
+  // emulator forever); the SIMT kernels are loaded by this context's earlier work
+  // or by the bench's profiling pass, the tcgen05 variants depend on the free SMs
+  if (ctx->dtype == STADI_DTYPE_BF16) {
+    CK(tc_gemm_preload());
+    CK(tc_attention_preload());
+  }
   *ctx->emu_flag_host = 0;
   CK(emulator_launch(n, ctx->emu_flag_dev, ctx->emu_stream));
   ctx->emu_ctas = n;

@@ -17,14 +17,15 @@ int main(int argc, char **argv) {
   cudaDeviceSynchronize();
   std::vector<long long> t(16 * 2 * 64);
   cudaMemcpyFromSymbol(t.data(), g_attn_trace, t.size() * 8);
-  const char *names[13] = {"mma:s_free", "mma:S_iss", "mma:p_full", "sm:s_full",
+  const char *names[15] = {"mma:s_free", "mma:S_iss", "mma:p_full", "sm:s_full",
                            "sm:loaded", "sm:max", "sm:p_arr", "sm:tok", "mma:PV_iss", "sm:o_done",
-                           "sm:exp_end", "sm:pv_wait", "sm:st_done"};
+                           "sm:exp_end", "sm:pv_wait", "sm:st_done", "mma:top(g0)/pre_v(g1)",
+                           "mma:k_full(g0)/v_full(g1)"};
   long long t0 = t[(3 * 2 + 0) * 64 + 0];
   for (int j = 0; j < 16; ++j)
     for (int g = 0; g < 2; ++g) {
       printf("j=%2d g=%d:", j, g);
-      for (int e = 0; e < 13; ++e) printf(" %s=%6lld", names[e], t[(e * 2 + g) * 64 + j] - t0);
+      for (int e = 0; e < 15; ++e) printf(" %s=%6lld", names[e], t[(e * 2 + g) * 64 + j] - t0);
       printf("\n");
     }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));

@@ -28,7 +28,8 @@ def attn(Nq, Nkv, B, H, hd):
     q = torch.randn(Nq * B, d, device="cuda").to(torch.bfloat16)
     kv = torch.randn(Nkv * B * 2, d, device="cuda").to(torch.bfloat16)
     o = torch.empty(Nq * B, d, device="cuda", dtype=torch.bfloat16)
-    ms = timeit(lambda: S.k_attention(0, q, kv, o, Nq, Nkv, B, H, hd))
+    ms = timeit(lambda: S.k_attention(0, q, kv, o, Nq, Nkv, B, H, hd,
+                                     stream=torch.cuda.current_stream()))
     fl = 4.0 * Nq * Nkv * hd * B * H
     print(f"attn Nq={Nq} Nkv={Nkv} B={B} H={H} hd={hd}: {ms:.3f} ms  {fl / ms / 1e9:.0f} TFLOP/s")
 
@@ -51,7 +52,7 @@ def gemm(M, N, K, epi):
     else:
         out = torch.empty(M, N, device="cuda")
         kw.update(out=out, ldo=N)
-    ms = timeit(lambda: S.k_gemm(0, A, W, M, N, K, epi, **kw))
+    ms = timeit(lambda: S.k_gemm(0, A, W, M, N, K, epi, stream=torch.cuda.current_stream(), **kw))
     print(f"gemm M={M} N={N} K={K} epi={epi}: {ms:.3f} ms  {2.0 * M * N * K / ms / 1e9:.0f} TFLOP/s")
 
 
