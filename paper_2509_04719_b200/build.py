@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-Xptxas", "-v",
-         "-DNDEBUG"]
+         "-DNDEBUG"] + os.environ.get("STADI_NVCC_EXTRA", "").split()  # experiment defines
 
 
 def sources():

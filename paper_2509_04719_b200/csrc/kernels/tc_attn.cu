@@ -504,8 +504,13 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
       tc_fence_after();
       const int valid = Nkv - j * AKT;
       float v[4 * NR];
+#ifdef STADI_ATTN_NOSLOAD  // timing experiment only (wrong results): no S read
+#pragma unroll
+      for (int i = 0; i < 4 * NR; ++i) v[i] = (float)(i + j) * 1e-3f;
+#else
       tmem_ld_q256<NR>(s_addr, reinterpret_cast<uint32_t *>(v));
       tmem_ld_wait();
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[g]);
@@ -586,6 +591,11 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
           const uint64_t xx =
               ffma_f32x2(pack_f32x2(v[4 * r + 2 * rr], v[4 * r + 2 * rr + 1]), sc2, nm2[rr]);
           float p0, p1;
+#ifdef STADI_ATTN_NOEXP  // timing experiment only (wrong results): no exp work
+          if (true) {
+            unpack_f32x2(xx, p0, p1);
+          } else
+#endif
           if (r % 8 < POLY) {
             ex2_poly_x2(xx, p0, p1);
           } else {
@@ -605,7 +615,11 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
         tc_fence_after();
       }
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(11, g, j);
+#ifndef STADI_ATTN_NOPST  // timing experiment only (wrong results): no P store
       tmem_st_q128<NR>(p_addr, pk);
+#else
+      if (pk[0] == 0x12345u) tmem_st_q128<NR>(p_addr, pk);
+#endif
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
         float s0, s1, s2, s3;

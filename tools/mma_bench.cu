@@ -46,6 +46,7 @@ void run(float *d) {
 }
 int main() {
   float *d; cudaMalloc(&d, 8);
+  run<16, false>(d); run<32, false>(d); run<16, true>(d); run<32, true>(d);
   run<64, false>(d); run<80, false>(d); run<112, false>(d); run<128, false>(d); run<256, false>(d);
   run<64, true>(d); run<80, true>(d); run<128, true>(d); run<256, true>(d);
 }
