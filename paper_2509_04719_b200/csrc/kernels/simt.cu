@@ -478,14 +478,16 @@ namespace {
 // 228 KB, so no other CTA (which needs at least its own reserved 1 KB) fits.
 // CTAs are launched in clusters of two, so the emulator takes whole TPCs and the
 // free SMs still pair up for the cta_group::2 GEMMs.
-// Thread 0 sleeps (nanosleep) between polls of the host-mapped stop flag, the
-// other warps wait at a barrier: the emulator holds SMs without issuing work or
-// memory traffic, so the free SMs run at their full speed (an FMA spin with every
-// thread polling host memory made the free SMs 2-5x slower, not 1/(1 - rho)).
+// Thread 0 sleeps (nanosleep) between polls of a stop flag in DEVICE memory (the
+// host sets it with a memset on another stream), the other warps wait at a
+// barrier: the emulator holds SMs without issuing work or memory traffic, so the
+// free SMs run at full speed.  Measured (tools/emu_bench.cu): polling a
+// host-mapped flag, even one thread per CTA every 20 us, made unrelated small
+// kernels on the free SMs 3-9x slower; a device flag costs nothing.
 __global__ void __launch_bounds__(1024, 1) emulator_kernel(volatile int *stop) {
   extern __shared__ float pad[];
-  if (threadIdx.x == 0) {  // one poller per CTA: 1024 pollers of host memory per SM
-    const uint64_t t0 = globaltimer();  // flooded PCIe and slowed the whole chip
+  if (threadIdx.x == 0) {  // one poller per CTA
+    const uint64_t t0 = globaltimer();
     while (!*stop && globaltimer() - t0 < 900000000000ull) __nanosleep(20000);
     pad[0] = 0.f;
   }

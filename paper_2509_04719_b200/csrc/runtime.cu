@@ -156,8 +156,9 @@ struct stadi_ctx {
   uint64_t exch_bytes = 0;
 
   // emulator
-  int *emu_flag_host = nullptr;
-  int *emu_flag_dev = nullptr;
+  int *emu_flag_dev = nullptr;       // emulator stop flag in DEVICE memory (polling
+                                     // host-mapped memory slowed every kernel 3-9x)
+  cudaStream_t emu_ctl = nullptr;    // non-blocking stream that writes the flag
   cudaStream_t emu_stream = nullptr;
   int emu_ctas = 0;
 
@@ -568,10 +569,10 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
       std::memcpy(&id, dist->nccl_id, 128);
       CKN(nccl().CommInitRank(&ctx->world_comm, dist->world, id, dist->rank));
     }
-    CK(cudaHostAlloc(&ctx->emu_flag_host, 64, cudaHostAllocMapped));
-    *ctx->emu_flag_host = 0;
-    CK(cudaHostGetDevicePointer(&ctx->emu_flag_dev, ctx->emu_flag_host, 0));
+    CK(cudaMalloc(&ctx->emu_flag_dev, 64));
+    CK(cudaMemset(ctx->emu_flag_dev, 0, 64));
     CK(cudaStreamCreateWithFlags(&ctx->emu_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->emu_ctl, cudaStreamNonBlocking));
   }
   *out = ctx.release();
   return STADI_OK;
@@ -581,7 +582,7 @@ extern "C" void stadi_destroy(stadi_ctx *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->emu_ctas) {
-    *ctx->emu_flag_host = 1;
+    cudaMemsetAsync(ctx->emu_flag_dev, 1, 4, ctx->emu_ctl);
     cudaStreamSynchronize(ctx->emu_stream);
   }
   cudaDeviceSynchronize();
@@ -594,13 +595,14 @@ extern "C" void stadi_destroy(stadi_ctx *ctx) {
   if (ctx->astream) cudaStreamDestroy(ctx->astream);
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   if (ctx->emu_stream) cudaStreamDestroy(ctx->emu_stream);
+  if (ctx->emu_ctl) cudaStreamDestroy(ctx->emu_ctl);
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
   for (auto &k : ctx->kt)
     for (auto &pr : k.ev) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
     }
-  if (ctx->emu_flag_host) cudaFreeHost(ctx->emu_flag_host);
+  if (ctx->emu_flag_dev) cudaFree(ctx->emu_flag_dev);
   cudaGetLastError();
   delete ctx;
 }
@@ -1348,7 +1350,7 @@ extern "C" stadi_status stadi_emulator_start(stadi_ctx *ctx, uint32_t pct) {
     CK(tc_gemm_preload());
     CK(tc_attention_preload());
   }
-  *ctx->emu_flag_host = 0;
+  CK(cudaMemsetAsync(ctx->emu_flag_dev, 0, 4, ctx->emu_stream));
   CK(emulator_launch(n, ctx->emu_flag_dev, ctx->emu_stream));
   ctx->emu_ctas = n;
   return STADI_OK;
@@ -1357,7 +1359,7 @@ extern "C" stadi_status stadi_emulator_start(stadi_ctx *ctx, uint32_t pct) {
 extern "C" stadi_status stadi_emulator_stop(stadi_ctx *ctx) {
   ALIVE();
   if (!ctx->emu_ctas) return STADI_OK;
-  *ctx->emu_flag_host = 1;
+  CK(cudaMemsetAsync(ctx->emu_flag_dev, 1, 4, ctx->emu_ctl));  // nonzero: stop
   CK(cudaStreamSynchronize(ctx->emu_stream));
   ctx->emu_ctas = 0;
   return STADI_OK;
