@@ -592,11 +592,12 @@ int device_sms() {
 }
 int pair_mode_for(int tm, int max_ctas, int epi) {
   // Fewer CTAs than SMs means the occupancy emulator holds the rest: launch
-  // single-CTA tiles (no clusters).  Measured on B200: with 40% of the SMs held,
-  // 2-CTA cluster launches of the C2-shaped GEMMs never got placed (hang), while
-  // cluster-free launches run on the free SMs.
-  if (tm < 4 || max_ctas < 2 || max_ctas < device_sms()) return 1;
+  // single-CTA tiles, free of cluster-placement constraints on a partly held GPU
+  // (measured on B200 with the C2 / C5 shapes at 20-60%: same speed as CTA pairs;
+  // STADI_GEMM_MC overrides).
+  if (tm < 4 || max_ctas < 2) return 1;
   if (gemm_pair_mode()) return gemm_pair_mode();
+  if (max_ctas < device_sms()) return 1;
   return (epi == EPI_GATED_RES || epi == EPI_RES) ? 2 : 3;
 }
 
