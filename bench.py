@@ -387,6 +387,13 @@ def main():
         run_reference(args, cfg, wl, rank, world)
         return
 
+    # stdout carries exactly one JSON line: everything else written to fd 1 (NCCL's
+    # "NCCL version" banner at communicator init, library / CUDA messages) goes to
+    # stderr; the result is written to the saved stdout at the end
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+
     import torch
     import torch.distributed as dist
     from paper_2509_04719_b200 import stadi as S
@@ -435,20 +442,31 @@ def main():
     # emulator's resident kernel runs can need a context sync -> deadlock; the
     # library force-loads the SM-count-dependent tcgen05 variants itself)
     ctx.profile_warmup(1, world)
+    # host-side buffers of the e2e leg, pinned now: nothing that may synchronise the
+    # device (allocator / stream-pool first use) runs while the emulator is resident
+    noise_h = torch.from_numpy(x).pin_memory()
+    out_h = torch.empty_like(noise_h).pin_memory()
+    cond_h = dict(c)
+    if "text" in c:
+        cond_h = {k: (torch.from_numpy(v).pin_memory() if k != "time_ids" else v)
+                  for k, v in c.items()}
+    noise_dev = torch.from_numpy(x).cuda()
+    cond = dict(c)
+    if "text" in c:  # conditioning resident in HBM for the device-timed legs
+        cond = {k: (torch.from_numpy(v).cuda() if k != "time_ids" else v) for k, v in c.items()}
+    out_dev = torch.empty_like(noise_dev)
+    stream = torch.cuda.current_stream()
+    e_pre = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e_pre[0].record(stream)
+    e_pre[1].record(stream)
+    stream.synchronize()
+
     if occ[rank]:
         ctx.emulator_start(occ[rank])
     barrier()
     ms_prof, speed = ctx.profile_warmup(3, world)
     plan = S.plan(speed, wl["m_base"], wl["m_warmup"], p_total, p)
     uplan = S.plan(speed, wl["m_base"], wl["m_warmup"], p_total, p, flags=S.NO_TA | S.NO_SA)
-
-    noise_dev = torch.from_numpy(x).cuda()
-    text_dev = None
-    cond = dict(c)
-    if "text" in c:  # conditioning resident in HBM for the device-timed legs
-        cond = {k: (torch.from_numpy(v).cuda() if k != "time_ids" else v) for k, v in c.items()}
-    out_dev = torch.empty_like(noise_dev)
-    stream = torch.cuda.current_stream()
 
     # NOTE: stream synchronisation, not torch.cuda.synchronize(): on the ranks with
     # emulated occupancy a persistent spin kernel stays resident on the device for
@@ -500,12 +518,6 @@ def main():
     # ---- e2e: through the C ABI with pinned HOST buffers (H2D + D2H inside)
     e2e = None
     if not args.no_e2e:
-        noise_h = torch.from_numpy(x).pin_memory()
-        out_h = torch.empty_like(noise_h).pin_memory()
-        cond_h = dict(c)
-        if "text" in c:
-            cond_h = {k: (torch.from_numpy(v).pin_memory() if k != "time_ids" else v)
-                      for k, v in c.items()}
         ems, _ = timed(plan, noise_h, out_h, cond_h, args.steps, 1)
         h2d = x.nbytes + sum(v.nbytes for v in c.values())
         e2e = {"value": 1e3 / (ems / args.steps), "unit": "images/s",
@@ -603,7 +615,8 @@ def main():
             "occupancy_sweep": occ_sweep,
             "context": PAPER_CONTEXT,
         }
-        print(json.dumps(res), flush=True)
+        sys.stdout.flush()
+        os.write(json_fd, (json.dumps(res) + "\n").encode())
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

@@ -102,6 +102,10 @@ struct stadi_ctx {
   int sampler = STADI_SAMPLER_DDIM;
   uint64_t ddpm_seed = 0;    // per request (stadi_cond), R19
   int device = 0, rank = 0, world = 1, n_local = 1, G = 1;
+  // NCCL mode: one rank per process, exchange by NCCL (world > 1; or world == 1 with
+  // STADI_FORCE_NCCL=1, a single-rank communicator that runs the NCCL code path --
+  // broadcasts, comm stream, version events, gather -- on one GPU for tests)
+  bool nccl = false;
   int num_sms = 148;
   std::string err;
   bool poisoned = false;
@@ -526,6 +530,10 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
   ctx->world = dist->world;
   ctx->n_local = dist->n_local;
   ctx->G = dist->world * dist->n_local;
+  {
+    const char *fe = getenv("STADI_FORCE_NCCL");
+    ctx->nccl = dist->world > 1 || (dist->n_local == 1 && fe && fe[0] == '1');
+  }
   ctx->man = manifest(dm);
   ctx->fin_ld = (int)rup(dm.p * dm.p * dm.c_out, 64);
   alpha_bar(dm.schedule_linear != 0, ctx->abar);
@@ -562,12 +570,42 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
       ctx->splitk_elems = (long)ctx->num_sms * 128 * 256;
       CK(dalloc(ctx, &ctx->splitk_ws, (size_t)ctx->splitk_elems * 4));
     }
-    if (dist->world > 1) {
+    if (ctx->nccl) {
       if (!nccl().ok) return ctx_fail(ctx, STADI_ENCCL, "libnccl.so.2 not loadable");
-      if (!dist->nccl_id) return ctx_fail(ctx, STADI_EINVAL, "nccl_id required when world > 1");
       ncclUniqueId id;
-      std::memcpy(&id, dist->nccl_id, 128);
+      if (dist->world == 1) {
+        CKN(nccl().GetUniqueId(&id));
+      } else {
+        if (!dist->nccl_id) return ctx_fail(ctx, STADI_EINVAL, "nccl_id required when world > 1");
+        std::memcpy(&id, dist->nccl_id, 128);
+      }
       CKN(nccl().CommInitRank(&ctx->world_comm, dist->world, id, dist->rank));
+      // Launch every collective this context uses once now (grouped broadcasts of
+      // bf16 / fp32 rows, small and large, and the fp64 all-gather of the
+      // profiler), so that NCCL's kernels are loaded before the occupancy emulator
+      // can be resident: CUDA lazy loading of a kernel first launched under a
+      // resident kernel may need a context synchronisation -> deadlock (observed).
+      {
+        const size_t big = (size_t)8 << 20;
+        void *buf = nullptr;
+        CK(cudaMalloc(&buf, big * 4 + 64 * dist->world));
+        CK(cudaMemset(buf, 0, big * 4 + 64 * dist->world));
+        for (size_t n : {(size_t)256, big}) {
+          for (ncclDataType_t dt : {ncclBfloat16, ncclFloat32}) {
+            CKN(nccl().GroupStart());
+            const size_t seg = n / dist->world;  // disjoint per-root segments
+            for (int r = 0; r < dist->world; ++r) {
+              void *p = (char *)buf + r * seg * 4;
+              CKN(nccl().Broadcast(p, p, seg, dt, r, ctx->world_comm, ctx->comm));
+            }
+            CKN(nccl().GroupEnd());
+          }
+        }
+        double *d64 = reinterpret_cast<double *>((char *)buf + big * 4);
+        CKN(nccl().AllGather(d64, d64 + 1, 1, ncclFloat64, ctx->world_comm, ctx->comm));
+        CK(cudaStreamSynchronize(ctx->comm));
+        CK(cudaFree(buf));
+      }
     }
     CK(cudaMalloc(&ctx->emu_flag_dev, 64));
     CK(cudaMemset(ctx->emu_flag_dev, 0, 64));
@@ -761,7 +799,7 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     ctx->ranks.push_back(std::move(r));
   }
   // program
-  if (ctx->world > 1) {
+  if (ctx->nccl) {
     if (!ctx->ranks.empty())
       for (auto &st : ctx->ranks[0].sched) ctx->program.push_back({Part{0, st}});
   } else {
@@ -774,7 +812,7 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     }
   }
   // NCCL: communicator over the included ranks + exchange events
-  if (ctx->world > 1) {
+  if (ctx->nccl) {
     const bool inc = !ctx->ranks.empty();
     bool all_inc = true;
     for (uint32_t i = 0; i < plan->n_gpus; ++i) all_inc &= plan->tier[i] != 0;
@@ -970,7 +1008,7 @@ stadi_status publish(stadi_ctx *ctx, int li, int l, int ver, cudaStream_t s) {
   int64_t off, cnt;
   seg_of(ctx, r.g, &off, &cnt);
   const size_t bytes = cnt * ctx->esz;
-  if (ctx->world == 1) {  // local mode: copy into every other hosted rank's slot
+  if (!ctx->nccl) {  // local mode: copy into every other hosted rank's slot
     for (auto &o : ctx->ranks) {
       if (o.g == r.g) continue;
       CK(cudaMemcpyAsync((char *)o.kv[slot] + off * ctx->esz, (char *)r.kv[slot] + off * ctx->esz,
@@ -1002,7 +1040,7 @@ stadi_status publish(stadi_ctx *ctx, int li, int l, int ver, cudaStream_t s) {
 
 // Make stream s wait until version `ver` of site l is complete (NCCL mode).
 stadi_status wait_version(stadi_ctx *ctx, int l, int ver, cudaStream_t s) {
-  if (ctx->world == 1 || ver < 0) return STADI_OK;
+  if (!ctx->nccl || ver < 0) return STADI_OK;
   const int slot = l * 2 + (ver & 1);
   if (ctx->ev_used[slot]) CK(cudaStreamWaitEvent(s, ctx->ev_done[slot], 0));
   return STADI_OK;
@@ -1129,7 +1167,7 @@ bool graphs_enabled(stadi_ctx *ctx) {
   }();
   // local mode only (NCCL mode's cross-stream exchange events stay eager), and not
   // while per-launch kernel timing is on (its events must see every launch)
-  return env && ctx->world == 1 && !ctx->ktime;
+  return env && !ctx->nccl && !ctx->ktime;
 }
 
 // Program step i on stream s: replay its graph, capturing it on first use.
@@ -1181,7 +1219,7 @@ extern "C" stadi_status stadi_gather(stadi_ctx *ctx, float *out_full, void *stre
   CK(cudaSetDevice(ctx->device));
   const bool dev = is_device_ptr(out_full);
   const size_t row_elems = (size_t)m.lat_w * m.c_in;
-  if (ctx->world == 1) {
+  if (!ctx->nccl) {
     for (auto &r : ctx->ranks)
       CK(cudaMemcpyAsync(out_full + (size_t)r.row_begin * row_elems, r.x_band,
                          (size_t)r.rows * row_elems * 4,
@@ -1310,7 +1348,7 @@ extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, d
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   std::vector<double> all(ctx->G, 0.0);
-  if (ctx->world == 1) {
+  if (!ctx->nccl) {
     for (size_t li = 0; li < ctx->ranks.size(); ++li) all[ctx->ranks[li].g] = ms_local[li];
   } else {
     double *dsend = nullptr, *drecv = nullptr;

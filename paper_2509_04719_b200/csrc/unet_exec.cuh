@@ -251,7 +251,7 @@ stadi_status u_publish(stadi_ctx *ctx, USite &S, int li, int ver, cudaStream_t s
   };
   int64_t off, bytes;
   seg(r.g, &off, &bytes);
-  if (ctx->world == 1) {
+  if (!ctx->nccl) {
     for (size_t lj = 0; lj < ctx->ranks.size(); ++lj) {
       if ((int)lj == li) continue;
       CK(cudaMemcpyAsync((char *)S.slot[lj][par] + off, (char *)S.slot[li][par] + off, bytes,
@@ -282,7 +282,7 @@ stadi_status u_publish(stadi_ctx *ctx, USite &S, int li, int ver, cudaStream_t s
 }
 
 stadi_status u_wait(stadi_ctx *ctx, USite &S, int ver, cudaStream_t s) {
-  if (ctx->world == 1 || ver < 0) return STADI_OK;
+  if (!ctx->nccl || ver < 0) return STADI_OK;
   if (S.used[ver & 1]) CK(cudaStreamWaitEvent(s, S.ev[ver & 1], 0));
   return STADI_OK;
 }
@@ -833,7 +833,7 @@ stadi_status unet_set_plan(stadi_ctx *ctx) {
         CK(pmalloc(ctx, &pr[par], std::max<int64_t>(bytes, 16)));
         CK(cudaMemsetAsync(pr[par], 0, std::max<int64_t>(bytes, 16), ctx->astream));
       }
-    if (ctx->world > 1)
+    if (ctx->nccl)
       for (auto &e : S.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   CK(cudaStreamSynchronize(ctx->astream));
