@@ -22,6 +22,13 @@ Readings:
   R6  one unit = rows_per_unit latent rows.
   R7  Eq. 5 uses M_i of Eq. 4 (flag SIZER_INTERVAL: per-round step counts).
   R8  rank order, top to bottom.
+  R30 (flag SIZER_AFFINE; L333: "the single-step delay no longer maintains a
+      linear relationship with the patch size due to some fixed overhead")
+      per-step latency of GPU i on P units modelled as alpha_i + beta_i P
+      (integer time units); Eq. 5 is replaced by minimising the makespan
+      max_i M_i (alpha_i + beta_i P_i): one unit per included GPU, then each
+      further unit to argmin_i M_i (alpha_i + beta_i (P_i + 1)), ties to the
+      lowest rank.  With alpha = 0 and beta_i = L / v_i this is R5's D'Hondt.
 Written with plain Python integers and fractions.Fraction (exact).
 """
 from __future__ import annotations
@@ -32,6 +39,7 @@ NO_TA = 1
 NO_SA = 2
 SIZER_INTERVAL = 4
 FORCE_UNITS = 8
+SIZER_AFFINE = 16
 
 
 class PlanError(ValueError):
@@ -64,7 +72,7 @@ def steps_of(tier, m_base, m_warmup):
 
 
 def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
-         flags=0, forced_units=None):
+         flags=0, forced_units=None, alpha=None, beta=None):
     """Return the assignment (M_i, P_i) per GPU plus derived schedule facts."""
     n = len(speed)
     if n < 1 or n > 64:
@@ -99,6 +107,16 @@ def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
             if (tier[i] == 0) != (forced_units[i] == 0):
                 raise PlanError("forced units: included GPUs need >= 1, excluded 0")
         units = list(forced_units)
+    elif flags & SIZER_AFFINE:
+        if alpha is None or beta is None or len(alpha) != n or len(beta) != n:
+            raise PlanError("SIZER_AFFINE needs alpha and beta")
+        if any(int(beta[i]) <= 0 for i in inc):
+            raise PlanError("beta must be > 0")
+        for i in inc:
+            units[i] = 1
+        for _ in range(p_total - len(inc)):          # R30: greedy min-makespan
+            best = min(inc, key=lambda i: (steps[i] * (int(alpha[i]) + int(beta[i]) * (units[i] + 1)), i))
+            units[best] += 1
     elif flags & NO_SA:
         q, r = divmod(p_total, len(inc))
         for k, i in enumerate(inc):
@@ -128,7 +146,10 @@ def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
         row_begin[i] = acc * rows_per_unit
         rows[i] = units[i] * rows_per_unit
         acc += units[i]
-    makespan = max(Fraction(steps[i] * units[i], int(speed[i])) for i in inc)
+    if flags & SIZER_AFFINE and not flags & (FORCE_UNITS | NO_SA):
+        makespan = Fraction(max(steps[i] * (int(alpha[i]) + int(beta[i]) * units[i]) for i in inc))
+    else:
+        makespan = max(Fraction(steps[i] * units[i], int(speed[i])) for i in inc)
     sync_period = 2 if any_slow else 1
     return dict(
         n_gpus=n, m_base=m_base, m_warmup=m_warmup, p_total=p_total,

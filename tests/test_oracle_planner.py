@@ -207,3 +207,67 @@ def test_schedule_uniform_and_excluded():
     assert [x.kind for x in s] == [schedule.WARMUP] * 2 + [schedule.UNIFORM] * 8
     assert all(x.read_ver == x.pub_ver - 1 for x in s[2:])
     assert p["n_exchange_rounds"] == 10
+
+
+# ------------------------------------------------------------ R30 affine sizer
+def _affine(speed, mb, mw, pt, alpha, beta):
+    return planner.plan(speed, mb, mw, pt, 1, flags=planner.SIZER_AFFINE, alpha=alpha, beta=beta)
+
+
+def test_affine_sizer_reduces_to_dhondt():
+    """alpha = 0, beta_i = L / v_i (exact): the affine sizer is Eq. 5 / D'Hondt."""
+    rng = random.Random(11)
+    for _ in range(300):
+        n = rng.randint(1, 6)
+        speed = [rng.choice([1, 2, 3, 4, 5, 6, 8, 10, 12]) for _ in range(n)]
+        L = 120 * 7 * 11
+        beta = [L // v for v in speed]
+        pt = rng.randint(n, 40)
+        mb, mw = rng.choice([(10, 2), (20, 4), (50, 4)])
+        a = _affine(speed, mb, mw, pt, [0] * n, beta)
+        d = planner.plan(speed, mb, mw, pt, 1)
+        assert a["units"] == d["units"], (speed, pt)
+
+
+def test_affine_sizer_is_min_makespan_bruteforce():
+    """Greedy == the minimum of max_i M_i (alpha_i + beta_i P_i) over every split
+    with P_i >= 1 on the included GPUs (tiny inputs, exhaustive)."""
+    rng = random.Random(5)
+    for _ in range(150):
+        n = rng.randint(1, 4)
+        speed = [rng.randint(1, 9) for _ in range(n)]
+        alpha = [rng.randint(0, 50) for _ in range(n)]
+        beta = [rng.randint(1, 20) for _ in range(n)]
+        pt = rng.randint(n, 9)
+        p = _affine(speed, 10, 2, pt, alpha, beta)
+        inc = [i for i in range(n) if p["tier"][i]]
+        if len(inc) > pt:
+            continue
+        best = None
+        for split in itertools.product(range(1, pt + 1), repeat=len(inc)):
+            if sum(split) != pt:
+                continue
+            ms = max(p["steps"][i] * (alpha[i] + beta[i] * u) for i, u in zip(inc, split))
+            best = ms if best is None else min(best, ms)
+        assert p["makespan"] == best
+        assert sum(p["units"]) == pt and all(p["units"][i] >= 1 for i in inc)
+
+
+def test_affine_fixed_overhead_moves_units():
+    """A fixed per-step overhead on a GPU never gives it more units (monotone),
+    and with equal speeds a large one moves units to the other GPUs."""
+    base = _affine([1, 1], 10, 10, 20, [0, 0], [10, 10])
+    assert base["units"] == [10, 10]
+    prev = 10
+    for a0 in (0, 10, 40, 100, 400):
+        u = _affine([1, 1], 10, 10, 20, [a0, 0], [10, 10])["units"][0]
+        assert u <= prev
+        prev = u
+    assert prev < 10
+
+
+def test_affine_errors():
+    with pytest.raises(planner.PlanError):
+        planner.plan([1, 1], 10, 2, 8, 1, flags=planner.SIZER_AFFINE)
+    with pytest.raises(planner.PlanError):
+        _affine([1, 1], 10, 2, 8, [0, 0], [1, 0])
