@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define STADI_ABI_VERSION 1u
+#define STADI_ABI_VERSION 2u
 #define STADI_MAX_GPUS 64
 
 typedef enum {
@@ -79,7 +79,9 @@ enum {
   STADI_NO_TA = 1u,           /* disable temporal adaptation (every GPU tier 1) */
   STADI_NO_SA = 2u,           /* disable spatial adaptation (uniform units)     */
   STADI_SIZER_INTERVAL = 4u,  /* Eq. 5 with per-round step counts (R7 variant)  */
-  STADI_FORCE_UNITS = 8u      /* use forced_units (Table II / Fig. 9 splits)    */
+  STADI_FORCE_UNITS = 8u,     /* use forced_units (Table II / Fig. 9 splits)    */
+  STADI_SIZER_AFFINE = 16u    /* Eq. 5 replaced by the affine step-cost model
+                                 alpha_i + beta_i P (R30, L333 fixed overhead)  */
 };
 
 typedef struct {
@@ -92,6 +94,10 @@ typedef struct {
   uint32_t rows_per_unit;      /* latent rows per unit (R6)                      */
   uint32_t flags;              /* STADI_NO_TA | STADI_NO_SA | ...                */
   const uint32_t *forced_units;/* [N] with STADI_FORCE_UNITS, else ignored       */
+  const uint64_t *alpha;       /* [N] with STADI_SIZER_AFFINE: fixed per-step cost
+                                  of GPU i (any integer time unit), else ignored */
+  const uint64_t *beta;        /* [N] with STADI_SIZER_AFFINE: per-step cost of one
+                                  unit on GPU i (> 0 for included GPUs)          */
 } stadi_plan_params;
 
 typedef struct {
@@ -104,17 +110,24 @@ typedef struct {
   uint32_t rows[STADI_MAX_GPUS];       /* latent rows of GPU i's band             */
   uint32_t sync_period;                /* lcm of post-warmup DDIM strides: 1 or 2 */
   uint32_t n_exchange_rounds;          /* M_warmup + (M_base-M_warmup)/sync_period */
-  uint64_t makespan_num, makespan_den; /* max_i M_i P_i / v_i, reduced fraction   */
+  uint64_t makespan_num, makespan_den; /* max_i M_i P_i / v_i, reduced fraction
+                                          (SIZER_AFFINE: max_i M_i (alpha_i +
+                                          beta_i P_i), den 1)                     */
 } stadi_plan_t;
 
 /* Eq. 4 (L179-L185) then Eq. 5 (L187-L198), as in Alg. 1 lines 1-6.
  * Thresholds compared exactly in 128-bit integers (R2: v_i <= b v_max is
  * excluded, tier 1 needs a v_max < v_i).  Eq. 5 is integerised with the
  * D'Hondt divisor method (R5): one unit per included GPU, then each further
- * unit to argmin (P_i + 1) M_i / v_i, ties to the lowest rank.
+ * unit to argmin (P_i + 1) M_i / v_i, ties to the lowest rank.  With
+ * STADI_SIZER_AFFINE (R30, L333: "the single-step delay no longer maintains a
+ * linear relationship with the patch size due to some fixed overhead") each
+ * further unit goes to argmin M_i (alpha_i + beta_i (P_i + 1)) instead, which
+ * minimises max_i M_i (alpha_i + beta_i P_i); Eq. 4 still uses speed.
  * EINVAL: N out of range, a zero speed, not 0<b<a<1, M_warmup out of range,
  * (M_base - M_warmup) odd with a tier-2 GPU (R3), P_total < #included, bad
- * forced units. */
+ * forced units, SIZER_AFFINE without alpha / beta or with beta_i == 0 on an
+ * included GPU. */
 stadi_status stadi_plan(const stadi_plan_params *in, stadi_plan_t *out);
 
 enum {

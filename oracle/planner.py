@@ -107,6 +107,10 @@ def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
             if (tier[i] == 0) != (forced_units[i] == 0):
                 raise PlanError("forced units: included GPUs need >= 1, excluded 0")
         units = list(forced_units)
+    elif flags & NO_SA:
+        q, r = divmod(p_total, len(inc))
+        for k, i in enumerate(inc):
+            units[i] = q + (1 if k < r else 0)
     elif flags & SIZER_AFFINE:
         if alpha is None or beta is None or len(alpha) != n or len(beta) != n:
             raise PlanError("SIZER_AFFINE needs alpha and beta")
@@ -117,10 +121,6 @@ def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
         for _ in range(p_total - len(inc)):          # R30: greedy min-makespan
             best = min(inc, key=lambda i: (steps[i] * (int(alpha[i]) + int(beta[i]) * (units[i] + 1)), i))
             units[best] += 1
-    elif flags & NO_SA:
-        q, r = divmod(p_total, len(inc))
-        for k, i in enumerate(inc):
-            units[i] = q + (1 if k < r else 0)
     else:
         # Eq. 5 weights w_i = v_i / M'_i.  D'Hondt: every included GPU starts
         # with one unit; each further unit goes to argmax w_i/(P_i+1), i.e.

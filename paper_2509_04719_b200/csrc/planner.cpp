@@ -126,6 +126,27 @@ extern "C" stadi_status stadi_plan(const stadi_plan_params *in, stadi_plan_t *ou
     uint32_t k = 0;
     for (uint32_t i = 0; i < n; ++i)
       if (p.tier[i]) p.units[i] = q + (k++ < r ? 1u : 0u);
+  } else if (in->flags & STADI_SIZER_AFFINE) {
+    // R30: greedy min-makespan of max_i M_i (alpha_i + beta_i P_i)
+    if (!in->alpha || !in->beta)
+      return fail(nullptr, STADI_EINVAL, "stadi_plan: SIZER_AFFINE needs alpha and beta");
+    for (uint32_t i = 0; i < n; ++i) {
+      if (p.tier[i] && in->beta[i] == 0)
+        return fail(nullptr, STADI_EINVAL, "stadi_plan: beta[%u] == 0", i);
+      if (p.tier[i]) p.units[i] = 1;
+    }
+    auto cost = [&](uint32_t i, uint64_t units) {
+      return (u128)p.steps[i] * ((u128)in->alpha[i] + (u128)in->beta[i] * units);
+    };
+    for (uint32_t u = n_inc; u < in->p_total; ++u) {
+      int best = -1;
+      for (uint32_t i = 0; i < n; ++i) {
+        if (!p.tier[i]) continue;
+        if (best < 0 || cost(i, p.units[i] + 1) < cost((uint32_t)best, p.units[best] + 1))
+          best = (int)i;
+      }
+      p.units[best] += 1;
+    }
   } else {
     // D'Hondt on weights v_i / M'_i (R5); M'_i = M_i, or the per-round step
     // count with SIZER_INTERVAL (R7 variant).
@@ -160,8 +181,19 @@ extern "C" stadi_status stadi_plan(const stadi_plan_params *in, stadi_plan_t *ou
     acc += p.units[i];
   }
   // makespan = max_i M_i P_i / v_i over included GPUs, reduced
+  // (SIZER_AFFINE: max_i M_i (alpha_i + beta_i P_i), an integer)
   uint64_t bn_ = 0, bd_ = 1;
-  for (uint32_t i = 0; i < n; ++i) {
+  const bool affine = (in->flags & STADI_SIZER_AFFINE) &&
+                      !(in->flags & (STADI_FORCE_UNITS | STADI_NO_SA));
+  if (affine) {
+    u128 mx = 0;
+    for (uint32_t i = 0; i < n; ++i)
+      if (p.tier[i])
+        mx = std::max(mx, (u128)p.steps[i] * ((u128)in->alpha[i] + (u128)in->beta[i] * p.units[i]));
+    if (mx >> 64) return fail(nullptr, STADI_EINVAL, "stadi_plan: affine makespan overflows");
+    bn_ = (uint64_t)mx;
+  }
+  for (uint32_t i = 0; i < n && !affine; ++i) {
     if (!p.tier[i]) continue;
     uint64_t num = (uint64_t)p.steps[i] * p.units[i], den = in->speed[i];
     if ((u128)num * bd_ > (u128)bn_ * den) {

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libstadi.so")
 
 MAX_GPUS = 64
-NO_TA, NO_SA, SIZER_INTERVAL, FORCE_UNITS = 1, 2, 4, 8
+NO_TA, NO_SA, SIZER_INTERVAL, FORCE_UNITS, SIZER_AFFINE = 1, 2, 4, 8, 16
 STEP_WARMUP, STEP_UNIFORM, STEP_FAST_EVEN, STEP_FAST_ODD, STEP_SLOW = range(5)
 T_FINAL = -1
 VER_NONE = -1
@@ -42,7 +42,8 @@ class PlanParams(C.Structure):
                 ("a_num", C.c_uint32), ("a_den", C.c_uint32),
                 ("b_num", C.c_uint32), ("b_den", C.c_uint32),
                 ("p_total", C.c_uint32), ("rows_per_unit", C.c_uint32),
-                ("flags", C.c_uint32), ("forced_units", C.POINTER(C.c_uint32))]
+                ("flags", C.c_uint32), ("forced_units", C.POINTER(C.c_uint32)),
+                ("alpha", C.POINTER(C.c_uint64)), ("beta", C.POINTER(C.c_uint64))]
 
 
 class Plan(C.Structure):
@@ -202,15 +203,21 @@ def stream_ptr(stream):
 
 # ---------------------------------------------------------------- planner
 def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4), flags=0,
-         forced_units=None) -> Plan:
+         forced_units=None, alpha=None, beta=None) -> Plan:
     n = len(speed)
     sp = (C.c_uint64 * max(n, 1))(*[int(v) for v in speed])
-    fu = None
+    fu = al = be = None
     if forced_units is not None:
         fu = (C.c_uint32 * n)(*[int(v) for v in forced_units])
+    if alpha is not None:
+        al = (C.c_uint64 * n)(*[int(v) for v in alpha])
+    if beta is not None:
+        be = (C.c_uint64 * n)(*[int(v) for v in beta])
     pp = PlanParams(n, C.cast(sp, C.POINTER(C.c_uint64)), m_base, m_warmup, a[0], a[1], b[0],
                     b[1], p_total, rows_per_unit, flags,
-                    C.cast(fu, C.POINTER(C.c_uint32)) if fu is not None else None)
+                    C.cast(fu, C.POINTER(C.c_uint32)) if fu is not None else None,
+                    C.cast(al, C.POINTER(C.c_uint64)) if al is not None else None,
+                    C.cast(be, C.POINTER(C.c_uint64)) if be is not None else None)
     out = Plan()
     _check(lib.stadi_plan(C.byref(pp), C.byref(out)))
     return out

@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol(S):
     for name in declared:
         assert hasattr(S.lib, name), name
     assert declared <= set(S.EXPORTS)
-    assert S.lib.stadi_abi_version() == 1
+    assert S.lib.stadi_abi_version() == 2
 
 
 def _oracle_plan(speed, mb, mw, P, rpu, flags, forced=None):
@@ -70,6 +70,37 @@ def test_plan_bit_exact_random(S):
         assert got["makespan"] == (ref["makespan"].numerator, ref["makespan"].denominator)
         n_checked += 1
     assert n_checked > 10000
+
+
+def test_plan_affine_bit_exact_random(S):
+    """R30 affine sizer: C++ == oracle bit for bit (units, rows, integer makespan),
+    including huge alpha / beta (128-bit products) and errors."""
+    rng = random.Random(4321)
+    n_checked = 0
+    for _ in range(5000):
+        n = rng.randint(1, 10)
+        speed = [rng.randint(1, 1 << 20) for _ in range(n)]
+        big = rng.choice([100, 1 << 20, 1 << 40])
+        alpha = [rng.randint(0, big) for _ in range(n)]
+        beta = [rng.randint(0 if rng.random() < 0.02 else 1, big) for _ in range(n)]
+        mb = rng.choice([10, 20, 50, 100])
+        mw = rng.choice([2, 4, mb])
+        P = rng.randint(1, 128)
+        flags = OP.SIZER_AFFINE | rng.choice([0, 0, OP.NO_TA, OP.SIZER_INTERVAL])
+        try:
+            ref = OP.plan(speed, mb, mw, P, 1, flags=flags, alpha=alpha, beta=beta)
+        except OP.PlanError:
+            with pytest.raises(S.StadiError):
+                S.plan(speed, mb, mw, P, 1, flags=flags, alpha=alpha, beta=beta)
+            continue
+        got = S.plan(speed, mb, mw, P, 1, flags=flags, alpha=alpha, beta=beta).to_dict()
+        for k in ("tier", "steps", "units", "row_begin", "rows"):
+            assert got[k] == ref[k], (k, speed, alpha, beta, P, flags)
+        assert got["makespan"] == (ref["makespan"].numerator, ref["makespan"].denominator)
+        n_checked += 1
+    assert n_checked > 3000
+    with pytest.raises(S.StadiError):
+        S.plan([1, 1], 10, 2, 8, flags=S.SIZER_AFFINE)
 
 
 def test_plan_forced_and_errors(S):
