@@ -120,7 +120,13 @@ struct AttnCfg {
   static constexpr int NCH = N64 + N32 + N16;
   // keys per tile: 112 with two query tiles so that S (2 x 112), O (2 x 80) and a
   // separate P region (2 x 64) fit the 512 TMEM columns; 128 with one tile
-  static constexpr int AKT = NQT == 2 ? 112 : 128;
+  // DUAL: one query tile per CTA and two CTAs per SM (each its own MMA issuer,
+  // softmax group and barriers; 256 TMEM columns each) for hd <= 80 -- used for
+  // the short-K/V cross-attention, where per-CTA latency, not K/V streaming, rules
+  static constexpr bool DUAL = NQT == 1 && 64 * N64 + 32 * N32 + 16 * N16 <= 80;
+  static constexpr int MINB = DUAL ? 2 : 1;      // CTAs per SM
+  static constexpr uint32_t TMEM_COLS = DUAL ? 256 : 512;
+  static constexpr int AKT = (NQT == 2 || DUAL) ? 112 : 128;
   static constexpr int QTILE = AQ * HDP * 2;   // one Q tile (128 rows), bytes
   static constexpr int KTILE = AKT * HDP * 2;  // one K or V tile, bytes
   __host__ __device__ static constexpr int cw(int c) {  // chunk width
@@ -145,7 +151,8 @@ struct AttnCfg {
 #ifndef STADI_ATTN_MAX_STAGES
 #define STADI_ATTN_MAX_STAGES 4
 #endif
-  static constexpr int STAGES_FIT = (STADI_ATTN_SMEM_KB * 1024 - NQT * QTILE) / (2 * KTILE);
+  static constexpr int STAGES_FIT =
+      ((DUAL ? 100 : STADI_ATTN_SMEM_KB) * 1024 - NQT * QTILE) / (2 * KTILE);
   static constexpr int STAGES =
       STAGES_FIT > STADI_ATTN_MAX_STAGES ? STADI_ATTN_MAX_STAGES : STAGES_FIT;
   static constexpr int OFF_K = NQT * QTILE;
@@ -168,7 +175,8 @@ struct AttnCfg {
   __host__ __device__ static constexpr uint32_t p_col(int g) {
     return (uint32_t)(NQT * (AKT + HDP) + 64 * g);
   }
-  static_assert(NQT * (AKT + HDP + 64) <= 512, "TMEM columns");
+  static_assert(NQT * (AKT + HDP + 64) <= (int)TMEM_COLS, "TMEM columns");
+  static_assert(!DUAL || 2 * (SMEM + 1024) <= 228 * 1024, "two CTAs per SM");
   static_assert(NQT == 1 || HDP <= 80, "two query tiles need HDP <= 80");
   static_assert(STAGES >= 2, "smem");
   static_assert(SMEM <= 227 * 1024, "smem");
@@ -237,7 +245,8 @@ __device__ __forceinline__ void tmem_store_packed(uint32_t taddr, const uint32_t
 }
 
 template <int N64, int N32, int N16, int NQT, int POLY, int QUAD>
-__global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
+__global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
+                                  AttnCfg<N64, N32, N16, NQT>::MINB)
     tc_attn_kernel(const __grid_constant__ CUtensorMap tq64, const __grid_constant__ CUtensorMap tq32,
                    const __grid_constant__ CUtensorMap tq16, const __grid_constant__ CUtensorMap tk64,
                    const __grid_constant__ CUtensorMap tk32, const __grid_constant__ CUtensorMap tk16,
@@ -287,7 +296,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -811,7 +820,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
 
@@ -932,9 +941,22 @@ cudaError_t tc_attention_preload() {
   preload_attn<0, 1, 1, 2>(&a);
   preload_attn<1, 0, 0, 2>(&a);
   preload_attn<0, 0, 5, 2>(&a);
+  preload_attn<0, 0, 5, 1>(&a);
   preload_attn<1, 0, 1, 2>(&a);
   preload_attn<2, 1, 0, 1>(&a);
   return cudaGetLastError();
+}
+
+// K/V lengths up to this use the two-CTAs-per-SM variant (hd 72 / 80): a few key
+// tiles leave each CTA latency bound, so a second resident CTA hides it; for long
+// K/V the shared ping-pong CTA wins (measured 786 vs 583 TFLOP/s at 16384 keys).
+// STADI_ATTN_DUAL_KV overrides (0 = never).
+int attn_dual_max_kv() {
+  static const int v = [] {
+    const char *e = getenv("STADI_ATTN_DUAL_KV");
+    return e ? atoi(e) : 256;
+  }();
+  return v;
 }
 
 // Supported head dims (padded to hd_pad): 16 (16), 40 (48 = 32 + 16), 64 (64),
@@ -953,6 +975,8 @@ cudaError_t tc_attention_bf16(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, in
     case 64: return launch_attn<1, 0, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 72:
     case 80:
+      if (Nkv <= attn_dual_max_kv())  // cross-attention to the text tokens
+        return launch_attn<0, 0, 5, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
       if (attn_narrow()) return launch_attn<0, 0, 5, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
       return launch_attn<1, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 160: return launch_attn<2, 1, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);

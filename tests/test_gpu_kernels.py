@@ -161,7 +161,7 @@ ATTN_CASES = [  # Nq, Nkv, B, H, hd
     (300, 1024, 2, 8, 40), (129, 77, 2, 8, 40),    # SD-1.5 level 0 self / cross (hd 40)
     (64, 256, 2, 8, 160), (200, 77, 2, 8, 160),    # SD-1.5 level 2 (hd 160, one Q tile/CTA)
     (500, 1500, 2, 10, 64), (255, 77, 2, 10, 64),  # SDXL level 1 self / cross (hd 64)
-    (257, 129, 1, 1, 16),
+    (257, 129, 1, 1, 16), (300, 200, 2, 4, 80),   # the last: two-CTAs-per-SM variant, ragged
 ]
 
 

@@ -72,6 +72,9 @@ elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "gemm":
                        (128, 1280, 11520, S.EPI_F32), (512, 1280, 11520, S.EPI_F32),
                        (8192, 320, 2880, S.EPI_F32), (256, 1280, 1280, S.EPI_STORE)]:
         gemm(M, N, K, e)
+elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "xattn":
+    attn(16384, 120, 2, 16, 72)
+    attn(4096, 120, 2, 16, 72)
 elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "attn":
     attn(16384, 16384, 2, 16, 72)
     attn(4096, 4096, 2, 10, 64)
