@@ -942,12 +942,13 @@ cudaError_t tc_attention_preload() {
   preload_attn<1, 0, 0, 2>(&a);
   preload_attn<0, 0, 5, 2>(&a);
   preload_attn<0, 0, 5, 1>(&a);
+  preload_attn<1, 0, 0, 1>(&a);
   preload_attn<1, 0, 1, 2>(&a);
   preload_attn<2, 1, 0, 1>(&a);
   return cudaGetLastError();
 }
 
-// K/V lengths up to this use the two-CTAs-per-SM variant (hd 72 / 80): a few key
+// K/V lengths up to this use the two-CTAs-per-SM variant (hd 64 / 72 / 80): a few key
 // tiles leave each CTA latency bound, so a second resident CTA hides it; for long
 // K/V the shared ping-pong CTA wins (measured 786 vs 583 TFLOP/s at 16384 keys).
 // STADI_ATTN_DUAL_KV overrides (0 = never).
@@ -971,8 +972,10 @@ cudaError_t tc_attention_bf16(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, in
   if (Nkv <= 0) return cudaErrorInvalidValue;
   switch (hd) {
     case 16: return launch_attn<0, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
-    case 40: return launch_attn<0, 1, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
-    case 64: return launch_attn<1, 0, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+    case 40: return launch_attn<0, 1, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);  // dual slower
+    case 64:  // dual: SDXL cross-attention 20 -> 16 us
+      if (Nkv <= attn_dual_max_kv()) return launch_attn<1, 0, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
+      return launch_attn<1, 0, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 72:
     case 80:
       if (Nkv <= attn_dual_max_kv())  // cross-attention to the text tokens

@@ -75,6 +75,8 @@ elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "gemm":
 elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "xattn":
     attn(16384, 120, 2, 16, 72)
     attn(4096, 120, 2, 16, 72)
+    attn(4096, 77, 2, 8, 40)       # SD-1.5 level 0 cross
+    attn(4096, 77, 2, 10, 64)      # SDXL level 1 cross
 elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "attn":
     attn(16384, 16384, 2, 16, 72)
     attn(4096, 4096, 2, 10, 64)
