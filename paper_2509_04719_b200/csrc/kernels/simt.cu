@@ -181,6 +181,16 @@ template cudaError_t simt_attention<bf16>(const bf16 *, const bf16 *, bf16 *, in
 namespace {
 constexpr int LN_MAXV = 12;  // float4 per lane: d <= 1536
 
+// four consecutive outputs as one vector store (8 B of bf16 / 16 B of fp32)
+__device__ __forceinline__ void store4(bf16 *p, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  *reinterpret_cast<uint2 *>(p) =
+      make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+}
+__device__ __forceinline__ void store4(float *p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4 *>(p) = make_float4(a, b, c, d);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) ln_mod_kernel(const float *__restrict__ x, T *__restrict__ y,
                                                      int M, int d, int B,
@@ -207,12 +217,7 @@ __global__ void __launch_bounds__(256) ln_mod_kernel(const float *__restrict__ x
 #pragma unroll
     for (int i = 0; i < LN_MAXV; ++i) {
       const int c = lane + 32 * i;
-      if (c < d4) {
-        yr[4 * c + 0] = from_f<T>(v[i].x);
-        yr[4 * c + 1] = from_f<T>(v[i].y);
-        yr[4 * c + 2] = from_f<T>(v[i].z);
-        yr[4 * c + 3] = from_f<T>(v[i].w);
-      }
+      if (c < d4) store4(yr + 4 * c, v[i].x, v[i].y, v[i].z, v[i].w);
     }
     return;
   }
@@ -237,10 +242,10 @@ __global__ void __launch_bounds__(256) ln_mod_kernel(const float *__restrict__ x
     if (c < d4) {
       const float4 s4 = reinterpret_cast<const float4 *>(sh)[c];
       const float4 c4 = reinterpret_cast<const float4 *>(sc)[c];
-      yr[4 * c + 0] = from_f<T>((v[i].x - mean) * rstd * (1.f + c4.x) + s4.x);
-      yr[4 * c + 1] = from_f<T>((v[i].y - mean) * rstd * (1.f + c4.y) + s4.y);
-      yr[4 * c + 2] = from_f<T>((v[i].z - mean) * rstd * (1.f + c4.z) + s4.z);
-      yr[4 * c + 3] = from_f<T>((v[i].w - mean) * rstd * (1.f + c4.w) + s4.w);
+      store4(yr + 4 * c, (v[i].x - mean) * rstd * (1.f + c4.x) + s4.x,
+             (v[i].y - mean) * rstd * (1.f + c4.y) + s4.y,
+             (v[i].z - mean) * rstd * (1.f + c4.z) + s4.z,
+             (v[i].w - mean) * rstd * (1.f + c4.w) + s4.w);
     }
   }
 }

@@ -72,6 +72,14 @@ elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "gemm":
                        (128, 1280, 11520, S.EPI_F32), (512, 1280, 11520, S.EPI_F32),
                        (8192, 320, 2880, S.EPI_F32), (256, 1280, 1280, S.EPI_STORE)]:
         gemm(M, N, K, e)
+elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ln":
+    M, d = 32768, 1152
+    x = torch.randn(M, d, device="cuda")
+    y = torch.empty(M, d, device="cuda", dtype=torch.bfloat16)
+    sh, sc = torch.randn(2, d, device="cuda"), torch.randn(2, d, device="cuda")
+    ms = timeit(lambda: S.k_ln_modulate(0, x, y, M, d, 2, sh, sc, d,
+                                        stream=torch.cuda.current_stream()))
+    print(f"ln_mod M={M} d={d}: {ms * 1e3:.1f} us  {(M * d * 6) / ms / 1e6:.0f} GB/s")
 elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "xattn":
     attn(16384, 120, 2, 16, 72)
     attn(4096, 120, 2, 16, 72)
