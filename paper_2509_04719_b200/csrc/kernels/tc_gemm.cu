@@ -590,7 +590,7 @@ int device_sms() {
   }();
   return v;
 }
-int pair_mode_for(int tm, int max_ctas, int epi) {
+int pair_mode_for(int tm, int max_ctas, int epi, int K) {
   // Fewer CTAs than SMs means the occupancy emulator holds the rest: launch
   // single-CTA tiles, free of cluster-placement constraints on a partly held GPU
   // (measured on B200 with the C2 / C5 shapes at 20-60%: same speed as CTA pairs;
@@ -598,7 +598,10 @@ int pair_mode_for(int tm, int max_ctas, int epi) {
   if (tm < 4 || max_ctas < 2) return 1;
   if (gemm_pair_mode()) return gemm_pair_mode();
   if (max_ctas < device_sms()) return 1;
-  return (epi == EPI_GATED_RES || epi == EPI_RES) ? 2 : 3;
+  // residual RMW epilogues: multicast pairs while the epilogue's HBM traffic rules
+  // (K = 1152 out-proj 143 vs 154 us), the cta_group::2 MMA once the K loop does
+  // (K = 4608 fc2 314 vs 320 us)
+  return ((epi == EPI_GATED_RES || epi == EPI_RES) && K < 2304) ? 2 : 3;
 }
 
 cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
@@ -608,7 +611,7 @@ cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int 
   if (reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(W) % 16)
     return cudaErrorInvalidValue;
   const int tm = (M + GBM - 1) / GBM;
-  const int mc = pair_mode_for(tm, max_ctas, epi);
+  const int mc = pair_mode_for(tm, max_ctas, epi, K);
   const GemmPlan g = plan_gemm(M, N, K, max_ctas, mc, ep.ws ? ep.ws_elems : 0);
   switch (g.bn) {
     case 256: return dispatch_mc<256>(A, W, M, N, K, epi, ep, max_ctas, mc, g.ks, s);
@@ -673,7 +676,7 @@ cudaError_t tc_conv3x3_bf16(const bf16 *P, const bf16 *Wt, int h, int W, int B, 
   if (C % GBK || N % 64 || max_ctas < 1 || (wb % GBM && GBM % wb)) return cudaErrorInvalidValue;
   const ConvGeo g{W, B, C};
   const int M = h * wb, tm = (M + GBM - 1) / GBM;
-  const int mc = pair_mode_for(tm, max_ctas, epi);
+  const int mc = pair_mode_for(tm, max_ctas, epi, 9 * C);
   const GemmPlan gp = plan_gemm(M, N, 9 * C, max_ctas, mc, ep.ws ? ep.ws_elems : 0);
   const int ks = gp.ks;
 #define STADI_CONV_CASE(BNV)                                                          \
