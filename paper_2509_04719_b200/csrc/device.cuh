@@ -58,6 +58,7 @@ struct EpiParams {
   int d;
   float *ws;           // tcgen05 GEMM split-K workspace (fp32 partial tiles), or nullptr
   long ws_elems;
+  int res_prefetch;    // tcgen05 GEMM: L2-prefetch the residual tile before the accumulator wait
 };
 
 // Apply the epilogue to `n` consecutive columns col..col+n-1 of one row.

@@ -294,9 +294,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tile_of(item, &mb, &nb);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
+      const int row0 = mb * GBM + qd * 32;
+      if constexpr (EPI == EPI_GATED_RES || EPI == EPI_RES || EPI == EPI_CONV) {
+        // the fp32 residual is the epilogue's only HBM read: pull this warp's
+        // rows x chunks (one 128-B line per row and 32-column chunk) into L2
+        // while the tile's MMAs still run, so the epilogue reads hit L2
+        if (ep.res_prefetch && ep.res && ksplit == 1 && row0 + lane < M) {
+          const float *rp = ep.res + (long)(row0 + lane) * ep.ldr + nb * BN;
+#pragma unroll 1
+          for (int ch = half; ch < NCHUNK; ch += 2)
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(rp + 32 * ch));
+        }
+      }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int row0 = mb * GBM + qd * 32;
       const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + acc * BN;
       float *stg = stg_all + (warp - 2) * 32 * EPI_LD;
 #pragma unroll 1
@@ -426,6 +437,14 @@ bool make_tmap(CUtensorMap *m, const void *base, int rank, const uint64_t *dims,
 namespace {
 constexpr int NCL_OF(int mc) { return mc == 1 ? 1 : 2; }
 // STADI_SPLITK=0 disables split-K (A/B comparisons).
+// STADI_RES_PREFETCH=0 disables the residual L2 prefetch (A/B comparisons).
+bool res_prefetch_enabled() {
+  static const int v = [] {
+    const char *e = getenv("STADI_RES_PREFETCH");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v != 0;
+}
 bool splitk_disabled() {
   static const int v = [] {
     const char *e = getenv("STADI_SPLITK");
@@ -478,7 +497,9 @@ cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, EPI, MC, AM>, ta, tb, M, N, K, ep,
+  EpiParams epk = ep;
+  epk.res_prefetch = res_prefetch_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, EPI, MC, AM>, ta, tb, M, N, K, epk,
                                      cg, ksplit);
   ++g_launches;
   if (e != cudaSuccess) return e;
