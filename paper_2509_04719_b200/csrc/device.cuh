@@ -59,6 +59,7 @@ struct EpiParams {
   float *ws;           // tcgen05 GEMM split-K workspace (fp32 partial tiles), or nullptr
   long ws_elems;
   int res_prefetch;    // tcgen05 GEMM: L2-prefetch the residual tile before the accumulator wait
+  int res_vec4;        // tcgen05 GEMM: 16-byte residual read-modify-write when aligned
 };
 
 // Apply the epilogue to `n` consecutive columns col..col+n-1 of one row.

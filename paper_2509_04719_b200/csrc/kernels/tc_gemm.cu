@@ -288,6 +288,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int half = (warp - 2) / 4;  // 32-column chunks half, half + 2, ... of the tile
     constexpr int NCHUNK = BN / 32;
     static_assert(BN % 32 == 0, "epilogue chunks");
+    // residual RMW epilogues use 16-byte accesses when every operand row is 16-B aligned
+    const bool vec4 = ep.res_vec4 && ep.res != nullptr &&
+                      ((reinterpret_cast<uintptr_t>(ep.res) | reinterpret_cast<uintptr_t>(ep.bias) |
+                        reinterpret_cast<uintptr_t>(ep.gate) | (uintptr_t)ep.ldr * 4u |
+                        (uintptr_t)ep.gate_bstride * 4u) & 15u) == 0;
     int it = 0;
     for (int item = item0; item < n_items; item += item_step, ++it) {
       int mb, nb;
@@ -340,6 +345,45 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           __syncwarp();
           continue;
+        }
+        if constexpr (EPI == EPI_GATED_RES || EPI == EPI_RES) {
+          if (vec4) {  // 16-byte residual RMW: 8 lanes per row, 4 rows per step
+            const int c4 = 4 * (lane & 7), col4 = nb * BN + c0 + c4;
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 b4 = ep.bias ? *reinterpret_cast<const float4 *>(ep.bias + col4) : z4;
+            float4 g0 = z4, g1 = z4;
+            if constexpr (EPI == EPI_GATED_RES) {
+              if (ep.gate) {
+                g0 = *reinterpret_cast<const float4 *>(ep.gate + col4);
+                g1 = ep.B > 1 ? *reinterpret_cast<const float4 *>(ep.gate + ep.gate_bstride + col4)
+                              : g0;
+              }
+            }
+            float4 rin[8];
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int row = row0 + 4 * it + (lane >> 3);
+              if (row < M) rin[it] = *reinterpret_cast<const float4 *>(ep.res + (long)row * ep.ldr + col4);
+            }
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int r = 4 * it + (lane >> 3), row = row0 + r;
+              if (row >= M) continue;
+              const float *sv = stg + r * EPI_LD + c4;
+              const float4 v = make_float4(sv[0] + b4.x, sv[1] + b4.y, sv[2] + b4.z, sv[3] + b4.w);
+              float4 o;  // the same expressions (and FMA contraction) as epi_finish
+              if constexpr (EPI == EPI_GATED_RES) {
+                const float4 g = (row % ep.B) ? g1 : g0;
+                o = make_float4(rin[it].x + g.x * v.x, rin[it].y + g.y * v.y,
+                                rin[it].z + g.z * v.z, rin[it].w + g.w * v.w);
+              } else {
+                o = make_float4(rin[it].x + v.x, rin[it].y + v.y, rin[it].z + v.z, rin[it].w + v.w);
+              }
+              *reinterpret_cast<float4 *>(ep.res + (long)row * ep.ldr + col4) = o;
+            }
+            __syncwarp();
+            continue;
+          }
         }
         const EpiCol ecol = epi_col<EPI>(ep, col);
         EpiIn in[16];
@@ -445,6 +489,14 @@ bool res_prefetch_enabled() {
   }();
   return v != 0;
 }
+// STADI_RES_VEC4=0 keeps the 8-byte residual epilogue (A/B comparisons).
+bool res_vec4_enabled() {
+  static const int v = [] {
+    const char *e = getenv("STADI_RES_VEC4");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v != 0;
+}
 bool splitk_disabled() {
   static const int v = [] {
     const char *e = getenv("STADI_SPLITK");
@@ -499,6 +551,7 @@ cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const
   cfg.numAttrs = 1;
   EpiParams epk = ep;
   epk.res_prefetch = res_prefetch_enabled() ? 1 : 0;
+  epk.res_vec4 = res_vec4_enabled() ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, EPI, MC, AM>, ta, tb, M, N, K, epk,
                                      cg, ksplit);
   ++g_launches;
