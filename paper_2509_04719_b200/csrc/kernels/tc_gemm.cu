@@ -293,6 +293,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                       ((reinterpret_cast<uintptr_t>(ep.res) | reinterpret_cast<uintptr_t>(ep.bias) |
                         reinterpret_cast<uintptr_t>(ep.gate) | (uintptr_t)ep.ldr * 4u |
                         (uintptr_t)ep.gate_bstride * 4u) & 15u) == 0;
+    // plain-store epilogues: 8-byte (bf16) / 16-byte (fp32) output rows, 16-byte bias
+    const bool vec4o =
+        EPI == EPI_QKV
+            ? ep.res_vec4 && (reinterpret_cast<uintptr_t>(ep.bias) & 15u) == 0 &&
+                  ((reinterpret_cast<uintptr_t>(ep.q) | reinterpret_cast<uintptr_t>(ep.kv_a) |
+                    reinterpret_cast<uintptr_t>(ep.kv_b) | (uintptr_t)ep.d * 2u) & 7u) == 0
+            : ep.res_vec4 && ep.out != nullptr && (reinterpret_cast<uintptr_t>(ep.bias) & 15u) == 0 &&
+                  ((reinterpret_cast<uintptr_t>(ep.out) |
+                    (uintptr_t)ep.ldo * (EPI == EPI_F32 ? 4u : 2u)) & (EPI == EPI_F32 ? 15u : 7u)) == 0;
     int it = 0;
     for (int item = item0; item < n_items; item += item_step, ++it) {
       int mb, nb;
@@ -380,6 +389,50 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 o = make_float4(rin[it].x + v.x, rin[it].y + v.y, rin[it].z + v.z, rin[it].w + v.w);
               }
               *reinterpret_cast<float4 *>(ep.res + (long)row * ep.ldr + col4) = o;
+            }
+            __syncwarp();
+            continue;
+          }
+        }
+        if constexpr (EPI == EPI_STORE || EPI == EPI_GELU || EPI == EPI_F32 || EPI == EPI_QKV) {
+          if (vec4o) {  // 8-byte bf16 / 16-byte fp32 stores: 8 lanes per row, 4 rows per step
+            const int c4 = 4 * (lane & 7), col4 = nb * BN + c0 + c4;
+            const float4 b4 = ep.bias ? *reinterpret_cast<const float4 *>(ep.bias + col4)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int r = 4 * it + (lane >> 3), row = row0 + r;
+              if (row >= M) continue;
+              const float *sv = stg + r * EPI_LD + c4;
+              float v0 = sv[0] + b4.x, v1 = sv[1] + b4.y, v2 = sv[2] + b4.z, v3 = sv[3] + b4.w;
+              if constexpr (EPI == EPI_F32) {
+                *reinterpret_cast<float4 *>(reinterpret_cast<float *>(ep.out) + (long)row * ep.ldo +
+                                            col4) = make_float4(v0, v1, v2, v3);
+              } else {
+                if constexpr (EPI == EPI_GELU) {
+                  v0 = gelu_tanh_fast(v0);
+                  v1 = gelu_tanh_fast(v1);
+                  v2 = gelu_tanh_fast(v2);
+                  v3 = gelu_tanh_fast(v3);
+                }
+                const __nv_bfloat162 lo = __floats2bfloat162_rn(v0, v1),
+                                     hi = __floats2bfloat162_rn(v2, v3);
+                uint2 pk;
+                pk.x = *reinterpret_cast<const uint32_t *>(&lo);
+                pk.y = *reinterpret_cast<const uint32_t *>(&hi);
+                if constexpr (EPI == EPI_QKV) {  // d % 4 == 0: a 4-column group never straddles q | kv
+                  if (col4 < ep.d) {
+                    *reinterpret_cast<uint2 *>(reinterpret_cast<bf16 *>(ep.q) + (long)row * ep.d + col4) = pk;
+                  } else {
+                    const long off = (ep.kv_row0 + row) * 2L * ep.d + (col4 - ep.d);
+                    *reinterpret_cast<uint2 *>(reinterpret_cast<bf16 *>(ep.kv_a) + off) = pk;
+                    if (ep.kv_b) *reinterpret_cast<uint2 *>(reinterpret_cast<bf16 *>(ep.kv_b) + off) = pk;
+                  }
+                } else {
+                  *reinterpret_cast<uint2 *>(reinterpret_cast<bf16 *>(ep.out) + (long)row * ep.ldo +
+                                             col4) = pk;
+                }
+              }
             }
             __syncwarp();
             continue;
