@@ -292,7 +292,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const bool vec4 = ep.res_vec4 && ep.res != nullptr &&
                       ((reinterpret_cast<uintptr_t>(ep.res) | reinterpret_cast<uintptr_t>(ep.bias) |
                         reinterpret_cast<uintptr_t>(ep.gate) | (uintptr_t)ep.ldr * 4u |
-                        (uintptr_t)ep.gate_bstride * 4u) & 15u) == 0;
+                        (uintptr_t)ep.gate_bstride * 4u) & 15u) == 0 &&
+                      (EPI != EPI_CONV ||
+                       ((reinterpret_cast<uintptr_t>(ep.out) | (uintptr_t)ep.ldo * 4u) & 15u) == 0);
     // plain-store epilogues: 8-byte (bf16) / 16-byte (fp32) output rows, 16-byte bias
     const bool vec4o =
         EPI == EPI_QKV
@@ -355,13 +357,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
           continue;
         }
-        if constexpr (EPI == EPI_GATED_RES || EPI == EPI_RES) {
+        if constexpr (EPI == EPI_GATED_RES || EPI == EPI_RES || EPI == EPI_CONV) {
           if (vec4) {  // 16-byte residual RMW: 8 lanes per row, 4 rows per step
             const int c4 = 4 * (lane & 7), col4 = nb * BN + c0 + c4;
             const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
             const float4 b4 = ep.bias ? *reinterpret_cast<const float4 *>(ep.bias + col4) : z4;
             float4 g0 = z4, g1 = z4;
-            if constexpr (EPI == EPI_GATED_RES) {
+            if constexpr (EPI == EPI_GATED_RES || EPI == EPI_CONV) {
               if (ep.gate) {
                 g0 = *reinterpret_cast<const float4 *>(ep.gate + col4);
                 g1 = ep.B > 1 ? *reinterpret_cast<const float4 *>(ep.gate + ep.gate_bstride + col4)
@@ -385,6 +387,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const float4 g = (row % ep.B) ? g1 : g0;
                 o = make_float4(rin[it].x + g.x * v.x, rin[it].y + g.y * v.y,
                                 rin[it].z + g.z * v.z, rin[it].w + g.w * v.w);
+              } else if constexpr (EPI == EPI_CONV) {  // v += (time bias + residual)
+                const float4 g = (row % ep.B) ? g1 : g0;
+                o = make_float4(v.x + (g.x + rin[it].x), v.y + (g.y + rin[it].y),
+                                v.z + (g.z + rin[it].z), v.w + (g.w + rin[it].w));
+                *reinterpret_cast<float4 *>(reinterpret_cast<float *>(ep.out) + (long)row * ep.ldo +
+                                            col4) = o;
+                continue;
               } else {
                 o = make_float4(rin[it].x + v.x, rin[it].y + v.y, rin[it].z + v.z, rin[it].w + v.w);
               }

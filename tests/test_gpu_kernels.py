@@ -109,6 +109,32 @@ def test_gemm_gated_residual_and_qkv(S, dtype):
         assert np.all(got[:tok0] == 0) and np.all(got[tok0 + ntok:] == 0)
 
 
+@pytest.mark.parametrize("M,N,K", [(300, 384, 1152), (77, 192, 256)])
+def test_gemm_epilogue_vector_and_scalar_paths_agree(S, M, N, K):
+    """The 16-byte / 8-byte epilogue (aligned rows) and the 8-byte / 4-byte one
+    (rows padded by 2 elements, so not 16-B / 8-B aligned) evaluate the same
+    expressions: bit-identical fp32 residual / fp32 output, identical bf16."""
+    rng = np.random.default_rng(M + N)
+    tA, _ = _bf(rng.standard_normal((M, K)))
+    tW, _ = _bf(rng.standard_normal((N, K)) / np.sqrt(K))
+    tb = torch.from_numpy((rng.standard_normal(N) * 0.1).astype(np.float32)).cuda()
+    gate = torch.from_numpy(rng.standard_normal((2, N)).astype(np.float32)).cuda()
+    res0 = rng.standard_normal((M, N + 2)).astype(np.float32)
+    outs = {}
+    for ld in (N, N + 2):
+        f32 = torch.zeros(M, ld, device="cuda")
+        S.k_gemm(0, tA, tW, M, N, K, S.EPI_F32, bias=tb, out=f32, ldo=ld, B=1)
+        gl = torch.zeros(M, ld, device="cuda", dtype=torch.bfloat16)
+        S.k_gemm(0, tA, tW, M, N, K, S.EPI_GELU, bias=tb, out=gl, ldo=ld, B=1)
+        res = torch.from_numpy(np.ascontiguousarray(res0[:, :ld])).cuda()
+        S.k_gemm(0, tA, tW, M, N, K, S.EPI_GATED_RES, bias=tb, res=res, ldr=ld, gate=gate,
+                 gate_bstride=N, B=2)
+        torch.cuda.synchronize()
+        outs[ld] = [t[:, :N].float().cpu().numpy() for t in (f32, gl, res)]
+    for a, b in zip(outs[N], outs[N + 2]):
+        assert np.array_equal(a, b)
+
+
 SPLITK_SHAPES = [(128, 1280, 11520), (256, 320, 2880), (300, 640, 1280), (64, 256, 4608),
                  (1000, 192, 2048)]
 
