@@ -303,7 +303,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     reinterpret_cast<uintptr_t>(ep.kv_b) | (uintptr_t)ep.d * 2u) & 7u) == 0
             : ep.res_vec4 && ep.out != nullptr && (reinterpret_cast<uintptr_t>(ep.bias) & 15u) == 0 &&
                   ((reinterpret_cast<uintptr_t>(ep.out) |
-                    (uintptr_t)ep.ldo * (EPI == EPI_F32 ? 4u : 2u)) & (EPI == EPI_F32 ? 15u : 7u)) == 0;
+                    (uintptr_t)ep.ldo * (EPI == EPI_F32 ? 4u : 2u)) &
+                   (EPI == EPI_F32 ? 15u : (EPI == EPI_GEGLU ? 3u : 7u))) == 0;
     int it = 0;
     for (int item = item0; item < n_items; item += item_step, ++it) {
       int mb, nb;
@@ -403,7 +404,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             continue;
           }
         }
-        if constexpr (EPI == EPI_STORE || EPI == EPI_GELU || EPI == EPI_F32 || EPI == EPI_QKV) {
+        if constexpr (EPI == EPI_STORE || EPI == EPI_GELU || EPI == EPI_F32 || EPI == EPI_QKV ||
+                      EPI == EPI_GEGLU) {
           if (vec4o) {  // 8-byte bf16 / 16-byte fp32 stores: 8 lanes per row, 4 rows per step
             const int c4 = 4 * (lane & 7), col4 = nb * BN + c0 + c4;
             const float4 b4 = ep.bias ? *reinterpret_cast<const float4 *>(ep.bias + col4)
@@ -414,7 +416,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               if (row >= M) continue;
               const float *sv = stg + r * EPI_LD + c4;
               float v0 = sv[0] + b4.x, v1 = sv[1] + b4.y, v2 = sv[2] + b4.z, v3 = sv[3] + b4.w;
-              if constexpr (EPI == EPI_F32) {
+              if constexpr (EPI == EPI_GEGLU) {  // (a, g) pairs -> two outputs, one 4-byte store
+                *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<bf16 *>(ep.out) +
+                                                    (long)row * ep.ldo + col4 / 2) =
+                    __floats2bfloat162_rn(v0 * gelu_erf(v1), v2 * gelu_erf(v3));
+              } else if constexpr (EPI == EPI_F32) {
                 *reinterpret_cast<float4 *>(reinterpret_cast<float *>(ep.out) + (long)row * ep.ldo +
                                             col4) = make_float4(v0, v1, v2, v3);
               } else {

@@ -129,8 +129,12 @@ def test_gemm_epilogue_vector_and_scalar_paths_agree(S, M, N, K):
         res = torch.from_numpy(np.ascontiguousarray(res0[:, :ld])).cuda()
         S.k_gemm(0, tA, tW, M, N, K, S.EPI_GATED_RES, bias=tb, res=res, ldr=ld, gate=gate,
                  gate_bstride=N, B=2)
+        # GEGLU: N / 2 outputs per row; row stride N / 2 + 1 (odd) breaks 4-byte alignment
+        gg = torch.zeros(M, N // 2 + (ld - N) // 2, device="cuda", dtype=torch.bfloat16)
+        S.k_gemm(0, tA, tW, M, N, K, S.EPI_GEGLU, bias=tb, out=gg, ldo=gg.shape[1], B=1)
         torch.cuda.synchronize()
-        outs[ld] = [t[:, :N].float().cpu().numpy() for t in (f32, gl, res)]
+        outs[ld] = [t[:, :n].float().cpu().numpy()
+                    for t, n in ((f32, N), (gl, N), (res, N), (gg, N // 2))]
     for a, b in zip(outs[N], outs[N + 2]):
         assert np.array_equal(a, b)
 
