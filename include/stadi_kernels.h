@@ -56,6 +56,14 @@ typedef struct {
 stadi_status stadi_k_gemm(int32_t dtype, const void *A, const void *W, int32_t M, int32_t N,
                           int32_t K, int32_t epi, const stadi_k_epi *ep, void *stream);
 
+/* As stadi_k_gemm, with the persistent grid capped at max_ctas CTAs (0 = all
+ * SMs).  max_ctas < #SMs reproduces the runtime's launch while the occupancy
+ * emulator holds SMs (R24): single-CTA tiles on a shrunk grid,
+ * and the split-K choice of that grid. */
+stadi_status stadi_k_gemm_ex(int32_t dtype, const void *A, const void *W, int32_t M, int32_t N,
+                             int32_t K, int32_t epi, const stadi_k_epi *ep, int32_t max_ctas,
+                             void *stream);
+
 /* o = softmax(q k^T / sqrt(hd)) v per (batch b, head h).
  * q, o: [Nq * B, H*hd] (row = token*B + b); kv: [Nkv, B, 2, H*hd].
  * BF16 path: hd in {16, 64, 72, 80}. */
@@ -77,6 +85,15 @@ stadi_status stadi_k_ln_modulate(int32_t dtype, const float *x, void *y, int32_t
 stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void *Wt, int32_t h, int32_t W,
                              int32_t B, int32_t C, int32_t N, int32_t mode, int32_t implicit,
                              const float *bias, float *out, void *stream);
+
+/* As stadi_k_conv3x3 with the full EPI_CONV epilogue of the U-Net ResBlock:
+ * out[f32] (row stride ep->ldo) = conv + bias + gate[row % B] (time-embedding
+ * term, batch stride ep->gate_bstride; NULL = none) + res[row] (f32, row stride
+ * ep->ldr; NULL = none); other ep fields ignored.  max_ctas as stadi_k_gemm_ex. */
+stadi_status stadi_k_conv3x3_ex(int32_t dtype, const void *P, const void *Wt, int32_t h,
+                                int32_t W, int32_t B, int32_t C, int32_t N, int32_t mode,
+                                int32_t implicit, const stadi_k_epi *ep, int32_t max_ctas,
+                                void *stream);
 
 /* Fused CFG + unpatchify + sampler update of an fp32 band x [rows, W, C]
  * (NHWC; Eq. 3, R19 DDPM): eps_raw f32 [tokens * B, ld], token

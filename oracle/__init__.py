@@ -22,8 +22,12 @@ diffusion noise schedule + Eq. 3 DDIM/DPM-Solver-1 update (O3)      — pinned
 dit       DiT-family eps_theta, full and band (patch) forward (O4/O5) — pinned
 stadi     Algorithm 1 end to end, all ranks simulated in one process (O6)
 
+unet      U-Net-family eps_theta, band forward with exchange sites     — pinned
+
 Parity status: the stale-activation protocol (which version each site
 reads) has no worked example in the paper; beyond the reductions pinned in
-tests/test_oracle_stadi.py it is "parity unpinned".
+tests/test_oracle_model.py and tests/test_oracle_unet.py (fresh exchange ==
+unpatched, time-invariant activations make staleness exact) it is "parity
+unpinned".
 """
-from . import planner, schedule, diffusion, dit, stadi  # noqa: F401
+from . import planner, schedule, diffusion, dit, stadi, unet  # noqa: F401

@@ -1,5 +1,7 @@
 // Kernel-level C entry points (include/stadi_kernels.h).
 #include "../../include/stadi_kernels.h"
+#include <algorithm>
+
 #include "common.h"
 #include "kernels.h"
 
@@ -14,11 +16,14 @@ stadi_status cu(cudaError_t e, const char *what) {
 }
 }  // namespace
 
-extern "C" stadi_status stadi_k_gemm(int32_t dtype, const void *A, const void *W, int32_t M,
-                                     int32_t N, int32_t K, int32_t epi, const stadi_k_epi *e,
-                                     void *stream) {
-  if (!A || !W || !e || M < 0 || N <= 0 || K <= 0 || epi < 0 || epi > 7)
-    return fail(nullptr, STADI_EINVAL, "stadi_k_gemm: bad argument");
+namespace {
+int device_sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+EpiParams to_epi(const stadi_k_epi *e) {
   EpiParams ep{};
   ep.bias = e->bias;
   ep.out = e->out;
@@ -35,12 +40,27 @@ extern "C" stadi_status stadi_k_gemm(int32_t dtype, const void *A, const void *W
   ep.d = e->d;
   ep.ws = e->ws;
   ep.ws_elems = e->ws ? e->ws_elems : 0;
+  return ep;
+}
+}  // namespace
+
+extern "C" stadi_status stadi_k_gemm(int32_t dtype, const void *A, const void *W, int32_t M,
+                                     int32_t N, int32_t K, int32_t epi, const stadi_k_epi *e,
+                                     void *stream) {
+  return stadi_k_gemm_ex(dtype, A, W, M, N, K, epi, e, 0, stream);
+}
+
+extern "C" stadi_status stadi_k_gemm_ex(int32_t dtype, const void *A, const void *W, int32_t M,
+                                        int32_t N, int32_t K, int32_t epi, const stadi_k_epi *e,
+                                        int32_t max_ctas, void *stream) {
+  if (!A || !W || !e || M < 0 || N <= 0 || K <= 0 || epi < 0 || epi > 7 || max_ctas < 0)
+    return fail(nullptr, STADI_EINVAL, "stadi_k_gemm: bad argument");
+  const EpiParams ep = to_epi(e);
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == STADI_DTYPE_BF16) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return cu(tc_gemm_bf16((const bf16 *)A, (const bf16 *)W, M, N, K, epi, ep, sms, s),
+    const int sms = device_sm_count();
+    const int ctas = max_ctas ? std::min<int>(max_ctas, sms) : sms;
+    return cu(tc_gemm_bf16((const bf16 *)A, (const bf16 *)W, M, N, K, epi, ep, ctas, s),
               "tc_gemm_bf16");
   }
   if (dtype == STADI_DTYPE_FP32_DEBUG)
@@ -84,8 +104,19 @@ extern "C" stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void
                                         int32_t W, int32_t B, int32_t C, int32_t N, int32_t mode,
                                         int32_t implicit, const float *bias, float *out,
                                         void *stream) {
-  if (!P || !Wt || !out || h <= 0 || W <= 0 || B <= 0 || C <= 0 || N <= 0 || mode < 0 ||
-      mode > 2)
+  stadi_k_epi e{};
+  e.bias = bias;
+  e.out = out;
+  e.ldo = N;
+  return stadi_k_conv3x3_ex(dtype, P, Wt, h, W, B, C, N, mode, implicit, &e, 0, stream);
+}
+
+extern "C" stadi_status stadi_k_conv3x3_ex(int32_t dtype, const void *P, const void *Wt,
+                                           int32_t h, int32_t W, int32_t B, int32_t C, int32_t N,
+                                           int32_t mode, int32_t implicit, const stadi_k_epi *ke,
+                                           int32_t max_ctas, void *stream) {
+  if (!P || !Wt || !ke || !ke->out || h <= 0 || W <= 0 || B <= 0 || C <= 0 || N <= 0 ||
+      mode < 0 || mode > 2 || ke->ldo < N || (ke->res && ke->ldr < N) || max_ctas < 0)
     return fail(nullptr, STADI_EINVAL, "stadi_k_conv3x3: bad argument");
   cudaStream_t s = (cudaStream_t)stream;
   const int ho = mode == 1 ? h / 2 : (mode == 2 ? 2 * h : h);
@@ -93,12 +124,14 @@ extern "C" stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void
   const int M = ho * wo * B, kp = (9 * C + 63) / 64 * 64;
   EpiParams ep{};
   ep.B = B;
-  ep.bias = bias;
-  ep.out = out;
-  ep.ldo = N;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  ep.bias = ke->bias;
+  ep.out = ke->out;
+  ep.ldo = ke->ldo;
+  ep.res = ke->res;
+  ep.ldr = ke->ldr;
+  ep.gate = ke->gate;
+  ep.gate_bstride = ke->gate_bstride;
+  const int sms = max_ctas ? std::min(max_ctas, device_sm_count()) : device_sm_count();
   // split-K workspace (used when the conv's tiles fill at most half the SMs)
   float *ws = nullptr;
   if (dtype == STADI_DTYPE_BF16) {
@@ -146,8 +179,8 @@ extern "C" stadi_status stadi_k_sampler(float *x, const float *eps_raw, int32_t 
   if (!x || !eps_raw || rows < 0 || W <= 0 || C <= 0 || p <= 0 || rows % p || W % p ||
       c_out < C || ld < p * p * c_out || (B != 1 && B != 2) || row0 < 0)
     return fail(nullptr, STADI_EINVAL, "stadi_k_sampler: bad argument");
-  return cu(sampler_update(x, eps_raw, rows, W, C, p, c_out, ld, B, guidance, A, Bc, Cz, seed, m,
-                           row0, (cudaStream_t)stream),
+  return cu(sampler_update(x, eps_raw, rows, W, C, p, c_out, ld, B, guidance, A, Bc, Cz, seed, nullptr,
+                           m, row0, (cudaStream_t)stream),
             "sampler_update");
 }
 

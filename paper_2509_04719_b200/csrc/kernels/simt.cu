@@ -365,7 +365,8 @@ __device__ __forceinline__ float philox_normal(uint64_t seed, uint32_t m, uint64
 
 __global__ void sampler_kernel(float *__restrict__ xb, const float *__restrict__ eps, int rows,
                                int W, int C, int p, int c_out, int ld, int B, float g, float A,
-                               float Bc, float Cz, uint64_t seed, uint32_t m, int row0) {
+                               float Bc, float Cz, uint64_t seed, const uint64_t *seed_dev,
+                               uint32_t m, int row0) {
   const long n = (long)rows * W * C;
   const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n) return;
@@ -382,8 +383,10 @@ __global__ void sampler_kernel(float *__restrict__ xb, const float *__restrict__
     e = e + g * (ec - e);                                   // CFG (R20)
   }
   float x = A * xb[idx] + Bc * e;                           // Eq. 3 (DDIM)
-  if (Cz != 0.f)                                            // R19 DDPM: + sigma_eta z_m
+  if (Cz != 0.f) {                                          // R19 DDPM: + sigma_eta z_m
+    if (seed_dev) seed = *seed_dev;                         // per-request key (graph-safe)
     x += Cz * philox_normal(seed, m, (uint64_t)row0 * W * C + (uint64_t)idx);
+  }
   xb[idx] = x;
 }
 
@@ -410,11 +413,12 @@ cudaError_t patch_embed(const float *x_band, int rows, int W, int C, int p, cons
 
 cudaError_t sampler_update(float *x_band, const float *eps_raw, int rows, int W, int C, int p,
                            int c_out, int ld, int B, float guidance, float A, float Bc,
-                           float Cz, uint64_t seed, uint32_t m, int row0, cudaStream_t s) {
+                           float Cz, uint64_t seed, const uint64_t *seed_dev, uint32_t m, int row0,
+                           cudaStream_t s) {
   const long n = (long)rows * W * C;
   if (n == 0) return cudaSuccess;
   sampler_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-      x_band, eps_raw, rows, W, C, p, c_out, ld, B, guidance, A, Bc, Cz, seed, m, row0);
+      x_band, eps_raw, rows, W, C, p, c_out, ld, B, guidance, A, Bc, Cz, seed, seed_dev, m, row0);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -101,6 +101,8 @@ struct stadi_ctx {
   int dtype = STADI_DTYPE_BF16;
   int sampler = STADI_SAMPLER_DDIM;
   uint64_t ddpm_seed = 0;    // per request (stadi_cond), R19
+  uint64_t *seed_dev = nullptr;  // device copy of ddpm_seed, read by the sampler kernel so a
+                                 // captured step graph serves every request's seed
   int device = 0, rank = 0, world = 1, n_local = 1, G = 1;
   // NCCL mode: one rank per process, exchange by NCCL (world > 1; or world == 1 with
   // STADI_FORCE_NCCL=1, a single-rank communicator that runs the NCCL code path --
@@ -179,6 +181,8 @@ struct stadi_ctx {
   struct StepGraph {
     cudaGraphExec_t exec = nullptr;
     unsigned long long launches = 0;  // kernels inside (for the launch counter)
+    uint64_t exch_bytes = 0;          // exchange bytes the step moves (counted per replay)
+    int emu_ctas = 0;                 // emulator SMs at capture (grid sizes depend on it)
   };
   std::vector<StepGraph> graphs;
   cudaStream_t gstream = nullptr;
@@ -607,6 +611,8 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
         CK(cudaFree(buf));
       }
     }
+    CK(dalloc(ctx, &ctx->seed_dev, 8));
+    CK(cudaMemset(ctx->seed_dev, 0, 8));
     CK(cudaMalloc(&ctx->emu_flag_dev, 64));
     CK(cudaMemset(ctx->emu_flag_dev, 0, 64));
     CK(cudaStreamCreateWithFlags(&ctx->emu_stream, cudaStreamNonBlocking));
@@ -845,6 +851,9 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(ctx->device));
   ctx->ddpm_seed = cond->ddpm_seed;
+  // the sampler reads the key from device memory (graph replays see this request's
+  // seed); the host copy stays alive in ctx until the stream has consumed it
+  CK(cudaMemcpyAsync(ctx->seed_dev, &ctx->ddpm_seed, 8, cudaMemcpyHostToDevice, s));
   // noise bands
   const bool dev = is_device_ptr(noise_full);
   const size_t row_bytes = (size_t)m.lat_w * m.c_in * 4;
@@ -1149,8 +1158,8 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
     const double sb = (double)r.rows * m.lat_w * m.c_in * 8 + (double)M * ctx->fin_ld * 4;
     CK(timed(ctx, STADI_KCLASS_SAMPLER, 0.0, sb, s, [&] {
       return sampler_update(r.x_band, r.eps_raw, r.rows, m.lat_w, m.c_in, m.p, m.c_out,
-                            ctx->fin_ld, B, m.guidance, A, Bc, Cz, ctx->ddpm_seed, P.st.m,
-                            r.row_begin, s);
+                            ctx->fin_ld, B, m.guidance, A, Bc, Cz, ctx->ddpm_seed, ctx->seed_dev,
+                            P.st.m, r.row_begin, s);
     }));
   }
   return STADI_OK;
@@ -1175,10 +1184,15 @@ stadi_status exec_step(stadi_ctx *ctx, uint32_t i, cudaStream_t s) {
   if (!graphs_enabled(ctx)) return run_phase(ctx, ctx->program[i], s);
   if (ctx->graphs.size() != ctx->program.size()) ctx->graphs.assign(ctx->program.size(), {});
   auto &G = ctx->graphs[i];
+  if (G.exec && G.emu_ctas != ctx->emu_ctas) {  // captured grids assume another free-SM count
+    cudaGraphExecDestroy(G.exec);
+    G.exec = nullptr;
+  }
   if (!G.exec) {
     // capture on the context's own stream (the caller's may be the legacy stream)
     CK(cudaStreamSynchronize(s));
     const unsigned long long l0 = g_launches;
+    const uint64_t b0 = ctx->exch_bytes;
     CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
     const stadi_status st = run_phase(ctx, ctx->program[i], ctx->gstream);
     cudaGraph_t graph = nullptr;
@@ -1193,9 +1207,13 @@ stadi_status exec_step(stadi_ctx *ctx, uint32_t i, cudaStream_t s) {
     CK(ei);
     G.launches = g_launches - l0;
     g_launches = l0;  // counted when the graph runs
+    G.exch_bytes = ctx->exch_bytes - b0;
+    ctx->exch_bytes = b0;
+    G.emu_ctas = ctx->emu_ctas;
   }
   CK(cudaGraphLaunch(G.exec, s));
   g_launches += G.launches;
+  ctx->exch_bytes += G.exch_bytes;
   return STADI_OK;
 }
 }  // namespace

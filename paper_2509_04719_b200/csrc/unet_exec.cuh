@@ -773,8 +773,8 @@ struct UBuilder {
         const double sb = (double)h * W * 4 * 8 + (double)h * W * B * 64 * 4;
         CK(timed(ctx, STADI_KCLASS_SAMPLER, 0.0, sb, s, [&] {
           return sampler_update(ctx->ranks[me].x_band, (const float *)E(), h, W, ctx->dm.c_in, 1,
-                                4, 64, B, ctx->dm.guidance, A, Bc, Cz, ctx->ddpm_seed, st.m,
-                                ctx->ranks[me].row_begin, s);
+                                4, 64, B, ctx->dm.guidance, A, Bc, Cz, ctx->ddpm_seed, ctx->seed_dev,
+                                st.m, ctx->ranks[me].row_begin, s);
         }));
         return STADI_OK;
       });

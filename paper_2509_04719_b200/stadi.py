@@ -110,7 +110,8 @@ EXPORTS = [
     "stadi_num_steps", "stadi_denoise_step", "stadi_gather", "stadi_run",
     "stadi_emulator_start", "stadi_emulator_stop", "stadi_nccl_unique_id",
     "stadi_kernel_timing", "stadi_kernel_stats",
-    "stadi_k_gemm", "stadi_k_attention", "stadi_k_ln_modulate", "stadi_k_conv3x3",
+    "stadi_k_gemm", "stadi_k_gemm_ex", "stadi_k_attention", "stadi_k_ln_modulate",
+    "stadi_k_conv3x3", "stadi_k_conv3x3_ex",
     "stadi_k_sampler", "stadi_k_ddpm_noise", "stadi_k_launch_count",
 ]
 
@@ -151,6 +152,11 @@ def _load():
                                          C.POINTER(C.c_double)]),
         "stadi_k_gemm": (C.c_int, [C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                    C.POINTER(KEpi), vp]),
+        "stadi_k_gemm_ex": (C.c_int, [C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_int32, C.POINTER(KEpi), C.c_int32, vp]),
+        "stadi_k_conv3x3_ex": (C.c_int, [C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32,
+                                         C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                         C.POINTER(KEpi), C.c_int32, vp]),
         "stadi_k_attention": (C.c_int, [C.c_int32, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, vp]),
         "stadi_k_ln_modulate": (C.c_int, [C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp,
@@ -369,12 +375,18 @@ class Context:
 
 
 # ---------------------------------------------------------------- kernel-level
-def k_gemm(dtype, A, W, M, N, K, epi, stream=None, **ep):
+def _kepi(ep):
     e = KEpi()
     for k, v in ep.items():
         setattr(e, k, ptr(v) if k in ("bias", "out", "res", "gate", "q", "kv_a", "kv_b", "ws")
                 else v)
-    _check(lib.stadi_k_gemm(dtype, ptr(A), ptr(W), M, N, K, epi, C.byref(e), stream_ptr(stream)))
+    return e
+
+
+def k_gemm(dtype, A, W, M, N, K, epi, stream=None, max_ctas=0, **ep):
+    e = _kepi(ep)
+    _check(lib.stadi_k_gemm_ex(dtype, ptr(A), ptr(W), M, N, K, epi, C.byref(e), max_ctas,
+                               stream_ptr(stream)))
 
 
 def k_attention(dtype, q, kv, o, Nq, Nkv, B, H, hd, stream=None):
@@ -390,6 +402,14 @@ def k_ln_modulate(dtype, x, y, M, d, B, shift, scale, bstride, stream=None):
 def k_conv3x3(dtype, P, Wt, h, W, B, C_, N, mode, implicit, bias, out, stream=None):
     _check(lib.stadi_k_conv3x3(dtype, ptr(P), ptr(Wt), h, W, B, C_, N, mode, implicit, ptr(bias),
                                ptr(out), stream_ptr(stream)))
+
+
+def k_conv3x3_ex(dtype, P, Wt, h, W, B, C_, N, mode, implicit, stream=None, max_ctas=0, **ep):
+    """Conv with the full EPI_CONV epilogue: ep = bias, out, ldo, res, ldr, gate,
+    gate_bstride (stadi_k_conv3x3_ex)."""
+    e = _kepi(ep)
+    _check(lib.stadi_k_conv3x3_ex(dtype, ptr(P), ptr(Wt), h, W, B, C_, N, mode, implicit,
+                                  C.byref(e), max_ctas, stream_ptr(stream)))
 
 
 def k_sampler(x, eps_raw, rows, W, C_, p, c_out, ld, B, guidance, A, Bc, Cz=0.0, seed=0, m=0,

@@ -90,17 +90,17 @@ def _inputs(name, **kw):
     return _cache[key]
 
 
-def _zf(cfg):
+def _zf(cfg, seed=SEED):
     shape = (cfg["latent_h"], cfg["latent_w"], cfg["c_in"])
-    return lambda m: gen.ddpm_noise(shape, m, SEED)
+    return lambda m: gen.ddpm_noise(shape, m, seed)
 
 
-def _oracle(cfg, W, x, c, plan, dtype):
-    key = dict(kind="stadi_run_ddpm", seed=SEED, cfg=cfg, dtype=dtype, plan=plan)
+def _oracle(cfg, W, x, c, plan, dtype, seed=SEED):
+    key = dict(kind="stadi_run_ddpm", seed=seed, cfg=cfg, dtype=dtype, plan=plan)
 
     def compute():
         return OR.run(cfg, gen.weights_bf16(W) if dtype == 0 else W, x, c, plan,
-                      ddpm_z=_zf(cfg))
+                      ddpm_z=_zf(cfg, seed))
     return refcache.cached(key, compute)
 
 
@@ -145,3 +145,33 @@ def test_ddpm_run(S, name, kw, speed, mb, mw, dtype):
     err = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
     print(f"DDPM {name} dtype={dtype} max-abs-rel={err:.3e}")
     assert err <= TOL[dtype]
+
+
+@pytest.mark.parametrize("name", ["tiny_dit", "tiny_unet"])
+def test_ddpm_seed_changes_between_requests(S, name):
+    """Two requests on ONE context and plan with different DDPM seeds: the step
+    graphs captured by the first request must draw the second request's z_m
+    (the sampler reads the key from device memory), each against the oracle."""
+    cfg, W, x, c = _inputs(name)
+    speed, mb, mw = [1 << 20, 1 << 19], 10, 2
+    plan = OR.plan_for(cfg, speed, mb, mw)
+    desc = S.model_desc(name, 0, latent_h=cfg["latent_h"], latent_w=cfg["latent_w"],
+                        sampler=S.SAMPLER_DDPM)
+    ctx = S.Context(desc, n_local=2)
+    try:
+        ctx.load_weights([W[n] for n, _, _ in configs.manifest(cfg)])
+        u = configs.rows_per_unit(cfg)
+        p = S.plan(speed, mb, mw, cfg["latent_h"] // u, u)
+        outs = []
+        for seed in (SEED, SEED + 1, SEED):
+            out = np.zeros_like(x)
+            ctx.run(p, x, dict(c, ddpm_seed=seed), out)
+            outs.append(out.astype(np.float64))
+    finally:
+        ctx.close()
+    assert np.array_equal(outs[0], outs[2])
+    for seed, got in ((SEED, outs[0]), (SEED + 1, outs[1])):
+        ref = _oracle(cfg, W, x, c, plan, 0, seed)
+        err = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
+        print(f"DDPM two-request {name} seed={seed} max-abs-rel={err:.3e}")
+        assert err <= TOL[0]

@@ -58,7 +58,7 @@ def test_gemm_store_f32_gelu(S, dtype, M, N, K):
     out = torch.zeros(M, N, device="cuda")
     S.k_gemm(dtype, tA, tW, M, N, K, S.EPI_F32, bias=tb, out=out, ldo=N, B=1)
     torch.cuda.synchronize()
-    assert _rel(out.cpu().numpy(), ref) < (1e-5 if True else tol)
+    assert _rel(out.cpu().numpy(), ref) < 1e-5      # fp32 output: fp32 accumulation only
     # T output, GELU
     outT = torch.zeros(M, N, device="cuda", dtype=tA.dtype)
     S.k_gemm(dtype, tA, tW, M, N, K, S.EPI_GELU, bias=tb, out=outT, ldo=N, B=1)
@@ -351,3 +351,85 @@ def test_conv3x3(S, dtype, h, W, B, C, N, mode, implicit):
     got = out.cpu().numpy().reshape(ho, wo, B, N).transpose(2, 0, 1, 3)
     assert np.all(np.isfinite(got))
     assert _rel(got, ref) < (1e-2 if dtype == 0 else 1e-5)
+
+
+@pytest.mark.parametrize("implicit,mode", [(1, 0), (0, 0), (0, 1), (0, 2)])
+def test_conv3x3_time_bias_and_residual(S, implicit, mode):
+    """The U-Net ResBlock conv epilogue (EPI_CONV): out = conv + bias + temb[row % B]
+    + res, against the oracle's conv3x3_valid plus the two terms; the 16-byte path
+    (aligned ldo / ldr) and the unaligned one (rows padded by 2 floats) must agree
+    bit for bit."""
+    from oracle import unet as OU
+    rng = np.random.default_rng(11 + mode + 10 * implicit)
+    h, W, B, C, N = 4, 32, 2, 64, 192
+    P = rng.standard_normal((h + 2, W + 2, B, C)).astype(np.float32)
+    P[:, 0] = 0
+    P[:, -1] = 0
+    w = (rng.standard_normal((N, C, 3, 3)) / np.sqrt(9 * C)).astype(np.float32)
+    bias = (rng.standard_normal(N) * 0.1).astype(np.float32)
+    temb = rng.standard_normal((B, N + 5)).astype(np.float32)     # batch stride N + 5
+    kp = (9 * C + 63) // 64 * 64
+    wt = np.zeros((N, kp), np.float32)
+    wt[:, :9 * C] = w.transpose(0, 2, 3, 1).reshape(N, 9 * C)
+    tP, nP = _bf(P)
+    tW, nW = _bf(wt)
+    nw = nW[:, :9 * C].reshape(N, 3, 3, C).transpose(0, 3, 1, 2)
+    ho = h // 2 if mode == 1 else (2 * h if mode == 2 else h)
+    wo = W // 2 if mode == 1 else (2 * W if mode == 2 else W)
+    M = ho * wo * B
+    res0 = rng.standard_normal((M, N + 2)).astype(np.float32)
+    outs = {}
+    for ld in (N, N + 2):
+        out = torch.full((M, ld), float("nan"), device="cuda")
+        res = torch.from_numpy(np.ascontiguousarray(res0[:, :ld])).cuda()
+        S.k_conv3x3_ex(0, tP, tW, h, W, B, C, N, mode, implicit,
+                       bias=torch.from_numpy(bias).cuda(), out=out, ldo=ld, res=res, ldr=ld,
+                       gate=torch.from_numpy(temb).cuda(), gate_bstride=N + 5)
+        torch.cuda.synchronize()
+        outs[ld] = out[:, :N].cpu().numpy()
+    assert np.array_equal(outs[N], outs[N + 2])
+    x = nP.transpose(2, 0, 1, 3)
+    if mode == 2:
+        inner = x[:, 1:-1, 1:-1].repeat(2, axis=1).repeat(2, axis=2)
+        top = x[:, :1, 1:-1].repeat(2, axis=2)
+        bot = x[:, -1:, 1:-1].repeat(2, axis=2)
+        x = OU.pad_cols(np.concatenate([top, inner, bot], axis=1))
+    if mode == 1:
+        x = x[:, :-1]
+    conv = OU.conv3x3_valid(x, nw, bias.astype(np.float64), 2 if mode == 1 else 1)
+    ref = conv.transpose(1, 2, 0, 3).reshape(M, N) \
+        + temb[np.arange(M) % B, :N].astype(np.float64) + res0[:, :N].astype(np.float64)
+    assert _rel(outs[N], ref) < 1e-5
+
+
+@pytest.mark.parametrize("max_ctas", [118, 88, 58, 7])
+@pytest.mark.parametrize("M,N,K", [(300, 384, 1152), (2048, 1152, 4608), (128, 1280, 11520)])
+def test_gemm_on_emulator_grid(S, max_ctas, M, N, K):
+    """Under the occupancy emulator (R24) the runtime launches its
+    GEMMs on the free SMs only (max_ctas = SMs - held): single-CTA tiles on a
+    shrunk persistent grid and that grid's split-K choice.  Every epilogue kind on
+    such grids (20 / 40 / 60 % held and an extreme) against the oracle."""
+    rng = np.random.default_rng(M + N + K + max_ctas)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    bias = (rng.standard_normal(N) * 0.1).astype(np.float32)
+    tA, nA = _bf(A)
+    tW, nW = _bf(W)
+    tb = torch.from_numpy(bias).cuda()
+    ws = torch.empty(16 * M * N, device="cuda")
+    wk = dict(ws=ws, ws_elems=ws.numel(), max_ctas=max_ctas)
+    ref = OD.linear(nA, nW, bias.astype(np.float64))
+    out = torch.zeros(M, N, device="cuda")
+    S.k_gemm(0, tA, tW, M, N, K, S.EPI_F32, bias=tb, out=out, ldo=N, B=1, **wk)
+    outT = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    S.k_gemm(0, tA, tW, M, N, K, S.EPI_GELU, bias=tb, out=outT, ldo=N, B=1, **wk)
+    gate = rng.standard_normal((2, N)).astype(np.float32)
+    res0 = rng.standard_normal((M, N)).astype(np.float32)
+    res = torch.from_numpy(res0.copy()).cuda()
+    S.k_gemm(0, tA, tW, M, N, K, S.EPI_GATED_RES, bias=tb, res=res, ldr=N,
+             gate=torch.from_numpy(gate).cuda(), gate_bstride=N, B=2, **wk)
+    torch.cuda.synchronize()
+    assert _rel(out.cpu().numpy(), ref) < 1e-5
+    assert _rel(outT.float().cpu().numpy(), OD.gelu_tanh(ref)) < 1e-2
+    g = gate[np.arange(M) % 2].astype(np.float64)
+    assert _rel(res.cpu().numpy() - res0, g * ref) < 1e-5

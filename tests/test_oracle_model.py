@@ -294,3 +294,31 @@ def test_time_invariant_activations_make_staleness_exact():
     seq2 = stadi.sequential(cfg, W2, x, c, 10)
     out2 = stadi.run(cfg, W2, x, c, stadi.plan_for(cfg, [2, 1], 10, 2))
     assert np.max(np.abs(out2 - seq2)) > 1e-9 * np.max(np.abs(seq2))
+
+
+def test_temporal_redundancy_trend_thm1_thm2():
+    """Theorems 1 and 2 (§IV, Eq. 6-7): the single-step
+    difference |x_{t_m} - x_{t_{m+1}}| of a GPU's state is O(1/M) -- for a fast
+    GPU (Thm 1) and for a slow GPU whose one step spans n = 2 fast-grid
+    intervals (Thm 2, n M_i = M).  On the C1 oracle run (speeds [2, 1]: tier 1 +
+    tier 2) the largest step difference of each rank must fall with M_base, M d
+    must approach a constant (d halves when M doubles, asymptotically), and the
+    slow rank's steps must be ~n = 2 times the fast rank's."""
+    cfg, W, x, c = _c1()
+    d = {}
+    for mb in (10, 20, 50, 100):
+        p = stadi.plan_for(cfg, [2, 1], mb, 2)
+        assert p["tier"] == [1, 2]
+        _, trace = stadi.run(cfg, W, x, c, p, return_trace=True)
+        prev = {r: x[p["row_begin"][r]:p["row_begin"][r] + p["rows"][r]].astype(np.float64)
+                for r in range(2)}
+        dm = [0.0, 0.0]
+        for _, r, _, band in trace:
+            dm[r] = max(dm[r], float(np.max(np.abs(band - prev[r]))))
+            prev[r] = band
+        d[mb] = dm
+    for r in range(2):
+        assert d[10][r] > d[20][r] > d[50][r] > d[100][r], (r, d)
+        assert 1.6 < d[50][r] / d[100][r] < 2.2, (r, d)        # O(1/M): M d -> const
+    for mb in (50, 100):
+        assert 1.6 < d[mb][1] / d[mb][0] < 2.5, d               # Thm 2, n = 2

@@ -7,6 +7,12 @@ What fixes the U-Net family independently of the oracle's own code:
 * the up-path ResBlock input widths of SD-1.5 (its conv1 weight shapes);
 * conv3x3 against a brute-force 7-deep loop; GroupNorm against a textbook
   formula; GELU(1) = Phi(1) = 0.8413447460685429; sinusoid closed forms;
+* the whole layer composition against an independent per-element evaluation
+  written from the diffusers layer definitions (test_unet_forward_bruteforce on
+  a micro config that has every layer kind; mutating the oracle -- swapped skip
+  concat, swapped GEGLU halves, GN eps 1e-6 -> 1e-5, LN eps 1e-5 -> 1e-6, a
+  dropped Transformer2D residual, a sign flip of the add-embedding -- moves it
+  by >= 4e-7 relative against a 1e-11 tolerance);
 * the patch protocol's reductions: with a fresh exchange (M_warmup = M_base)
   the band-parallel run equals the unpatched sequential run for any split
   (halos, GroupNorm partial sums, K/V, stride-2 and upsample halos all
@@ -139,3 +145,211 @@ def test_time_invariant_activations_make_staleness_exact(tiny):
         p = OR.plan_for(cfg, speed, 6, 2, flags=flags)
         out = OR.run(cfg, W, x, c, p)
         assert np.max(np.abs(out - seq)) <= 1e-12 * np.max(np.abs(seq)), (speed, flags)
+
+
+# ----------------------------------------------------------- brute-force U-Net
+def _micro_cfg():
+    """Micro U-Net that still exercises every layer kind of the diffusers
+    UNet2DConditionModel: 2 levels (channels 32 / 64, GroupNorm 32 groups),
+    2 ResBlocks per down level (so the up path pops 3 skips per level, one
+    from a Downsample), a 1x1 skip conv where channels change, Transformer2D
+    (depth 1) on BOTH levels and in the mid block, Downsample / Upsample,
+    SDXL add-embedding, CFG batch of 2."""
+    return dict(family="unet", cond="text", channels=[32, 64], tdepth=[1, 1], mid_depth=1,
+                heads=None, head_dim=16, layers_per_block=2, c_in=4, c_out=4, latent_h=8,
+                latent_w=8, text_len=3, text_dim=8, add_embed=True, pooled_dim=8,
+                time_ids=[16, 16, 0, 0, 16, 16], guidance=5.0, schedule="scaled_linear",
+                name="micro_unet")
+
+
+def _brute_unet(cfg, W, x, t, cond):
+    """eps_theta of the U-Net family by per-element loops, written from the
+    diffusers UNet2DConditionModel / ResnetBlock2D / Transformer2DModel /
+    BasicTransformerBlock / GEGLU / Downsample2D / Upsample2D definitions
+    (SURVEY §8(c) O4), independently of oracle/unet.py: matrix-vector products
+    per pixel / token are the only library primitive.  Channel counts are read
+    off the tensors (the up path's concat widths are not taken from the
+    architecture description).  Returns [B, H, W, C_out]."""
+    W = {k: np.asarray(v, np.float64) for k, v in W.items()}
+    ch = cfg["channels"]
+    nlev, nres = len(ch), cfg["layers_per_block"]
+    B = 2 if cfg.get("guidance") else 1
+    text = np.asarray(cond["text"], np.float64)
+
+    def silu(v):
+        return v / (1.0 + np.exp(-v))
+
+    def sinusoid(tv, dim):                      # Timesteps(dim, flip_sin_to_cos=True, shift 0)
+        half = dim // 2
+        f = [math.exp(-math.log(10000.0) * k / half) for k in range(half)]
+        return np.array([math.cos(tv * fk) for fk in f] + [math.sin(tv * fk) for fk in f])
+
+    def mv(w, v, b=None):                       # Linear: y = W v (+ b)
+        y = w @ v
+        return y if b is None else y + b
+
+    def conv(h, p, stride=1):                   # Conv2d(k=3, padding=1, stride)
+        wt, bs = W[p + ".w"], W[p + ".b"]
+        nb, H, Wd, _ = h.shape
+        Ho, Wo = (H - 1) // stride + 1, (Wd - 1) // stride + 1
+        out = np.zeros((nb, Ho, Wo, wt.shape[0]))
+        for b in range(nb):
+            for oy in range(Ho):
+                for ox in range(Wo):
+                    acc = bs.copy()
+                    for ky in range(3):
+                        iy = oy * stride + ky - 1
+                        if not 0 <= iy < H:
+                            continue
+                        for kx in range(3):
+                            ix = ox * stride + kx - 1
+                            if 0 <= ix < Wd:
+                                acc += wt[:, :, ky, kx] @ h[b, iy, ix]
+                    out[b, oy, ox] = acc
+        return out
+
+    def groupnorm(h, p, eps):                   # GroupNorm(32, C, eps, affine)
+        nb, H, Wd, C = h.shape
+        cg = C // 32
+        out = np.zeros_like(h)
+        for b in range(nb):
+            for g in range(32):
+                vals = [h[b, y, xx, c] for y in range(H) for xx in range(Wd)
+                        for c in range(g * cg, (g + 1) * cg)]
+                mu = math.fsum(vals) / len(vals)
+                var = math.fsum((v - mu) ** 2 for v in vals) / len(vals)
+                for c in range(g * cg, (g + 1) * cg):
+                    out[b, :, :, c] = (h[b, :, :, c] - mu) / math.sqrt(var + eps) \
+                        * W[p + ".w"][c] + W[p + ".b"][c]
+        return out
+
+    def layernorm(v, p):                        # LayerNorm(C, eps 1e-5, affine)
+        mu = math.fsum(v) / len(v)
+        var = math.fsum((a - mu) ** 2 for a in v) / len(v)
+        return (v - mu) / math.sqrt(var + 1e-5) * W[p + ".w"] + W[p + ".b"]
+
+    def attend(qs, ks, vs, heads):              # softmax(q k^T / sqrt(hd)) v per head
+        C = qs[0].shape[0]
+        hd = C // heads
+        out = []
+        for qv in qs:
+            o = np.zeros(C)
+            for hh in range(heads):
+                sl = slice(hh * hd, (hh + 1) * hd)
+                sc = [float(qv[sl] @ kv[sl]) / math.sqrt(hd) for kv in ks]
+                mx = max(sc)
+                e = [math.exp(s - mx) for s in sc]
+                z = math.fsum(e)
+                for j, vv in enumerate(vs):
+                    o[sl] += e[j] / z * vv[sl]
+            out.append(o)
+        return out
+
+    def resnet(h, p, temb):                     # ResnetBlock2D
+        y = silu(groupnorm(h, p + "norm1", 1e-5))
+        y = conv(y, p + "conv1")
+        for b in range(h.shape[0]):
+            y[b] += mv(W[p + "temb.w"], silu(temb[b]), W[p + "temb.b"])
+        y = silu(groupnorm(y, p + "norm2", 1e-5))
+        y = conv(y, p + "conv2")
+        if p + "skip.w" in W:                   # conv_shortcut (1x1) when C_in != C_out
+            sk = np.zeros(h.shape[:3] + (y.shape[3],))
+            for b in range(h.shape[0]):
+                for yy in range(h.shape[1]):
+                    for xx in range(h.shape[2]):
+                        sk[b, yy, xx] = mv(W[p + "skip.w"], h[b, yy, xx], W[p + "skip.b"])
+        else:
+            sk = h
+        return sk + y
+
+    def transformer(h, p, depth, heads):        # Transformer2DModel (linear projection)
+        nb, H, Wd, C = h.shape
+        g = groupnorm(h, p + "norm", 1e-6)
+        out = np.zeros_like(h)
+        for b in range(nb):
+            toks = [mv(W[p + "proj_in.w"], g[b, y, xx], W[p + "proj_in.b"])
+                    for y in range(H) for xx in range(Wd)]
+            ctx = [text[b, j] for j in range(text.shape[1])]
+            for k in range(depth):              # BasicTransformerBlock
+                q = f"{p}blk{k}."
+                n1 = [layernorm(v, q + "ln1") for v in toks]
+                a1 = attend([mv(W[q + "attn1.q"], v) for v in n1],
+                            [mv(W[q + "attn1.k"], v) for v in n1],
+                            [mv(W[q + "attn1.v"], v) for v in n1], heads)
+                toks = [v + mv(W[q + "attn1.o"], a, W[q + "attn1.ob"]) for v, a in zip(toks, a1)]
+                n2 = [layernorm(v, q + "ln2") for v in toks]
+                a2 = attend([mv(W[q + "attn2.q"], v) for v in n2],
+                            [mv(W[q + "attn2.k"], c) for c in ctx],
+                            [mv(W[q + "attn2.v"], c) for c in ctx], heads)
+                toks = [v + mv(W[q + "attn2.o"], a, W[q + "attn2.ob"]) for v, a in zip(toks, a2)]
+                new = []
+                for v in toks:                  # FeedForward(GEGLU): hidden, gate = chunk(2)
+                    pr = mv(W[q + "ff1.w"], layernorm(v, q + "ln3"), W[q + "ff1.b"])
+                    hid, gate = pr[:4 * C], pr[4 * C:]
+                    gl = np.array([0.5 * a * (1.0 + math.erf(a / math.sqrt(2.0))) for a in gate])
+                    new.append(v + mv(W[q + "ff2.w"], hid * gl, W[q + "ff2.b"]))
+                toks = new
+            for i, v in enumerate(toks):
+                y, xx = divmod(i, Wd)
+                out[b, y, xx] = h[b, y, xx] + mv(W[p + "proj_out.w"], v, W[p + "proj_out.b"])
+        return out
+
+    # time embedding (+ SDXL "text_time" add embedding: concat[pooled, time_ids proj])
+    temb = []
+    for b in range(B):
+        e = mv(W["time.w2"], silu(mv(W["time.w1"], sinusoid(float(t), ch[0]), W["time.b1"])),
+               W["time.b2"])
+        if cfg.get("add_embed"):
+            tid = np.concatenate([sinusoid(float(v), 256) for v in cond["time_ids"][b]])
+            a = np.concatenate([np.asarray(cond["pooled"][b], np.float64), tid])
+            e = e + mv(W["add.w2"], silu(mv(W["add.w1"], a, W["add.b1"])), W["add.b2"])
+        temb.append(e)
+    h = conv(np.stack([np.asarray(x, np.float64)] * B), "conv_in")
+    res_samples = [h]
+    for i in range(nlev):
+        heads = ch[i] // cfg["head_dim"]
+        for j in range(nres):
+            h = resnet(h, f"down{i}.res{j}.", temb)
+            if cfg["tdepth"][i]:
+                h = transformer(h, f"down{i}.attn{j}.", cfg["tdepth"][i], heads)
+            res_samples.append(h)
+        if i < nlev - 1:
+            h = conv(h, f"down{i}.ds", stride=2)
+            res_samples.append(h)
+    h = resnet(h, "mid.res0.", temb)
+    h = transformer(h, "mid.attn.", cfg["mid_depth"], ch[-1] // cfg["head_dim"])
+    h = resnet(h, "mid.res1.", temb)
+    for i in range(nlev):
+        lev = nlev - 1 - i
+        for j in range(nres + 1):
+            skip = res_samples.pop()
+            h = np.concatenate([h, skip], axis=-1)          # torch.cat([h, res_hidden], dim=1)
+            h = resnet(h, f"up{i}.res{j}.", temb)
+            if cfg["tdepth"][lev]:
+                h = transformer(h, f"up{i}.attn{j}.", cfg["tdepth"][lev], ch[lev] // cfg["head_dim"])
+        if i < nlev - 1:                                    # Upsample2D: nearest x2, conv
+            nb, H, Wd, C = h.shape
+            up = np.zeros((nb, 2 * H, 2 * Wd, C))
+            for y in range(2 * H):
+                for xx in range(2 * Wd):
+                    up[:, y, xx] = h[:, y // 2, xx // 2]
+            h = conv(up, f"up{i}.us")
+    assert not res_samples
+    h = silu(groupnorm(h, "out.norm", 1e-5))
+    return conv(h, "out.conv")
+
+
+def test_unet_forward_bruteforce():
+    """oracle/unet.py's whole-image forward (its band generator with every
+    exchange answered alone) against the independent per-element evaluation:
+    pins the layer composition (ResBlock / Transformer2D order, GEGLU halves,
+    GN / LN eps, add-embedding, skip-concat order, up / down sampling)."""
+    cfg = _micro_cfg()
+    W = gen.weights(cfg, seed=3)
+    x = gen.noise(cfg, seed=4).astype(np.float64)
+    c = gen.cond(cfg, seed=5)
+    got = OU.UNet(cfg, W).forward_full(x, 601, c)
+    ref = _brute_unet(cfg, W, x, 601, c)
+    assert got.shape == ref.shape == (2, 8, 8, 4)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
+    assert np.max(np.abs(ref[0] - ref[1])) > 1e-3 * np.max(np.abs(ref))   # CFG rows differ
