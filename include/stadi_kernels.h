@@ -52,7 +52,9 @@ typedef struct {
   int64_t ws_elems;
 } stadi_k_epi;
 
-/* out = epilogue(A[M,K] . W[N,K]^T).  BF16 path: K % 64 == 0, N % 64 == 0. */
+/* out = epilogue(A[M,K] . W[N,K]^T).  BF16 path: K % 64 == 0, N % 64 == 0.
+ * Column pairs are accessed as 8-byte vectors: ldo, ldr and gate_bstride must be
+ * even (EINVAL otherwise); 16-byte rows take the 16-byte epilogue. */
 stadi_status stadi_k_gemm(int32_t dtype, const void *A, const void *W, int32_t M, int32_t N,
                           int32_t K, int32_t epi, const stadi_k_epi *ep, void *stream);
 

@@ -54,9 +54,17 @@ def linear(x, w, b):
     return x @ w.T + b
 
 
-def attention(q, k, v, heads):
-    """softmax(q k^T / sqrt(hd)) v per head.  q [B,n,d], k/v [B,N,d]."""
+def attention(q, k, v, heads, q_chunk=1024):
+    """softmax(q k^T / sqrt(hd)) v per head.  q [B,n,d], k/v [B,N,d].
+
+    Every query row's softmax is independent of the others, so rows are
+    evaluated in chunks of q_chunk (a memory bound for the full-resolution
+    parity refs: 16384 x 16384 scores per head would not fit); the arithmetic of
+    each row is the definition above, whatever the chunking."""
     B, n, d = q.shape
+    if n > q_chunk:
+        return np.concatenate([attention(q[:, i:i + q_chunk], k, v, heads, q_chunk)
+                               for i in range(0, n, q_chunk)], axis=1)
     N = k.shape[1]
     hd = d // heads
     qh = q.reshape(B, n, heads, hd).transpose(0, 2, 1, 3)

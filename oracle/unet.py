@@ -80,12 +80,13 @@ def conv3x3_valid(xp, w, b, stride=1):
     B, Hp, Wp, Cin = xp.shape
     Ho = (Hp - 3) // stride + 1
     Wo = (Wp - 3) // stride + 1
-    out = np.zeros((B, Ho, Wo, w.shape[0]))
+    out = np.zeros((B * Ho * Wo, w.shape[0]))
     for ky in range(3):
         for kx in range(3):
             patch = xp[:, ky:ky + stride * (Ho - 1) + 1:stride, kx:kx + stride * (Wo - 1) + 1:stride]
-            out += patch @ w[:, :, ky, kx].T
-    return out + b
+            # contiguous [pixels, Cin] x [Cin, Cout] operands: one BLAS product per tap
+            out += np.ascontiguousarray(patch).reshape(-1, Cin) @ np.ascontiguousarray(w[:, :, ky, kx].T)
+    return out.reshape(B, Ho, Wo, w.shape[0]) + b
 
 
 def pad_cols(x):

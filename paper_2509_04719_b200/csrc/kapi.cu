@@ -53,7 +53,8 @@ extern "C" stadi_status stadi_k_gemm(int32_t dtype, const void *A, const void *W
 extern "C" stadi_status stadi_k_gemm_ex(int32_t dtype, const void *A, const void *W, int32_t M,
                                         int32_t N, int32_t K, int32_t epi, const stadi_k_epi *e,
                                         int32_t max_ctas, void *stream) {
-  if (!A || !W || !e || M < 0 || N <= 0 || K <= 0 || epi < 0 || epi > 7 || max_ctas < 0)
+  if (!A || !W || !e || M < 0 || N <= 0 || K <= 0 || epi < 0 || epi > 7 || max_ctas < 0 ||
+      (e->gate && (e->gate_bstride & 1)) || (e->res && (e->ldr & 1)))
     return fail(nullptr, STADI_EINVAL, "stadi_k_gemm: bad argument");
   const EpiParams ep = to_epi(e);
   cudaStream_t s = (cudaStream_t)stream;
@@ -116,7 +117,8 @@ extern "C" stadi_status stadi_k_conv3x3_ex(int32_t dtype, const void *P, const v
                                            int32_t mode, int32_t implicit, const stadi_k_epi *ke,
                                            int32_t max_ctas, void *stream) {
   if (!P || !Wt || !ke || !ke->out || h <= 0 || W <= 0 || B <= 0 || C <= 0 || N <= 0 ||
-      mode < 0 || mode > 2 || ke->ldo < N || (ke->res && ke->ldr < N) || max_ctas < 0)
+      mode < 0 || mode > 2 || ke->ldo < N || (ke->res && ke->ldr < N) || max_ctas < 0 ||
+      (ke->ldo | ke->ldr | ke->gate_bstride) & 1)
     return fail(nullptr, STADI_EINVAL, "stadi_k_conv3x3: bad argument");
   cudaStream_t s = (cudaStream_t)stream;
   const int ho = mode == 1 ? h / 2 : (mode == 2 ? 2 * h : h);

@@ -33,6 +33,27 @@ def cached(key: dict, compute):
     if os.environ.get("STADI_WRITE_REFS") == "1":
         os.makedirs(DIR, exist_ok=True)
         np.save(p, np.asarray(out, dtype=np.float64))
+        _KEYS[os.path.basename(p)] = key
         with open(os.path.join(DIR, "index.jsonl"), "a") as f:
             f.write(json.dumps({"file": os.path.basename(p), "key": key}, sort_keys=True, default=str) + "\n")
+    else:
+        _KEYS[os.path.basename(p)] = key
     return out
+
+
+_KEYS: dict = {}
+
+
+def rewrite_index():
+    """index.jsonl = one line per .npy present whose key this process saw
+    (make_oracle_refs.py visits every case); files no case refers to are removed."""
+    lines = []
+    for f in sorted(os.listdir(DIR)):
+        if not f.endswith(".npy"):
+            continue
+        if f not in _KEYS:
+            os.remove(os.path.join(DIR, f))
+            continue
+        lines.append(json.dumps({"file": f, "key": _KEYS[f]}, sort_keys=True, default=str))
+    with open(os.path.join(DIR, "index.jsonl"), "w") as f:
+        f.write("\n".join(lines) + "\n")

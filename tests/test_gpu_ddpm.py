@@ -114,6 +114,9 @@ def oracle_cases():
         for dtype in ((1, 0) if name == "tiny_dit" else (0,)):
             cfg, W, x, c = _inputs(name, **kw)
             yield cfg, W, x, c, OR.plan_for(cfg, speed, mb, mw), dtype
+    for name in ("tiny_dit", "tiny_unet"):          # the second request's seed
+        cfg, W, x, c = _inputs(name)
+        yield cfg, W, x, c, OR.plan_for(cfg, [1 << 20, 1 << 19], 10, 2), 0, SEED + 1
 
 
 def _gpu_run(S, name, cfg, W, x, c, speed, mb, mw, dtype):

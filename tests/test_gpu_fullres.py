@@ -1,0 +1,189 @@
+"""Oracle parity at each config's OWN resolution, and under emulated occupancy (GPU).
+
+SURVEY §8(d): the large configs are checked on a depth-reduced variant with the
+same widths, resolution, bands and steps; BASELINE.json north star: "oracle-
+matching latents on every config".  The fp64 oracle outputs are generated once
+offline by tests/golden/make_oracle_refs.py (it calls only oracle/):
+
+* C5 PixArt-alpha 2048^2: the full 256 x 256 latent (16384 tokens, d 1152, 16
+  heads, 120 x 4096 text), depth 1, M_base 8 / M_warmup 2, 2 GPUs with the second
+  at 50% occupancy (v = 0.5 -> tier 2, stride-2 steps);
+* C4 SDXL 1024^2: the full 128 x 128 latent, transformer depth capped at 1, 3 GPUs
+  at occupancy {0, 20, 60}% (v = 1, 0.8, 0.4 -> tiers [1, 1, 2]), M_base 10 / 2;
+* C3 SD-1.5 512^2: the full 64 x 64 latent at full depth, 4 GPUs at occupancy
+  {0, 20, 40, 60}% (tiers [1, 1, 2, 2]), M_base 10 / 2;
+* C2 DiT-XL/2 256^2 is already at its own 32 x 32 resolution (test_gpu_parity).
+
+Occupancy ("Occupancy Simulation", R24): with the emulator holding
+20 / 40 / 60 % of the SMs the GEMMs run single-CTA tiles on a shrunk persistent
+grid with that grid's split-K choice; the result must still match the oracle
+("results must be independent of occupancy"), in local mode and
+on the NCCL code path.
+
+Every case prints its measured max-abs-rel (visible in the -rA summary).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import stadi as OR
+from synth import configs, gen
+import refcache
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {0: 2e-2, 1: 1e-4}
+_cache = {}
+
+# occupancy -> speed v = 1 - rho (fixed-point, fastest = 2^16), the proxy of SURVEY §6
+def _v(occ):
+    return [int(round(65536 * (100 - o) / 100)) for o in occ]
+
+
+FULLRES = {
+    "c5": ("pixart_alpha", dict(depth=1), _v([0, 50]), 8, 2),
+    "c4": ("sdxl", dict(tdepth=[0, 1, 1], mid_depth=1), _v([0, 20, 60]), 10, 2),
+    "c3": ("sd15", {}, _v([0, 20, 40, 60]), 10, 2),
+}
+
+
+def _inputs(name, **kw):
+    key = (name, tuple(sorted((k, str(v)) for k, v in kw.items())))
+    if key not in _cache:
+        cfg = configs.model(name, **kw)
+        _cache[key] = (cfg, gen.weights(cfg), gen.noise(cfg), gen.cond(cfg))
+    return _cache[key]
+
+
+def _oracle(cfg, W, x, c, plan, dtype):
+    key = dict(kind="stadi_run", cfg=cfg, dtype=dtype, plan=plan)
+
+    def compute():
+        return OR.run(cfg, gen.weights_bf16(W) if dtype == 0 else W, x, c, plan)
+    return refcache.cached(key, compute)
+
+
+def oracle_cases():
+    for name, kw, speed, mb, mw in FULLRES.values():
+        cfg, W, x, c = _inputs(name, **kw)
+        yield cfg, W, x, c, OR.plan_for(cfg, speed, mb, mw), 0
+
+
+def _seq_ref(cfg, W, x, c, mb):
+    return refcache.cached(dict(kind="sequential", cfg=cfg, dtype=0, m_base=mb),
+                           lambda: OR.sequential(cfg, gen.weights_bf16(W), x, c, mb))
+
+
+def extra_refs():
+    """Oracle outputs beyond _oracle(*case) (tests/golden/make_oracle_refs.py)."""
+    for name, kw, _, _, _ in EMU_CASES:
+        cfg, W, x, c = _inputs(name, **kw)
+        yield f"sequential {name}", lambda cfg=cfg, W=W, x=x, c=c: _seq_ref(cfg, W, x, c, 10)
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2509_04719_b200 import stadi
+    return stadi
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+def _desc(S, name, cfg, dtype):
+    depth = cfg.get("depth", 0) if cfg["family"] == "dit" else max(
+        [cfg["mid_depth"]] + list(cfg["tdepth"]))
+    return S.model_desc(name, dtype, depth=depth, latent_h=cfg["latent_h"],
+                        latent_w=cfg["latent_w"])
+
+
+@pytest.mark.parametrize("case", list(FULLRES))
+def test_fullres_parity(S, case):
+    name, kw, speed, mb, mw = FULLRES[case]
+    cfg, W, x, c = _inputs(name, **kw)
+    plan = OR.plan_for(cfg, speed, mb, mw)
+    assert 2 in plan["tier"] and plan["m_warmup"] < plan["m_base"]   # stale rounds + tier 2
+    ref = _oracle(cfg, W, x, c, plan, 0)
+    ctx = S.Context(_desc(S, name, cfg, 0), n_local=len(speed))
+    try:
+        ctx.load_weights([W[n] for n, _, _ in configs.manifest(cfg)])
+        u = configs.rows_per_unit(cfg)
+        p = S.plan(speed, mb, mw, cfg["latent_h"] // u, u)
+        assert p.to_dict()["rows"] == plan["rows"] and p.to_dict()["steps"] == plan["steps"]
+        out = np.zeros_like(x)
+        ctx.run(p, x, c, out)
+    finally:
+        ctx.close()
+    got = out.astype(np.float64)
+    assert np.all(np.isfinite(got))
+    err = _rel(got, ref)
+    print(f"FULLRES {case} {name} {cfg['latent_h']}x{cfg['latent_w']} steps={plan['steps']} "
+          f"rows={plan['rows']} bf16 max-abs-rel={err:.3e}")
+    assert err <= TOL[0]
+
+
+# ---------------------------------------------------------------- occupancy
+def _emu_run(S, name, cfg, W, x, c, speed, mb, mw, dtype, occ, nccl):
+    old = os.environ.get("STADI_FORCE_NCCL")
+    os.environ["STADI_FORCE_NCCL"] = "1" if nccl else "0"
+    try:
+        ctx = S.Context(_desc(S, name, cfg, dtype), n_local=len(speed))
+    finally:
+        if old is None:
+            del os.environ["STADI_FORCE_NCCL"]
+        else:
+            os.environ["STADI_FORCE_NCCL"] = old
+    try:
+        ctx.load_weights([W[n] for n, _, _ in configs.manifest(cfg)])
+        u = configs.rows_per_unit(cfg)
+        p = S.plan(speed, mb, mw, cfg["latent_h"] // u, u)
+        out0 = np.zeros_like(x)
+        ctx.run(p, x, c, out0)              # loads every kernel, captures graphs (0% held)
+        st = torch.cuda.Stream()            # before the emulator (see test_gpu_nccl_mode)
+        ctx.emulator_start(occ)
+        try:
+            out = np.zeros_like(x)
+            ctx.run(p, x, c, out, stream=st)
+        finally:
+            ctx.emulator_stop()
+        return out0.astype(np.float64), out.astype(np.float64)
+    finally:
+        ctx.close()
+
+
+EMU_CASES = [("dit_xl2", dict(depth=2), [65536, 39322], 50, 4),
+             ("tiny_unet", {}, [1 << 20, 1 << 19], 10, 2)]
+
+
+@pytest.mark.parametrize("occ", [20, 40, 60])
+@pytest.mark.parametrize("ci", [0, 1], ids=["c2_depth2", "tiny_unet"])
+def test_parity_under_emulator_local(S, ci, occ):
+    """Local mode (all ranks on one GPU) with the emulator holding occ% of the
+    SMs: same oracle reference as the unloaded run (tests/test_gpu_parity.py,
+    test_gpu_unet.py caches)."""
+    name, kw, speed, mb, mw = EMU_CASES[ci]
+    cfg, W, x, c = _inputs(name, **kw)
+    plan = OR.plan_for(cfg, speed, mb, mw)
+    ref = _oracle(cfg, W, x, c, plan, 0)
+    free, held = _emu_run(S, name, cfg, W, x, c, speed, mb, mw, 0, occ, nccl=False)
+    e0, e1 = _rel(free, ref), _rel(held, ref)
+    print(f"EMU local {name} occ={occ}% max-abs-rel free={e0:.3e} held={e1:.3e}")
+    assert e0 <= TOL[0] and e1 <= TOL[0]
+
+
+@pytest.mark.parametrize("occ", [20, 60])
+@pytest.mark.parametrize("ci", [0, 1], ids=["c2_depth2", "tiny_unet"])
+def test_parity_under_emulator_nccl(S, ci, occ):
+    """The NCCL code path (single-rank communicator) under the emulator against
+    the oracle's sequential run (one rank == sequential DDIM)."""
+    name, kw, _, mb, mw = EMU_CASES[ci]
+    cfg, W, x, c = _inputs(name, **kw)
+    mb = 10
+    ref = _seq_ref(cfg, W, x, c, mb)
+    free, held = _emu_run(S, name, cfg, W, x, c, [1 << 20], mb, mw, 0, occ, nccl=True)
+    e0, e1 = _rel(free, ref), _rel(held, ref)
+    print(f"EMU nccl {name} occ={occ}% max-abs-rel free={e0:.3e} held={e1:.3e}")
+    assert e0 <= TOL[0] and e1 <= TOL[0]
