@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define STADI_ABI_VERSION 2u
+#define STADI_ABI_VERSION 3u
 #define STADI_MAX_GPUS 64
 
 typedef enum {
@@ -194,11 +194,27 @@ stadi_status stadi_weight_info(const stadi_model_desc *desc, uint32_t index,
  * NCCL over NVLink) or n_local ranks on one device (world == 1; exchange by
  * device copies — used to run the multi-rank protocol on a single GPU).
  * ====================================================================== */
+/* Transport of the exchange when world > 1 (one rank per process):
+ *  NCCL: grouped ncclBroadcast / ncclAllGather on a high-priority side stream
+ *        (the variable-size all-gather of L288); one GPU per process.
+ *  IPC:  one-sided, CUDA IPC between the processes of ONE node (any GPUs with
+ *        peer access, or several processes sharing one GPU): the QKV GEMM
+ *        epilogue stores its K/V rows straight into the peers' slots (the
+ *        all-gather fused into the producer), halo rows go to the two
+ *        neighbour ranks only, GroupNorm partials to all, and completion is
+ *        signalled by stream memory operations on flags in the receiver's
+ *        memory (no SM spins, no host round trips).  nccl_id then carries a
+ *        128-byte session id (stadi_ipc_session_id) that namespaces the
+ *        node-local control files (/dev/shm) used to swap IPC handles. */
+enum { STADI_TRANSPORT_NCCL = 0, STADI_TRANSPORT_IPC = 1 };
+
 typedef struct {
-  int32_t rank, world;       /* process rank / number of processes (1 GPU each)  */
+  int32_t rank, world;       /* process rank / number of processes               */
   int32_t device;            /* CUDA device ordinal                              */
   int32_t n_local;           /* ranks hosted by this ctx (>1 only if world == 1) */
-  const uint8_t *nccl_id;    /* 128-byte ncclUniqueId from rank 0 when world > 1 */
+  const uint8_t *nccl_id;    /* 128 bytes from rank 0 when world > 1: the
+                                ncclUniqueId (NCCL) or the session id (IPC)      */
+  int32_t transport;         /* STADI_TRANSPORT_* (world > 1)                    */
 } stadi_dist_desc;
 
 typedef struct {
@@ -217,7 +233,10 @@ typedef struct {
 
 typedef struct {
   double ms_total;           /* device time of the request on this process       */
-  double ms_exchange_wait;   /* reserved (0)                                     */
+  double ms_exchange_wait;   /* device time the compute stream spent blocked on
+                                exchange completion (NCCL events / IPC flags);
+                                measured only while kernel timing is enabled
+                                (stadi_kernel_timing), else 0                   */
   uint64_t exchange_bytes;   /* bytes this process sent in exchange rounds       */
   uint32_t kernel_launches;  /* kernels this process launched for the request    */
   uint32_t steps_run;        /* program steps executed                           */
@@ -245,7 +264,8 @@ stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan);
 
 /* Start a request: take this context's rows of the full noise [H, W, C_in]
  * (host or device pointer) and the conditioning; precompute per-timestep
- * modulation and text K/V.  Stream-ordered on `stream`. */
+ * modulation and text K/V.  Stream-ordered on `stream`.  COLLECTIVE with the
+ * IPC transport (resets the exchange flags behind a device-side barrier). */
 stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full, const stadi_cond *cond,
                          void *stream);
 /* Number of program steps of the installed plan (local mode: steps grouped by
@@ -286,7 +306,9 @@ enum {
   STADI_KCLASS_XATTN = 2,    /* cross-attention to the text tokens             */
   STADI_KCLASS_NORM = 3,     /* LayerNorm + adaLN modulate                     */
   STADI_KCLASS_SAMPLER = 4,  /* CFG + unpatchify + Eq. 3 update                */
-  STADI_KCLASS_COUNT = 5
+  STADI_KCLASS_XWAIT = 5,    /* exchange waits (no kernel: the time the stream
+                                is blocked on a peer's version; flops = bytes = 0) */
+  STADI_KCLASS_COUNT = 6
 };
 stadi_status stadi_kernel_timing(stadi_ctx *ctx, int32_t enable);
 stadi_status stadi_kernel_stats(stadi_ctx *ctx, int32_t kclass, uint64_t *launches, double *ms,
@@ -294,6 +316,9 @@ stadi_status stadi_kernel_stats(stadi_ctx *ctx, int32_t kclass, uint64_t *launch
 
 /* ncclGetUniqueId through the library's NCCL (dlopen'ed; ENCCL if absent). */
 stadi_status stadi_nccl_unique_id(uint8_t out[128]);
+/* A fresh random session id for the IPC transport (rank 0 calls it and
+ * broadcasts the bytes, like an ncclUniqueId). */
+stadi_status stadi_ipc_session_id(uint8_t out[128]);
 
 #ifdef __cplusplus
 }

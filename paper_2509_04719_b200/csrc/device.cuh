@@ -60,6 +60,11 @@ struct EpiParams {
   long ws_elems;
   int res_prefetch;    // tcgen05 GEMM: L2-prefetch the residual tile before the accumulator wait
   int res_vec4;        // tcgen05 GEMM: 16-byte residual read-modify-write when aligned
+  // EPI_QKV, IPC transport: the publish version's own K/V rows are also stored straight
+  // into n_kv_peer peers' slots (device array of their slot bases, same layout, mapped
+  // with CUDA IPC): the variable-size all-gather fused into the epilogue (P2P stores)
+  void *const *kv_peer;
+  int n_kv_peer;
 };
 
 // Apply the epilogue to `n` consecutive columns col..col+n-1 of one row.
@@ -116,6 +121,11 @@ __device__ __forceinline__ void epi_apply(const EpiParams &p, int row, int col, 
       for (int i = 0; i < n; ++i) a[i] = from_f<T>(v[i]);
       if (p.kv_b) {
         T *b = reinterpret_cast<T *>(p.kv_b) + off;
+#pragma unroll 8
+        for (int i = 0; i < n; ++i) b[i] = from_f<T>(v[i]);
+      }
+      for (int k = 0; k < p.n_kv_peer; ++k) {
+        T *b = reinterpret_cast<T *>(p.kv_peer[k]) + off;
 #pragma unroll 8
         for (int i = 0; i < n; ++i) b[i] = from_f<T>(v[i]);
       }

@@ -129,6 +129,8 @@ __device__ __forceinline__ void epi_finish(const EpiParams &p, int row, int col,
       const long off = (p.kv_row0 + row) * 2L * p.d + (col - p.d);
       *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<bf16 *>(p.kv_a) + off) = t;
       if (p.kv_b) *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<bf16 *>(p.kv_b) + off) = t;
+      for (int k = 0; k < p.n_kv_peer; ++k)  // IPC peers (P2P stores over NVLink)
+        *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<bf16 *>(p.kv_peer[k]) + off) = t;
     }
   }
 }
@@ -442,6 +444,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     const long off = (ep.kv_row0 + row) * 2L * ep.d + (col4 - ep.d);
                     *reinterpret_cast<uint2 *>(reinterpret_cast<bf16 *>(ep.kv_a) + off) = pk;
                     if (ep.kv_b) *reinterpret_cast<uint2 *>(reinterpret_cast<bf16 *>(ep.kv_b) + off) = pk;
+                    for (int k = 0; k < ep.n_kv_peer; ++k)  // IPC peers (P2P stores)
+                      *reinterpret_cast<uint2 *>(reinterpret_cast<bf16 *>(ep.kv_peer[k]) + off) = pk;
                   }
                 } else {
                   *reinterpret_cast<uint2 *>(reinterpret_cast<bf16 *>(ep.out) + (long)row * ep.ldo +

@@ -90,9 +90,11 @@ struct Rank {
 struct Part {  // one (hosted rank, schedule entry) executed in a program step
   int li;      // index into ctx->ranks
   stadi_step_t st;
+  int idx = 0; // index of the entry in the rank's step table
 };
 
 struct UNetState;  // unet_exec.cuh
+struct IpcState;   // ipc.cuh
 
 }  // namespace
 
@@ -108,6 +110,12 @@ struct stadi_ctx {
   // STADI_FORCE_NCCL=1, a single-rank communicator that runs the NCCL code path --
   // broadcasts, comm stream, version events, gather -- on one GPU for tests)
   bool nccl = false;
+  // IPC mode: one rank per process (world > 1, STADI_TRANSPORT_IPC), one-sided
+  // exchange through CUDA IPC mappings of the peers' slots (ipc.cuh)
+  bool ipc_mode = false;
+  std::unique_ptr<IpcState> ipc;
+  bool probe = false;        // profiling probe steps: no exchange waits / signals
+  int ipc_idx = 0;           // IPC mode: step-table index of the step being built / run
   int num_sms = 148;
   std::string err;
   bool poisoned = false;
@@ -426,6 +434,7 @@ void free_graphs(stadi_ctx *ctx);
 
 }  // namespace
 
+#include "ipc.cuh"
 #include "unet_exec.cuh"
 
 namespace {
@@ -442,7 +451,8 @@ void free_plan_buffers(stadi_ctx *ctx) {
   for (auto &r : ctx->ranks) {
     for (void *p : {(void *)r.x_band, (void *)r.x_res, r.xmod, r.q, r.o, r.h1, (void *)r.eps_raw})
       pfree(ctx, p);
-    for (void *p : r.kv) pfree(ctx, p);
+    if (!ctx->ipc_mode)  // IPC mode: the slots live in the (persistent) exchange arena
+      for (void *p : r.kv) pfree(ctx, p);
   }
   ctx->ranks.clear();
   ctx->program.clear();
@@ -490,6 +500,21 @@ extern "C" stadi_status stadi_weight_info(const stadi_model_desc *desc, uint32_t
   return STADI_OK;
 }
 
+extern "C" stadi_status stadi_ipc_session_id(uint8_t out[128]) {
+  if (!out) return fail(nullptr, STADI_EINVAL, "NULL argument");
+  std::memset(out, 0, 128);
+  FILE *f = std::fopen("/dev/urandom", "rb");
+  size_t n = f ? std::fread(out, 1, 16, f) : 0;
+  if (f) std::fclose(f);
+  if (n != 16) {  // no urandom: pid + clock
+    const uint64_t a = (uint64_t)getpid(), b = (uint64_t)std::chrono::steady_clock::now()
+                                                   .time_since_epoch().count();
+    std::memcpy(out, &a, 8);
+    std::memcpy(out + 8, &b, 8);
+  }
+  return STADI_OK;
+}
+
 extern "C" stadi_status stadi_nccl_unique_id(uint8_t out[128]) {
   if (!out) return fail(nullptr, STADI_EINVAL, "NULL argument");
   if (!nccl().ok) return fail(nullptr, STADI_ENCCL, "libnccl.so.2 not loadable");
@@ -534,9 +559,14 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
   ctx->world = dist->world;
   ctx->n_local = dist->n_local;
   ctx->G = dist->world * dist->n_local;
+  if (dist->world > 1 && dist->transport != STADI_TRANSPORT_NCCL &&
+      dist->transport != STADI_TRANSPORT_IPC)
+    return fail(nullptr, STADI_EINVAL, "bad transport");
   {
     const char *fe = getenv("STADI_FORCE_NCCL");
-    ctx->nccl = dist->world > 1 || (dist->n_local == 1 && fe && fe[0] == '1');
+    ctx->ipc_mode = dist->world > 1 && dist->transport == STADI_TRANSPORT_IPC;
+    ctx->nccl = (dist->world > 1 && !ctx->ipc_mode) ||
+                (dist->world == 1 && dist->n_local == 1 && fe && fe[0] == '1');
   }
   ctx->man = manifest(dm);
   ctx->fin_ld = (int)rup(dm.p * dm.p * dm.c_out, 64);
@@ -611,6 +641,19 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
         CK(cudaFree(buf));
       }
     }
+    if (ctx->ipc_mode) {
+      if (!dist->nccl_id) return ctx_fail(ctx, STADI_EINVAL, "IPC transport needs a session id");
+      if (!memops().ok)
+        return ctx_fail(ctx, STADI_EUNSUPPORTED, "stream memory operations unavailable");
+      ctx->ipc = std::make_unique<IpcState>();
+      IpcState &I = *ctx->ipc;
+      I.session = hexs(dist->nccl_id, 16);
+      struct stat sb;
+      I.dir = (stat("/dev/shm", &sb) == 0 && access("/dev/shm", W_OK) == 0) ? "/dev/shm" : "/tmp";
+      CK(dalloc(ctx, &I.probe, 256));
+      CK(cudaMemset(I.probe, 0, 256));
+      I.graphs_ok = ipc_probe_graphs(ctx);
+    }
     CK(dalloc(ctx, &ctx->seed_dev, 8));
     CK(cudaMemset(ctx->seed_dev, 0, 8));
     CK(cudaMalloc(&ctx->emu_flag_dev, 64));
@@ -631,6 +674,7 @@ extern "C" void stadi_destroy(stadi_ctx *ctx) {
   }
   cudaDeviceSynchronize();
   free_plan_buffers(ctx);
+  ipc_release(ctx);
   for (void *p : ctx->allocs) cudaFree(p);
   for (void *p : ctx->wT) cudaFree(p);
   for (float *p : ctx->wf) cudaFree(p);
@@ -797,23 +841,26 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     CK(pmalloc(ctx, &r.eps_raw, std::max<int64_t>(16, M * ctx->fin_ld * 4)));
     r.kv.assign(m.depth * 2, nullptr);
     CK(cudaStreamSynchronize(ctx->astream));
-    for (auto &p : r.kv) {
-      CK(pmalloc(ctx, &p, slot_elems(m) * ctx->esz));
-      CK(cudaMemsetAsync(p, 0, slot_elems(m) * ctx->esz, ctx->astream));
+    if (!ctx->ipc_mode) {
+      for (auto &p : r.kv) {
+        CK(pmalloc(ctx, &p, slot_elems(m) * ctx->esz));
+        CK(cudaMemsetAsync(p, 0, slot_elems(m) * ctx->esz, ctx->astream));
+      }
     }
     CK(cudaStreamSynchronize(ctx->astream));
     ctx->ranks.push_back(std::move(r));
   }
   // program
-  if (ctx->nccl) {
+  if (ctx->nccl || ctx->ipc_mode) {
     if (!ctx->ranks.empty())
-      for (auto &st : ctx->ranks[0].sched) ctx->program.push_back({Part{0, st}});
+      for (size_t k = 0; k < ctx->ranks[0].sched.size(); ++k)
+        ctx->program.push_back({Part{0, ctx->ranks[0].sched[k], (int)k}});
   } else {
     for (int mm = 0; mm < (int)plan->m_base; ++mm) {
       std::vector<Part> ph;
       for (int li = 0; li < (int)ctx->ranks.size(); ++li)
-        for (auto &st : ctx->ranks[li].sched)
-          if (st.m == mm) ph.push_back(Part{li, st});
+        for (size_t k = 0; k < ctx->ranks[li].sched.size(); ++k)
+          if (ctx->ranks[li].sched[k].m == mm) ph.push_back(Part{li, ctx->ranks[li].sched[k], (int)k});
       if (!ph.empty()) ctx->program.push_back(ph);
     }
   }
@@ -833,7 +880,19 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     ctx->ev_used.assign(m.depth * 2, 0);
     for (auto &e : ctx->ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  if (m.unet) ST(unet_set_plan(ctx));
+  if (m.unet) {
+    ST(unet_set_plan(ctx));
+  } else if (ctx->ipc_mode) {  // K/V slots of every site and parity in the IPC arena
+    ipc_layout_begin(ctx);
+    IpcState &I = *ctx->ipc;
+    for (int l = 0; l < m.depth; ++l)
+      for (int par = 0; par < 2; ++par)
+        I.site_off[par].push_back(ipc_reserve(ctx, slot_elems(m) * ctx->esz));
+    ST(ipc_commit(ctx, m.depth));
+    for (auto &r : ctx->ranks)
+      for (int l = 0; l < m.depth; ++l)
+        for (int par = 0; par < 2; ++par) r.kv[l * 2 + par] = I.arena + I.site_off[par][l];
+  }
   ctx->has_plan = true;
   return STADI_OK;
 }
@@ -861,6 +920,7 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
     CK(cudaMemcpyAsync(r.x_band, noise_full + (size_t)r.row_begin * m.lat_w * m.c_in,
                        row_bytes * r.rows, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        s));
+  if (ctx->ipc_mode) ST(ipc_begin(ctx, s));  // flag reset + device-side barrier
   // ---- conditioning for every fast-grid timestep (one batched GEMM each)
   const int nt = (int)ctx->plan.m_base;
   const int64_t d = m.d;
@@ -1017,6 +1077,11 @@ stadi_status publish(stadi_ctx *ctx, int li, int l, int ver, cudaStream_t s) {
   int64_t off, cnt;
   seg_of(ctx, r.g, &off, &cnt);
   const size_t bytes = cnt * ctx->esz;
+  if (ctx->ipc_mode) {  // IPC: the QKV epilogue already stored the rows at the peers
+    if (ctx->probe) return STADI_OK;
+    ctx->exch_bytes += bytes * ctx->ipc->peers.size();
+    return ipc_ready(ctx, l, ver, false, s);
+  }
   if (!ctx->nccl) {  // local mode: copy into every other hosted rank's slot
     for (auto &o : ctx->ranks) {
       if (o.g == r.g) continue;
@@ -1051,7 +1116,9 @@ stadi_status publish(stadi_ctx *ctx, int li, int l, int ver, cudaStream_t s) {
 stadi_status wait_version(stadi_ctx *ctx, int l, int ver, cudaStream_t s) {
   if (!ctx->nccl || ver < 0) return STADI_OK;
   const int slot = l * 2 + (ver & 1);
-  if (ctx->ev_used[slot]) CK(cudaStreamWaitEvent(s, ctx->ev_done[slot], 0));
+  if (ctx->ev_used[slot])
+    CK(timed(ctx, STADI_KCLASS_XWAIT, 0.0, 0.0, s,
+             [&] { return cudaStreamWaitEvent(s, ctx->ev_done[slot], 0); }));
   return STADI_OK;
 }
 
@@ -1081,6 +1148,10 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
       // own rows may only be overwritten once this rank's earlier sends of
       // the read version completed (NCCL mode)
       if (P.st.pub_ver != P.st.read_ver) ST(wait_version(ctx, l, P.st.read_ver, s));
+      // IPC: the epilogue writes the publish version into the peers' slots; they
+      // must be done reading that slot's previous version first
+      const bool ipcx = ctx->ipc_mode && !ctx->probe && P.st.pub_ver >= 0;
+      if (ipcx) ST(ipc_war_wait(ctx, l, P.st.pub_ver, false, s));
       EpiParams ep{};
       ep.bias = WF(ctx, pre + "qkv.b");
       ep.B = B;
@@ -1091,6 +1162,10 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
                     ? r.kv[l * 2 + (P.st.pub_ver & 1)]
                     : nullptr;
       ep.kv_row0 = (int64_t)r.tok_begin * B;
+      if (ipcx) {
+        ep.kv_peer = ipc_peer_slots(ctx, l, P.st.pub_ver & 1);
+        ep.n_kv_peer = ep.kv_peer ? (int)ctx->ipc->peers.size() : 0;
+      }
       CK(gemm(ctx, r.xmod, WT(ctx, pre + "qkv.w"), M, (int)(3 * d), (int)d, EPI_QKV, ep, s));
       if (P.st.pub_ver >= 0) ST(publish(ctx, P.li, l, P.st.pub_ver, s));
       if (P.st.pub_ver == P.st.read_ver) ST(wait_version(ctx, l, P.st.read_ver, s));  // fresh
@@ -1099,8 +1174,11 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
       Rank &r = ctx->ranks[P.li];
       const int M = r.n_tok * B;
       const float *mb = ctx->mod + ((int64_t)P.st.m * B * m.depth + l) * 6 * d;
+      const bool ipcr = ctx->ipc_mode && !ctx->probe;
+      if (ipcr) ST(ipc_read_wait(ctx, l, P.st.read_ver, false, s));  // peers' rows of read_ver
       CK(attention(ctx, STADI_KCLASS_ATTN, r.q, r.kv[l * 2 + (P.st.read_ver & 1)], r.o, r.n_tok,
                     ntok_full, s));
+      if (ipcr) ST(ipc_read_done(ctx, l, (uint32_t)P.idx + 1, false, s));
       EpiParams ep{};
       ep.B = B;
       ep.bias = WF(ctx, pre + "proj.b");
@@ -1174,9 +1252,10 @@ bool graphs_enabled(stadi_ctx *ctx) {
     const char *e = getenv("STADI_GRAPHS");
     return (e && e[0] == '0') ? 0 : 1;
   }();
-  // local mode only (NCCL mode's cross-stream exchange events stay eager), and not
-  // while per-launch kernel timing is on (its events must see every launch)
-  return env && !ctx->nccl && !ctx->ktime;
+  // local mode, and IPC mode when the driver can capture its stream memory operations
+  // (NCCL mode's cross-stream exchange events stay eager); not while per-launch kernel
+  // timing is on (its events must see every launch)
+  return env && !ctx->nccl && (!ctx->ipc_mode || ctx->ipc->graphs_ok) && !ctx->ktime;
 }
 
 // Program step i on stream s: replay its graph, capturing it on first use.
@@ -1237,6 +1316,7 @@ extern "C" stadi_status stadi_gather(stadi_ctx *ctx, float *out_full, void *stre
   CK(cudaSetDevice(ctx->device));
   const bool dev = is_device_ptr(out_full);
   const size_t row_elems = (size_t)m.lat_w * m.c_in;
+  if (ctx->ipc_mode) return ipc_gather(ctx, out_full, dev, s);
   if (!ctx->nccl) {
     for (auto &r : ctx->ranks)
       CK(cudaMemcpyAsync(out_full + (size_t)r.row_begin * row_elems, r.x_band,
@@ -1284,6 +1364,8 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   const unsigned long long l0 = g_launches;
+  CK(collect_timing(ctx));  // (no-op unless timing) so the exchange-wait delta is this request's
+  const double w0 = ctx->kt[STADI_KCLASS_XWAIT].ms;
   CK(cudaEventRecord(e0, s));
   ST(stadi_begin(ctx, noise_full, cond, stream));
   for (uint32_t i = 0; i < ctx->program.size(); ++i) ST(exec_step(ctx, i, s));
@@ -1297,7 +1379,7 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
   CK(collect_timing(ctx));
   if (stats) {
     stats->ms_total = ms;
-    stats->ms_exchange_wait = 0;
+    stats->ms_exchange_wait = ctx->kt[STADI_KCLASS_XWAIT].ms - w0;
     stats->exchange_bytes = ctx->exch_bytes;
     stats->kernel_launches = (uint32_t)(g_launches - l0);
     stats->steps_run = (uint32_t)ctx->program.size();
@@ -1344,6 +1426,7 @@ extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, d
   cudaStream_t s = nullptr;
   ST(stadi_begin(ctx, zeros.data(), &cond, s));
   std::vector<double> ms_local(ctx->ranks.size(), 0.0);
+  ctx->probe = true;  // compute-only probe steps: no exchange waits / signals
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -1363,10 +1446,13 @@ extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, d
     std::sort(v.begin(), v.end());
     ms_local[li] = v[v.size() / 2];
   }
+  ctx->probe = false;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   std::vector<double> all(ctx->G, 0.0);
-  if (!ctx->nccl) {
+  if (ctx->ipc_mode) {
+    ST(ipc_allgather_f64(ctx, ms_local.empty() ? 0.0 : ms_local[0], all));
+  } else if (!ctx->nccl) {
     for (size_t li = 0; li < ctx->ranks.size(); ++li) all[ctx->ranks[li].g] = ms_local[li];
   } else {
     double *dsend = nullptr, *drecv = nullptr;

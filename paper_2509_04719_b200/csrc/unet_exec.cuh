@@ -25,6 +25,7 @@ namespace {
 enum USiteKind { US_KV = 0, US_HALO = 1, US_GN = 2 };
 
 struct USite {
+  int id = 0;  // index in UNetState::sites (IPC flag index)
   int kind = 0, level = 0, C = 0;
   int64_t seg_bytes = 0;  // HALO / GN: bytes per rank segment; KV: bytes per token row
   std::vector<std::array<void *, 2>> slot;  // [hosted rank][parity]
@@ -251,6 +252,16 @@ stadi_status u_publish(stadi_ctx *ctx, USite &S, int li, int ver, cudaStream_t s
   };
   int64_t off, bytes;
   seg(r.g, &off, &bytes);
+  if (ctx->ipc_mode) {  // one-sided: K/V rows were stored by the QKV epilogue
+    const bool nb = S.kind == US_HALO;  // halos go to the row neighbours only
+    if (S.kind == US_KV) {
+      ctx->exch_bytes += bytes * ctx->ipc->peers.size();
+    } else {
+      ST(ipc_war_wait(ctx, S.id, ver, nb, s));
+      ST(ipc_push(ctx, (const char *)S.slot[li][par] + off, (size_t)bytes, nb, s));
+    }
+    return ipc_ready(ctx, S.id, ver, nb, s);
+  }
   if (!ctx->nccl) {
     for (size_t lj = 0; lj < ctx->ranks.size(); ++lj) {
       if ((int)lj == li) continue;
@@ -282,9 +293,19 @@ stadi_status u_publish(stadi_ctx *ctx, USite &S, int li, int ver, cudaStream_t s
 }
 
 stadi_status u_wait(stadi_ctx *ctx, USite &S, int ver, cudaStream_t s) {
+  if (ctx->ipc_mode && !ctx->probe && ver >= 0)
+    return ipc_read_wait(ctx, S.id, ver, S.kind == US_HALO, s);
   if (!ctx->nccl || ver < 0) return STADI_OK;
-  if (S.used[ver & 1]) CK(cudaStreamWaitEvent(s, S.ev[ver & 1], 0));
+  if (S.used[ver & 1])
+    CK(timed(ctx, STADI_KCLASS_XWAIT, 0.0, 0.0, s,
+             [&] { return cudaStreamWaitEvent(s, S.ev[ver & 1], 0); }));
   return STADI_OK;
+}
+
+// IPC: after the consumer of site S, tell the sources this rank finished the step.
+stadi_status u_done(stadi_ctx *ctx, USite &S, cudaStream_t s) {
+  if (!ctx->ipc_mode || ctx->probe) return STADI_OK;
+  return ipc_read_done(ctx, S.id, (uint32_t)ctx->ipc_idx + 1, S.kind == US_HALO, s);
 }
 
 // ------------------------------------------------------------------ program builder
@@ -326,6 +347,7 @@ struct UBuilder {
 
   int add_site(int kind, int level, int C, int64_t seg_bytes) {
     USite S;
+    S.id = (int)U->sites.size();
     S.kind = kind;
     S.level = level;
     S.C = C;
@@ -387,7 +409,7 @@ struct UBuilder {
         return gn_apply<float>((const float *)X(), h, W, B, C, stats, G_, n_total, gw, gb, eps,
                                act, pad ? 1 : 0, (float *)D(), s);
       }));
-      return STADI_OK;
+      return u_done(ctx, S, s);
     });
   }
   static size_t esz_of(stadi_ctx *c) { return c->esz; }
@@ -482,6 +504,7 @@ struct UBuilder {
                          (size_t)B * C * ctx->esz, s));
       CK(cudaMemsetAsync((char *)D() + ((size_t)(h + 1) * (W + 2) + W + 1) * B * C * ctx->esz,
                          0, (size_t)B * C * ctx->esz, s));
+      ST(u_done(ctx, S, s));
       EpiParams ep{};
       ep.B = B;
       ep.bias = bias;
@@ -603,10 +626,16 @@ struct UBuilder {
         stadi_ctx *ctx = c;
         USite &S = ctx->un->sites[sid];
         if (st.pub_ver != st.read_ver) ST(u_wait(ctx, S, st.read_ver, s));
+        const bool ipcx = ctx->ipc_mode && !ctx->probe && st.pub_ver >= 0;
+        if (ipcx) ST(ipc_war_wait(ctx, S.id, st.pub_ver, false, s));
         EpiParams ep{};
         ep.B = B;
         ep.q = Q();
         ep.d = C;
+        if (ipcx) {  // the all-gather fused into the epilogue: P2P stores to the peers
+          ep.kv_peer = ipc_peer_slots(ctx, S.id, st.pub_ver & 1);
+          ep.n_kv_peer = ep.kv_peer ? (int)ctx->ipc->peers.size() : 0;
+        }
         ep.kv_a = S.slot[me][st.read_ver & 1];
         ep.kv_b = (st.pub_ver >= 0 && st.pub_ver != st.read_ver) ? S.slot[me][st.pub_ver & 1]
                                                                  : nullptr;
@@ -623,6 +652,7 @@ struct UBuilder {
         if (st.pub_ver == st.read_ver) ST(u_wait(ctx, S, st.read_ver, s));
         CK(attention_h(ctx, STADI_KCLASS_ATTN, Q(), S.slot[me][st.read_ver & 1], O(), ntok,
                        ntok_full, heads, C, s));
+        ST(u_done(ctx, S, s));
         EpiParams ep{};
         ep.B = B;
         ep.bias = bo;
@@ -793,10 +823,11 @@ void unet_free_plan(stadi_ctx *ctx) {
   for (auto &R : U->ranks)
     for (void *p : R.buf) pfree(ctx, p);
   for (auto &S : U->sites) {
-    for (auto &pr : S.slot) {
-      pfree(ctx, pr[0]);
-      pfree(ctx, pr[1]);
-    }
+    if (!ctx->ipc_mode)  // IPC: slots live in the persistent exchange arena
+      for (auto &pr : S.slot) {
+        pfree(ctx, pr[0]);
+        pfree(ctx, pr[1]);
+      }
     for (auto e : S.ev)
       if (e) cudaEventDestroy(e);
   }
@@ -823,6 +854,24 @@ stadi_status unet_set_plan(stadi_ctx *ctx) {
         CK(cudaMemsetAsync(R.buf[i], 0, R.size[i], ctx->astream));
       }
   const int n_inc = (int)U->inc.size();
+  if (ctx->ipc_mode) {  // every site's two slots in the IPC arena (identical layout on all ranks)
+    ipc_layout_begin(ctx);
+    IpcState &I = *ctx->ipc;
+    for (auto &S : U->sites) {
+      const int64_t bytes = S.kind == US_KV ? (int64_t)(m.lat_h >> S.level) *
+                                                  (m.lat_w >> S.level) * S.seg_bytes
+                                            : n_inc * S.seg_bytes;
+      for (int par = 0; par < 2; ++par) I.site_off[par].push_back(ipc_reserve(ctx, bytes));
+    }
+    ST(ipc_commit(ctx, (int)U->sites.size()));
+    for (auto &S : U->sites) {
+      S.slot.assign(ctx->ranks.size(), {nullptr, nullptr});
+      for (auto &pr : S.slot)
+        for (int par = 0; par < 2; ++par) pr[par] = I.arena + I.site_off[par][S.id];
+    }
+    CK(cudaStreamSynchronize(ctx->astream));
+    return STADI_OK;
+  }
   for (auto &S : U->sites) {
     int64_t bytes = S.kind == US_KV
                         ? (int64_t)(m.lat_h >> S.level) * (m.lat_w >> S.level) * S.seg_bytes
@@ -983,6 +1032,7 @@ stadi_status unet_run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cuda
   UNetState *U = ctx->un.get();
   if (phase.empty()) return STADI_OK;
   const size_t n = U->ranks[phase[0].li].prog.size();
+  ctx->ipc_idx = phase[0].idx;  // IPC mode: one hosted rank; its step index (done counts)
   for (size_t i = 0; i < n; ++i)
     for (const Part &P : phase) ST(U->ranks[P.li].prog[i](P.st, s));
   return STADI_OK;

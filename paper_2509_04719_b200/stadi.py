@@ -25,7 +25,8 @@ PRESET = {"tiny_dit": 0, "dit_xl2": 1, "pixart_alpha": 2, "sd15": 3, "sdxl": 4, 
 DTYPE_BF16, DTYPE_FP32_DEBUG = 0, 1
 SAMPLER_DDIM, SAMPLER_DDPM = 0, 1
 EPI_STORE, EPI_GELU, EPI_GATED_RES, EPI_RES, EPI_QKV, EPI_F32, EPI_CONV, EPI_GEGLU = range(8)
-KCLASS = {"gemm": 0, "attn": 1, "xattn": 2, "norm": 3, "sampler": 4}
+KCLASS = {"gemm": 0, "attn": 1, "xattn": 2, "norm": 3, "sampler": 4, "xwait": 5}
+TRANSPORT_NCCL, TRANSPORT_IPC = 0, 1
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE",
           6: "EUNSUPPORTED"}
 
@@ -80,7 +81,8 @@ class ModelDesc(C.Structure):
 
 class DistDesc(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
-                ("n_local", C.c_int32), ("nccl_id", C.POINTER(C.c_uint8))]
+                ("n_local", C.c_int32), ("nccl_id", C.POINTER(C.c_uint8)),
+                ("transport", C.c_int32)]
 
 
 class Cond(C.Structure):
@@ -109,6 +111,7 @@ EXPORTS = [
     "stadi_load_weights", "stadi_profile_warmup", "stadi_set_plan", "stadi_begin",
     "stadi_num_steps", "stadi_denoise_step", "stadi_gather", "stadi_run",
     "stadi_emulator_start", "stadi_emulator_stop", "stadi_nccl_unique_id",
+    "stadi_ipc_session_id",
     "stadi_kernel_timing", "stadi_kernel_stats",
     "stadi_k_gemm", "stadi_k_gemm_ex", "stadi_k_attention", "stadi_k_ln_modulate",
     "stadi_k_conv3x3", "stadi_k_conv3x3_ex",
@@ -146,6 +149,7 @@ def _load():
         "stadi_emulator_start": (C.c_int, [vp, C.c_uint32]),
         "stadi_emulator_stop": (C.c_int, [vp]),
         "stadi_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+        "stadi_ipc_session_id": (C.c_int, [C.POINTER(C.c_uint8)]),
         "stadi_kernel_timing": (C.c_int, [vp, C.c_int32]),
         "stadi_kernel_stats": (C.c_int, [vp, C.c_int32, C.POINTER(C.c_uint64),
                                          C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -261,17 +265,24 @@ def nccl_unique_id() -> bytes:
     return bytes(b)
 
 
+def ipc_session_id() -> bytes:
+    b = (C.c_uint8 * 128)()
+    _check(lib.stadi_ipc_session_id(b))
+    return bytes(b)
+
+
 class Context:
     """One stadi_ctx (one process; hosts one rank or n_local ranks on one device)."""
 
-    def __init__(self, desc: ModelDesc, rank=0, world=1, device=0, n_local=1, nccl_id=None):
+    def __init__(self, desc: ModelDesc, rank=0, world=1, device=0, n_local=1, nccl_id=None,
+                 transport=TRANSPORT_NCCL):
         self._keep = []
         nid = None
         if nccl_id is not None:
             nb = (C.c_uint8 * 128)(*nccl_id)
             self._keep.append(nb)
             nid = C.cast(nb, C.POINTER(C.c_uint8))
-        dd = DistDesc(rank, world, device, n_local, nid)
+        dd = DistDesc(rank, world, device, n_local, nid, transport)
         h = C.c_void_p()
         _check(lib.stadi_create(C.byref(desc), C.byref(dd), C.byref(h)))
         self.h = h

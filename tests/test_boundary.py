@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol(S):
     for name in declared:
         assert hasattr(S.lib, name), name
     assert declared <= set(S.EXPORTS)
-    assert S.lib.stadi_abi_version() == 2
+    assert S.lib.stadi_abi_version() == 3
 
 
 def _oracle_plan(speed, mb, mw, P, rpu, flags, forced=None):
