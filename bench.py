@@ -363,6 +363,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--occupancy", default="half50")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="N > 1 exchange transport (IPC: fused one-sided P2P, the default)")
     ap.add_argument("--no-uniform", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -419,14 +421,19 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- context (NCCL communicator of the library, id through torch.distributed)
+    # ---- context.  N > 1: the IPC transport by default (one-sided: the QKV epilogue
+    # stores K/V straight into the peers' slots over NVLink, flags by stream memory
+    # ops), or the library's NCCL communicator (--transport nccl); the 128-byte
+    # session / unique id goes through torch.distributed
     nid = None
+    transport = S.TRANSPORT_IPC if args.transport == "ipc" else S.TRANSPORT_NCCL
     if world > 1:
-        obj = [S.nccl_unique_id() if rank == 0 else None]
+        obj = [(S.ipc_session_id() if transport == S.TRANSPORT_IPC else S.nccl_unique_id())
+               if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     desc = S.model_desc(wl["model"], S.DTYPE_BF16)
-    ctx = S.Context(desc, rank=rank, world=world, device=local, nccl_id=nid)
+    ctx = S.Context(desc, rank=rank, world=world, device=local, nccl_id=nid, transport=transport)
     W = gen.weights(cfg)
     ctx.load_weights([W[n] for n, _, _ in configs.manifest(cfg)])
     del W
@@ -608,7 +615,8 @@ def main():
                        "plan": _plan_json(plan),
                        "l2": "inputs larger than L2: the K/V slots + bf16 weights streamed per "
                              "image exceed the 126 MB L2 (C5: 8.5 GB + 1.3 GB)",
-                       "parallelism": f"stadi-patch{world}"},
+                       "parallelism": f"stadi-patch{world}",
+                       "transport": args.transport if world > 1 else "none"},
             "uniform_pp": uni, "e2e": e2e, "roofline": roof, "path_roofline": path_roof,
             "kernels": kernels,
             "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(launches),

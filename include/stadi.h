@@ -240,6 +240,7 @@ typedef struct {
   uint64_t exchange_bytes;   /* bytes this process sent in exchange rounds       */
   uint32_t kernel_launches;  /* kernels this process launched for the request    */
   uint32_t steps_run;        /* program steps executed                           */
+  uint32_t graph_steps;      /* of which replayed from per-step CUDA graphs      */
 } stadi_run_stats;
 
 stadi_status stadi_create(const stadi_model_desc *model, const stadi_dist_desc *dist,

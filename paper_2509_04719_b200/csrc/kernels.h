@@ -75,8 +75,13 @@ cudaError_t pixart_mods(const float *t0, const float *temb, const float *sst_all
 
 // ---- U-Net band kernels (unet_ops.cu): X = [h, W, B, C] fp32 token-major,
 // P = [h+2, W+2, B, C] halo-padded conv input (see unet_ops.cu) --------------
-// GroupNorm partial sums of the band: out[b][g][{S1, S2}] (fp64, zeroed first).
-cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, cudaStream_t s);
+// GroupNorm partial sums of the band: out[b][g][{S1, S2}] (fp64), reduced across
+// blocks in a fixed order (bitwise reproducible): ws = GN_PARTIAL_BLOCKS * 2 * B * 32
+// doubles of workspace, ticket = one zero-initialised unsigned (reset by the kernel);
+// one (ws, ticket) pair per stream.
+constexpr int GN_PARTIAL_BLOCKS = 592;
+cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, double *ws,
+                        unsigned *ticket, cudaStream_t s);
 // GroupNorm with the statistics summed over G rank segments [G][B][32][2]
 // (stats == null: plain cast), optional SiLU, pad = write into P's interior.
 template <typename T>

@@ -824,18 +824,23 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
   }
 }
 
-// STADI_ATTN_TOK=0: the two softmax groups' exp phases are not serialised by tokens;
+// Run-time switches (A/B measurements, C5 shape 16384 x 16384, hd 72, B200, round 2
+// tools/gpu_attn_env.sh): exp-phase tokens per group 787 TFLOP/s, no tokens 807, per-SMSP
+// tokens (the two warps of a group on one sub-partition hand the MUFU to the other
+// group's two warps there) 816; MMA order S_0(j+1), PV_1(j-1), S_1(j+1), PV_0(j) +1%.
+// Defaults: per-SMSP tokens + that MMA order.
+// STADI_ATTN_TOK=1: per-group tokens instead (TOK=0 together with TOK4=0: none);
+// STADI_ATTN_TOK4=0: no per-SMSP tokens;
 // STADI_ATTN_DEFER=0: wait for PV(j-1) before the rescale check, not before the P store;
-// STADI_ATTN_ORDER=1: MMA issue order S_0(j+1), PV_1(j-1), S_1(j+1), PV_0(j) instead of
-// S_0(j+1), S_1(j+1), PV_0(j), PV_1(j) (measured 0.5% slower);
-// STADI_ATTN_TOK4=1: per-SMSP exp-phase tokens
+// STADI_ATTN_ORDER=0: MMA issue order S_0(j+1), S_1(j+1), PV_0(j), PV_1(j).
 int attn_flags() {
   static const int v = [] {
     const char *e = getenv("STADI_ATTN_TOK"), *d = getenv("STADI_ATTN_DEFER"),
                *o = getenv("STADI_ATTN_ORDER");
     const char *t4 = getenv("STADI_ATTN_TOK4");
-    return ((e && e[0] == '0') ? 0 : 1) | ((d && d[0] == '0') ? 0 : 2) |
-           ((o && o[0] == '1') ? 4 : 0) | ((t4 && t4[0] == '1') ? 8 : 0);
+    const bool tok4 = !(t4 && t4[0] == '0');
+    return ((e && e[0] == '1') ? 1 : 0) | ((d && d[0] == '0') ? 0 : 2) |
+           ((o && o[0] == '0') ? 0 : 4) | (tok4 && !(e && e[0] == '1') ? 8 : 0);
   }();
   return v;
 }

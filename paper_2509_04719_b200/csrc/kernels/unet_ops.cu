@@ -19,14 +19,19 @@ namespace {
 constexpr int GN_G = 32;
 
 // ------------------------------------------------------------- GN partials
-// out[b][g][0] += sum x, out[b][g][1] += sum x^2 over the band.  One block = a
-// chunk of rows; thread t owns float4 channel vector t % nvec of row slots
-// t / nvec (all 256 threads busy when nvec < 256), fp32 per thread, reduced in
-// smem per (b, channel), then per (b, group) with fp64 atomics across blocks.
+// out[b][g][0] = sum x, out[b][g][1] = sum x^2 over the band, DETERMINISTIC: one
+// block = a chunk of rows; thread t owns float4 channel vector t % nvec of row
+// slots t / nvec (all 256 threads busy when nvec < 256), fp32 per thread, reduced
+// in smem per (b, channel), then per (b, group) in fp64 into the block's own
+// workspace row; the last block to finish (atomic ticket) sums the rows in block
+// order and resets the ticket -- the same bits on every run (no fp64 atomics).
 __global__ void __launch_bounds__(256) gn_partials_kernel(const float *__restrict__ x, long M,
                                                           int B, int C, int rows_per_block,
+                                                          double *__restrict__ ws,
+                                                          unsigned *__restrict__ ticket,
                                                           double *__restrict__ out) {
   extern __shared__ float sm[];  // [2 stats][slots][B][C]
+  __shared__ bool last;
   const int nvec = C / 4;
   const int slots = nvec >= 256 ? 1 : 256 / nvec;
   const long r0 = (long)blockIdx.x * rows_per_block;
@@ -54,14 +59,26 @@ __global__ void __launch_bounds__(256) gn_partials_kernel(const float *__restric
     }
   }
   __syncthreads();
-  const int cg = C / GN_G;
-  for (int jj = threadIdx.x; jj < 2 * B * GN_G; jj += blockDim.x) {
+  const int cg = C / GN_G, nst = 2 * B * GN_G;
+  for (int jj = threadIdx.x; jj < nst; jj += blockDim.x) {
     const int st = jj / (B * GN_G), b = (jj / GN_G) % B, g = jj % GN_G;
-    float acc = 0.f;
+    double acc = 0.0;
     for (int sl = 0; sl < slots; ++sl)
-      for (int c = 0; c < cg; ++c) acc += sm[((st * slots + sl) * B + b) * C + g * cg + c];
-    atomicAdd(out + ((long)b * GN_G + g) * 2 + st, (double)acc);
+      for (int c = 0; c < cg; ++c) acc += (double)sm[((st * slots + sl) * B + b) * C + g * cg + c];
+    ws[(long)blockIdx.x * nst + ((long)b * GN_G + g) * 2 + st] = acc;
   }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int jj = threadIdx.x; jj < nst; jj += blockDim.x) {
+    double acc = 0.0;
+    for (unsigned k = 0; k < gridDim.x; ++k) acc += __ldcg(ws + (long)k * nst + jj);
+    out[jj] = acc;
+  }
+  if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
 }
 
 // ------------------------------------------------------------- GN apply
@@ -226,17 +243,17 @@ inline unsigned grid_for(long work, int per_block = 256) {
 
 }  // namespace
 
-cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, cudaStream_t s) {
+cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, double *ws,
+                        unsigned *ticket, cudaStream_t s) {
   if (C % (4 * GN_G) && C % 4) return cudaErrorInvalidValue;
-  if (B > 2 || C % 4 || C % GN_G) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(out, 0, (size_t)B * GN_G * 2 * sizeof(double), s);
-  if (e != cudaSuccess || M == 0) return e;
-  const int blocks = (int)std::min<long>(592, M);
+  if (B > 2 || C % 4 || C % GN_G || !ws || !ticket) return cudaErrorInvalidValue;
+  if (M == 0) return cudaMemsetAsync(out, 0, (size_t)B * GN_G * 2 * sizeof(double), s);
+  const int blocks = (int)std::min<long>(GN_PARTIAL_BLOCKS, M);
   int rpb = (int)((M + blocks - 1) / blocks);
   const int nb = (int)((M + rpb - 1) / rpb);
   const int nvec = C / 4, slots = nvec >= 256 ? 1 : 256 / nvec;
   const size_t smem = (size_t)2 * slots * B * C * sizeof(float);
-  gn_partials_kernel<<<nb, 256, smem, s>>>(x, M, B, C, rpb, out);
+  gn_partials_kernel<<<nb, 256, smem, s>>>(x, M, B, C, rpb, ws, ticket, out);
   ++g_launches;
   return cudaGetLastError();
 }

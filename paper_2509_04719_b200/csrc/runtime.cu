@@ -116,6 +116,7 @@ struct stadi_ctx {
   std::unique_ptr<IpcState> ipc;
   bool probe = false;        // profiling probe steps: no exchange waits / signals
   int ipc_idx = 0;           // IPC mode: step-table index of the step being built / run
+  uint32_t graph_steps = 0;  // steps replayed from CUDA graphs (stats of stadi_run)
   int num_sms = 148;
   std::string err;
   bool poisoned = false;
@@ -1291,6 +1292,7 @@ stadi_status exec_step(stadi_ctx *ctx, uint32_t i, cudaStream_t s) {
     G.emu_ctas = ctx->emu_ctas;
   }
   CK(cudaGraphLaunch(G.exec, s));
+  ++ctx->graph_steps;
   g_launches += G.launches;
   ctx->exch_bytes += G.exch_bytes;
   return STADI_OK;
@@ -1365,6 +1367,7 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
   CK(cudaEventCreate(&e1));
   const unsigned long long l0 = g_launches;
   CK(collect_timing(ctx));  // (no-op unless timing) so the exchange-wait delta is this request's
+  ctx->graph_steps = 0;
   const double w0 = ctx->kt[STADI_KCLASS_XWAIT].ms;
   CK(cudaEventRecord(e0, s));
   ST(stadi_begin(ctx, noise_full, cond, stream));
@@ -1383,6 +1386,7 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
     stats->exchange_bytes = ctx->exch_bytes;
     stats->kernel_launches = (uint32_t)(g_launches - l0);
     stats->steps_run = (uint32_t)ctx->program.size();
+    stats->graph_steps = ctx->graph_steps;
   }
   return STADI_OK;
 }

@@ -63,6 +63,8 @@ struct UNetState {
   void *tsilu = nullptr;
   std::vector<void *> text_kv;        // per transformer block [L, B, 2, C]
   int cap_nt = 0;
+  double *gn_ws = nullptr;            // fixed-order GN partial reduction (one stream at a time)
+  unsigned *gn_ticket = nullptr;
 };
 
 inline int64_t rup64(int64_t a) { return (a + 63) / 64 * 64; }
@@ -215,6 +217,9 @@ stadi_status unet_load_weights(stadi_ctx *ctx, const float *const *host) {
       CK(upload_vec(ctx, vec(n), &U->wf[n]));
     }
   }
+  CK(dalloc(ctx, &U->gn_ws, (size_t)GN_PARTIAL_BLOCKS * 2 * 2 * 32 * sizeof(double)));
+  CK(dalloc(ctx, &U->gn_ticket, 256));
+  CK(cudaMemset(U->gn_ticket, 0, 256));
   CK(upload_gemm(ctx, temb_w, &U->wt["temb_all.w"]));
   CK(upload_vec(ctx, temb_b, &U->wf["temb_all.b"]));
   (void)m;
@@ -382,8 +387,10 @@ struct UBuilder {
       stadi_ctx *ctx = c;
       USite &S = ctx->un->sites[sid];
       const int pos = inc_pos(ctx->un.get(), ctx->ranks[me].g);
-      CK(timed(ctx, STADI_KCLASS_NORM, 0.0, (double)Ml * C * 4, s,
-               [&] { return gn_partials((const float *)X(), Ml, B, C, (double *)G(), s); }));
+      CK(timed(ctx, STADI_KCLASS_NORM, 0.0, (double)Ml * C * 4, s, [&] {
+        return gn_partials((const float *)X(), Ml, B, C, (double *)G(), ctx->un->gn_ws,
+                           ctx->un->gn_ticket, s);
+      }));
       if (st.pub_ver != st.read_ver) ST(u_wait(ctx, S, st.read_ver, s));
       const int64_t off = pos * S.seg_bytes;
       CK(cudaMemcpyAsync((char *)S.slot[me][st.read_ver & 1] + off, G(), S.seg_bytes,

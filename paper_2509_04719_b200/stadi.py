@@ -94,7 +94,7 @@ class Cond(C.Structure):
 class RunStats(C.Structure):
     _fields_ = [("ms_total", C.c_double), ("ms_exchange_wait", C.c_double),
                 ("exchange_bytes", C.c_uint64), ("kernel_launches", C.c_uint32),
-                ("steps_run", C.c_uint32)]
+                ("steps_run", C.c_uint32), ("graph_steps", C.c_uint32)]
 
 
 class KEpi(C.Structure):

@@ -48,7 +48,8 @@ def main():
             outs.append(out)
             stats.append(dict(ms_total=st.ms_total, ms_exchange_wait=st.ms_exchange_wait,
                               exchange_bytes=st.exchange_bytes,
-                              kernel_launches=st.kernel_launches, steps_run=st.steps_run))
+                              kernel_launches=st.kernel_launches, steps_run=st.steps_run,
+                              graph_steps=st.graph_steps))
         np.save(os.path.join(out_dir, f"rank{rank}.npy"), np.stack(outs))
         with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
             json.dump(dict(stats=stats, plan=p.to_dict(), probe_ms=ms), f)

@@ -113,8 +113,9 @@ def test_ipc_multiprocess(S, case):
     inc = [r for r in range(world) if plan["tier"][r]]
     xb = [m["stats"][-1]["exchange_bytes"] for m in meta]
     wt = [round(m["stats"][-1]["ms_exchange_wait"], 3) for m in meta]
+    gs = [m["stats"][1]["graph_steps"] for m in meta]     # second request: graph replays
     print(f"IPC {cid}: {world} processes on one GPU, steps={plan['steps']} rows={plan['rows']} "
-          f"max-abs-rel={err:.3e} exchange_bytes={xb} exchange_wait_ms={wt}")
+          f"max-abs-rel={err:.3e} exchange_bytes={xb} exchange_wait_ms={wt} graph_steps={gs}")
     assert err <= TOL[dtype]
     for r in inc:
         if len(inc) > 1:
