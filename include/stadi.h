@@ -215,6 +215,17 @@ typedef struct {
   const uint8_t *nccl_id;    /* 128 bytes from rank 0 when world > 1: the
                                 ncclUniqueId (NCCL) or the session id (IPC)      */
   int32_t transport;         /* STADI_TRANSPORT_* (world > 1)                    */
+  int32_t vgpu_sms;          /* 0: the whole device.  > 0 (multiple of 8): a
+                                VIRTUAL GPU -- every kernel of the context runs in
+                                green-context SM partition number `rank` of this
+                                many SMs (disjoint per rank), so several contexts
+                                of one process, one per host thread, compute a
+                                multi-rank request concurrently on one device
+                                (IPC transport between them; HBM / L2 shared).
+                                A NULL stream argument then means the context's
+                                own stream (the legacy stream is not joined: it
+                                is shared by all threads of the process).
+                                EUNSUPPORTED if the partition does not fit       */
 } stadi_dist_desc;
 
 typedef struct {

@@ -293,10 +293,18 @@ stadi_status ipc_commit(stadi_ctx *ctx, int n_sites) {
   }
   CK(cudaMemsetAsync(I.arena, 0, I.used, ctx->astream));
   CK(cudaStreamSynchronize(ctx->astream));
-  cudaIpcMemHandle_t h;
-  CK(cudaIpcGetMemHandle(&h, I.arena));
+  // record: IPC handle, pid, arena pointer (ranks of the SAME process -- virtual GPUs,
+  // green.cuh -- use the pointer directly: a process cannot open its own handles)
+  struct Rec {
+    cudaIpcMemHandle_t h;
+    int64_t pid;
+    uint64_t ptr;
+  } rec{};
+  CK(cudaIpcGetMemHandle(&rec.h, I.arena));
+  rec.pid = (int64_t)getpid();
+  rec.ptr = (uint64_t)(uintptr_t)I.arena;
   std::vector<std::string> all;
-  ST(rdv_allgather(ctx, "arena", std::string((const char *)&h, sizeof(h)), all));
+  ST(rdv_allgather(ctx, "arena", std::string((const char *)&rec, sizeof(rec)), all));
   I.peer.resize(Gw, nullptr);
   I.peer_handle.resize(Gw);
   for (int g = 0; g < Gw; ++g) {
@@ -304,16 +312,20 @@ stadi_status ipc_commit(stadi_ctx *ctx, int n_sites) {
       I.peer[g] = I.arena;
       continue;
     }
-    if (all[g].size() != sizeof(h)) return ctx_fail(ctx, STADI_ESTATE, "IPC: bad handle");
+    if (all[g].size() != sizeof(Rec)) return ctx_fail(ctx, STADI_ESTATE, "IPC: bad handle");
     if (I.peer[g] && I.peer_handle[g] == all[g]) continue;  // unchanged mapping
+    Rec pr;
+    std::memcpy(&pr, all[g].data(), sizeof(pr));
+    I.peer_handle[g] = all[g];
+    if (pr.pid == rec.pid) {  // same process: the pointer is valid here
+      I.peer[g] = (char *)(uintptr_t)pr.ptr;
+      continue;
+    }
     // a replaced peer mapping stays open (closing may synchronise); closed at destroy
     if (I.peer[g]) I.opened.push_back(I.peer[g]);
     void *p = nullptr;
-    cudaIpcMemHandle_t ph;
-    std::memcpy(&ph, all[g].data(), sizeof(ph));
-    CK(cudaIpcOpenMemHandle(&p, ph, cudaIpcMemLazyEnablePeerAccess));
+    CK(cudaIpcOpenMemHandle(&p, pr.h, cudaIpcMemLazyEnablePeerAccess));
     I.peer[g] = (char *)p;
-    I.peer_handle[g] = all[g];
   }
   I.peers.clear();
   for (uint32_t g = 0; g < ctx->plan.n_gpus; ++g)
@@ -398,8 +410,11 @@ stadi_status ipc_gather(stadi_ctx *ctx, float *out_full, bool dev, cudaStream_t 
     if (ctx->plan.tier[g] && (int)g != ctx->rank)
       CKD(memops().wait32((CUstream)s, flag_at(I.arena, I.off_gflag, g), 1,
                           CU_STREAM_WAIT_VALUE_GEQ));
-  CK(cudaMemcpyAsync(out_full, I.arena + I.off_gather, (size_t)m.lat_h * row,
-                     dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  if (dev)
+    CK(cudaMemcpyAsync(out_full, I.arena + I.off_gather, (size_t)m.lat_h * row,
+                       cudaMemcpyDeviceToDevice, s));
+  else
+    CK(stage_d2h(ctx, out_full, I.arena + I.off_gather, (size_t)m.lat_h * row, s));
   return STADI_OK;
 }
 
@@ -440,12 +455,19 @@ bool ipc_probe_graphs(stadi_ctx *ctx) {
 void ipc_release(stadi_ctx *ctx) {  // destroy (device already synchronised)
   if (!ctx->ipc) return;
   IpcState &I = *ctx->ipc;
-  for (int g = 0; g < (int)I.peer.size(); ++g)
-    if (g != ctx->rank && I.peer[g]) cudaIpcCloseMemHandle(I.peer[g]);
+  const int64_t me = (int64_t)getpid();
+  for (int g = 0; g < (int)I.peer.size(); ++g) {
+    if (g == ctx->rank || !I.peer[g] || I.peer_handle[g].size() < sizeof(cudaIpcMemHandle_t) + 8)
+      continue;
+    int64_t pid;
+    std::memcpy(&pid, I.peer_handle[g].data() + sizeof(cudaIpcMemHandle_t), 8);
+    if (pid != me) cudaIpcCloseMemHandle(I.peer[g]);  // in-process peers were not opened
+  }
   for (char *p : I.opened) cudaIpcCloseMemHandle(p);
   if (I.arena) cudaFree(I.arena);
   for (char *p : I.retired) cudaFree(p);
-  if (!I.last_file.empty()) std::remove(I.last_file.c_str());
+  // the last rendezvous file stays: a slower peer may not have read it yet (the
+  // files of earlier rounds are removed as the protocol goes, see rdv_allgather)
   ctx->ipc.reset();
 }
 

@@ -159,6 +159,18 @@ struct stadi_ctx {
   std::vector<void *> kv_text;
   double abar[1000];
 
+  // virtual GPU (green-context SM partition, green.cuh): every kernel goes to wstream
+  CUgreenCtx green_ctx = nullptr;
+  cudaStream_t wstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  // pinned staging of a request's host <-> device copies (stage_h2d / stage_d2h): no
+  // copy from pageable memory, whose implicit synchronisation could wait for another
+  // rank's stream (virtual GPUs of one process) or stall the host thread
+  char *stage = nullptr;
+  size_t stage_cap = 0, stage_off = 0;
+  cudaEvent_t stage_ev = nullptr;
+  bool stage_pending = false;
+
   // streams / NCCL
   cudaStream_t comm = nullptr;
   cudaStream_t astream = nullptr;      // stream-ordered plan / request allocations
@@ -203,6 +215,20 @@ struct stadi_ctx {
 };
 
 namespace {
+
+// STADI_DEBUG=1: progress trace of the request calls on stderr (hang diagnostics)
+bool debug_on() {
+  static const bool v = getenv("STADI_DEBUG") != nullptr;
+  return v;
+}
+#define DBG(...)                                                                         \
+  do {                                                                                   \
+    if (debug_on()) {                                                                    \
+      fprintf(stderr, "[stadi r%d] ", ctx->rank);                                        \
+      fprintf(stderr, __VA_ARGS__);                                                      \
+      fprintf(stderr, "\n");                                                             \
+    }                                                                                    \
+  } while (0)
 
 stadi_status ctx_fail(stadi_ctx *c, stadi_status st, const char *fmt, ...) {
   char buf[1024];
@@ -268,6 +294,7 @@ cudaError_t quiesce(stadi_ctx *ctx) {
   if (e == cudaSuccess && ctx->comm) e = cudaStreamSynchronize(ctx->comm);
   if (e == cudaSuccess) e = cudaStreamSynchronize(0);
   if (e == cudaSuccess && ctx->astream) e = cudaStreamSynchronize(ctx->astream);
+  if (e == cudaSuccess && ctx->wstream) e = cudaStreamSynchronize(ctx->wstream);
   return e;
 }
 
@@ -288,6 +315,64 @@ bool is_device_ptr(const void *p) {
     return false;
   }
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+bool is_pageable(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+// ---------------------------------------------------------------- host staging
+// A request's staged copies go through one pinned buffer (sized at create); begin
+// waits for the previous request's staged copies, then reuses it from the start.
+cudaError_t stage_reset(stadi_ctx *ctx) {
+  if (ctx->stage_pending) {
+    cudaError_t e = cudaEventSynchronize(ctx->stage_ev);
+    if (e != cudaSuccess) return e;
+  }
+  ctx->stage_pending = false;
+  ctx->stage_off = 0;
+  return cudaSuccess;
+}
+char *stage_take(stadi_ctx *ctx, size_t bytes) {
+  const size_t off = (ctx->stage_off + 255) / 256 * 256;
+  if (off + bytes > ctx->stage_cap) return nullptr;
+  ctx->stage_off = off + bytes;
+  return ctx->stage + off;
+}
+// Source pointer for an async host->device copy of `bytes` at src: src itself when it
+// is device or pinned memory, else a pinned copy (nullptr: staging exhausted).
+const void *stage_h2d(stadi_ctx *ctx, const void *src, size_t bytes) {
+  if (!is_pageable(src)) return src;
+  char *p = stage_take(ctx, bytes);
+  if (p) std::memcpy(p, src, bytes);
+  return p;
+}
+struct D2HCopy {
+  void *dst;
+  const void *src;
+  size_t bytes;
+};
+void CUDART_CB d2h_finish(void *arg) {  // stream-ordered host copy out of the staging
+  D2HCopy *c = static_cast<D2HCopy *>(arg);
+  std::memcpy(c->dst, c->src, c->bytes);
+  delete c;
+}
+// Stream-ordered device->host copy into dst (pinned or pageable).
+cudaError_t stage_d2h(stadi_ctx *ctx, void *dst, const void *src_dev, size_t bytes,
+                      cudaStream_t s) {
+  if (!is_pageable(dst))
+    return cudaMemcpyAsync(dst, src_dev, bytes, cudaMemcpyDeviceToHost, s);
+  char *p = stage_take(ctx, bytes);
+  if (!p) return cudaErrorMemoryAllocation;
+  cudaError_t e = cudaMemcpyAsync(p, src_dev, bytes, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaLaunchHostFunc(s, d2h_finish, new D2HCopy{dst, p, bytes});
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->stage_ev, s);
+  ctx->stage_pending = true;
+  return e;
 }
 
 // ---------------------------------------------------------------- host math (fp64)
@@ -436,6 +521,7 @@ void free_graphs(stadi_ctx *ctx);
 }  // namespace
 
 #include "ipc.cuh"
+#include "green.cuh"
 #include "unet_exec.cuh"
 
 namespace {
@@ -579,9 +665,14 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dist->device));
     int lo, hi;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi));
-    CK(cudaStreamCreateWithFlags(&ctx->astream, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+    if (dist->vgpu_sms > 0) {  // virtual GPU: an SM partition of the device (green.cuh)
+      if (dist->n_local != 1) return ctx_fail(ctx, STADI_EINVAL, "vgpu_sms needs n_local == 1");
+      ST(green_init(ctx, dist->rank, dist->vgpu_sms, hi));
+    } else {
+      CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi));
+      CK(cudaStreamCreateWithFlags(&ctx->astream, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+    }
     CK(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
     // positional embedding of the full token grid, fp64 on the host (pins the
     // values to 1 ulp of fp32), [sin(c w), cos(c w), sin(r w), cos(r w)]
@@ -655,12 +746,23 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
       CK(cudaMemset(I.probe, 0, 256));
       I.graphs_ok = ipc_probe_graphs(ctx);
     }
+    {  // pinned staging: noise + result + text + pooled + time features + small items
+      const size_t lat = (size_t)dm.lat_h * dm.lat_w * dm.c_in * 4;
+      const size_t txt = (size_t)dm.B * dm.txt_len * dm.txt_dim * 4;
+      const size_t tf = (size_t)1000 * std::max(256, dm.unet ? dm.ch[0] : 256) * 4;
+      ctx->stage_cap = 2 * lat + txt + (size_t)dm.B * (dm.pooled_dim + 6 * 256 + 64) * 4 + tf +
+                       (64 << 10);
+      CK(cudaMallocHost(&ctx->stage, ctx->stage_cap));
+      CK(cudaEventCreateWithFlags(&ctx->stage_ev, cudaEventDisableTiming));
+    }
     CK(dalloc(ctx, &ctx->seed_dev, 8));
     CK(cudaMemset(ctx->seed_dev, 0, 8));
     CK(cudaMalloc(&ctx->emu_flag_dev, 64));
     CK(cudaMemset(ctx->emu_flag_dev, 0, 64));
-    CK(cudaStreamCreateWithFlags(&ctx->emu_stream, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&ctx->emu_ctl, cudaStreamNonBlocking));
+    if (!ctx->green_ctx) {
+      CK(cudaStreamCreateWithFlags(&ctx->emu_stream, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&ctx->emu_ctl, cudaStreamNonBlocking));
+    }
   }
   *out = ctx.release();
   return STADI_OK;
@@ -685,6 +787,12 @@ extern "C" void stadi_destroy(stadi_ctx *ctx) {
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   if (ctx->emu_stream) cudaStreamDestroy(ctx->emu_stream);
   if (ctx->emu_ctl) cudaStreamDestroy(ctx->emu_ctl);
+  if (ctx->wstream) cudaStreamDestroy(ctx->wstream);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->stage_ev) cudaEventDestroy(ctx->stage_ev);
+  if (ctx->stage) cudaFreeHost(ctx->stage);
+  if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+  if (ctx->green_ctx && green_api().GreenCtxDestroy) green_api().GreenCtxDestroy(ctx->green_ctx);
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
   for (auto &k : ctx->kt)
     for (auto &pr : k.ev) {
@@ -809,7 +917,9 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
                     plan->p_total, plan->rows_per_unit, m.lat_h, unit);
   if (plan->m_base > 1000) return ctx_fail(ctx, STADI_EINVAL, "M_base > 1000");
   CK(cudaSetDevice(ctx->device));
+  DBG("set_plan: quiesce");
   CK(quiesce(ctx));
+  DBG("set_plan: quiesced");
   free_plan_buffers(ctx);
   ctx->plan = *plan;
   const int g0 = ctx->rank * ctx->n_local;
@@ -899,8 +1009,35 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
 }
 
 // ---------------------------------------------------------------- request begin
+namespace {
+stadi_status begin_impl(stadi_ctx *ctx, const float *noise_full, const stadi_cond *cond,
+                        void *stream);
+stadi_status gather_impl(stadi_ctx *ctx, float *out_full, void *stream);
+}  // namespace
+
+// Public entry points: (virtual GPU) the work runs on the context's green stream,
+// joined after / before the caller's stream.
 extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
                                     const stadi_cond *cond, void *stream) {
+  ALIVE();
+  cudaStream_t w;
+  CK(enter_stream(ctx, (cudaStream_t)stream, &w));
+  ST(begin_impl(ctx, noise_full, cond, w));
+  CK(leave_stream(ctx, (cudaStream_t)stream));
+  return STADI_OK;
+}
+extern "C" stadi_status stadi_gather(stadi_ctx *ctx, float *out_full, void *stream) {
+  ALIVE();
+  cudaStream_t w;
+  CK(enter_stream(ctx, (cudaStream_t)stream, &w));
+  ST(gather_impl(ctx, out_full, w));
+  CK(leave_stream(ctx, (cudaStream_t)stream));
+  return STADI_OK;
+}
+
+namespace {
+stadi_status begin_impl(stadi_ctx *ctx, const float *noise_full, const stadi_cond *cond,
+                        void *stream) {
   ALIVE();
   if (!ctx->has_plan) return ctx_fail(ctx, STADI_ESTATE, "stadi_begin before stadi_set_plan");
   if (!ctx->weights_loaded) return ctx_fail(ctx, STADI_ESTATE, "weights not loaded");
@@ -911,17 +1048,23 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(ctx->device));
   ctx->ddpm_seed = cond->ddpm_seed;
-  // the sampler reads the key from device memory (graph replays see this request's
-  // seed); the host copy stays alive in ctx until the stream has consumed it
-  CK(cudaMemcpyAsync(ctx->seed_dev, &ctx->ddpm_seed, 8, cudaMemcpyHostToDevice, s));
+  CK(stage_reset(ctx));
+  // the sampler reads the key from device memory (graph replays see this request's seed)
+  CK(cudaMemcpyAsync(ctx->seed_dev, stage_h2d(ctx, &ctx->ddpm_seed, 8), 8,
+                     cudaMemcpyHostToDevice, s));
   // noise bands
   const bool dev = is_device_ptr(noise_full);
   const size_t row_bytes = (size_t)m.lat_w * m.c_in * 4;
-  for (auto &r : ctx->ranks)
-    CK(cudaMemcpyAsync(r.x_band, noise_full + (size_t)r.row_begin * m.lat_w * m.c_in,
-                       row_bytes * r.rows, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                       s));
+  for (auto &r : ctx->ranks) {
+    const float *src = noise_full + (size_t)r.row_begin * m.lat_w * m.c_in;
+    const void *st = dev ? src : stage_h2d(ctx, src, row_bytes * r.rows);
+    if (!st) return ctx_fail(ctx, STADI_ENOMEM, "host staging exhausted");
+    CK(cudaMemcpyAsync(r.x_band, st, row_bytes * r.rows,
+                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  }
+  DBG("begin: noise copied");
   if (ctx->ipc_mode) ST(ipc_begin(ctx, s));  // flag reset + device-side barrier
+  DBG("begin: barrier enqueued");
   // ---- conditioning for every fast-grid timestep (one batched GEMM each)
   const int nt = (int)ctx->plan.m_base;
   const int64_t d = m.d;
@@ -946,6 +1089,8 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
   ctx->n_t = nt;
   if (m.unet) {
     ST(unet_begin(ctx, cond, s));
+    CK(cudaEventRecord(ctx->stage_ev, s));
+    ctx->stage_pending = true;
     ctx->begun = true;
     ctx->exch_bytes = 0;
     return STADI_OK;
@@ -963,7 +1108,9 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
         tf[(size_t)i * 256 + 128 + k] = (float)std::sin(t * f);
       }
     }
-    CK(cudaMemcpy(ctx->tfreq, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice));
+    const void *st = stage_h2d(ctx, tf.data(), tf.size() * 4);
+    if (!st) return ctx_fail(ctx, STADI_ENOMEM, "host staging exhausted");
+    CK(cudaMemcpyAsync(ctx->tfreq, st, tf.size() * 4, cudaMemcpyHostToDevice, s));
     ctx->tfreq_nt = nt;
   }
   EpiParams ep{};
@@ -981,7 +1128,8 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
     for (int b = 0; b < B; ++b)
       if (cond->labels[b] < 0 || cond->labels[b] > m.num_classes)
         return ctx_fail(ctx, STADI_EINVAL, "class label out of range");
-    CK(cudaMemcpyAsync(ctx->labels_dev, cond->labels, B * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->labels_dev, stage_h2d(ctx, cond->labels, B * 4), B * 4,
+                       cudaMemcpyHostToDevice, s));
     if (ctx->dtype == STADI_DTYPE_BF16)
       CK(class_cond<bf16>(ctx->temb, WF(ctx, "y_embed.table"), ctx->labels_dev, nt, B, (int)d,
                           (bf16 *)ctx->csilu, s));
@@ -1024,9 +1172,11 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
     // [B, L, D] -> [L, B, D] (token-major, batch innermost) by strided copies;
     // text may be a host or a device pointer (cudaMemcpyDefault)
     if (!ctx->text_f) CK(dalloc(ctx, &ctx->text_f, Mt * Dt * 4));
+    const float *txt = (const float *)stage_h2d(ctx, cond->text, (size_t)Mt * Dt * 4);
+    if (!txt) return ctx_fail(ctx, STADI_ENOMEM, "host staging exhausted");
     for (int b = 0; b < B; ++b)
       CK(cudaMemcpy2DAsync(ctx->text_f + (size_t)b * Dt, (size_t)B * Dt * 4,
-                           cond->text + (size_t)b * L * Dt, (size_t)Dt * 4, (size_t)Dt * 4, L,
+                           txt + (size_t)b * L * Dt, (size_t)Dt * 4, (size_t)Dt * 4, L,
                            cudaMemcpyDefault, s));
     if (ctx->dtype == STADI_DTYPE_BF16)
       CK(cast_f32<bf16>(ctx->text_f, (bf16 *)ctx->text_T, (long)(Mt * Dt), s));
@@ -1047,10 +1197,13 @@ extern "C" stadi_status stadi_begin(stadi_ctx *ctx, const float *noise_full,
       CK(gemm(ctx, ctx->y, WT(ctx, p + "xkv.w"), (int)Mt, (int)(2 * d), (int)d, EPI_STORE, ep, s));
     }
   }
+  CK(cudaEventRecord(ctx->stage_ev, s));
+  ctx->stage_pending = true;
   ctx->begun = true;
   ctx->exch_bytes = 0;
   return STADI_OK;
 }
+}  // namespace
 
 extern "C" stadi_status stadi_num_steps(stadi_ctx *ctx, uint32_t *n) {
   ALIVE();
@@ -1256,7 +1409,11 @@ bool graphs_enabled(stadi_ctx *ctx) {
   // local mode, and IPC mode when the driver can capture its stream memory operations
   // (NCCL mode's cross-stream exchange events stay eager); not while per-launch kernel
   // timing is on (its events must see every launch)
-  return env && !ctx->nccl && (!ctx->ipc_mode || ctx->ipc->graphs_ok) && !ctx->ktime;
+  // Virtual GPUs (several contexts of one process) stay eager: a stream capture in one
+  // thread can block behind another thread's synchronous pageable copy (which waits for
+  // that rank's stream, which waits for this rank's flags): observed to deadlock.
+  return env && !ctx->nccl && (!ctx->ipc_mode || ctx->ipc->graphs_ok) && !ctx->ktime &&
+         !ctx->green_ctx;
 }
 
 // Program step i on stream s: replay its graph, capturing it on first use.
@@ -1268,9 +1425,12 @@ stadi_status exec_step(stadi_ctx *ctx, uint32_t i, cudaStream_t s) {
     cudaGraphExecDestroy(G.exec);
     G.exec = nullptr;
   }
+  static const bool dbg = getenv("STADI_DEBUG_GRAPHS") != nullptr;
   if (!G.exec) {
     // capture on the context's own stream (the caller's may be the legacy stream)
+    if (dbg) fprintf(stderr, "[stadi r%d] step %u: sync\n", ctx->rank, i);
     CK(cudaStreamSynchronize(s));
+    if (dbg) fprintf(stderr, "[stadi r%d] step %u: capture\n", ctx->rank, i);
     const unsigned long long l0 = g_launches;
     const uint64_t b0 = ctx->exch_bytes;
     CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
@@ -1282,6 +1442,7 @@ stadi_status exec_step(stadi_ctx *ctx, uint32_t i, cudaStream_t s) {
       return st;
     }
     CK(ec);
+    if (dbg) fprintf(stderr, "[stadi r%d] step %u: instantiate\n", ctx->rank, i);
     const cudaError_t ei = cudaGraphInstantiate(&G.exec, graph, 0);
     cudaGraphDestroy(graph);
     CK(ei);
@@ -1291,6 +1452,7 @@ stadi_status exec_step(stadi_ctx *ctx, uint32_t i, cudaStream_t s) {
     ctx->exch_bytes = b0;
     G.emu_ctas = ctx->emu_ctas;
   }
+  if (dbg) fprintf(stderr, "[stadi r%d] step %u: launch\n", ctx->rank, i);
   CK(cudaGraphLaunch(G.exec, s));
   ++ctx->graph_steps;
   g_launches += G.launches;
@@ -1306,11 +1468,15 @@ extern "C" stadi_status stadi_denoise_step(stadi_ctx *ctx, uint32_t step, void *
   if (!ctx->begun) return ctx_fail(ctx, STADI_ESTATE, "stadi_denoise_step before stadi_begin");
   if (step >= ctx->program.size()) return ctx_fail(ctx, STADI_EINVAL, "step out of range");
   CK(cudaSetDevice(ctx->device));
-  return exec_step(ctx, step, (cudaStream_t)stream);
+  cudaStream_t w;
+  CK(enter_stream(ctx, (cudaStream_t)stream, &w));
+  ST(exec_step(ctx, step, w));
+  CK(leave_stream(ctx, (cudaStream_t)stream));
+  return STADI_OK;
 }
 
-extern "C" stadi_status stadi_gather(stadi_ctx *ctx, float *out_full, void *stream) {
-  ALIVE();
+namespace {
+stadi_status gather_impl(stadi_ctx *ctx, float *out_full, void *stream) {
   if (!ctx->begun) return ctx_fail(ctx, STADI_ESTATE, "stadi_gather before stadi_begin");
   if (!out_full) return ctx_fail(ctx, STADI_EINVAL, "NULL argument");
   const Dims &m = ctx->dm;
@@ -1320,10 +1486,12 @@ extern "C" stadi_status stadi_gather(stadi_ctx *ctx, float *out_full, void *stre
   const size_t row_elems = (size_t)m.lat_w * m.c_in;
   if (ctx->ipc_mode) return ipc_gather(ctx, out_full, dev, s);
   if (!ctx->nccl) {
-    for (auto &r : ctx->ranks)
-      CK(cudaMemcpyAsync(out_full + (size_t)r.row_begin * row_elems, r.x_band,
-                         (size_t)r.rows * row_elems * 4,
-                         dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    for (auto &r : ctx->ranks) {
+      float *dst = out_full + (size_t)r.row_begin * row_elems;
+      const size_t bytes = (size_t)r.rows * row_elems * 4;
+      if (dev) CK(cudaMemcpyAsync(dst, r.x_band, bytes, cudaMemcpyDeviceToDevice, s));
+      else CK(stage_d2h(ctx, dst, r.x_band, bytes, s));
+    }
     return STADI_OK;
   }
   // NCCL: every rank (excluded ones too) receives every band (world communicator).
@@ -1344,11 +1512,15 @@ extern "C" stadi_status stadi_gather(stadi_ctx *ctx, float *out_full, void *stre
                          ctx->world_comm, s));
   }
   CKN(nccl().GroupEnd());
-  CK(cudaMemcpyAsync(out_full, full, (size_t)m.lat_h * row_elems * 4,
-                     dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  if (dev)
+    CK(cudaMemcpyAsync(out_full, full, (size_t)m.lat_h * row_elems * 4, cudaMemcpyDeviceToDevice,
+                       s));
+  else
+    CK(stage_d2h(ctx, out_full, full, (size_t)m.lat_h * row_elems * 4, s));
   CK(cudaFreeAsync(full, s));
   return STADI_OK;
 }
+}  // namespace
 
 extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, const float *noise_full,
                                   const stadi_cond *cond, float *out_full, stadi_run_stats *stats,
@@ -1357,9 +1529,12 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
   if (!plan || !noise_full || !cond || !out_full)
     return ctx_fail(ctx, STADI_EINVAL, "NULL argument");
   CK(cudaSetDevice(ctx->device));
+  DBG("run: start");
   if (!ctx->has_plan || std::memcmp(plan, &ctx->plan, sizeof(stadi_plan_t)) != 0)
     ST(stadi_set_plan(ctx, plan));
-  cudaStream_t s = (cudaStream_t)stream;
+  DBG("run: plan installed");
+  cudaStream_t s;
+  CK(enter_stream(ctx, (cudaStream_t)stream, &s));
   ctx->last_stream = s;
   ctx->last_stream_set = true;
   cudaEvent_t e0, e1;
@@ -1370,11 +1545,16 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
   ctx->graph_steps = 0;
   const double w0 = ctx->kt[STADI_KCLASS_XWAIT].ms;
   CK(cudaEventRecord(e0, s));
-  ST(stadi_begin(ctx, noise_full, cond, stream));
+  ST(begin_impl(ctx, noise_full, cond, s));
+  DBG("run: begun");
   for (uint32_t i = 0; i < ctx->program.size(); ++i) ST(exec_step(ctx, i, s));
-  ST(stadi_gather(ctx, out_full, stream));
+  DBG("run: steps enqueued");
+  ST(gather_impl(ctx, out_full, s));
+  DBG("run: gather enqueued");
   CK(cudaEventRecord(e1, s));
+  CK(leave_stream(ctx, (cudaStream_t)stream));
   CK(cudaEventSynchronize(e1));
+  DBG("run: done");
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);
@@ -1427,8 +1607,8 @@ extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, d
     pooled.assign((size_t)m.B * m.pooled_dim, 0.f);
     cond.pooled = pooled.data();
   }
-  cudaStream_t s = nullptr;
-  ST(stadi_begin(ctx, zeros.data(), &cond, s));
+  cudaStream_t s = ctx->green_ctx ? ctx->wstream : nullptr;
+  ST(begin_impl(ctx, zeros.data(), &cond, s));
   std::vector<double> ms_local(ctx->ranks.size(), 0.0);
   ctx->probe = true;  // compute-only probe steps: no exchange waits / signals
   cudaEvent_t e0, e1;

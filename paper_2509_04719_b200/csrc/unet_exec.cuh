@@ -938,7 +938,9 @@ stadi_status unet_begin(stadi_ctx *ctx, const stadi_cond *cond, cudaStream_t s) 
         tf[(size_t)i * C0 + half + k] = (float)std::sin(t * f);
       }
     }
-    CK(cudaMemcpy(U->tfeat, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice));
+    const void *st = stage_h2d(ctx, tf.data(), tf.size() * 4);
+    if (!st) return ctx_fail(ctx, STADI_ENOMEM, "host staging exhausted");
+    CK(cudaMemcpyAsync(U->tfeat, st, tf.size() * 4, cudaMemcpyHostToDevice, s));
     ctx->tfreq_nt = nt;
   }
   EpiParams ep{};
@@ -963,11 +965,13 @@ stadi_status unet_begin(stadi_ctx *ctx, const stadi_cond *cond, cudaStream_t s) 
           tid[(size_t)b * 1536 + j * 256 + 128 + k] = (float)std::sin(t * f);
         }
       }
-    CK(cudaMemcpy2DAsync(U->addin, (size_t)an * 4, cond->pooled, (size_t)m.pooled_dim * 4,
+    const void *pl = stage_h2d(ctx, cond->pooled, (size_t)B * m.pooled_dim * 4);
+    const void *ti = stage_h2d(ctx, tid.data(), tid.size() * 4);  // pinned copy of a temporary
+    if (!pl || !ti) return ctx_fail(ctx, STADI_ENOMEM, "host staging exhausted");
+    CK(cudaMemcpy2DAsync(U->addin, (size_t)an * 4, pl, (size_t)m.pooled_dim * 4,
                          (size_t)m.pooled_dim * 4, B, cudaMemcpyDefault, s));
-    CK(cudaMemcpy2DAsync(U->addin + m.pooled_dim, (size_t)an * 4, tid.data(), 1536 * 4,
-                         1536 * 4, B, cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));  // tid is a host temporary
+    CK(cudaMemcpy2DAsync(U->addin + m.pooled_dim, (size_t)an * 4, ti, 1536 * 4, 1536 * 4, B,
+                         cudaMemcpyDefault, s));
     ep.bias = U->wf.at("add.b1");
     ep.out = U->aug1;
     CK(simt_gemm<float>(U->addin, U->wf.at("add.w1"), B, td, an, EPI_F32, ep, s));
@@ -1001,9 +1005,11 @@ stadi_status unet_begin(stadi_ctx *ctx, const stadi_cond *cond, cudaStream_t s) 
     CK(dalloc(ctx, &ctx->text_T, Mt * Dt * ctx->esz));
     CK(dalloc(ctx, &ctx->text_f, Mt * Dt * 4));
   }
+  const float *txt = (const float *)stage_h2d(ctx, cond->text, (size_t)Mt * Dt * 4);
+  if (!txt) return ctx_fail(ctx, STADI_ENOMEM, "host staging exhausted");
   for (int b = 0; b < B; ++b)
     CK(cudaMemcpy2DAsync(ctx->text_f + (size_t)b * Dt, (size_t)B * Dt * 4,
-                         cond->text + (size_t)b * L * Dt, (size_t)Dt * 4, (size_t)Dt * 4, L,
+                         txt + (size_t)b * L * Dt, (size_t)Dt * 4, (size_t)Dt * 4, L,
                          cudaMemcpyDefault, s));
   if (ctx->dtype == STADI_DTYPE_BF16)
     CK(cast_f32<bf16>(ctx->text_f, (bf16 *)ctx->text_T, (long)(Mt * Dt), s));

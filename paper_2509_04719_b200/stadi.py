@@ -82,7 +82,7 @@ class ModelDesc(C.Structure):
 class DistDesc(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
                 ("n_local", C.c_int32), ("nccl_id", C.POINTER(C.c_uint8)),
-                ("transport", C.c_int32)]
+                ("transport", C.c_int32), ("vgpu_sms", C.c_int32)]
 
 
 class Cond(C.Structure):
@@ -275,14 +275,14 @@ class Context:
     """One stadi_ctx (one process; hosts one rank or n_local ranks on one device)."""
 
     def __init__(self, desc: ModelDesc, rank=0, world=1, device=0, n_local=1, nccl_id=None,
-                 transport=TRANSPORT_NCCL):
+                 transport=TRANSPORT_NCCL, vgpu_sms=0):
         self._keep = []
         nid = None
         if nccl_id is not None:
             nb = (C.c_uint8 * 128)(*nccl_id)
             self._keep.append(nb)
             nid = C.cast(nb, C.POINTER(C.c_uint8))
-        dd = DistDesc(rank, world, device, n_local, nid, transport)
+        dd = DistDesc(rank, world, device, n_local, nid, transport, vgpu_sms)
         h = C.c_void_p()
         _check(lib.stadi_create(C.byref(desc), C.byref(dd), C.byref(h)))
         self.h = h
