@@ -14,7 +14,13 @@ P_total=32, a=0.75, b=0.25.
 Readings:
   R2  Eq. 4 boundaries as printed (v <= b*v_max is excluded), exact
       rational comparisons.
-  R3  (M_base - M_warmup) must be even when a tier-2 GPU exists.
+  R3  (round 1: (M_base - M_warmup) must be even with a tier-2 GPU; superseded by R32)
+  R32 tier-2 stride n: K = M_base - M_warmup post-warmup intervals; n = 2 when K is
+      even (Eq. 4: M_warmup + K/2 = (M_base + M_warmup)/2 steps), else the smallest
+      prime factor of K, so the slow grid still lands on every n-th
+      fast-grid point (Thm 2 with n M_i = M, L234-L238) and the "lowest common
+      multiple of inference step sizes" (L185) is n; K = 1: n = 1 (no reduction
+      possible: tier 2 runs every step).  Tier-2 steps = M_warmup + K / n.
   R4  "LCM-minimising": tier 2 runs stride 2 after warmup; sync_period =
       lcm of post-warmup strides (1 or 2).
   R5  Eq. 5 integerised by the D'Hondt divisor method on weights v_i/M_i,
@@ -62,12 +68,31 @@ def tiers(speed, a=(3, 4), b=(1, 4), flags=0):
     return out
 
 
+def smallest_prime_factor(k):
+    """Smallest prime p dividing k >= 2 (trial division)."""
+    p = 2
+    while p * p <= k:
+        if k % p == 0:
+            return p
+        p += 1
+    return k
+
+
+def slow_stride(m_base, m_warmup):
+    """R32: the tier-2 DDIM stride n for K = M_base - M_warmup post-warmup intervals."""
+    K = m_base - m_warmup
+    if K % 2 == 0:
+        return 2
+    return 1 if K == 1 else smallest_prime_factor(K)
+
+
 def steps_of(tier, m_base, m_warmup):
-    """Eq. 4 right-hand sides (L183)."""
+    """Eq. 4 right-hand sides (L183): tier 2 = M_warmup + K/n (= (M_base+M_warmup)/2
+    for n = 2, R32)."""
     if tier == 1:
         return m_base
     if tier == 2:
-        return Fraction(m_base, 2) + Fraction(m_warmup, 2)
+        return m_warmup + Fraction(m_base - m_warmup, slow_stride(m_base, m_warmup))
     return 0
 
 
@@ -88,8 +113,7 @@ def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
 
     tier = tiers(speed, a, b, flags)
     any_slow = any(t == 2 for t in tier)
-    if any_slow and (m_base - m_warmup) % 2:
-        raise PlanError("R3: (M_base - M_warmup) must be even with a tier-2 GPU")
+    stride = slow_stride(m_base, m_warmup) if any_slow else 1
     steps = [steps_of(t, m_base, m_warmup) for t in tier]
     assert all(Fraction(s).denominator == 1 for s in steps)
     steps = [int(s) for s in steps]
@@ -126,7 +150,7 @@ def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
         # with one unit; each further unit goes to argmax w_i/(P_i+1), i.e.
         # argmin (P_i+1) * M'_i / v_i, ties to the smallest rank (R5).
         if flags & SIZER_INTERVAL:
-            mprime = [(2 if (tier[i] == 1 and any_slow) else 1) for i in range(n)]
+            mprime = [(stride if (tier[i] == 1 and any_slow) else 1) for i in range(n)]
         else:
             mprime = steps
         for i in inc:
@@ -150,7 +174,7 @@ def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
         makespan = Fraction(max(steps[i] * (int(alpha[i]) + int(beta[i]) * units[i]) for i in inc))
     else:
         makespan = max(Fraction(steps[i] * units[i], int(speed[i])) for i in inc)
-    sync_period = 2 if any_slow else 1
+    sync_period = stride
     return dict(
         n_gpus=n, m_base=m_base, m_warmup=m_warmup, p_total=p_total,
         rows_per_unit=rows_per_unit, tier=tier, steps=steps, units=units,

@@ -11,7 +11,9 @@ Readings:
        warmup step's activations seed version V_{-1}.
   R10  a fast GPU's odd step reads the newest complete version V_k and
        publishes nothing ("No update for buffer", L144).
-  R11  the slow grid is the warmup prefix plus every 2nd fast-grid point.
+  R11  the slow grid is the warmup prefix plus every n-th fast-grid point (n = 2,
+       or R32's smallest prime factor of an odd K; a fast GPU publishes on the
+       slow grid's points only).
   R13  with no slow GPU every GPU exchanges every step (DistriFusion).
   R18  fast grid: "leading" spacing, steps_offset 1:
        tau_m = (T // M_base) * (M_base - 1 - m) + 1,  T = 1000.
@@ -69,11 +71,13 @@ def schedule(plan: dict, rank: int) -> list[Step]:
             m, e = mw + j, mw + j
             out.append(Step(m, grid[m], nxt(m + 1), UNIFORM, e - 1, e))
         return out
-    for k in range(K // 2):                        # Alg. 1
-        m, e = mw + 2 * k, mw + k
+    n = plan["sync_period"]                        # slow stride (2, or R32's spf(K))
+    for k in range(K // n):                        # Alg. 1
+        m, e = mw + n * k, mw + k
         if tier == 1:                              # fast GPU (L134-L146)
             out.append(Step(m, grid[m], nxt(m + 1), FAST_EVEN, e - 1, e))
-            out.append(Step(m + 1, grid[m + 1], nxt(m + 2), FAST_ODD, e, NONE))
-        else:                                      # slow GPU (L148-L152), stride 2
-            out.append(Step(m, grid[m], nxt(m + 2), SLOW, e - 1, e))
+            for q in range(1, n):                  # "no update for buffer" steps
+                out.append(Step(m + q, grid[m + q], nxt(m + q + 1), FAST_ODD, e, NONE))
+        else:                                      # slow GPU (L148-L152), stride n
+            out.append(Step(m, grid[m], nxt(m + n), SLOW, e - 1, e))
     return out

@@ -287,6 +287,15 @@ def test_time_invariant_activations_make_staleness_exact():
         p = stadi.plan_for(cfg, speed, 10, 2, flags=flags)
         out = stadi.run(cfg, W, x, c, p)
         assert np.max(np.abs(out - seq)) <= 1e-12 * np.max(np.abs(seq)), (speed, flags)
+    # R32 odd K: the slow GPU's stride is the smallest prime factor of K (3 for
+    # M_base 11, 7 for M_base 9); Eq. 3 composes exactly over n intervals under a
+    # constant eps, so the stale plan must still equal the sequential run
+    for mb, n in ((11, 3), (9, 7)):
+        seq_n = stadi.sequential(cfg, W, x, c, mb)
+        p = stadi.plan_for(cfg, [2, 1], mb, 2)
+        assert p["tier"] == [1, 2] and p["sync_period"] == n
+        out = stadi.run(cfg, W, x, c, p)
+        assert np.max(np.abs(out - seq_n)) <= 1e-12 * np.max(np.abs(seq_n)), mb
     # the pin is sensitive to the time dependence it removes: restoring the
     # t-embedding makes the same stale plan deviate
     W0 = _c1()[1]

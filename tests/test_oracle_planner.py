@@ -137,7 +137,6 @@ def test_plan_errors():
         dict(speed=[1, 1], m_base=10, m_warmup=11, p_total=8),
         dict(speed=[1, 1], m_base=10, m_warmup=0, p_total=8),
         dict(speed=[1, 1, 1], m_base=10, m_warmup=2, p_total=2),
-        dict(speed=[10, 6], m_base=11, m_warmup=2, p_total=8),   # R3: odd K with tier 2
     ]
     for kw in bad:
         with pytest.raises(planner.PlanError):
@@ -171,32 +170,60 @@ def test_fast_grid_leading_spacing():
     assert schedule.fast_grid(20)[0] == 951
 
 
-@pytest.mark.parametrize("mb,mw", [(10, 2), (50, 4), (100, 4), (20, 4)])
-def test_schedule_counts_and_alignment(mb, mw):
+@pytest.mark.parametrize("mb,mw,n", [(10, 2, 2), (50, 4, 2), (100, 4, 2), (20, 4, 2),
+                                     (11, 2, 3), (27, 2, 5), (51, 4, 47), (9, 2, 7)])
+def test_schedule_counts_and_alignment(mb, mw, n):
+    """Eq. 4 counts, exchange rounds and Thm 2 grid alignment for the slow stride n
+    (2 for an even K = M_base - M_warmup; R32: smallest prime factor of an odd K)."""
     p = planner.plan([100, 60, 100, 30], mb, mw, 16)
     assert p["tier"] == [1, 2, 1, 2]
+    assert p["sync_period"] == n == planner.slow_stride(mb, mw)
+    assert (mb - mw) % n == 0
     fast = schedule.schedule(p, 0)
     slow = schedule.schedule(p, 1)
-    # Eq. 4 step counts
-    assert len(fast) == mb and len(slow) == (mb + mw) // 2 == p["steps"][1]
-    # exchange rounds: M_warmup + K/2
+    # Eq. 4 step counts: tier 2 = M_warmup + K / n ((M_base + M_warmup) / 2 for n = 2)
+    assert len(fast) == mb and len(slow) == mw + (mb - mw) // n == p["steps"][1]
+    if n == 2:
+        assert p["steps"][1] == (mb + mw) // 2
+    # exchange rounds: M_warmup + K/n
     pubs = {s.pub_ver for s in fast if s.pub_ver >= 0}
-    assert len(pubs) == mw + (mb - mw) // 2 == p["n_exchange_rounds"]
+    assert len(pubs) == mw + (mb - mw) // n == p["n_exchange_rounds"]
     # Thm 2 (L234-L238): slow grid is a subsample of the fast grid, both end at final
     fast_t = [s.t for s in fast]
     assert all(s.t in fast_t for s in slow)
     assert fast[-1].t_prev == slow[-1].t_prev == schedule.FINAL
-    # every slow step spans exactly the two fast steps starting at the same t
+    # every slow step spans exactly the n fast steps starting at the same t
     for s in slow:
         if s.kind == schedule.SLOW:
             i = fast_t.index(s.t)
-            assert fast[i].kind == schedule.FAST_EVEN and fast[i + 1].kind == schedule.FAST_ODD
-            assert s.t_prev == fast[i + 1].t_prev
+            assert fast[i].kind == schedule.FAST_EVEN
+            assert all(fast[i + q].kind == schedule.FAST_ODD for q in range(1, n))
+            assert s.t_prev == fast[i + n - 1].t_prev
             assert s.read_ver == fast[i].read_ver and s.pub_ver == fast[i].pub_ver
-    # odd steps publish nothing and read the version their even step published
-    for a, b in zip(fast, fast[1:]):
+    # non-publishing steps read the version the last publishing step published
+    last = None
+    for b in fast:
         if b.kind == schedule.FAST_ODD:
-            assert b.pub_ver == schedule.NONE and b.read_ver == a.pub_ver
+            assert b.pub_ver == schedule.NONE and b.read_ver == last
+        elif b.pub_ver >= 0:
+            last = b.pub_ver
+
+
+def test_slow_stride_r32():
+    """R32: n = 2 for even K, else the smallest prime factor of K (K = 1: n = 1)."""
+    assert [planner.slow_stride(2 + k, 2) for k in range(0, 12)] == \
+        [2, 1, 2, 3, 2, 5, 2, 7, 2, 3, 2, 11]
+    assert planner.slow_stride(4 + 91, 4) == 7 and planner.slow_stride(4 + 121, 4) == 11
+    for K in range(2, 300):                      # brute-force definition
+        n = planner.slow_stride(K + 3, 3)
+        if K % 2 == 0:
+            assert n == 2
+        else:
+            assert K % n == 0 and all(n % d for d in range(2, n))
+            assert all(K % d for d in range(2, n))
+    # K = 1: no stride can skip a point: tier 2 runs every step, nobody is slow
+    p = planner.plan([100, 60], 5, 4, 8)
+    assert p["tier"] == [1, 2] and p["sync_period"] == 1 and p["steps"] == [5, 5]
 
 
 def test_schedule_uniform_and_excluded():

@@ -145,6 +145,12 @@ def test_time_invariant_activations_make_staleness_exact(tiny):
         p = OR.plan_for(cfg, speed, 6, 2, flags=flags)
         out = OR.run(cfg, W, x, c, p)
         assert np.max(np.abs(out - seq)) <= 1e-12 * np.max(np.abs(seq)), (speed, flags)
+    # R32 odd K = 3: the slow GPU's stride is 3
+    seq5 = OR.sequential(cfg, W, x, c, 5)
+    p = OR.plan_for(cfg, [4, 2], 5, 2)
+    assert p["sync_period"] == 3 and p["steps"] == [5, 3]
+    out = OR.run(cfg, W, x, c, p)
+    assert np.max(np.abs(out - seq5)) <= 1e-12 * np.max(np.abs(seq5))
 
 
 # ----------------------------------------------------------- brute-force U-Net
