@@ -354,6 +354,148 @@ def run_reference(args, cfg, wl, rank, world):
     print(json.dumps(out), flush=True)
 
 
+# --------------------------------------------------------------------- method modes
+# PAPER.md §V: Table III ablation (None / +SA / +TA / +TA+SA, L316-L323), Fig. 8 occupancy
+# pairs (L292, L310), Fig. 9 forced patch ratios (L325-L333), and the alpha/beta probe of
+# the affine sizer (R30).  On ONE physical GPU the ranks are VIRTUAL GPUs: green-context
+# SM partitions computing concurrently (paper_2509_04719_b200/vgpu.py), with the
+# occupancy emulator holding rho of each partition's SMs -- HBM, L2 and copy engines are
+# shared, there is no NVLink hop.  Latency of a request = max over ranks
+# of its device time (stadi_run_stats.ms_total), averaged over the timed requests.
+FLAGS_ABLATION = [("none", 1 | 2), ("+SA", 1), ("+TA", 2), ("+TA+SA", 0)]
+FIG8_PAIRS = [[0, 20], [0, 40], [0, 60], [35, 45], [30, 50], [25, 55]]
+
+
+class _Group:
+    """The ranks of a method run: virtual GPUs on this device (world == 1)."""
+
+    def __init__(self, S, desc, weights, n, sms):
+        from paper_2509_04719_b200.vgpu import VirtualGpus
+        self.vg = VirtualGpus(desc, n, sms, weights)
+        self.n = n
+
+    def call(self, *a, **kw):
+        return self.vg.call(*a, **kw)
+
+    def close(self):
+        self.vg.close()
+
+
+def _time_plan(S, grp, plan, x, c, k, w):
+    outs = [np.zeros_like(x) for _ in range(grp.n)]
+    for _ in range(w):
+        grp.call("run", plan, x, c, per_rank=lambda r: {"out": outs[r]})
+    lat = []
+    for _ in range(k):
+        st = grp.call("run", plan, x, c, per_rank=lambda r: {"out": outs[r]})
+        lat.append(max(t.ms_total for t in st))
+    return float(np.mean(lat)), [float(v) for v in lat]
+
+
+def run_method(args, cfg, wl, mode=None, pairs=None, steps=None):
+    """Returns the method-mode JSON object (see the block comment above)."""
+    from paper_2509_04719_b200 import stadi as S
+    mode = mode or args.mode
+    steps = steps or args.steps
+    if pairs is None:
+        pairs = ([[int(v) for v in args.occupancy.split(",")]] if "," in args.occupancy
+                 else (FIG8_PAIRS if mode == "fig8" else FIG8_PAIRS[:3]))
+    n = len(pairs[0])
+    sms = args.vgpu_sms or max(8, (112 // n) // 8 * 8)
+    mb = args.m_base or wl["m_base"]
+    mw = wl["m_warmup"]
+    p = configs.rows_per_unit(cfg)
+    P = cfg["latent_h"] // p
+    x, c = gen.noise(cfg), gen.cond(cfg)
+    W = gen.weights(cfg)
+    desc = S.model_desc(wl["model"], S.DTYPE_BF16)
+    grp = _Group(S, desc, [W[k] for k, _, _ in configs.manifest(cfg)], n, sms)
+    del W
+    grp.call("profile_warmup", 1, n)        # loads every kernel before any emulator
+    rows = []
+    t0 = time.time()
+    try:
+        for occ in pairs:
+            grp.call("emulator_start", per_rank=lambda r: {"pct": occ[r]})
+            try:
+                ms, speed = grp.call("profile_warmup", 3, n)[0]
+                row = {"occupancy_pct": occ, "speed_q20": [int(v) for v in speed],
+                       "probe_ms": ms}
+                if mode in ("ablation", "fig8"):
+                    fl = FLAGS_ABLATION if mode == "ablation" else [("none", 3), ("+TA+SA", 0)]
+                    for name, f in fl:
+                        pl = S.plan(speed, mb, mw, P, p, flags=f)
+                        lat, all_ = _time_plan(S, grp, pl, x, c, steps, 1)
+                        row[name] = {"ms_per_image": lat, "runs_ms": all_,
+                                     "plan": _plan_json(pl)}
+                    base = row["none"]["ms_per_image"]
+                    for name, _ in fl[1:]:
+                        row[name]["speedup_vs_none"] = base / row[name]["ms_per_image"]
+                        row[name]["latency_reduction"] = 1.0 - row[name]["ms_per_image"] / base
+                elif mode == "fig9":
+                    sweep = []
+                    for k8 in range(1, 8):   # rank 0 share k/8 of the rows (2 ranks), TA off
+                        u0 = max(1, min(P - 1, round(P * k8 / 8)))
+                        fu = [u0, P - u0] if n == 2 else None
+                        if fu is None:
+                            break
+                        pl = S.plan(speed, mb, mw, P, p, flags=1 | 8, forced_units=fu)
+                        lat, _ = _time_plan(S, grp, pl, x, c, steps, 1)
+                        sweep.append({"units": fu, "ms_per_image": lat})
+                    pl_sa = S.plan(speed, mb, mw, P, p, flags=1)
+                    lat_sa, _ = _time_plan(S, grp, pl_sa, x, c, steps, 1)
+                    pl_pp = S.plan(speed, mb, mw, P, p, flags=3)
+                    lat_pp, _ = _time_plan(S, grp, pl_pp, x, c, steps, 1)
+                    row.update(sweep=sweep, stadi_sa={"units": _plan_json(pl_sa)["units"],
+                                                      "ms_per_image": lat_sa},
+                               uniform_pp_ms=lat_pp)
+                elif mode == "alphabeta":
+                    # two probe band heights per rank (complementary forced splits)
+                    a_u = [max(1, P // (4 * n)) if r % 2 == 0 else 0 for r in range(n)]
+                    rest = P - sum(a_u)
+                    odd = [r for r in range(n) if r % 2 == 1] or [n - 1]
+                    for r in odd:
+                        a_u[r] += rest // len(odd)
+                    a_u[odd[-1]] += P - sum(a_u)
+                    b_u = list(reversed(a_u)) if n == 2 else a_u[1:] + a_u[:1]
+                    ms_a = grp.call("profile_band", 3, a_u)[0]
+                    ms_b = grp.call("profile_band", 3, b_u)[0]
+                    alpha, beta = [], []
+                    for r in range(n):
+                        if a_u[r] == b_u[r]:
+                            bt = ms_a[r] / a_u[r]
+                        else:
+                            bt = (ms_b[r] - ms_a[r]) / (b_u[r] - a_u[r])
+                        bt = max(bt, 1e-6)
+                        alpha.append(max(0.0, ms_a[r] - bt * a_u[r]))
+                        beta.append(bt)
+                    ns = 1e6  # ms -> integer ns for the C ABI
+                    pl_aff = S.plan(speed, mb, mw, P, p, flags=16,
+                                    alpha=[int(v * ns) for v in alpha],
+                                    beta=[max(1, int(v * ns)) for v in beta])
+                    pl_dh = S.plan(speed, mb, mw, P, p)
+                    lat_aff, _ = _time_plan(S, grp, pl_aff, x, c, steps, 1)
+                    lat_dh, _ = _time_plan(S, grp, pl_dh, x, c, steps, 1)
+                    row.update(probe_units=[a_u, b_u], probe_ms=[ms_a, ms_b],
+                               alpha_ms=alpha, beta_ms_per_unit=beta,
+                               affine={"plan": _plan_json(pl_aff), "ms_per_image": lat_aff},
+                               dhondt={"plan": _plan_json(pl_dh), "ms_per_image": lat_dh})
+                rows.append(row)
+            finally:
+                grp.call("emulator_stop")
+    finally:
+        grp.close()
+    out = {"mode": mode, "metric": args.metric, "unit": "ms/image", "n_gpus": 1,
+           "virtual_gpus": n, "vgpu_sms": sms, "steps": steps, "m_base": mb,
+           "m_warmup": mw, "workload": wl["name"], "results": rows,
+           "wall_s": time.time() - t0,
+           "note": ("ranks are virtual GPUs: disjoint green-context SM partitions of one B200 "
+                    "computing concurrently, occupancy emulated inside each partition; HBM/L2 "
+                    "shared, no NVLink hop"),
+           "context": PAPER_CONTEXT}
+    return out
+
+
 # --------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -365,6 +507,13 @@ def main():
     ap.add_argument("--occupancy", default="half50")
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="N > 1 exchange transport (IPC: fused one-sided P2P, the default)")
+    ap.add_argument("--mode", default="headline",
+                    choices=["headline", "ablation", "fig8", "fig9", "alphabeta"],
+                    help="method-level measurements on virtual GPUs (one device)")
+    ap.add_argument("--vgpu-sms", type=int, default=0, help="SMs per virtual GPU (mult. of 8)")
+    ap.add_argument("--m-base", type=int, default=0, help="override the workload's M_base")
+    ap.add_argument("--no-method", action="store_true",
+                    help="skip the default run's 2-virtual-GPU STADI vs uniform-PP leg")
     ap.add_argument("--no-uniform", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -387,6 +536,10 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, cfg, wl, rank, world)
+        return
+    if args.mode != "headline":
+        assert world == 1, "method modes run on virtual GPUs of one device"
+        print(json.dumps(run_method(args, cfg, wl)), flush=True)
         return
 
     # stdout carries exactly one JSON line: everything else written to fd 1 (NCCL's
@@ -603,6 +756,15 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, wl)
 
+    # ---- the method on one device: 2 virtual GPUs (SM partitions), the second at 50%
+    # emulated occupancy (C5's "half50" pattern), STADI vs same-kernel uniform PP
+    method = None
+    if world == 1 and not args.no_method and not args.ncu:
+        try:
+            method = run_method(args, cfg, wl, mode="fig8", pairs=[[0, 50]], steps=2)
+        except Exception as e:  # reported, never silently dropped
+            method = {"error": str(e)}
+
     if rank == 0:
         res = {
             "metric": args.metric, "value": value, "unit": "images/s", "n_gpus": world,
@@ -620,7 +782,7 @@ def main():
             "uniform_pp": uni, "e2e": e2e, "roofline": roof, "path_roofline": path_roof,
             "kernels": kernels,
             "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(launches),
-            "occupancy_sweep": occ_sweep,
+            "occupancy_sweep": occ_sweep, "method_vgpu": method,
             "context": PAPER_CONTEXT,
         }
         sys.stdout.flush()

@@ -108,7 +108,10 @@ typedef struct {
   uint32_t units[STADI_MAX_GPUS];      /* P_i in units (Eq. 5, D'Hondt, R5)       */
   uint32_t row_begin[STADI_MAX_GPUS];  /* first latent row of GPU i's band        */
   uint32_t rows[STADI_MAX_GPUS];       /* latent rows of GPU i's band             */
-  uint32_t sync_period;                /* lcm of post-warmup DDIM strides: 1 or 2 */
+  uint32_t sync_period;                /* lcm of post-warmup DDIM strides = the
+                                          tier-2 stride n: 1 (nobody slow), 2 (K =
+                                          M_base - M_warmup even), else the smallest
+                                          prime factor of K (R32)                 */
   uint32_t n_exchange_rounds;          /* M_warmup + (M_base-M_warmup)/sync_period */
   uint64_t makespan_num, makespan_den; /* max_i M_i P_i / v_i, reduced fraction
                                           (SIZER_AFFINE: max_i M_i (alpha_i +
@@ -124,8 +127,11 @@ typedef struct {
  * linear relationship with the patch size due to some fixed overhead") each
  * further unit goes to argmin M_i (alpha_i + beta_i (P_i + 1)) instead, which
  * minimises max_i M_i (alpha_i + beta_i P_i); Eq. 4 still uses speed.
+ * Tier 2 runs M_warmup + K/n steps, K = M_base - M_warmup, stride n = 2 for even K
+ * ((M_base + M_warmup)/2 as printed in Eq. 4), else the smallest prime factor of K
+ * (R32, keeps Thm 2's aligned grids).
  * EINVAL: N out of range, a zero speed, not 0<b<a<1, M_warmup out of range,
- * (M_base - M_warmup) odd with a tier-2 GPU (R3), P_total < #included, bad
+ * P_total < #included, bad
  * forced units, SIZER_AFFINE without alpha / beta or with beta_i == 0 on an
  * included GPU. */
 stadi_status stadi_plan(const stadi_plan_params *in, stadi_plan_t *out);
@@ -269,6 +275,13 @@ stadi_status stadi_load_weights(stadi_ctx *ctx, uint32_t n_tensors,
  * where G = world * n_local. */
 stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, double *ms_out,
                                   uint64_t *speed_out);
+
+/* COLLECTIVE.  As stadi_profile_warmup, with the probe band of group rank g forced
+ * to units[g] planner units (sum = the latent's units; every entry >= 1): two
+ * calls with different sizes give each GPU's per-step cost alpha_g + beta_g P, the
+ * input of STADI_SIZER_AFFINE (R30; L333 "fixed overhead").  ms_out: [G]. */
+stadi_status stadi_profile_band(stadi_ctx *ctx, uint32_t n_steps, const uint32_t *units,
+                                double *ms_out);
 
 /* COLLECTIVE.  Install a plan (n_gpus == G, p_total * rows_per_unit == latent
  * height).  Allocates bands and exchange slots. */

@@ -98,12 +98,25 @@ extern "C" stadi_status stadi_plan(const stadi_plan_params *in, stadi_plan_t *ou
     any_slow |= (t == 2);
     n_inc += (t > 0);
   }
-  if (any_slow && ((in->m_base - in->m_warmup) & 1u))
-    return fail(nullptr, STADI_EINVAL,
-                "stadi_plan: (M_base - M_warmup) must be even with a tier-2 GPU (R3)");
+  // R32: tier-2 stride n over the K post-warmup intervals: 2 for even K (Eq. 4's
+  // (M_base + M_warmup) / 2), else the smallest prime factor of K (K = 1: 1)
+  const uint32_t K = in->m_base - in->m_warmup;
+  uint32_t stride = 1;
+  if (any_slow) {
+    if (K % 2 == 0) {
+      stride = 2;
+    } else if (K > 1) {
+      stride = K;
+      for (uint32_t d = 3; d * d <= K; d += 2)
+        if (K % d == 0) {
+          stride = d;
+          break;
+        }
+    }
+  }
   for (uint32_t i = 0; i < n; ++i)
     p.steps[i] = p.tier[i] == 1 ? in->m_base
-               : p.tier[i] == 2 ? (in->m_base + in->m_warmup) / 2 : 0;
+               : p.tier[i] == 2 ? in->m_warmup + K / stride : 0;
   if (in->p_total < n_inc)
     return fail(nullptr, STADI_EINVAL, "stadi_plan: P_total %u < %u included GPUs",
                 in->p_total, n_inc);
@@ -153,7 +166,7 @@ extern "C" stadi_status stadi_plan(const stadi_plan_params *in, stadi_plan_t *ou
     uint64_t mp[STADI_MAX_GPUS];
     for (uint32_t i = 0; i < n; ++i) {
       if (in->flags & STADI_SIZER_INTERVAL)
-        mp[i] = (p.tier[i] == 1 && any_slow) ? 2 : 1;
+        mp[i] = (p.tier[i] == 1 && any_slow) ? stride : 1;
       else
         mp[i] = p.steps[i];
       if (p.tier[i]) p.units[i] = 1;
@@ -204,7 +217,7 @@ extern "C" stadi_status stadi_plan(const stadi_plan_params *in, stadi_plan_t *ou
   uint64_t g = gcd_u64(bn_, bd_);
   p.makespan_num = bn_ / g;
   p.makespan_den = bd_ / g;
-  p.sync_period = any_slow ? 2 : 1;
+  p.sync_period = stride;
   p.n_exchange_rounds = in->m_warmup + (in->m_base - in->m_warmup) / p.sync_period;
   *out = p;
   return STADI_OK;
@@ -215,7 +228,8 @@ extern "C" stadi_status stadi_schedule(const stadi_plan_t *plan, uint32_t rank,
   if (!plan || !n_out) return fail(nullptr, STADI_EINVAL, "stadi_schedule: NULL argument");
   if (rank >= plan->n_gpus) return fail(nullptr, STADI_EINVAL, "stadi_schedule: bad rank");
   const int32_t mb = (int32_t)plan->m_base, mw = (int32_t)plan->m_warmup;
-  if (mb < 1 || mw < 1 || mw > mb || mb > kTrainT)
+  if (mb < 1 || mw < 1 || mw > mb || mb > kTrainT || plan->sync_period < 1 ||
+      (mb - mw) % (int32_t)plan->sync_period)
     return fail(nullptr, STADI_EINVAL, "stadi_schedule: bad plan");
   const int32_t ratio = kTrainT / mb;
   auto grid = [&](int32_t i) { return i < mb ? ratio * (mb - 1 - i) + 1 : STADI_T_FINAL; };
@@ -235,13 +249,15 @@ extern "C" stadi_status stadi_schedule(const stadi_plan_t *plan, uint32_t rank,
         emit(m, grid(m), grid(m + 1), STADI_STEP_UNIFORM, e - 1, e);
       }
     } else {
-      for (int32_t k = 0; k < K / 2; ++k) {  // Alg. 1, R10, R11
-        const int32_t m = mw + 2 * k, e = mw + k;
+      const int32_t sn = (int32_t)plan->sync_period;  // slow stride (R11, R32)
+      for (int32_t k = 0; k < K / sn; ++k) {  // Alg. 1, R10, R11
+        const int32_t m = mw + sn * k, e = mw + k;
         if (tier == 1) {
           emit(m, grid(m), grid(m + 1), STADI_STEP_FAST_EVEN, e - 1, e);
-          emit(m + 1, grid(m + 1), grid(m + 2), STADI_STEP_FAST_ODD, e, STADI_VER_NONE);
+          for (int32_t q = 1; q < sn; ++q)
+            emit(m + q, grid(m + q), grid(m + q + 1), STADI_STEP_FAST_ODD, e, STADI_VER_NONE);
         } else {
-          emit(m, grid(m), grid(m + 2), STADI_STEP_SLOW, e - 1, e);
+          emit(m, grid(m), grid(m + sn), STADI_STEP_SLOW, e - 1, e);
         }
       }
     }

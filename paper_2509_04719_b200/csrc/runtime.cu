@@ -1572,10 +1572,27 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
 }
 
 // ---------------------------------------------------------------- profiling (a1)
+namespace {
+stadi_status profile_impl(stadi_ctx *ctx, uint32_t n_steps, const uint32_t *units, double *ms_out,
+                          uint64_t *speed_out);
+}
 extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, double *ms_out,
                                              uint64_t *speed_out) {
   ALIVE();
   if (!ms_out || !speed_out || n_steps == 0) return ctx_fail(ctx, STADI_EINVAL, "bad argument");
+  return profile_impl(ctx, n_steps, nullptr, ms_out, speed_out);
+}
+extern "C" stadi_status stadi_profile_band(stadi_ctx *ctx, uint32_t n_steps, const uint32_t *units,
+                                           double *ms_out) {
+  ALIVE();
+  if (!ms_out || !units || n_steps == 0) return ctx_fail(ctx, STADI_EINVAL, "bad argument");
+  std::vector<uint64_t> sp(ctx->G);
+  return profile_impl(ctx, n_steps, units, ms_out, sp.data());
+}
+
+namespace {
+stadi_status profile_impl(stadi_ctx *ctx, uint32_t n_steps, const uint32_t *units, double *ms_out,
+                          uint64_t *speed_out) {
   if (!ctx->weights_loaded) return ctx_fail(ctx, STADI_ESTATE, "weights not loaded");
   const Dims &m = ctx->dm;
   CK(cudaSetDevice(ctx->device));
@@ -1590,6 +1607,10 @@ extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, d
   pp.rows_per_unit = m.unet ? (1u << (m.levels() - 1)) : (uint32_t)m.p;
   pp.p_total = m.lat_h / pp.rows_per_unit;
   pp.flags = STADI_NO_TA | STADI_NO_SA;
+  if (units) {  // stadi_profile_band: the caller's band sizes (forced units, R6 units)
+    pp.flags |= STADI_FORCE_UNITS;
+    pp.forced_units = units;
+  }
   if ((int)pp.p_total < ctx->G) return ctx_fail(ctx, STADI_EINVAL, "latent too small for group");
   stadi_plan_t probe;
   if (stadi_plan(&pp, &probe) != STADI_OK)
@@ -1659,6 +1680,7 @@ extern "C" stadi_status stadi_profile_warmup(stadi_ctx *ctx, uint32_t n_steps, d
   free_plan_buffers(ctx);
   return STADI_OK;
 }
+}  // namespace
 
 // ---------------------------------------------------------------- emulator (a9)
 extern "C" stadi_status stadi_emulator_start(stadi_ctx *ctx, uint32_t pct) {

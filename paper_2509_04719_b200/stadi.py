@@ -111,7 +111,7 @@ EXPORTS = [
     "stadi_load_weights", "stadi_profile_warmup", "stadi_set_plan", "stadi_begin",
     "stadi_num_steps", "stadi_denoise_step", "stadi_gather", "stadi_run",
     "stadi_emulator_start", "stadi_emulator_stop", "stadi_nccl_unique_id",
-    "stadi_ipc_session_id",
+    "stadi_ipc_session_id", "stadi_profile_band",
     "stadi_kernel_timing", "stadi_kernel_stats",
     "stadi_k_gemm", "stadi_k_gemm_ex", "stadi_k_attention", "stadi_k_ln_modulate",
     "stadi_k_conv3x3", "stadi_k_conv3x3_ex",
@@ -150,6 +150,8 @@ def _load():
         "stadi_emulator_stop": (C.c_int, [vp]),
         "stadi_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
         "stadi_ipc_session_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+        "stadi_profile_band": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_uint32),
+                                         C.POINTER(C.c_double)]),
         "stadi_kernel_timing": (C.c_int, [vp, C.c_int32]),
         "stadi_kernel_stats": (C.c_int, [vp, C.c_int32, C.POINTER(C.c_uint64),
                                          C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -314,6 +316,13 @@ class Context:
         sp = (C.c_uint64 * group)()
         self._c(lib.stadi_profile_warmup(self.h, n_steps, ms, sp))
         return list(ms), list(sp)
+
+    def profile_band(self, n_steps, units):
+        """Compute-only probe step ms of every rank's forced band (units per rank)."""
+        u = (C.c_uint32 * len(units))(*[int(v) for v in units])
+        ms = (C.c_double * len(units))()
+        self._c(lib.stadi_profile_band(self.h, n_steps, u, ms))
+        return list(ms)
 
     def set_plan(self, p: Plan):
         self._c(lib.stadi_set_plan(self.h, C.byref(p)))

@@ -28,6 +28,7 @@ def cached(key: dict, compute):
     STADI_WRITE_REFS=1 a computed result is stored (make_oracle_refs.py)."""
     p = key_path(key)
     if os.path.exists(p):
+        _KEYS[os.path.basename(p)] = key
         return np.load(p)
     out = compute()
     if os.environ.get("STADI_WRITE_REFS") == "1":
@@ -36,8 +37,6 @@ def cached(key: dict, compute):
         _KEYS[os.path.basename(p)] = key
         with open(os.path.join(DIR, "index.jsonl"), "a") as f:
             f.write(json.dumps({"file": os.path.basename(p), "key": key}, sort_keys=True, default=str) + "\n")
-    else:
-        _KEYS[os.path.basename(p)] = key
     return out
 
 

@@ -107,10 +107,12 @@ def test_plan_forced_and_errors(S):
     p = S.plan([10, 6], 100, 4, 32, flags=S.FORCE_UNITS, forced_units=[24, 8]).to_dict()
     assert p["units"] == [24, 8]
     for kw in [dict(speed=[0, 1], m_base=10, m_warmup=2, p_total=8),
-               dict(speed=[1, 1], m_base=10, m_warmup=11, p_total=8),
-               dict(speed=[10, 6], m_base=11, m_warmup=2, p_total=8)]:
+               dict(speed=[1, 1], m_base=10, m_warmup=11, p_total=8)]:
         with pytest.raises(S.StadiError):
             S.plan(**kw)
+    # R32: an odd K with a tier-2 GPU is planned with stride spf(K), not rejected
+    p = S.plan([10, 6], 11, 2, 8).to_dict()
+    assert p["sync_period"] == 3 and p["steps"] == [11, 5]
     with pytest.raises(S.StadiError):
         S.plan([1, 1], 10, 2, 8, a=(1, 4), b=(3, 4))
 
@@ -120,7 +122,7 @@ def test_schedule_bit_exact(S):
     for _ in range(500):
         n = rng.randint(1, 6)
         speed = [rng.randint(1, 1000) for _ in range(n)]
-        mb = rng.choice([10, 20, 50, 100])
+        mb = rng.choice([10, 20, 50, 100, 11, 27, 9, 51])
         mw = rng.choice([2, 4])
         try:
             ref = OP.plan(speed, mb, mw, 64, 2)

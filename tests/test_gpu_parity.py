@@ -95,6 +95,29 @@ def oracle_cases():
         yield cfg, W, x, c, OR.plan_for(cfg, C2_SPEED, 50, 4), dtype
         cfg, W, x, c = _inputs("pixart_alpha", **C5_KW)
         yield cfg, W, x, c, OR.plan_for(cfg, C5_SPEED, 20, 4), dtype
+        cfg, W, x, c = _inputs("tiny_dit")
+        for mb in ODD_K_MB:
+            yield cfg, W, x, c, OR.plan_for(cfg, [1 << 20, 1 << 19], mb, 2), dtype
+
+
+ODD_K_MB = (11, 9)   # K = 9 -> stride 3, K = 7 -> stride 7 (R32)
+
+
+@pytest.mark.parametrize("dtype", [1, 0], ids=["fp32", "bf16"])
+@pytest.mark.parametrize("mb", ODD_K_MB)
+def test_odd_k_slow_stride(S, dtype, mb):
+    """R32: an odd K = M_base - M_warmup gives the tier-2 rank stride spf(K) (3 or 7
+    fast-grid intervals per step) and the fast rank n - 1 non-publishing steps per
+    round; the schedule runs through the same exchange protocol."""
+    cfg, W, x, c = _inputs("tiny_dit")
+    speed = [1 << 20, 1 << 19]
+    plan = OR.plan_for(cfg, speed, mb, 2)
+    ref = _oracle(cfg, W, x, c, plan, dtype)
+    got, p, _ = _gpu_run(S, "tiny_dit", cfg, W, x, c, speed, mb, 2, dtype)
+    assert p.to_dict()["steps"] == plan["steps"] and p.sync_period == plan["sync_period"]
+    err = _rel(got, ref)
+    print(f"odd-K M_base={mb} stride={plan['sync_period']} dtype={dtype} max-abs-rel={err:.3e}")
+    assert err <= TOL[dtype]
 
 
 def _rel(a, b):
