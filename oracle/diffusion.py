@@ -24,6 +24,15 @@ Readings:
        z the full-image N(0, 1) draw of fast-grid index m (an INPUT here:
        synth/gen.py ddpm_noise); a stride-2 jump uses the same formula
        with t' = t_{m+2} and z_m.
+  R34  second-order multistep solver (L66: "Lu et al. [31], [32] identified the
+       semi-linear structure of diffusion ODEs and devised higher-order solvers"):
+       the multistep DPM-Solver-2 of [31]/[32] in noise-prediction form, i.e. Eq. 3
+       with eps replaced by
+         D = eps_s + (eps_s - eps_prev) / (2 r),   r = h_prev / h,
+       h = lambda_{t'} - lambda_s, h_prev = lambda_s - lambda_{s_prev}, where
+       (eps_prev, s_prev) are the eps and timestep of the SAME band's previous
+       step (a tier-2 rank's history spans its own stride); the first step of a
+       band has no history and is Eq. 3 itself.
 """
 from __future__ import annotations
 
@@ -74,6 +83,24 @@ def ddpm_step(abar, x, eps, t, t_prev, z):
     x0 = (x - np.sqrt(1.0 - ab) * eps) / np.sqrt(ab)
     s_eta = np.sqrt((1.0 - ab2) / (1.0 - ab)) * np.sqrt(1.0 - ab / ab2)
     return np.sqrt(ab2) * x0 + np.sqrt(1.0 - ab2 - s_eta ** 2) * eps + s_eta * z
+
+
+def lam(abar, t):
+    """lambda_t = log(alpha_t / sigma_t) (t = -1: alpha_bar_0, R18)."""
+    return alpha_sigma(abar, t)[2]
+
+
+def dpm2m_step(abar, x, eps, t, t_prev, hist):
+    """R34: multistep DPM-Solver-2 (noise prediction) from t to t_prev.  hist =
+    None (first step: Eq. 3) or (eps_prev, s_prev): the previous step of this band
+    went s_prev -> t with eps_prev."""
+    A, Bc = ddim_coeffs(abar, t, t_prev)
+    if hist is None:
+        return A * x + Bc * eps
+    eps_p, s_prev = hist
+    h = lam(abar, t_prev) - lam(abar, t)
+    r = (lam(abar, t) - lam(abar, s_prev)) / h
+    return A * x + Bc * (eps + (eps - eps_p) / (2.0 * r))
 
 
 def cfg_combine(eps_u, eps_c, w):

@@ -38,24 +38,31 @@ def _group_phases(plan):
     return [phases[m] for m in sorted(phases)]
 
 
-def _update(abar, x, eps, st, ddpm_z, r0):
+def _update(abar, x, eps, st, ddpm_z, r0, hist=None):
     """Sampler update of one band (rows [r0, r0 + len(x)) of the image): Eq. 3
-    DDIM, or the R19 DDPM step with the band's rows of z_m when ddpm_z (a
-    callable m -> full-image z_m, an input) is given."""
+    DDIM, the R19 DDPM step with the band's rows of z_m when ddpm_z (a callable
+    m -> full-image z_m, an input) is given, or (hist a dict: the band's history)
+    the R34 multistep DPM-Solver-2."""
+    if hist is not None:
+        out = diffusion.dpm2m_step(abar, x, eps, st.t, st.t_prev, hist.get("h"))
+        hist["h"] = (eps, st.t)
+        return out
     if ddpm_z is None:
         return diffusion.ddim_step(abar, x, eps, st.t, st.t_prev)
     z = ddpm_z(st.m)[r0:r0 + x.shape[0]]
     return diffusion.ddpm_step(abar, x, eps, st.t, st.t_prev, z)
 
 
-def run(cfg, weights, x_T, cond, plan, return_trace=False, ddpm_z=None):
+def run(cfg, weights, x_T, cond, plan, return_trace=False, ddpm_z=None, sampler="ddim"):
     """Execute STADI for one request.  x_T: full noise [H, W, C] (any float).
-    ddpm_z: None (DDIM, Eq. 3) or m -> z_m [H, W, C] (DDPM, R19).
+    ddpm_z: None (DDIM, Eq. 3) or m -> z_m [H, W, C] (DDPM, R19); sampler="dpm2m":
+    the R34 multistep DPM-Solver-2 (each band keeps its own history).
 
     Returns the final latent [H, W, C] (float64) assembled from the bands.
     """
+    hist = {r: {} for r in range(plan["n_gpus"])} if sampler == "dpm2m" else {}
     if cfg["family"] == "unet":
-        return run_unet(cfg, weights, x_T, cond, plan, return_trace, ddpm_z)
+        return run_unet(cfg, weights, x_T, cond, plan, return_trace, ddpm_z, hist)
     model = dit.DiT(cfg, weights)
     abar = diffusion.alpha_bar("linear" if cfg["schedule"] == "linear" else "scaled_linear")
     B = dit.batch_of(cfg)
@@ -94,7 +101,7 @@ def run(cfg, weights, x_T, cond, plan, return_trace=False, ddpm_z=None):
         for P in parts:                          # eps on own band + Eq. 3 on own rows
             r, st = P["r"], P["st"]
             eps = dit.guided_eps(cfg, model.final(P["h"], P["fin"], band[r].shape[0]))
-            band[r] = _update(abar, band[r], eps, st, ddpm_z, plan["row_begin"][r])
+            band[r] = _update(abar, band[r], eps, st, ddpm_z, plan["row_begin"][r], hist.get(r))
             if return_trace:
                 trace.append((st.m, r, st.kind, band[r].copy()))
     import numpy as np
@@ -126,7 +133,7 @@ def _assemble(kind, r, inc, own, stale):
     raise ValueError(kind)
 
 
-def run_unet(cfg, weights, x_T, cond, plan, return_trace=False, ddpm_z=None):
+def run_unet(cfg, weights, x_T, cond, plan, return_trace=False, ddpm_z=None, hist=None):
     """Algorithm 1 for the U-Net family: every rank's band forward is a
     generator (oracle/unet.py) that yields at each exchange site; ranks of a
     phase advance in lock-step site by site: all publish (pub_ver), then all
@@ -163,7 +170,7 @@ def run_unet(cfg, weights, x_T, cond, plan, return_trace=False, ddpm_z=None):
             site += 1
         for r, st in phase:                      # eps on own band + Eq. 3 on own rows
             band[r] = _update(abar, band[r], unet.guided_eps(cfg, eps[r]), st, ddpm_z,
-                              plan["row_begin"][r])
+                              plan["row_begin"][r], (hist or {}).get(r))
             if return_trace:
                 trace.append((st.m, r, st.kind, band[r].copy()))
     out = np.concatenate([band[r] for r in inc], axis=0)   # final synchronous all-gather
@@ -175,11 +182,16 @@ def _cat(xs):
     return np.concatenate(xs, axis=1)
 
 
-def sequential(cfg, weights, x_T, cond, m_base, ddpm_z=None):
-    """Non-distributed DDIM (or R19 DDPM) with M_base steps on the fast grid
-    (the "Origin" method of Table II)."""
+def sequential(cfg, weights, x_T, cond, m_base, ddpm_z=None, sampler="ddim"):
+    """Non-distributed DDIM (or R19 DDPM, or R34 DPM-Solver-2M) with M_base steps on
+    the fast grid (the "Origin" method of Table II)."""
+    hist = {}
 
     def upd(abar, x, eps, m, t, t_prev):
+        if sampler == "dpm2m":
+            out = diffusion.dpm2m_step(abar, x, eps, t, t_prev, hist.get("h"))
+            hist["h"] = (eps, t)
+            return out
         if ddpm_z is None:
             return diffusion.ddim_step(abar, x, eps, t, t_prev)
         return diffusion.ddpm_step(abar, x, eps, t, t_prev, ddpm_z(m))
