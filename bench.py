@@ -414,6 +414,34 @@ def run_method(args, cfg, wl, mode=None, pairs=None, steps=None):
     grp.call("profile_warmup", 1, n)        # loads every kernel before any emulator
     rows = []
     t0 = time.time()
+    if mode == "replan":
+        # SURVEY §8(f)4 dynamic re-planning: the occupancy changes between requests;
+        # a static plan (profiled once, under the first setting) vs re-profiling (a
+        # 1-step probe) and re-planning before every request
+        seq = pairs if len(pairs) > 1 else [[0, 50], [50, 0], [0, 0], [0, 60]][: max(2, len(pairs))]
+        static = None
+        try:
+            for occ in seq:
+                grp.call("emulator_start", per_rank=lambda r: {"pct": occ[r]})
+                try:
+                    tp = time.time()
+                    ms, speed = grp.call("profile_warmup", 1, n)[0]
+                    t_prof = (time.time() - tp) * 1e3
+                    pl = S.plan(speed, mb, mw, P, p)
+                    if static is None:
+                        static = pl
+                    lat_s, _ = _time_plan(S, grp, static, x, c, steps, 1)
+                    lat_r, _ = _time_plan(S, grp, pl, x, c, steps, 1)
+                    rows.append({"occupancy_pct": occ, "speed_q20": [int(v) for v in speed],
+                                 "static": {"plan": _plan_json(static), "ms_per_image": lat_s},
+                                 "replanned": {"plan": _plan_json(pl), "ms_per_image": lat_r,
+                                               "probe_overhead_ms": t_prof},
+                                 "replan_latency_reduction": 1.0 - lat_r / lat_s})
+                finally:
+                    grp.call("emulator_stop")
+        finally:
+            grp.close()
+        pairs = []
     try:
         for occ in pairs:
             grp.call("emulator_start", per_rank=lambda r: {"pct": occ[r]})
@@ -508,7 +536,7 @@ def main():
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="N > 1 exchange transport (IPC: fused one-sided P2P, the default)")
     ap.add_argument("--mode", default="headline",
-                    choices=["headline", "ablation", "fig8", "fig9", "alphabeta"],
+                    choices=["headline", "ablation", "fig8", "fig9", "alphabeta", "replan"],
                     help="method-level measurements on virtual GPUs (one device)")
     ap.add_argument("--vgpu-sms", type=int, default=0, help="SMs per virtual GPU (mult. of 8)")
     ap.add_argument("--m-base", type=int, default=0, help="override the workload's M_base")

@@ -176,14 +176,18 @@ enum { STADI_DTYPE_BF16 = 0, STADI_DTYPE_FP32_DEBUG = 1 };
  * step of ref. [28] (R19): x' = alpha' x0_hat + sqrt(1 - abar' - s^2) eps + s z_m,
  * s = sqrt((1 - abar')/(1 - abar)) sqrt(1 - abar/abar'), z_m drawn in the
  * sampler kernel from the counter-based generator keyed by stadi_cond.ddpm_seed. */
-enum { STADI_SAMPLER_DDIM = 0, STADI_SAMPLER_DDPM = 1 };
+/* DPM2M: R34, the multistep DPM-Solver-2 of Lu et al. (L66 "higher-order solvers",
+ * refs [31], [32]) in noise-prediction form: Eq. 3 with eps replaced by
+ * eps + (eps - eps_prev) / (2 r), r = h_prev / h, eps_prev the band's previous own
+ * step (first step: Eq. 3). */
+enum { STADI_SAMPLER_DDIM = 0, STADI_SAMPLER_DDPM = 1, STADI_SAMPLER_DPM2M = 2 };
 
 typedef struct {
   int32_t preset;          /* STADI_PRESET_*                                     */
   int32_t dtype;           /* BF16: tcgen05 bf16 GEMM/attention, fp32 accumulate,
                               fp32 residual + latent; FP32_DEBUG: SIMT fp32 (no
                               TF32) kernels for the <=1e-4 parity build         */
-  int32_t sampler;         /* STADI_SAMPLER_DDIM | STADI_SAMPLER_DDPM (EINVAL else) */
+  int32_t sampler;         /* STADI_SAMPLER_DDIM | _DDPM | _DPM2M (EINVAL else)   */
   int32_t depth;           /* 0 = preset depth; >0: DiT blocks, or the cap on every
                               U-Net transformer depth (reduced parity variants)  */
   int32_t latent_h, latent_w; /* 0 = preset resolution                           */

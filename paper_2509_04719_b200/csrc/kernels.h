@@ -52,11 +52,13 @@ cudaError_t patch_embed(const float *x_band, int rows, int W, int C, int p, cons
 //   Philox4x64-10 with key (seed, m) at the element's full-image index, the
 //   band starting at latent row row0).  eps_raw row stride = ld (>= p*p*c_out).
 //   The key is *seed_dev when seed_dev != NULL (read at run time, so a captured
-//   CUDA graph serves every request), else `seed`.
+//   CUDA graph serves every request), else `seed`.  hist != NULL (R34 multistep
+//   DPM-Solver-2): eps -> c1 eps + c2 hist (hist = the band's previous combined eps;
+//   c2 == 0: first step), and hist <- eps.
 cudaError_t sampler_update(float *x_band, const float *eps_raw, int rows, int W, int C, int p,
                            int c_out, int ld, int B, float guidance, float A, float Bc,
                            float Cz, uint64_t seed, const uint64_t *seed_dev, uint32_t m, int row0,
-                           cudaStream_t s);
+                           cudaStream_t s, float *hist = nullptr, float c1 = 1.f, float c2 = 0.f);
 // z_m elements [e0, e0 + n) of the R19 generator (parity tests).
 cudaError_t philox_normal_fill(float *out, long n, uint64_t seed, uint32_t m, long e0,
                                cudaStream_t s);

@@ -366,7 +366,8 @@ __device__ __forceinline__ float philox_normal(uint64_t seed, uint32_t m, uint64
 __global__ void sampler_kernel(float *__restrict__ xb, const float *__restrict__ eps, int rows,
                                int W, int C, int p, int c_out, int ld, int B, float g, float A,
                                float Bc, float Cz, uint64_t seed, const uint64_t *seed_dev,
-                               uint32_t m, int row0) {
+                               uint32_t m, int row0, float *__restrict__ hist, float c1,
+                               float c2) {
   const long n = (long)rows * W * C;
   const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n) return;
@@ -381,6 +382,11 @@ __global__ void sampler_kernel(float *__restrict__ xb, const float *__restrict__
   if (B == 2) {
     const float ec = eps[(tok * B + 1) * ncol + j];
     e = e + g * (ec - e);                                   // CFG (R20)
+  }
+  if (hist) {  // R34 multistep DPM-Solver-2: D = c1 eps + c2 eps_prev; keep eps
+    const float d = c2 != 0.f ? c1 * e + c2 * hist[idx] : e;
+    hist[idx] = e;
+    e = d;
   }
   float x = A * xb[idx] + Bc * e;                           // Eq. 3 (DDIM)
   if (Cz != 0.f) {                                          // R19 DDPM: + sigma_eta z_m
@@ -414,11 +420,12 @@ cudaError_t patch_embed(const float *x_band, int rows, int W, int C, int p, cons
 cudaError_t sampler_update(float *x_band, const float *eps_raw, int rows, int W, int C, int p,
                            int c_out, int ld, int B, float guidance, float A, float Bc,
                            float Cz, uint64_t seed, const uint64_t *seed_dev, uint32_t m, int row0,
-                           cudaStream_t s) {
+                           cudaStream_t s, float *hist, float c1, float c2) {
   const long n = (long)rows * W * C;
   if (n == 0) return cudaSuccess;
   sampler_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-      x_band, eps_raw, rows, W, C, p, c_out, ld, B, guidance, A, Bc, Cz, seed, seed_dev, m, row0);
+      x_band, eps_raw, rows, W, C, p, c_out, ld, B, guidance, A, Bc, Cz, seed, seed_dev, m, row0,
+      hist, c1, c2);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -81,6 +81,7 @@ struct Rank {
   int tier = 0;
   std::vector<stadi_step_t> sched;
   float *x_band = nullptr;         // [rows, W, C_in] fp32
+  float *hist = nullptr;           // [rows, W, C_in] fp32 previous combined eps (DPM2M, R34)
   float *x_res = nullptr;          // [n_tok*B, d] fp32 residual stream
   void *xmod = nullptr, *q = nullptr, *o = nullptr, *h1 = nullptr;  // T activations
   float *eps_raw = nullptr;        // [n_tok*B, fin_ld] fp32
@@ -404,7 +405,7 @@ void ddim_coeffs(const double *ab, int t, int t_prev, float *A, float *Bc) {
 // R19 DDPM (eta = 1) as x' = A x + Bc eps + Cz z:  with x0 = (x - sigma eps) / alpha,
 // x' = alpha' x0 + sqrt(1 - abar' - s^2) eps + s z, s = sqrt((1-abar')/(1-abar)) sqrt(1 - abar/abar').
 void sampler_coeffs(const stadi_ctx *ctx, int t, int t_prev, float *A, float *Bc, float *Cz) {
-  if (ctx->sampler == STADI_SAMPLER_DDIM) {
+  if (ctx->sampler != STADI_SAMPLER_DDPM) {  // DDIM and DPM2M: Eq. 3's A, Bc
     ddim_coeffs(ctx->abar, t, t_prev, A, Bc);
     *Cz = 0.f;
     return;
@@ -414,6 +415,25 @@ void sampler_coeffs(const stadi_ctx *ctx, int t, int t_prev, float *A, float *Bc
   *A = (float)(std::sqrt(a2) / std::sqrt(a1));
   *Bc = (float)(std::sqrt(1 - a2 - se * se) - std::sqrt(a2) * std::sqrt(1 - a1) / std::sqrt(a1));
   *Cz = (float)se;
+}
+
+// R34 multistep DPM-Solver-2: D = c1 eps + c2 eps_prev, c1 = 1 + 1/(2r), c2 = -1/(2r),
+// r = h_prev / h from the band's own previous step (schedule entry idx - 1); the first
+// step (idx 0) is Eq. 3 (c2 = 0).
+void dpm2m_coeffs(const stadi_ctx *ctx, const std::vector<stadi_step_t> &sched, int idx,
+                  float *c1, float *c2) {
+  *c1 = 1.f;
+  *c2 = 0.f;
+  if (ctx->sampler != STADI_SAMPLER_DPM2M || idx <= 0) return;
+  auto lam = [&](int t) {
+    const double ab = t < 0 ? ctx->abar[0] : ctx->abar[t];
+    return 0.5 * std::log(ab / (1.0 - ab));
+  };
+  const stadi_step_t &st = sched[idx];
+  const double h = lam(st.t_prev) - lam(st.t), hp = lam(st.t) - lam(sched[idx - 1].t);
+  const double r = hp / h;
+  *c1 = (float)(1.0 + 0.5 / r);
+  *c2 = (float)(-0.5 / r);
 }
 
 // ---------------------------------------------------------------- kernel timing
@@ -536,7 +556,8 @@ void free_plan_buffers(stadi_ctx *ctx) {
   free_graphs(ctx);
   unet_free_plan(ctx);
   for (auto &r : ctx->ranks) {
-    for (void *p : {(void *)r.x_band, (void *)r.x_res, r.xmod, r.q, r.o, r.h1, (void *)r.eps_raw})
+    for (void *p : {(void *)r.x_band, (void *)r.x_res, r.xmod, r.q, r.o, r.h1, (void *)r.eps_raw,
+                    (void *)r.hist})
       pfree(ctx, p);
     if (!ctx->ipc_mode)  // IPC mode: the slots live in the (persistent) exchange arena
       for (void *p : r.kv) pfree(ctx, p);
@@ -621,7 +642,8 @@ extern "C" stadi_status stadi_create(const stadi_model_desc *model, const stadi_
   if (!make_dims(*model, dm, e)) return fail(nullptr, STADI_EINVAL, "%s", e.c_str());
   if (model->dtype != STADI_DTYPE_BF16 && model->dtype != STADI_DTYPE_FP32_DEBUG)
     return fail(nullptr, STADI_EINVAL, "bad dtype");
-  if (model->sampler != STADI_SAMPLER_DDIM && model->sampler != STADI_SAMPLER_DDPM)
+  if (model->sampler != STADI_SAMPLER_DDIM && model->sampler != STADI_SAMPLER_DDPM &&
+      model->sampler != STADI_SAMPLER_DPM2M)
     return fail(nullptr, STADI_EINVAL, "bad sampler");
   if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || dist->n_local < 1 ||
       (dist->world > 1 && dist->n_local != 1) || dist->world * dist->n_local > STADI_MAX_GPUS)
@@ -940,6 +962,8 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     stadi_schedule(plan, g, r.sched.data(), n, &n);
     const int64_t M = (int64_t)r.n_tok * m.B;
     CK(pmalloc(ctx, &r.x_band, std::max<int64_t>(16, (int64_t)r.rows * m.lat_w * m.c_in * 4)));
+    if (ctx->sampler == STADI_SAMPLER_DPM2M)
+      CK(pmalloc(ctx, &r.hist, std::max<int64_t>(16, (int64_t)r.rows * m.lat_w * m.c_in * 4)));
     if (m.unet) {  // the U-Net program owns its buffers (unet_set_plan)
       ctx->ranks.push_back(std::move(r));
       continue;
@@ -1385,13 +1409,14 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
     ef.out = r.eps_raw;
     ef.ldo = ctx->fin_ld;
     CK(gemm(ctx, r.xmod, ctx->final_w, M, ctx->fin_ld, (int)d, EPI_F32, ef, s));
-    float A, Bc, Cz;
+    float A, Bc, Cz, c1, c2;
     sampler_coeffs(ctx, P.st.t, P.st.t_prev, &A, &Bc, &Cz);
+    dpm2m_coeffs(ctx, r.sched, P.idx, &c1, &c2);
     const double sb = (double)r.rows * m.lat_w * m.c_in * 8 + (double)M * ctx->fin_ld * 4;
     CK(timed(ctx, STADI_KCLASS_SAMPLER, 0.0, sb, s, [&] {
       return sampler_update(r.x_band, r.eps_raw, r.rows, m.lat_w, m.c_in, m.p, m.c_out,
                             ctx->fin_ld, B, m.guidance, A, Bc, Cz, ctx->ddpm_seed, ctx->seed_dev,
-                            P.st.m, r.row_begin, s);
+                            P.st.m, r.row_begin, s, r.hist, c1, c2);
     }));
   }
   return STADI_OK;

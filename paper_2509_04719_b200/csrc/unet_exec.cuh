@@ -805,13 +805,17 @@ struct UBuilder {
       const int h = rows(0), W = width(0);
       op([=](const stadi_step_t &st, cudaStream_t s) -> stadi_status {
         stadi_ctx *ctx = c;
-        float A, Bc, Cz;
+        float A, Bc, Cz, c1, c2;
         sampler_coeffs(ctx, st.t, st.t_prev, &A, &Bc, &Cz);
+        const auto &sc = ctx->ranks[me].sched;
+        int idx = 0;
+        while (idx < (int)sc.size() && sc[idx].m != st.m) ++idx;
+        dpm2m_coeffs(ctx, sc, idx, &c1, &c2);
         const double sb = (double)h * W * 4 * 8 + (double)h * W * B * 64 * 4;
         CK(timed(ctx, STADI_KCLASS_SAMPLER, 0.0, sb, s, [&] {
           return sampler_update(ctx->ranks[me].x_band, (const float *)E(), h, W, ctx->dm.c_in, 1,
                                 4, 64, B, ctx->dm.guidance, A, Bc, Cz, ctx->ddpm_seed, ctx->seed_dev,
-                                st.m, ctx->ranks[me].row_begin, s);
+                                st.m, ctx->ranks[me].row_begin, s, ctx->ranks[me].hist, c1, c2);
         }));
         return STADI_OK;
       });

@@ -23,7 +23,7 @@ T_FINAL = -1
 VER_NONE = -1
 PRESET = {"tiny_dit": 0, "dit_xl2": 1, "pixart_alpha": 2, "sd15": 3, "sdxl": 4, "tiny_unet": 5}
 DTYPE_BF16, DTYPE_FP32_DEBUG = 0, 1
-SAMPLER_DDIM, SAMPLER_DDPM = 0, 1
+SAMPLER_DDIM, SAMPLER_DDPM, SAMPLER_DPM2M = 0, 1, 2
 EPI_STORE, EPI_GELU, EPI_GATED_RES, EPI_RES, EPI_QKV, EPI_F32, EPI_CONV, EPI_GEGLU = range(8)
 KCLASS = {"gemm": 0, "attn": 1, "xattn": 2, "norm": 3, "sampler": 4, "xwait": 5}
 TRANSPORT_NCCL, TRANSPORT_IPC = 0, 1
