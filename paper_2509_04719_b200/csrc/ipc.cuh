@@ -452,6 +452,22 @@ bool ipc_probe_graphs(stadi_ctx *ctx) {
   return ok;
 }
 
+// Watchdog fired (a peer is gone): set every flag of this rank's arena to its maximum
+// from a side stream so the streams blocked in flag waits drain (the request's
+// results are void; the context is poisoned by the caller).
+void ipc_unblock(stadi_ctx *ctx) {
+  if (!ctx->ipc || !ctx->ipc->arena) return;
+  IpcState &I = *ctx->ipc;
+  // 0x7F7F7F7F: above every version / count / request id under the wrap-safe
+  // GEQ compare ((int32_t)(*addr - v) >= 0), which 0xFFFFFFFF would fail
+  cudaMemsetAsync(I.arena + I.off_gflag, 0x7F, 4 * (size_t)ctx->world, ctx->astream);
+  cudaMemsetAsync(I.arena + I.off_barrier, 0x7F, 4 * (size_t)ctx->world, ctx->astream);
+  if (I.n_sites)
+    cudaMemsetAsync(I.arena + I.off_ready, 0x7F,
+                    I.off_done - I.off_ready + (size_t)4 * I.n_sites * ctx->world, ctx->astream);
+  cudaStreamSynchronize(ctx->astream);
+}
+
 void ipc_release(stadi_ctx *ctx) {  // destroy (device already synchronised)
   if (!ctx->ipc) return;
   IpcState &I = *ctx->ipc;

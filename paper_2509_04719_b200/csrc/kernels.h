@@ -84,6 +84,11 @@ cudaError_t pixart_mods(const float *t0, const float *temb, const float *sst_all
 constexpr int GN_PARTIAL_BLOCKS = 592;
 cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, double *ws,
                         unsigned *ticket, cudaStream_t s);
+// Halo rows of the padded conv input P [h+2, W+2, B, C]: row 0 <- above, row h+1
+// <- below (W*B*C elements each; NULL = zeros at the image edge), corners zero.
+template <typename T>
+cudaError_t halo_fill(T *P, int h, int W, int B, int C, const T *above, const T *below,
+                      cudaStream_t s);
 // GroupNorm with the statistics summed over G rank segments [G][B][32][2]
 // (stats == null: plain cast), optional SiLU, pad = write into P's interior.
 template <typename T>

@@ -220,6 +220,40 @@ __global__ void __launch_bounds__(256) im2col_kernel(const T *__restrict__ P, in
   }
 }
 
+// ------------------------------------------------------------- halo rows
+// The two halo rows of the padded conv input P [h+2, W+2, B, C]: row 0 = `above`
+// (W * B * C elements, or zeros at the image's top edge when null), row h+1 =
+// `below` (or zeros), and the four corner cells zero.  One launch replaces two
+// copies and four memsets per conv.  16-byte vectors (C * esz % 16 == 0) when aligned.
+template <typename T>
+__global__ void __launch_bounds__(256) halo_fill_kernel(T *__restrict__ P, int h, int W, int B,
+                                                        int C, const T *__restrict__ above,
+                                                        const T *__restrict__ below) {
+  const long rowe = (long)(W + 2) * B * C;        // elements of one padded row
+  const long inner = (long)W * B * C;             // interior elements of a row
+  const long cell = (long)B * C;
+  constexpr int V = 16 / sizeof(T);
+  const bool vec = (cell % V) == 0;
+  const long n = vec ? 2 * rowe / V : 2 * rowe;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x) {
+    const long e = vec ? i * V : i;               // element offset within the two rows
+    const int r = (int)(e / rowe);                 // 0: top halo, 1: bottom halo
+    const long off = e % rowe;                     // within the padded row
+    const long x = off - cell;                     // within the interior
+    const T *src = r ? below : above;
+    T *dst = P + (r ? (long)(h + 1) * rowe : 0) + off;
+    const bool interior = x >= 0 && x < inner;
+    if (vec) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (interior && src) v = *reinterpret_cast<const uint4 *>(src + x);
+      *reinterpret_cast<uint4 *>(dst) = v;
+    } else {
+      *dst = (interior && src) ? src[x] : from_f<T>(0.f);
+    }
+  }
+}
+
 // ------------------------------------------------------------- concat
 __global__ void concat_kernel(const float *__restrict__ a, int Ca, const float *__restrict__ b,
                               int Cb, long M, float *__restrict__ out) {
@@ -276,6 +310,20 @@ template cudaError_t gn_apply<bf16>(const float *, int, int, int, int, const dou
 template cudaError_t gn_apply<float>(const float *, int, int, int, int, const double *, int,
                                      double, const float *, const float *, float, int, int,
                                      float *, cudaStream_t);
+
+template <typename T>
+cudaError_t halo_fill(T *P, int h, int W, int B, int C, const T *above, const T *below,
+                      cudaStream_t s) {
+  const long rowe = (long)(W + 2) * B * C;
+  const long work = 2 * rowe / (((long)B * C) % (16 / sizeof(T)) == 0 ? 16 / sizeof(T) : 1);
+  halo_fill_kernel<T><<<grid_for(work), 256, 0, s>>>(P, h, W, B, C, above, below);
+  ++g_launches;
+  return cudaGetLastError();
+}
+template cudaError_t halo_fill<bf16>(bf16 *, int, int, int, int, const bf16 *, const bf16 *,
+                                     cudaStream_t);
+template cudaError_t halo_fill<float>(float *, int, int, int, int, const float *, const float *,
+                                      cudaStream_t);
 
 template <typename T>
 cudaError_t latent_pad(const float *x, int h, int W, int Cl, int B, T *out, cudaStream_t s) {

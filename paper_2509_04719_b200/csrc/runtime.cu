@@ -23,12 +23,14 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <functional>
 #include <map>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.h"
@@ -51,6 +53,8 @@ struct NcclApi {
   decltype(&ncclGroupStart) GroupStart = nullptr;
   decltype(&ncclGroupEnd) GroupEnd = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
+  decltype(&ncclCommAbort) CommAbort = nullptr;
 };
 NcclApi &nccl() {
   static NcclApi api;
@@ -62,7 +66,8 @@ NcclApi &nccl() {
     if (h) {
 #define LD(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f))
       LD(GetUniqueId); LD(CommInitRank); LD(CommDestroy); LD(CommSplit); LD(Broadcast);
-      LD(AllGather); LD(GroupStart); LD(GroupEnd); LD(GetErrorString);
+      LD(AllGather); LD(GroupStart); LD(GroupEnd); LD(GetErrorString); LD(CommGetAsyncError);
+      LD(CommAbort);
 #undef LD
       api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast &&
                api.AllGather && api.GroupStart && api.GroupEnd;
@@ -297,6 +302,63 @@ cudaError_t quiesce(stadi_ctx *ctx) {
   if (e == cudaSuccess && ctx->astream) e = cudaStreamSynchronize(ctx->astream);
   if (e == cudaSuccess && ctx->wstream) e = cudaStreamSynchronize(ctx->wstream);
   return e;
+}
+
+void ipc_unblock(stadi_ctx *ctx);  // ipc.cuh
+
+// Host wait for an event with a watchdog (SURVEY §5 failure detection): in NCCL mode
+// poll ncclCommGetAsyncError; with any exchange transport give up after
+// STADI_EXCHANGE_TIMEOUT_S seconds (default 600) -- a dead peer or a broken
+// collective then poisons the context (NCCL: the communicators are aborted) instead
+// of hanging the process forever.
+double exchange_timeout_s() {
+  static const double v = [] {
+    const char *e = getenv("STADI_EXCHANGE_TIMEOUT_S");
+    return e ? atof(e) : 600.0;
+  }();
+  return v;
+}
+stadi_status wait_event_watchdog(stadi_ctx *ctx, cudaEvent_t ev) {
+  if (!ctx->nccl && !ctx->ipc_mode) {
+    const cudaError_t e = cudaEventSynchronize(ev);
+    return e == cudaSuccess ? STADI_OK
+                            : ctx_fail(ctx, STADI_ECUDA, "event sync: %s", cudaGetErrorString(e));
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t it = 0;; ++it) {
+    const cudaError_t e = cudaEventQuery(ev);
+    if (e == cudaSuccess) return STADI_OK;
+    if (e != cudaErrorNotReady)
+      return ctx_fail(ctx, STADI_ECUDA, "event query: %s", cudaGetErrorString(e));
+    if (ctx->nccl && nccl().CommGetAsyncError) {
+      for (ncclComm_t c : {ctx->world_comm, ctx->sub_comm}) {
+        ncclResult_t ar = ncclSuccess;
+        if (c && nccl().CommGetAsyncError(c, &ar) == ncclSuccess && ar != ncclSuccess &&
+            ar != ncclInProgress) {
+          if (nccl().CommAbort) {
+            if (ctx->sub_comm && ctx->sub_comm != ctx->world_comm) nccl().CommAbort(ctx->sub_comm);
+            if (ctx->world_comm) nccl().CommAbort(ctx->world_comm);
+            ctx->sub_comm = ctx->world_comm = nullptr;
+          }
+          return ctx_fail(ctx, STADI_ENCCL, "NCCL asynchronous error: %s",
+                          nccl().GetErrorString ? nccl().GetErrorString(ar) : "?");
+        }
+      }
+    }
+    const double el =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > exchange_timeout_s()) {
+      if (ctx->nccl && nccl().CommAbort) {
+        if (ctx->sub_comm && ctx->sub_comm != ctx->world_comm) nccl().CommAbort(ctx->sub_comm);
+        if (ctx->world_comm) nccl().CommAbort(ctx->world_comm);
+        ctx->sub_comm = ctx->world_comm = nullptr;
+      }
+      if (ctx->ipc_mode) ipc_unblock(ctx);  // release this rank's flag waits (results void)
+      return ctx_fail(ctx, ctx->nccl ? STADI_ENCCL : STADI_ECUDA,
+                      "exchange watchdog: request not complete after %.0f s (peer lost?)", el);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(it < 1000 ? 20 : 200));
+  }
 }
 
 template <typename P>
@@ -1578,7 +1640,7 @@ extern "C" stadi_status stadi_run(stadi_ctx *ctx, const stadi_plan_t *plan, cons
   DBG("run: gather enqueued");
   CK(cudaEventRecord(e1, s));
   CK(leave_stream(ctx, (cudaStream_t)stream));
-  CK(cudaEventSynchronize(e1));
+  ST(wait_event_watchdog(ctx, e1));
   DBG("run: done");
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, e0, e1));

@@ -494,23 +494,16 @@ struct UBuilder {
       if (st.pub_ver == st.read_ver) ST(u_wait(ctx, S, st.read_ver, s));
       const int pos = inc_pos(U, ctx->ranks[me].g);
       const size_t rb = (size_t)rowe * ctx->esz;
-      char *above = (char *)D() + ((size_t)0 * (W + 2) + 1) * B * C * ctx->esz;
-      char *below = (char *)D() + ((size_t)(h + 1) * (W + 2) + 1) * B * C * ctx->esz;
       const char *sl = (const char *)S.slot[me][st.read_ver & 1];
-      if (top) CK(cudaMemsetAsync(above, 0, rb, s));
-      else CK(cudaMemcpyAsync(above, sl + (pos - 1) * S.seg_bytes + rb, rb,
-                              cudaMemcpyDeviceToDevice, s));
-      if (bottom) CK(cudaMemsetAsync(below, 0, rb, s));
-      else CK(cudaMemcpyAsync(below, sl + (pos + 1) * S.seg_bytes, rb,
-                              cudaMemcpyDeviceToDevice, s));
-      // corner cells of the halo rows (border columns) are zero
-      CK(cudaMemsetAsync((char *)D(), 0, (size_t)B * C * ctx->esz, s));
-      CK(cudaMemsetAsync((char *)D() + ((size_t)0 * (W + 2) + W + 1) * B * C * ctx->esz, 0,
-                         (size_t)B * C * ctx->esz, s));
-      CK(cudaMemsetAsync((char *)D() + ((size_t)(h + 1) * (W + 2)) * B * C * ctx->esz, 0,
-                         (size_t)B * C * ctx->esz, s));
-      CK(cudaMemsetAsync((char *)D() + ((size_t)(h + 1) * (W + 2) + W + 1) * B * C * ctx->esz,
-                         0, (size_t)B * C * ctx->esz, s));
+      // the neighbours' boundary rows (or zeros at the image edge) into the two halo
+      // rows, corner cells zero: one kernel
+      const void *above = top ? nullptr : sl + (pos - 1) * S.seg_bytes + rb;
+      const void *below = bottom ? nullptr : sl + (pos + 1) * S.seg_bytes;
+      if (ctx->dtype == STADI_DTYPE_BF16)
+        CK(halo_fill<bf16>((bf16 *)D(), h, W, B, C, (const bf16 *)above, (const bf16 *)below, s));
+      else
+        CK(halo_fill<float>((float *)D(), h, W, B, C, (const float *)above, (const float *)below,
+                            s));
       ST(u_done(ctx, S, s));
       EpiParams ep{};
       ep.B = B;

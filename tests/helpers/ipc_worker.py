@@ -24,6 +24,7 @@ def main():
     out_dir, rank, world, sess, name, dtype, speeds, mb, mw, flags = sys.argv[1:11]
     kw = json.loads(sys.argv[11]) if len(sys.argv) > 11 else {}
     requests = int(sys.argv[12]) if len(sys.argv) > 12 else 1
+    role = sys.argv[13] if len(sys.argv) > 13 else ""   # "die": install the plan, then vanish
     rank, world, dtype, mb, mw, flags = int(rank), int(world), int(dtype), int(mb), int(mw), int(flags)
     speed = [int(v) for v in speeds.split(",")]
     cfg = configs.model(name, **kw)
@@ -40,6 +41,18 @@ def main():
         ms, sp = ctx.profile_warmup(2, world)          # collective probe through the files
         assert len(ms) == world and all(m > 0 for m in ms)
         p = S.plan(speed, mb, mw, cfg["latent_h"] // u, u, flags=flags)
+        if role:
+            ctx.set_plan(p)
+            if role == "die":
+                os._exit(0)                              # a lost peer: no request, no close
+            try:                                         # role "survive": the watchdog fires
+                ctx.run(p, x, c, np.zeros_like(x))
+                status = "completed"
+            except S.StadiError as e:
+                status = f"error {e.status}: {e}"
+            with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+                json.dump(dict(watchdog=status), f)
+            return
         outs, stats = [], []
         for q in range(requests):
             ctx.kernel_timing(q == requests - 1)        # last request: eager, timed waits

@@ -120,3 +120,31 @@ def test_ipc_multiprocess(S, case):
     for r in inc:
         if len(inc) > 1:
             assert xb[r] > 0                     # bytes did cross between processes
+
+
+def test_ipc_watchdog_lost_peer(S):
+    """SURVEY §5 failure detection: a peer that installs the plan and then vanishes
+    must not hang the survivor.  Its request's flag waits never complete; the host
+    watchdog (STADI_EXCHANGE_TIMEOUT_S) releases the waits, poisons the context and
+    stadi_run returns an error; close() then returns."""
+    sess = S.ipc_session_id()[:16].hex()
+    env = dict(os.environ, STADI_EXCHANGE_TIMEOUT_S="5")
+    with tempfile.TemporaryDirectory() as d:
+        args = [d, "", "2", sess, "tiny_dit", "0", f"{1 << 20},{1 << 19}", "10", "2", "0", "{}", "1"]
+        procs = []
+        for r, role in ((0, "survive"), (1, "die")):
+            a = list(args)
+            a[1] = str(r)
+            procs.append(subprocess.Popen([sys.executable, WORKER] + a + [role], env=env,
+                                          stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                          text=True))
+        try:
+            logs = [p.communicate(timeout=180)[0] for p in procs]
+        finally:
+            for p in procs:
+                if p.poll() is None:
+                    p.kill()
+        assert procs[0].returncode == 0, logs[0][-2000:]
+        res = json.load(open(os.path.join(d, "rank0.json")))
+    print(f"IPC watchdog: survivor saw {res['watchdog']}")
+    assert res["watchdog"].startswith("error")   # an error, not a hang (watchdog or lost peer)
