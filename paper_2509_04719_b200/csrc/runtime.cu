@@ -1516,7 +1516,8 @@ stadi_status exec_step(stadi_ctx *ctx, uint32_t i, cudaStream_t s) {
   if (!G.exec) {
     // capture on the context's own stream (the caller's may be the legacy stream)
     if (dbg) fprintf(stderr, "[stadi r%d] step %u: sync\n", ctx->rank, i);
-    CK(cudaStreamSynchronize(s));
+    CK(cudaEventRecord(ctx->ev_ready, s));  // host wait under the exchange watchdog
+    ST(wait_event_watchdog(ctx, ctx->ev_ready));
     if (dbg) fprintf(stderr, "[stadi r%d] step %u: capture\n", ctx->rank, i);
     const unsigned long long l0 = g_launches;
     const uint64_t b0 = ctx->exch_bytes;
