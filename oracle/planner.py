@@ -35,6 +35,16 @@ Readings:
       max_i M_i (alpha_i + beta_i P_i): one unit per included GPU, then each
       further unit to argmin_i M_i (alpha_i + beta_i (P_i + 1)), ties to the
       lowest rank.  With alpha = 0 and beta_i = L / v_i this is R5's D'Hondt.
+  R33 (flag CFG_SPLIT; DistriFusion's "batch splitting" of the CFG batch, L284 names
+      it as an acceleration technique): the GPUs are PAIRED and each
+      member of a pair computes one CFG branch (B = 1) of the pair's band; the two
+      eps bands are combined every step, so a pair advances at its slower member's
+      speed.  Pairing: GPUs sorted by speed (descending, ties to the lower index),
+      consecutive ones paired; an odd GPU out (the slowest) is excluded.  Eq. 4/5
+      then plan the pairs with pair speed min(v_a, v_b); the pairs' bands go top to
+      bottom in the order of each pair's lower GPU index (R8).  Both members take the
+      pair's tier, steps and rows; the lower index computes branch 0 (uncond).
+      FORCE_UNITS / SIZER_AFFINE (per-GPU inputs) are not combined with it.
 Written with plain Python integers and fractions.Fraction (exact).
 """
 from __future__ import annotations
@@ -46,6 +56,7 @@ NO_SA = 2
 SIZER_INTERVAL = 4
 FORCE_UNITS = 8
 SIZER_AFFINE = 16
+CFG_SPLIT = 32
 
 
 class PlanError(ValueError):
@@ -182,3 +193,27 @@ def plan(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
         n_exchange_rounds=m_warmup + (m_base - m_warmup) // sync_period,
         makespan=makespan,
     )
+
+
+def plan_cfg_split(speed, m_base, m_warmup, p_total, rows_per_unit=1, a=(3, 4), b=(1, 4),
+                   flags=0):
+    """R33: per-GPU plan of the CFG batch split plus the pair plan it expands."""
+    n = len(speed)
+    if flags & (FORCE_UNITS | SIZER_AFFINE):
+        raise PlanError("CFG_SPLIT does not combine with FORCE_UNITS / SIZER_AFFINE")
+    if n < 2:
+        raise PlanError("CFG_SPLIT needs >= 2 GPUs")
+    order = sorted(range(n), key=lambda i: (-int(speed[i]), i))
+    pairs = [tuple(sorted(order[2 * k:2 * k + 2])) for k in range(n // 2)]
+    pairs.sort(key=lambda pr: pr[0])                      # R8 on the pairs' lower index
+    pspeed = [min(int(speed[i]), int(speed[j])) for i, j in pairs]
+    pp = plan(pspeed, m_base, m_warmup, p_total, rows_per_unit, a, b, flags & ~CFG_SPLIT)
+    out = dict(pp, n_gpus=n, tier=[0] * n, steps=[0] * n, units=[0] * n, row_begin=[0] * n,
+               rows=[0] * n, branch=[0] * n, partner=[-1] * n, pairs=pairs, pair_plan=pp)
+    for k, (i, j) in enumerate(pairs):
+        for g, br, other in ((i, 0, j), (j, 1, i)):
+            for key in ("tier", "steps", "units", "row_begin", "rows"):
+                out[key][g] = pp[key][k]
+            out["branch"][g] = br
+            out["partner"][g] = other
+    return out

@@ -225,3 +225,57 @@ def plan_for(cfg, speed, m_base, m_warmup, flags=0, forced_units=None):
     u = rows_per_unit(cfg)
     return planner.plan(speed, m_base, m_warmup, cfg["latent_h"] // u, u,
                         flags=flags, forced_units=forced_units)
+
+
+def run_cfg_split(cfg, weights, x_T, cond, splan, return_trace=False):
+    """R33 CFG batch split (DiT family): every included GPU runs ONE CFG branch
+    (B = 1 conditioning) on its pair's band, exchanges K/V with the GPUs of its own
+    branch only (versions as in Alg. 1), and combines its eps band with its
+    partner's every step (R20) before the identical Eq. 3 update on both members.
+    Equal to run(cfg, ..., splan["pair_plan"]) -- the pin that the split changes
+    nothing but the placement (tests/test_oracle_model.py)."""
+    import numpy as np
+    assert cfg["family"] == "dit" and dit.batch_of(cfg) == 2
+    model = dit.DiT(cfg, weights)
+    abar = diffusion.alpha_bar("linear" if cfg["schedule"] == "linear" else "scaled_linear")
+    p = cfg["patch"]
+    inc = [r for r in range(splan["n_gpus"]) if splan["tier"][r] > 0]
+    br = splan["branch"]
+    cond_b = [{k: np.asarray(v)[b:b + 1] for k, v in cond.items() if k in ("labels", "text")}
+              for b in (0, 1)]
+    y_b = [model.caption(cond_b[b]) for b in (0, 1)]
+    band = {r: x_T[splan["row_begin"][r]:splan["row_begin"][r] + splan["rows"][r]].astype("float64")
+            for r in inc}
+    store = {}                                   # (version, layer, rank) -> (k, v)
+    trace = []
+    for phase in _group_phases(splan):
+        parts = []
+        for r, st in phase:
+            mods, fin = model.modulations(st.t, cond_b[br[r]])
+            h = model.embed(band[r], splan["row_begin"][r] // p, 1)
+            parts.append(dict(r=r, st=st, mods=mods, fin=fin, h=h))
+        for l in range(model.depth):
+            fresh = {}
+            for P in parts:
+                q, k, v = model.block_qkv(l, P["h"], P["mods"][l])
+                fresh[P["r"]] = (q, k, v)
+                if P["st"].pub_ver != schedule.NONE:
+                    store[(P["st"].pub_ver, l, P["r"])] = (k, v)
+            for P in parts:
+                r, st = P["r"], P["st"]
+                same = [j for j in inc if br[j] == br[r]]          # own branch, row order
+                ks = [fresh[r][1] if j == r else store[(st.read_ver, l, j)][0] for j in same]
+                vs = [fresh[r][2] if j == r else store[(st.read_ver, l, j)][1] for j in same]
+                P["h"] = model.block_rest(l, P["h"], fresh[r][0], _cat(ks), _cat(vs),
+                                          P["mods"][l], y_b[br[r]])
+        eps_b = {P["r"]: model.final(P["h"], P["fin"], band[P["r"]].shape[0])[0] for P in parts}
+        for P in parts:                          # pair exchange of eps, CFG, Eq. 3
+            r, st = P["r"], P["st"]
+            e_u = eps_b[r] if br[r] == 0 else eps_b[splan["partner"][r]]
+            e_c = eps_b[r] if br[r] == 1 else eps_b[splan["partner"][r]]
+            eps = diffusion.cfg_combine(e_u, e_c, cfg["guidance"])
+            band[r] = diffusion.ddim_step(abar, band[r], eps, st.t, st.t_prev)
+            if return_trace:
+                trace.append((st.m, r, st.kind, band[r].copy()))
+    out = np.concatenate([band[r] for r in inc if br[r] == 0], axis=0)
+    return (out, trace) if return_trace else out

@@ -331,3 +331,21 @@ def test_temporal_redundancy_trend_thm1_thm2():
         assert 1.6 < d[50][r] / d[100][r] < 2.2, (r, d)        # O(1/M): M d -> const
     for mb in (50, 100):
         assert 1.6 < d[mb][1] / d[mb][0] < 2.5, d               # Thm 2, n = 2
+
+
+def test_cfg_split_equals_pair_plan():
+    """R33: running each CFG branch on its own GPU (B = 1 conditioning, K/V exchanged
+    within the branch, eps bands combined per step inside a pair) reproduces the
+    unsplit run of the pair plan -- the batch split changes placement only; with
+    stale rounds and a tier-2 pair, class (C1 + CFG) and text (tiny PixArt) models."""
+    from oracle import planner as OP
+    for cfg in (configs.model("tiny_dit", guidance=3.0), _tiny_cfg("text", 2.0)):
+        W = gen.weights(cfg, seed=2)
+        x = gen.noise(cfg, seed=3).astype(np.float64)
+        c = gen.cond(cfg, seed=4)
+        u = configs.rows_per_unit(cfg)
+        sp = OP.plan_cfg_split([100, 60, 90, 30, 5], 10, 2, cfg["latent_h"] // u, u)
+        assert 2 in sp["tier"] and sp["tier"][4] == 0            # tier-2 pair, odd GPU out
+        a = stadi.run_cfg_split(cfg, W, x, c, sp)
+        b = stadi.run(cfg, W, x, c, sp["pair_plan"])
+        assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(b))

@@ -298,3 +298,43 @@ def test_affine_errors():
         planner.plan([1, 1], 10, 2, 8, 1, flags=planner.SIZER_AFFINE)
     with pytest.raises(planner.PlanError):
         _affine([1, 1], 10, 2, 8, [0, 0], [1, 0])
+
+
+# ------------------------------------------------------------ R33 CFG batch split
+def test_cfg_split_pairing_bruteforce():
+    """R33: consecutive GPUs in speed order are paired (the odd slowest one out is
+    excluded), a pair runs at its slower member's speed, both members share the
+    pair's tier / steps / band, the lower index computes branch 0."""
+    import itertools
+    rng = __import__("random").Random(5)
+    for _ in range(300):
+        n = rng.randint(2, 9)
+        speed = [rng.randint(1, 100) for _ in range(n)]
+        sp = planner.plan_cfg_split(speed, 10, 2, 16, 2)
+        order = sorted(range(n), key=lambda i: (-speed[i], i))
+        want = sorted(tuple(sorted(order[2 * k:2 * k + 2])) for k in range(n // 2))
+        assert sorted(sp["pairs"]) == want
+        if n % 2:
+            assert sp["tier"][order[-1]] == 0 and sp["rows"][order[-1]] == 0
+        pp = sp["pair_plan"]
+        assert pp["n_gpus"] == n // 2
+        for k, (i, j) in enumerate(sp["pairs"]):
+            assert sp["branch"][i] == 0 and sp["branch"][j] == 1 and i < j
+            assert sp["partner"][i] == j and sp["partner"][j] == i
+            for key in ("tier", "steps", "rows", "row_begin"):
+                assert sp[key][i] == sp[key][j] == pp[key][k]
+        # the pair plan is the ordinary plan of the pairs' min speeds
+        ref = planner.plan([min(speed[i], speed[j]) for i, j in sp["pairs"]], 10, 2, 16, 2)
+        assert {k: ref[k] for k in ("tier", "steps", "units")} == \
+            {k: pp[k] for k in ("tier", "steps", "units")}
+        # pairing consecutive speeds maximises the slowest pair speed (brute force, n <= 6)
+        if n <= 6 and n % 2 == 0:
+            best = 0
+            for perm in itertools.permutations(range(n)):
+                best = max(best, min(min(speed[perm[2 * k]], speed[perm[2 * k + 1]])
+                                     for k in range(n // 2)))
+            assert min(min(speed[i], speed[j]) for i, j in sp["pairs"]) == best
+    with pytest.raises(planner.PlanError):
+        planner.plan_cfg_split([1], 10, 2, 8)
+    with pytest.raises(planner.PlanError):
+        planner.plan_cfg_split([1, 1], 10, 2, 8, flags=planner.FORCE_UNITS)
