@@ -80,8 +80,12 @@ enum {
   STADI_NO_SA = 2u,           /* disable spatial adaptation (uniform units)     */
   STADI_SIZER_INTERVAL = 4u,  /* Eq. 5 with per-round step counts (R7 variant)  */
   STADI_FORCE_UNITS = 8u,     /* use forced_units (Table II / Fig. 9 splits)    */
-  STADI_SIZER_AFFINE = 16u    /* Eq. 5 replaced by the affine step-cost model
+  STADI_SIZER_AFFINE = 16u,   /* Eq. 5 replaced by the affine step-cost model
                                  alpha_i + beta_i P (R30, L333 fixed overhead)  */
+  STADI_CFG_SPLIT = 32u       /* R33: CFG batch split -- GPUs paired by speed, each
+                                 member computes one CFG branch of the pair's band
+                                 (B = 1), Eq. 4/5 plan the pairs (speed = min of the
+                                 pair); not with FORCE_UNITS / SIZER_AFFINE         */
 };
 
 typedef struct {
@@ -116,6 +120,9 @@ typedef struct {
   uint64_t makespan_num, makespan_den; /* max_i M_i P_i / v_i, reduced fraction
                                           (SIZER_AFFINE: max_i M_i (alpha_i +
                                           beta_i P_i), den 1)                     */
+  uint32_t cfg_split;                  /* 1: STADI_CFG_SPLIT plan (R33)           */
+  uint8_t branch[STADI_MAX_GPUS];      /* CFG branch of GPU i (0 uncond, 1 cond)  */
+  int8_t partner[STADI_MAX_GPUS];      /* the other member of GPU i's pair, or -1 */
 } stadi_plan_t;
 
 /* Eq. 4 (L179-L185) then Eq. 5 (L187-L198), as in Alg. 1 lines 1-6.

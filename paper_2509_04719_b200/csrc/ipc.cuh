@@ -329,7 +329,9 @@ stadi_status ipc_commit(stadi_ctx *ctx, int n_sites) {
   }
   I.peers.clear();
   for (uint32_t g = 0; g < ctx->plan.n_gpus; ++g)
-    if (ctx->plan.tier[g] && (int)g != ctx->rank) I.peers.push_back((int)g);
+    if (ctx->plan.tier[g] && (int)g != ctx->rank &&  // R33: K/V only within a CFG branch
+        (!ctx->plan.cfg_split || ctx->plan.branch[g] == ctx->plan.branch[ctx->rank]))
+      I.peers.push_back((int)g);
   // peer slot table for the fused QKV-epilogue all-gather
   const size_t np = I.peers.size();
   if (I.peer_tab) pfree(ctx, I.peer_tab);
@@ -362,6 +364,30 @@ stadi_status ipc_commit(stadi_ctx *ctx, int n_sites) {
           I.need[g][P] = k + 1;
   }
   return STADI_OK;
+}
+
+// R33 pair exchange of the eps rows (site `site` = the arena's eps buffer
+// [tokens, 2, fin_ld] f32, both members use the band's rows): push this rank's branch
+// columns of step `idx` to the partner, then wait for the partner's.  WAR: before
+// overwriting, the partner must have finished the sampler of step idx - 1.
+stadi_status ipc_pair_push(stadi_ctx *ctx, int site, int partner, uint32_t idx, const float *eps,
+                           int rows, int ld, int branch, cudaStream_t s) {
+  IpcState &I = *ctx->ipc;
+  ST(ipc_wait(ctx, I.off_done, (size_t)site * ctx->world + partner, idx, s));
+  const size_t off = (const char *)eps - I.arena;
+  const size_t pitch = (size_t)2 * ld * 4;
+  CK(cudaMemcpy2DAsync(I.peer[partner] + off + (size_t)branch * ld * 4, pitch,
+                       (const char *)eps + (size_t)branch * ld * 4, pitch, (size_t)ld * 4, rows,
+                       cudaMemcpyDeviceToDevice, s));
+  ctx->exch_bytes += (size_t)rows * ld * 4;
+  return ipc_signal(ctx, partner, I.off_ready, (size_t)site * ctx->world + ctx->rank, idx + 1, s);
+}
+stadi_status ipc_pair_wait(stadi_ctx *ctx, int site, int partner, uint32_t idx, cudaStream_t s) {
+  return ipc_wait(ctx, ctx->ipc->off_ready, (size_t)site * ctx->world + partner, idx + 1, s);
+}
+stadi_status ipc_pair_done(stadi_ctx *ctx, int site, int partner, uint32_t idx, cudaStream_t s) {
+  return ipc_signal(ctx, partner, ctx->ipc->off_done, (size_t)site * ctx->world + ctx->rank,
+                    idx + 1, s);
 }
 
 // Device array of the peers' copies of site `site`'s slot of parity `par`.

@@ -79,8 +79,64 @@ extern "C" stadi_status stadi_plan(const stadi_plan_params *in, stadi_plan_t *ou
   if ((uint64_t)in->p_total * in->rows_per_unit > 0xFFFFFFFFull)
     return fail(nullptr, STADI_EINVAL, "stadi_plan: p_total * rows_per_unit overflows");
 
+  if (in->flags & STADI_CFG_SPLIT) {  // R33: plan the speed-ordered pairs, then expand
+    if (in->flags & (STADI_FORCE_UNITS | STADI_SIZER_AFFINE))
+      return fail(nullptr, STADI_EINVAL, "stadi_plan: CFG_SPLIT with FORCE_UNITS / SIZER_AFFINE");
+    if (n < 2) return fail(nullptr, STADI_EINVAL, "stadi_plan: CFG_SPLIT needs >= 2 GPUs");
+    uint32_t order[STADI_MAX_GPUS];
+    for (uint32_t i = 0; i < n; ++i) order[i] = i;
+    std::stable_sort(order, order + n, [&](uint32_t x, uint32_t y) {
+      return in->speed[x] > in->speed[y];  // descending, ties keep the lower index first
+    });
+    uint32_t npair = n / 2, pa[STADI_MAX_GPUS / 2], pb[STADI_MAX_GPUS / 2];
+    for (uint32_t k = 0; k < npair; ++k) {
+      pa[k] = std::min(order[2 * k], order[2 * k + 1]);
+      pb[k] = std::max(order[2 * k], order[2 * k + 1]);
+    }
+    uint32_t idx[STADI_MAX_GPUS / 2];  // pairs in the order of their lower index (R8)
+    for (uint32_t k = 0; k < npair; ++k) idx[k] = k;
+    std::sort(idx, idx + npair, [&](uint32_t x, uint32_t y) { return pa[x] < pa[y]; });
+    uint64_t psp[STADI_MAX_GPUS / 2];
+    for (uint32_t k = 0; k < npair; ++k)
+      psp[k] = std::min(in->speed[pa[idx[k]]], in->speed[pb[idx[k]]]);
+    stadi_plan_params q = *in;
+    q.n_gpus = npair;
+    q.speed = psp;
+    q.flags &= ~STADI_CFG_SPLIT;
+    stadi_plan_t pp;
+    const stadi_status st = stadi_plan(&q, &pp);
+    if (st != STADI_OK) return st;
+    stadi_plan_t p = pp;
+    p.n_gpus = n;
+    std::memset(p.tier, 0, sizeof(p.tier));
+    std::memset(p.steps, 0, sizeof(p.steps));
+    std::memset(p.units, 0, sizeof(p.units));
+    std::memset(p.row_begin, 0, sizeof(p.row_begin));
+    std::memset(p.rows, 0, sizeof(p.rows));
+    std::memset(p.branch, 0, sizeof(p.branch));
+    std::memset(p.partner, -1, sizeof(p.partner));
+    for (uint32_t k = 0; k < npair; ++k) {
+      const uint32_t a = pa[idx[k]], b = pb[idx[k]];
+      for (uint32_t g : {a, b}) {
+        p.tier[g] = pp.tier[k];
+        p.steps[g] = pp.steps[k];
+        p.units[g] = pp.units[k];
+        p.row_begin[g] = pp.row_begin[k];
+        p.rows[g] = pp.rows[k];
+      }
+      p.branch[a] = 0;
+      p.branch[b] = 1;
+      p.partner[a] = (int8_t)b;
+      p.partner[b] = (int8_t)a;
+    }
+    p.cfg_split = 1;
+    *out = p;
+    return STADI_OK;
+  }
+
   stadi_plan_t p;
   std::memset(&p, 0, sizeof(p));
+  std::memset(p.partner, -1, sizeof(p.partner));
   p.n_gpus = n;
   p.m_base = in->m_base;
   p.m_warmup = in->m_warmup;

@@ -84,6 +84,7 @@ struct Rank {
   int row_begin = 0, rows = 0;     // latent rows
   int tok_begin = 0, n_tok = 0;    // tokens (token rows * wp)
   int tier = 0;
+  int branch = 0, partner = -1;    // R33 CFG split: CFG branch and pair partner (group rank)
   std::vector<stadi_step_t> sched;
   float *x_band = nullptr;         // [rows, W, C_in] fp32
   float *hist = nullptr;           // [rows, W, C_in] fp32 previous combined eps (DPM2M, R34)
@@ -121,6 +122,10 @@ struct stadi_ctx {
   bool ipc_mode = false;
   std::unique_ptr<IpcState> ipc;
   bool probe = false;        // profiling probe steps: no exchange waits / signals
+  // R33 CFG batch split (plan.cfg_split): every hosted rank runs ONE CFG branch with a
+  // forward batch Bf = 1; otherwise Bf = dm.B
+  int Bf = 1;
+  std::vector<void *> kv_text_b[2];  // per branch: cross-attention text K/V [L, 1, 2, d]
   int ipc_idx = 0;           // IPC mode: step-table index of the step being built / run
   uint32_t graph_steps = 0;  // steps replayed from CUDA graphs (stats of stadi_run)
   int num_sms = 148;
@@ -555,12 +560,13 @@ cudaError_t gemm(stadi_ctx *ctx, const void *A, const void *W, int M, int N, int
 cudaError_t attention(stadi_ctx *ctx, int cls, const void *q, const void *kv, void *o, int Nq,
                       int Nkv, cudaStream_t s) {
   const Dims &m = ctx->dm;
-  const double flops = 4.0 * Nq * Nkv * m.hd * m.B * m.H;  // QK^T + PV, 2 flops per MAC
+  const int B = ctx->Bf;
+  const double flops = 4.0 * Nq * Nkv * m.hd * B * m.H;  // QK^T + PV, 2 flops per MAC
   return timed(ctx, cls, flops, 0.0, s, [&] {
     if (ctx->dtype == STADI_DTYPE_BF16)
-      return tc_attention_bf16((const bf16 *)q, (const bf16 *)kv, (bf16 *)o, Nq, Nkv, m.B, m.H,
+      return tc_attention_bf16((const bf16 *)q, (const bf16 *)kv, (bf16 *)o, Nq, Nkv, B, m.H,
                                m.hd, s);
-    return simt_attention<float>((const float *)q, (const float *)kv, (float *)o, Nq, Nkv, m.B,
+    return simt_attention<float>((const float *)q, (const float *)kv, (float *)o, Nq, Nkv, B,
                                  m.H, m.hd, s);
   });
 }
@@ -569,9 +575,9 @@ cudaError_t lnmod(stadi_ctx *ctx, const float *x, void *y, int M, const float *s
   const double bytes = (double)M * ctx->dm.d * (4 + ctx->esz);  // fp32 in, T out
   return timed(ctx, STADI_KCLASS_NORM, 0.0, bytes, s, [&] {
     if (ctx->dtype == STADI_DTYPE_BF16)
-      return ln_modulate<bf16>(x, (bf16 *)y, M, ctx->dm.d, ctx->dm.B, shift, scale, bs, do_norm,
+      return ln_modulate<bf16>(x, (bf16 *)y, M, ctx->dm.d, ctx->Bf, shift, scale, bs, do_norm,
                                s);
-    return ln_modulate<float>(x, (float *)y, M, ctx->dm.d, ctx->dm.B, shift, scale, bs, do_norm,
+    return ln_modulate<float>(x, (float *)y, M, ctx->dm.d, ctx->Bf, shift, scale, bs, do_norm,
                               s);
   });
 }
@@ -618,9 +624,9 @@ void free_plan_buffers(stadi_ctx *ctx) {
   free_graphs(ctx);
   unet_free_plan(ctx);
   for (auto &r : ctx->ranks) {
-    for (void *p : {(void *)r.x_band, (void *)r.x_res, r.xmod, r.q, r.o, r.h1, (void *)r.eps_raw,
-                    (void *)r.hist})
+    for (void *p : {(void *)r.x_band, (void *)r.x_res, r.xmod, r.q, r.o, r.h1, (void *)r.hist})
       pfree(ctx, p);
+    if (!(ctx->ipc_mode && ctx->plan.cfg_split)) pfree(ctx, r.eps_raw);  // else in the arena
     if (!ctx->ipc_mode)  // IPC mode: the slots live in the (persistent) exchange arena
       for (void *p : r.kv) pfree(ctx, p);
   }
@@ -636,7 +642,10 @@ void free_plan_buffers(stadi_ctx *ctx) {
   ctx->begun = false;
 }
 
-int64_t slot_elems(const Dims &m) { return (int64_t)m.hp * m.wp * m.B * 2 * m.d; }
+int64_t slot_elems(const stadi_ctx *ctx) {
+  const Dims &m = ctx->dm;
+  return (int64_t)m.hp * m.wp * ctx->Bf * 2 * m.d;
+}
 
 }  // namespace
 
@@ -1005,7 +1014,11 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
   CK(quiesce(ctx));
   DBG("set_plan: quiesced");
   free_plan_buffers(ctx);
+  if (plan->cfg_split && (m.unet || m.B != 2 || ctx->nccl))
+    return ctx_fail(ctx, STADI_EUNSUPPORTED,
+                    "CFG batch split (R33) needs a DiT-family model with CFG, local / IPC mode");
   ctx->plan = *plan;
+  ctx->Bf = plan->cfg_split ? 1 : m.B;
   const int g0 = ctx->rank * ctx->n_local;
   for (int k = 0; k < ctx->n_local; ++k) {
     const int g = g0 + k;
@@ -1017,12 +1030,14 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     r.rows = (int)plan->rows[g];
     r.tok_begin = r.row_begin / m.p * m.wp;
     r.n_tok = r.rows / m.p * m.wp;
+    r.branch = plan->cfg_split ? plan->branch[g] : 0;
+    r.partner = plan->cfg_split ? plan->partner[g] : -1;
     uint32_t n = 0;
     if (stadi_schedule(plan, g, nullptr, 0, &n) != STADI_OK)
       return ctx_fail(ctx, STADI_EINVAL, "bad plan: %s", tls_error().c_str());
     r.sched.resize(n);
     stadi_schedule(plan, g, r.sched.data(), n, &n);
-    const int64_t M = (int64_t)r.n_tok * m.B;
+    const int64_t M = (int64_t)r.n_tok * ctx->Bf;
     CK(pmalloc(ctx, &r.x_band, std::max<int64_t>(16, (int64_t)r.rows * m.lat_w * m.c_in * 4)));
     if (ctx->sampler == STADI_SAMPLER_DPM2M)
       CK(pmalloc(ctx, &r.hist, std::max<int64_t>(16, (int64_t)r.rows * m.lat_w * m.c_in * 4)));
@@ -1035,13 +1050,16 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     CK(pmalloc(ctx, &r.q, std::max<int64_t>(16, M * m.d * ctx->esz)));
     CK(pmalloc(ctx, &r.o, std::max<int64_t>(16, M * m.d * ctx->esz)));
     CK(pmalloc(ctx, &r.h1, std::max<int64_t>(16, M * 4 * m.d * ctx->esz)));
-    CK(pmalloc(ctx, &r.eps_raw, std::max<int64_t>(16, M * ctx->fin_ld * 4)));
+    // eps of both CFG rows [n_tok, B, fin_ld]: under the CFG split the rank writes its
+    // branch's columns, the partner's arrive by the pair exchange (IPC: in the arena)
+    if (!(ctx->ipc_mode && plan->cfg_split))
+      CK(pmalloc(ctx, &r.eps_raw, std::max<int64_t>(16, (int64_t)r.n_tok * m.B * ctx->fin_ld * 4)));
     r.kv.assign(m.depth * 2, nullptr);
     CK(cudaStreamSynchronize(ctx->astream));
     if (!ctx->ipc_mode) {
       for (auto &p : r.kv) {
-        CK(pmalloc(ctx, &p, slot_elems(m) * ctx->esz));
-        CK(cudaMemsetAsync(p, 0, slot_elems(m) * ctx->esz, ctx->astream));
+        CK(pmalloc(ctx, &p, slot_elems(ctx) * ctx->esz));
+        CK(cudaMemsetAsync(p, 0, slot_elems(ctx) * ctx->esz, ctx->astream));
       }
     }
     CK(cudaStreamSynchronize(ctx->astream));
@@ -1084,11 +1102,20 @@ extern "C" stadi_status stadi_set_plan(stadi_ctx *ctx, const stadi_plan_t *plan)
     IpcState &I = *ctx->ipc;
     for (int l = 0; l < m.depth; ++l)
       for (int par = 0; par < 2; ++par)
-        I.site_off[par].push_back(ipc_reserve(ctx, slot_elems(m) * ctx->esz));
-    ST(ipc_commit(ctx, m.depth));
-    for (auto &r : ctx->ranks)
+        I.site_off[par].push_back(ipc_reserve(ctx, slot_elems(ctx) * ctx->esz));
+    int n_sites = m.depth;
+    if (plan->cfg_split) {  // site `depth`: the pair's eps exchange [tokens, 2, fin_ld] f32
+      const size_t eb = (size_t)m.hp * m.wp * 2 * ctx->fin_ld * 4;
+      I.site_off[0].push_back(ipc_reserve(ctx, eb));
+      I.site_off[1].push_back(I.site_off[0].back());
+      ++n_sites;
+    }
+    ST(ipc_commit(ctx, n_sites));
+    for (auto &r : ctx->ranks) {
       for (int l = 0; l < m.depth; ++l)
         for (int par = 0; par < 2; ++par) r.kv[l * 2 + par] = I.arena + I.site_off[par][l];
+      if (plan->cfg_split) r.eps_raw = (float *)(I.arena + I.site_off[0][m.depth]);
+    }
   }
   ctx->has_plan = true;
   return STADI_OK;
@@ -1282,6 +1309,19 @@ stadi_status begin_impl(stadi_ctx *ctx, const float *noise_full, const stadi_con
       ep.ldo = (int)(2 * d);
       CK(gemm(ctx, ctx->y, WT(ctx, p + "xkv.w"), (int)Mt, (int)(2 * d), (int)d, EPI_STORE, ep, s));
     }
+    if (ctx->plan.cfg_split) {  // R33: each branch's text K/V rows, contiguous [L, 1, 2, d]
+      for (int b = 0; b < 2; ++b) {
+        if (ctx->kv_text_b[b].empty()) {
+          ctx->kv_text_b[b].assign(m.depth, nullptr);
+          for (auto &q : ctx->kv_text_b[b]) CK(dalloc(ctx, &q, (size_t)L * 2 * d * ctx->esz));
+        }
+        for (int l = 0; l < m.depth; ++l)
+          CK(cudaMemcpy2DAsync(ctx->kv_text_b[b][l], (size_t)2 * d * ctx->esz,
+                               (const char *)ctx->kv_text[l] + (size_t)b * 2 * d * ctx->esz,
+                               (size_t)B * 2 * d * ctx->esz, (size_t)2 * d * ctx->esz, L,
+                               cudaMemcpyDeviceToDevice, s));
+      }
+    }
   }
   CK(cudaEventRecord(ctx->stage_ev, s));
   ctx->stage_pending = true;
@@ -1305,7 +1345,7 @@ namespace {
 // Rows of group rank g in a slot (element offset, element count).
 void seg_of(stadi_ctx *ctx, int g, int64_t *off, int64_t *cnt) {
   const Dims &m = ctx->dm;
-  const int64_t per_tok = (int64_t)m.B * 2 * m.d;
+  const int64_t per_tok = (int64_t)ctx->Bf * 2 * m.d;
   *off = (int64_t)ctx->plan.row_begin[g] / m.p * m.wp * per_tok;
   *cnt = (int64_t)ctx->plan.rows[g] / m.p * m.wp * per_tok;
 }
@@ -1322,9 +1362,9 @@ stadi_status publish(stadi_ctx *ctx, int li, int l, int ver, cudaStream_t s) {
     ctx->exch_bytes += bytes * ctx->ipc->peers.size();
     return ipc_ready(ctx, l, ver, false, s);
   }
-  if (!ctx->nccl) {  // local mode: copy into every other hosted rank's slot
+  if (!ctx->nccl) {  // local mode: copy into every other hosted rank's slot (same branch)
     for (auto &o : ctx->ranks) {
-      if (o.g == r.g) continue;
+      if (o.g == r.g || o.branch != r.branch) continue;
       CK(cudaMemcpyAsync((char *)o.kv[slot] + off * ctx->esz, (char *)r.kv[slot] + off * ctx->esz,
                          bytes, cudaMemcpyDeviceToDevice, s));
       ctx->exch_bytes += bytes;
@@ -1369,7 +1409,8 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
   if (ctx->dm.unet) return unet_run_phase(ctx, phase, s);
   const Dims &m = ctx->dm;
   const int64_t d = m.d;
-  const int B = m.B;
+  const int B = ctx->Bf;   // forward batch: 1 under the R33 CFG split, else the CFG batch
+  const int BM = m.B;      // conditioning batch (mod / fmod rows per timestep)
   const int64_t mod_bs = (int64_t)m.depth * 6 * d;  // batch stride in mod
   const int ntok_full = m.hp * m.wp;
   for (const Part &P : phase) {  // x_res = patch embedding of the band (+ pos)
@@ -1383,7 +1424,7 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
     for (const Part &P : phase) {  // ---- LN/modulate + QKV (+ publish)
       Rank &r = ctx->ranks[P.li];
       const int M = r.n_tok * B;
-      const float *mb = ctx->mod + ((int64_t)P.st.m * B * m.depth + l) * 6 * d;
+      const float *mb = ctx->mod + ((int64_t)P.st.m * BM * m.depth + l) * 6 * d + r.branch * mod_bs;
       CK(lnmod(ctx, r.x_res, r.xmod, M, mb, mb + d, (int)mod_bs, 1, s));
       // own rows may only be overwritten once this rank's earlier sends of
       // the read version completed (NCCL mode)
@@ -1413,7 +1454,7 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
     for (const Part &P : phase) {  // ---- attention + rest of the block
       Rank &r = ctx->ranks[P.li];
       const int M = r.n_tok * B;
-      const float *mb = ctx->mod + ((int64_t)P.st.m * B * m.depth + l) * 6 * d;
+      const float *mb = ctx->mod + ((int64_t)P.st.m * BM * m.depth + l) * 6 * d + r.branch * mod_bs;
       const bool ipcr = ctx->ipc_mode && !ctx->probe;
       if (ipcr) ST(ipc_read_wait(ctx, l, P.st.read_ver, false, s));  // peers' rows of read_ver
       CK(attention(ctx, STADI_KCLASS_ATTN, r.q, r.kv[l * 2 + (P.st.read_ver & 1)], r.o, r.n_tok,
@@ -1435,7 +1476,9 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
         eq.out = r.q;
         eq.ldo = (int)d;
         CK(gemm(ctx, r.xmod, WT(ctx, pre + "xq.w"), M, (int)d, (int)d, EPI_STORE, eq, s));
-        CK(attention(ctx, STADI_KCLASS_XATTN, r.q, ctx->kv_text[l], r.o, r.n_tok, m.txt_len, s));
+        CK(attention(ctx, STADI_KCLASS_XATTN, r.q,
+                     ctx->plan.cfg_split ? ctx->kv_text_b[r.branch][l] : ctx->kv_text[l], r.o,
+                     r.n_tok, m.txt_len, s));
         EpiParams er{};
         er.B = B;
         er.bias = WF(ctx, pre + "xproj.b");
@@ -1460,26 +1503,53 @@ stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStrea
       CK(gemm(ctx, r.h1, WT(ctx, pre + "fc2.w"), M, (int)d, (int)(4 * d), EPI_GATED_RES, e2, s));
     }
   }
-  for (const Part &P : phase) {  // ---- final layer + CFG + unpatchify + Eq. 3
+  for (const Part &P : phase) {  // ---- final layer
     Rank &r = ctx->ranks[P.li];
     const int M = r.n_tok * B;
-    const float *fb = ctx->fmod + (int64_t)P.st.m * B * 2 * d;
+    const float *fb = ctx->fmod + (int64_t)P.st.m * BM * 2 * d + r.branch * 2 * d;
     CK(lnmod(ctx, r.x_res, r.xmod, M, fb, fb + d, (int)(2 * d), 1, s));
     EpiParams ef{};
     ef.B = B;
     ef.bias = ctx->final_b;
-    ef.out = r.eps_raw;
-    ef.ldo = ctx->fin_ld;
+    // eps rows [n_tok, BM, fin_ld]; under the CFG split this rank fills its branch's
+    ef.out = r.eps_raw + (ctx->plan.cfg_split ? r.branch * ctx->fin_ld : 0);
+    ef.ldo = ctx->plan.cfg_split ? 2 * ctx->fin_ld : ctx->fin_ld;
     CK(gemm(ctx, r.xmod, ctx->final_w, M, ctx->fin_ld, (int)d, EPI_F32, ef, s));
+  }
+  const bool pair_ipc = ctx->plan.cfg_split && ctx->ipc_mode && !ctx->probe;
+  if (ctx->plan.cfg_split && !ctx->probe) {  // R33: the pair swaps its eps rows
+    for (const Part &P : phase) {
+      Rank &r = ctx->ranks[P.li];
+      if (pair_ipc) {
+        ST(ipc_pair_push(ctx, m.depth, r.partner, (uint32_t)P.idx, r.eps_raw, r.n_tok,
+                         ctx->fin_ld, r.branch, s));
+        ST(ipc_pair_wait(ctx, m.depth, r.partner, (uint32_t)P.idx, s));
+        continue;
+      }
+      for (auto &o : ctx->ranks)  // local mode: the partner is hosted here too
+        if (o.g == r.partner) {
+          const size_t pitch = (size_t)2 * ctx->fin_ld * 4;
+          CK(cudaMemcpy2DAsync((char *)o.eps_raw + (size_t)r.branch * ctx->fin_ld * 4, pitch,
+                               (const char *)r.eps_raw + (size_t)r.branch * ctx->fin_ld * 4,
+                               pitch, (size_t)ctx->fin_ld * 4, r.n_tok,
+                               cudaMemcpyDeviceToDevice, s));
+          ctx->exch_bytes += (size_t)r.n_tok * ctx->fin_ld * 4;
+        }
+    }
+  }
+  for (const Part &P : phase) {  // ---- CFG + unpatchify + Eq. 3 on the band
+    Rank &r = ctx->ranks[P.li];
+    const int M = r.n_tok * BM;
     float A, Bc, Cz, c1, c2;
     sampler_coeffs(ctx, P.st.t, P.st.t_prev, &A, &Bc, &Cz);
     dpm2m_coeffs(ctx, r.sched, P.idx, &c1, &c2);
     const double sb = (double)r.rows * m.lat_w * m.c_in * 8 + (double)M * ctx->fin_ld * 4;
     CK(timed(ctx, STADI_KCLASS_SAMPLER, 0.0, sb, s, [&] {
       return sampler_update(r.x_band, r.eps_raw, r.rows, m.lat_w, m.c_in, m.p, m.c_out,
-                            ctx->fin_ld, B, m.guidance, A, Bc, Cz, ctx->ddpm_seed, ctx->seed_dev,
+                            ctx->fin_ld, BM, m.guidance, A, Bc, Cz, ctx->ddpm_seed, ctx->seed_dev,
                             P.st.m, r.row_begin, s, r.hist, c1, c2);
     }));
+    if (pair_ipc) ST(ipc_pair_done(ctx, m.depth, r.partner, (uint32_t)P.idx, s));
   }
   return STADI_OK;
 }

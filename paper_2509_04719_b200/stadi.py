@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libstadi.so")
 
 MAX_GPUS = 64
-NO_TA, NO_SA, SIZER_INTERVAL, FORCE_UNITS, SIZER_AFFINE = 1, 2, 4, 8, 16
+NO_TA, NO_SA, SIZER_INTERVAL, FORCE_UNITS, SIZER_AFFINE, CFG_SPLIT = 1, 2, 4, 8, 16, 32
 STEP_WARMUP, STEP_UNIFORM, STEP_FAST_EVEN, STEP_FAST_ODD, STEP_SLOW = range(5)
 T_FINAL = -1
 VER_NONE = -1
@@ -54,7 +54,8 @@ class Plan(C.Structure):
                 ("units", C.c_uint32 * MAX_GPUS), ("row_begin", C.c_uint32 * MAX_GPUS),
                 ("rows", C.c_uint32 * MAX_GPUS), ("sync_period", C.c_uint32),
                 ("n_exchange_rounds", C.c_uint32), ("makespan_num", C.c_uint64),
-                ("makespan_den", C.c_uint64)]
+                ("makespan_den", C.c_uint64), ("cfg_split", C.c_uint32),
+                ("branch", C.c_uint8 * MAX_GPUS), ("partner", C.c_int8 * MAX_GPUS)]
 
     def to_dict(self):
         n = self.n_gpus
@@ -63,7 +64,8 @@ class Plan(C.Structure):
                     steps=list(self.steps[:n]), units=list(self.units[:n]),
                     row_begin=list(self.row_begin[:n]), rows=list(self.rows[:n]),
                     sync_period=self.sync_period, n_exchange_rounds=self.n_exchange_rounds,
-                    makespan=(self.makespan_num, self.makespan_den))
+                    makespan=(self.makespan_num, self.makespan_den), cfg_split=self.cfg_split,
+                    branch=list(self.branch[:n]), partner=list(self.partner[:n]))
 
 
 class Step(C.Structure):

@@ -23,13 +23,14 @@ os.environ["STADI_WRITE_REFS"] = "1"
 import refcache  # noqa: E402
 import test_gpu_ddpm as TD  # noqa: E402
 import test_gpu_dpm2m as TM  # noqa: E402
+import test_gpu_cfgsplit as TC  # noqa: E402
 import test_gpu_fullres as TF  # noqa: E402
 import test_gpu_parity as T  # noqa: E402
 import test_gpu_unet as TU  # noqa: E402
 
 if __name__ == "__main__":
     filt = sys.argv[1] if len(sys.argv) > 1 else ""
-    for mod in (T, TU, TD, TF, TM):
+    for mod in (T, TU, TD, TF, TM, TC):
         if filt not in mod.__name__:
             continue
         for case in mod.oracle_cases():

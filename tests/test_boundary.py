@@ -146,3 +146,27 @@ def test_weight_manifest_matches_synth(S, name, kw, depth):
     got = S.weight_manifest(desc)
     want = [(n, int(__import__("numpy").prod(shape))) for n, shape, _ in configs.manifest(cfg)]
     assert got == want
+
+
+def test_cfg_split_plan_bit_exact(S):
+    """R33 CFG batch split: C++ == oracle (pairs, pair plan expansion, branches)."""
+    rng = random.Random(77)
+    for _ in range(2000):
+        n = rng.randint(2, 12)
+        speed = [rng.randint(1, 1 << 20) for _ in range(n)]
+        if rng.random() < 0.3:
+            speed = [rng.choice([1, 2, 3, 4]) << 16 for _ in range(n)]
+        mb = rng.choice([10, 20, 50, 11])
+        flags = rng.choice([0, OP.NO_TA, OP.NO_SA, OP.SIZER_INTERVAL])
+        P = rng.randint(1, 64)
+        try:
+            ref = OP.plan_cfg_split(speed, mb, 2, P, 2, flags=flags)
+        except OP.PlanError:
+            with pytest.raises(S.StadiError):
+                S.plan(speed, mb, 2, P, 2, flags=flags | S.CFG_SPLIT)
+            continue
+        got = S.plan(speed, mb, 2, P, 2, flags=flags | S.CFG_SPLIT).to_dict()
+        for k in ("tier", "steps", "units", "row_begin", "rows", "branch", "partner",
+                  "sync_period", "n_exchange_rounds"):
+            assert got[k] == ref[k], (k, speed, flags)
+        assert got["cfg_split"] == 1
