@@ -449,8 +449,10 @@ def run_method(args, cfg, wl, mode=None, pairs=None, steps=None):
                 ms, speed = grp.call("profile_warmup", 3, n)[0]
                 row = {"occupancy_pct": occ, "speed_q20": [int(v) for v in speed],
                        "probe_ms": ms}
-                if mode in ("ablation", "fig8"):
-                    fl = FLAGS_ABLATION if mode == "ablation" else [("none", 3), ("+TA+SA", 0)]
+                if mode in ("ablation", "fig8", "cfgsplit"):
+                    fl = (FLAGS_ABLATION if mode == "ablation" else
+                          [("none", 3), ("+TA+SA", 0)] if mode == "fig8" else
+                          [("none", 3), ("+TA+SA", 0), ("cfg_split+TA+SA", 32)])
                     for name, f in fl:
                         pl = S.plan(speed, mb, mw, P, p, flags=f)
                         lat, all_ = _time_plan(S, grp, pl, x, c, steps, 1)
@@ -536,7 +538,8 @@ def main():
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="N > 1 exchange transport (IPC: fused one-sided P2P, the default)")
     ap.add_argument("--mode", default="headline",
-                    choices=["headline", "ablation", "fig8", "fig9", "alphabeta", "replan"],
+                    choices=["headline", "ablation", "fig8", "fig9", "alphabeta", "replan",
+                             "cfgsplit"],
                     help="method-level measurements on virtual GPUs (one device)")
     ap.add_argument("--vgpu-sms", type=int, default=0, help="SMs per virtual GPU (mult. of 8)")
     ap.add_argument("--m-base", type=int, default=0, help="override the workload's M_base")

@@ -127,6 +127,7 @@ struct stadi_ctx {
   int Bf = 1;
   std::vector<void *> kv_text_b[2];  // per branch: cross-attention text K/V [L, 1, 2, d]
   int ipc_idx = 0;           // IPC mode: step-table index of the step being built / run
+  bool kernels_warm = false; // IPC: every kernel of the path loaded (first begin of a ctx)
   uint32_t graph_steps = 0;  // steps replayed from CUDA graphs (stats of stadi_run)
   int num_sms = 148;
   std::string err;
@@ -1126,6 +1127,7 @@ namespace {
 stadi_status begin_impl(stadi_ctx *ctx, const float *noise_full, const stadi_cond *cond,
                         void *stream);
 stadi_status gather_impl(stadi_ctx *ctx, float *out_full, void *stream);
+stadi_status run_phase(stadi_ctx *ctx, const std::vector<Part> &phase, cudaStream_t s);
 }  // namespace
 
 // Public entry points: (virtual GPU) the work runs on the context's green stream,
@@ -1165,19 +1167,39 @@ stadi_status begin_impl(stadi_ctx *ctx, const float *noise_full, const stadi_con
   // the sampler reads the key from device memory (graph replays see this request's seed)
   CK(cudaMemcpyAsync(ctx->seed_dev, stage_h2d(ctx, &ctx->ddpm_seed, 8), 8,
                      cudaMemcpyHostToDevice, s));
-  // noise bands
-  const bool dev = is_device_ptr(noise_full);
-  const size_t row_bytes = (size_t)m.lat_w * m.c_in * 4;
-  for (auto &r : ctx->ranks) {
-    const float *src = noise_full + (size_t)r.row_begin * m.lat_w * m.c_in;
-    const void *st = dev ? src : stage_h2d(ctx, src, row_bytes * r.rows);
-    if (!st) return ctx_fail(ctx, STADI_ENOMEM, "host staging exhausted");
-    CK(cudaMemcpyAsync(r.x_band, st, row_bytes * r.rows,
-                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-  }
-  DBG("begin: noise copied");
-  if (ctx->ipc_mode) ST(ipc_begin(ctx, s));  // flag reset + device-side barrier
-  DBG("begin: barrier enqueued");
+  // Tail of the call, after the conditioning: (IPC, first request of a plan) one
+  // compute-only probe step that loads every kernel of the path -- CUDA lazy loading of
+  // a kernel first launched while this process has a stream blocked in an exchange wait
+  // can need a context synchronisation that never completes (the flag comes from a
+  // peer that waits for us); then the noise bands and the flag barrier.
+  auto finish = [&]() -> stadi_status {
+    if (ctx->ipc_mode && !ctx->kernels_warm && !ctx->ranks.empty() && !ctx->program.empty()) {
+      ctx->probe = true;
+      const stadi_status st = run_phase(ctx, {ctx->program[0][0]}, s);
+      ctx->probe = false;
+      ST(st);
+      CK(cudaStreamSynchronize(s));
+      ctx->kernels_warm = true;
+      DBG("begin: kernels loaded");
+    }
+    const bool dev = is_device_ptr(noise_full);
+    const size_t row_bytes = (size_t)m.lat_w * m.c_in * 4;
+    for (auto &r : ctx->ranks) {  // noise bands (overwrite the probe's band)
+      const float *src = noise_full + (size_t)r.row_begin * m.lat_w * m.c_in;
+      const void *st = dev ? src : stage_h2d(ctx, src, row_bytes * r.rows);
+      if (!st) return ctx_fail(ctx, STADI_ENOMEM, "host staging exhausted");
+      CK(cudaMemcpyAsync(r.x_band, st, row_bytes * r.rows,
+                         dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    }
+    DBG("begin: noise copied");
+    if (ctx->ipc_mode) ST(ipc_begin(ctx, s));  // flag reset + device-side barrier
+    DBG("begin: barrier enqueued");
+    CK(cudaEventRecord(ctx->stage_ev, s));
+    ctx->stage_pending = true;
+    ctx->begun = true;
+    ctx->exch_bytes = 0;
+    return STADI_OK;
+  };
   // ---- conditioning for every fast-grid timestep (one batched GEMM each)
   const int nt = (int)ctx->plan.m_base;
   const int64_t d = m.d;
@@ -1202,11 +1224,7 @@ stadi_status begin_impl(stadi_ctx *ctx, const float *noise_full, const stadi_con
   ctx->n_t = nt;
   if (m.unet) {
     ST(unet_begin(ctx, cond, s));
-    CK(cudaEventRecord(ctx->stage_ev, s));
-    ctx->stage_pending = true;
-    ctx->begun = true;
-    ctx->exch_bytes = 0;
-    return STADI_OK;
+    return finish();
   }
   if (ctx->tfreq_nt != nt) {
     // sinusoidal timestep features of the fast grid, fp64 on the host (DiT
@@ -1323,11 +1341,7 @@ stadi_status begin_impl(stadi_ctx *ctx, const float *noise_full, const stadi_con
       }
     }
   }
-  CK(cudaEventRecord(ctx->stage_ev, s));
-  ctx->stage_pending = true;
-  ctx->begun = true;
-  ctx->exch_bytes = 0;
-  return STADI_OK;
+  return finish();
 }
 }  // namespace
 

@@ -258,6 +258,7 @@ stadi_status u_publish(stadi_ctx *ctx, USite &S, int li, int ver, cudaStream_t s
   int64_t off, bytes;
   seg(r.g, &off, &bytes);
   if (ctx->ipc_mode) {  // one-sided: K/V rows were stored by the QKV epilogue
+    if (ctx->probe) return STADI_OK;    // compute-only probe: nothing leaves the rank
     const bool nb = S.kind == US_HALO;  // halos go to the row neighbours only
     if (S.kind == US_KV) {
       ctx->exch_bytes += bytes * ctx->ipc->peers.size();

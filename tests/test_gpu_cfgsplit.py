@@ -103,8 +103,9 @@ def test_cfg_split_local(S, case):
 
 
 def test_cfg_split_ipc_and_vgpu(S):
-    """The C2 4-GPU split as 4 processes on one GPU (IPC) and as 4 virtual GPUs: the
-    same bits as local mode."""
+    """The C2 4-GPU split as 4 processes on one GPU (IPC): the same bits as local mode;
+    as 4 virtual GPUs of 24 SMs: within tolerance of the oracle (a 24-SM persistent
+    grid picks other split-K factors, so the fp32 summation order differs)."""
     from paper_2509_04719_b200.vgpu import VirtualGpus
     _, name, kw, speed, mb, mw = CASES[0]
     cfg, W, x, c = _inputs(name, **kw)
@@ -134,6 +135,9 @@ def test_cfg_split_ipc_and_vgpu(S):
         vg.call("run", p, x, c, per_rank=lambda r: {"out": vo[r]})
     finally:
         vg.close()
+    ref = _oracle(cfg, W, x, c, _split(cfg, speed, mb, mw)["pair_plan"], 0)
     for r in range(world):
-        assert np.array_equal(vo[r], loc), r
-    print("CFG-split C2 4 ranks: IPC processes and virtual GPUs == local mode")
+        assert np.array_equal(vo[r], vo[0]), r
+    err = float(np.max(np.abs(vo[0].astype(np.float64) - ref)) / np.max(np.abs(ref)))
+    print(f"CFG-split C2 4 ranks: IPC processes == local mode; virtual GPUs max-abs-rel={err:.3e}")
+    assert err <= TOL
