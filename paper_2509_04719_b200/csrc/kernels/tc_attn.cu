@@ -343,6 +343,9 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
       // (16-byte granular) start-address offset into their low field: the single
       // issuing thread must not spend ~10 dependent ALU ops per MMA on them.
       auto issue_s = [&](int g, int st) {
+#ifdef STADI_ATTN_NOSMMA  // timing experiment only (wrong results): no S MMAs
+        if (st >= 0) return;
+#endif
         const uint32_t dt = tmem + C::s_col(g);
         const uint32_t qa = smem_u32(sQ + g * C::QTILE), ka = smem_u32(sK + st * C::KTILE);
         int kk = 0;
@@ -357,6 +360,9 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
         }
       };
       auto issue_pv = [&](int g, int st, int j) {
+#ifdef STADI_ATTN_NOPV  // timing experiment only (wrong results): no PV MMAs
+        if (st >= 0) return;
+#endif
         const uint32_t pa = tmem + C::p_col(g);  // P: AKT / 2 columns of packed bf16
         const uint32_t va = smem_u32(sV + st * C::KTILE);
         if constexpr (C::NARROW) {
