@@ -254,6 +254,11 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
                    int flags) {  // bit 0: exp-phase tokens, bit 1: deferred PV wait (QUAD), bit 2: MMA order
   using C = AttnCfg<N64, N32, N16, NQT>;
   constexpr int AKT = C::AKT;
+  // QUAD == 2: P aliased over S.  PV_g(j) and S_g(j+1) are issued back to back once
+  // P_g(j) is stored and committed to ONE barrier (s_full), so a key tile costs each
+  // group two handoffs (s_full, p_full) instead of four: s_full(j) also tells the group
+  // that PV_g(j-1) is done (O may be rescaled, the S/P columns rewritten).
+  constexpr bool ALIAS = QUAD == 2 && NQT == 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -363,7 +368,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
 #ifdef STADI_ATTN_NOPV  // timing experiment only (wrong results): no PV MMAs
         if (st >= 0) return;
 #endif
-        const uint32_t pa = tmem + C::p_col(g);  // P: AKT / 2 columns of packed bf16
+        // P: AKT / 2 columns of packed bf16 (its own region, or over S when ALIAS)
+        const uint32_t pa = tmem + (ALIAS ? C::s_col(g) : C::p_col(g));
         const uint32_t va = smem_u32(sV + st * C::KTILE);
         if constexpr (C::NARROW) {
           constexpr uint32_t idp = umma_idesc_bf16(128, C::HDP, 0, 1);
@@ -398,7 +404,37 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
       umma_commit(&k_empty[0]);
       int ks = 1 % C::STAGES, vs = 0;
       uint32_t kph = (ks == 0), vph = 0;
-      if (NQT == 2 && (flags & 4)) {
+      if constexpr (ALIAS) {
+        // per tile j and group g: wait P_g(j), PV_g(j), S_g(j+1) into the same
+        // columns (in-order tensor pipe: PV reads P before S overwrites it), one commit
+        for (int j = 0; j < n_kv; ++j) {
+          mbar_wait(&v_full[vs], vph);
+          const bool more = j + 1 < n_kv;
+          if (more) mbar_wait(&k_full[ks], kph);
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            mbar_wait(&p_full[g], j & 1);
+            ATTN_TRACE(2, g, j);
+            tc_fence_after();
+            issue_pv(g, vs, j);
+            if (more) issue_s(g, ks);
+            umma_commit(&s_full[g]);
+            ATTN_TRACE(8, g, j);
+          }
+          umma_commit(&v_empty[vs]);
+          if (++vs == C::STAGES) {
+            vs = 0;
+            vph ^= 1;
+          }
+          if (more) {
+            umma_commit(&k_empty[ks]);
+            if (++ks == C::STAGES) {
+              ks = 0;
+              kph ^= 1;
+            }
+          }
+        }
+      } else if (NQT == 2 && (flags & 4)) {
         // Event order S_0(j+1), PV_1(j-1), S_1(j+1), PV_0(j): each S is issued as
         // soon as its group has read the previous S, not queued behind the other
         // group's PV of the same tile (which waits for that group's whole exp phase).
@@ -510,7 +546,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
     const int cq = 2 * (lane & 3);
     const uint32_t lane_off = (uint32_t)lb << 16;
     const uint32_t s_addr = tmem + lane_off + C::s_col(g);
-    const uint32_t p_addr = tmem + lane_off + C::p_col(g);
+    const uint32_t p_addr = tmem + lane_off + (ALIAS ? C::s_col(g) : C::p_col(g));
     const uint32_t o_addr = tmem + lane_off + C::o_col(g);
     float m_run[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
     for (int j = 0; j < n_kv; ++j) {
@@ -526,9 +562,11 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
       tmem_ld_q256<NR>(s_addr, reinterpret_cast<uint32_t *>(v));
       tmem_ld_wait();
 #endif
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[g]);
+      if constexpr (!ALIAS) {  // ALIAS: S is rewritten only after P_g(j) -- no s_free
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[g]);
+      }
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(4, g, j);
       if (valid < AKT) {
 #pragma unroll
@@ -564,7 +602,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
       // `defer` the wait moves to just before the P store unless this warp rescales,
       // so the PV latency overlaps the token wait and the exp phase.
       const bool any_grow = __any_sync(0xffffffffu, grow);
-      const bool wait_now = j > 0 && (!(flags & 2) || any_grow);
+      // ALIAS: s_full(j) already implied PV_g(j-1) complete
+      const bool wait_now = !ALIAS && j > 0 && (!(flags & 2) || any_grow);
       if (wait_now) {
         mbar_wait(&o_done[g], (j - 1) & 1);
         tc_fence_after();
@@ -625,7 +664,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
         }
       }
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(10, g, j);
-      if (j > 0 && !wait_now) {
+      if (!ALIAS && j > 0 && !wait_now) {
         mbar_wait(&o_done[g], (j - 1) & 1);
         tc_fence_after();
       }
@@ -662,7 +701,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
       l[rr] += __shfl_xor_sync(0xffffffffu, l[rr], 1);
       l[rr] += __shfl_xor_sync(0xffffffffu, l[rr], 2);
     }
-    mbar_wait(&o_done[g], (n_kv - 1) & 1);
+    if constexpr (ALIAS) mbar_wait(&s_full[g], n_kv & 1);  // the commit after PV_g(n-1)
+    else mbar_wait(&o_done[g], (n_kv - 1) & 1);
     tc_fence_after();
     float o[4 * NO];
     tmem_ld_q256<NO>(o_addr, reinterpret_cast<uint32_t *>(o));
@@ -909,10 +949,22 @@ int attn_quad() {
   }();
   return v;
 }
+// STADI_ATTN_ALIAS=1: P aliased over S, two handoffs per key tile and group instead of
+// four (QUAD == 2).  Measured slower on the C5 shape (774 vs 815 TFLOP/s: S(j+1) can no
+// longer overlap the group's exp phase), so off by default; it is parity-tested.
+int attn_alias() {
+  static const int v = [] {
+    const char *e = getenv("STADI_ATTN_ALIAS");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return v;
+}
 template <int N64, int N32, int N16, int NQT>
 cudaError_t launch_attn(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B, int H,
                         int hd, cudaStream_t s) {
   if (!attn_quad()) return launch_attn_p<N64, N32, N16, NQT, 0, 0>(q, kv, o, Nq, Nkv, B, H, hd, s);
+  if (NQT == 2 && attn_alias() && attn_poly() == 0)
+    return launch_attn_p<N64, N32, N16, NQT, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
   switch (attn_poly()) {
     case 0: return launch_attn_p<N64, N32, N16, NQT, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 1: return launch_attn_p<N64, N32, N16, NQT, 1, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
@@ -944,6 +996,7 @@ void preload_attn(cudaFuncAttributes *a) {
   cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 2, 1>);
   cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 3, 1>);
   cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 4, 1>);
+  cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 2>);
 }
 }  // namespace
 cudaError_t tc_attention_preload() {

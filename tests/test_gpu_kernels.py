@@ -436,3 +436,27 @@ def test_gemm_on_emulator_grid(S, max_ctas, M, N, K):
     assert _rel(outT.float().cpu().numpy(), OD.gelu_tanh(ref)) < 1e-2
     g = gate[np.arange(M) % 2].astype(np.float64)
     assert _rel(res.cpu().numpy() - res0, g * ref) < tol
+
+
+def test_attention_alias_variant(S):
+    """The P-over-S variant (STADI_ATTN_ALIAS=1, QUAD == 2: two handoffs per key tile)
+    against the oracle, in a subprocess (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, torch, sys; sys.path.insert(0, '.');"
+            "from paper_2509_04719_b200 import stadi as S; from oracle import dit as OD;"
+            "rng = np.random.default_rng(9); Nq, Nkv, B, H, hd = 300, 777, 2, 2, 72; d = H * hd;"
+            "q = torch.from_numpy(rng.standard_normal((Nq, B, d)).astype(np.float32)).cuda().bfloat16();"
+            "kv = torch.from_numpy(rng.standard_normal((Nkv, B, 2, d)).astype(np.float32)).cuda().bfloat16();"
+            "o = torch.empty(Nq * B, d, device='cuda', dtype=torch.bfloat16);"
+            "S.k_attention(0, q, kv, o, Nq, Nkv, B, H, hd); torch.cuda.synchronize();"
+            "nq = q.float().cpu().numpy().astype(np.float64); nkv = kv.float().cpu().numpy().astype(np.float64);"
+            "ref = OD.attention(nq.transpose(1, 0, 2), nkv[:, :, 0].transpose(1, 0, 2), nkv[:, :, 1].transpose(1, 0, 2), H).transpose(1, 0, 2);"
+            "got = o.float().cpu().numpy().reshape(Nq, B, d);"
+            "print(float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       env=dict(os.environ, STADI_ATTN_ALIAS="1"), timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) < 1e-2
