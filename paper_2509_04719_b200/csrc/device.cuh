@@ -2,6 +2,7 @@
 // Bit layouts of the UMMA shared-memory / instruction descriptors follow the
 // PTX ISA tcgen05 "matrix descriptor" and "instruction descriptor" tables.
 #pragma once
+#include <utility>
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -131,6 +132,30 @@ __device__ __forceinline__ void epi_apply(const EpiParams &p, int row, int col, 
       }
     }
   }
+}
+
+// ----------------------------------------------------------------- PDL
+// Programmatic dependent launch: a hot-path kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start (prologue: barrier
+// init, TMEM alloc, descriptor prefetch) while its predecessor's last blocks still
+// run; every such kernel calls pdl_wait() before touching global memory, which
+// returns once the predecessor has completed and its writes are visible.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();  // STADI_PDL=0 disables (tc_gemm.cu)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args &&...args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // ----------------------------------------------------------------- PTX wrappers

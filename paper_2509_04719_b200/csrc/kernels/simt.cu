@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(256) ln_mod_kernel(const float *__restrict__ x
                                                      const float *__restrict__ shift,
                                                      const float *__restrict__ scale, int bs,
                                                      int do_norm, float eps) {
+  pdl_wait();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long row = (long)blockIdx.x * 8 + warp;
   if (row >= M) return;
@@ -257,10 +258,10 @@ cudaError_t ln_modulate(const float *x, T *y, int M, int d, int B, const float *
                         float eps) {
   if (d % 4 || d / 4 > 32 * LN_MAXV) return cudaErrorInvalidValue;
   if (M <= 0) return cudaSuccess;
-  ln_mod_kernel<T><<<(M + 7) / 8, 256, 0, s>>>(x, y, M, d, B, shift, scale, mod_bstride, do_norm,
-                                               eps);
+  const cudaError_t el = launch_pdl(ln_mod_kernel<T>, dim3((M + 7) / 8), dim3(256), 0, s, x, y,
+                                    M, d, B, shift, scale, mod_bstride, do_norm, eps);
   ++g_launches;
-  return cudaGetLastError();
+  return el;
 }
 template cudaError_t ln_modulate<float>(const float *, float *, int, int, int, const float *,
                                         const float *, int, int, cudaStream_t, float);
@@ -274,6 +275,7 @@ __global__ void __launch_bounds__(256) patch_embed_kernel(const float *__restric
                                                           const float *__restrict__ bias,
                                                           const float *__restrict__ pos, int d,
                                                           int B, float *__restrict__ xres) {
+  pdl_wait();
   __shared__ float patch[64];
   const int i = blockIdx.x;  // band-local token
   const int wp = W / p;
@@ -301,6 +303,7 @@ __global__ void __launch_bounds__(256) patch_embed16_kernel(
     const float *__restrict__ xb, int W, int C, int p, const float *__restrict__ w,
     const float *__restrict__ bias, const float *__restrict__ pos, int d, int B, int ntok,
     float *__restrict__ xres) {
+  pdl_wait();
   __shared__ float patch[PE_TOK][16];
   const int i0 = blockIdx.x * PE_TOK;
   const int wp = W / p;
@@ -368,6 +371,7 @@ __global__ void sampler_kernel(float *__restrict__ xb, const float *__restrict__
                                float Bc, float Cz, uint64_t seed, const uint64_t *seed_dev,
                                uint32_t m, int row0, float *__restrict__ hist, float c1,
                                float c2) {
+  pdl_wait();
   const long n = (long)rows * W * C;
   const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n) return;
@@ -408,13 +412,15 @@ cudaError_t patch_embed(const float *x_band, int rows, int W, int C, int p, cons
   const int ntok = (rows / p) * (W / p);
   if (C * p * p > 64) return cudaErrorInvalidValue;
   if (ntok == 0) return cudaSuccess;
+  cudaError_t el;
   if (C * p * p == 16)
-    patch_embed16_kernel<<<(ntok + PE_TOK - 1) / PE_TOK, 256, 0, s>>>(x_band, W, C, p, w, b,
-                                                                      pos_rows, d, B, ntok, x_res);
+    el = launch_pdl(patch_embed16_kernel, dim3((ntok + PE_TOK - 1) / PE_TOK), dim3(256), 0, s,
+                    x_band, W, C, p, w, b, pos_rows, d, B, ntok, x_res);
   else
-    patch_embed_kernel<<<ntok, 256, 0, s>>>(x_band, W, C, p, w, b, pos_rows, d, B, x_res);
+    el = launch_pdl(patch_embed_kernel, dim3(ntok), dim3(256), 0, s, x_band, W, C, p, w, b,
+                    pos_rows, d, B, x_res);
   ++g_launches;
-  return cudaGetLastError();
+  return el;
 }
 
 cudaError_t sampler_update(float *x_band, const float *eps_raw, int rows, int W, int C, int p,
@@ -423,11 +429,11 @@ cudaError_t sampler_update(float *x_band, const float *eps_raw, int rows, int W,
                            cudaStream_t s, float *hist, float c1, float c2) {
   const long n = (long)rows * W * C;
   if (n == 0) return cudaSuccess;
-  sampler_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-      x_band, eps_raw, rows, W, C, p, c_out, ld, B, guidance, A, Bc, Cz, seed, seed_dev, m, row0,
-      hist, c1, c2);
+  const cudaError_t el = launch_pdl(sampler_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0,
+                                    s, x_band, eps_raw, rows, W, C, p, c_out, ld, B, guidance, A,
+                                    Bc, Cz, seed, seed_dev, m, row0, hist, c1, c2);
   ++g_launches;
-  return cudaGetLastError();
+  return el;
 }
 
 cudaError_t philox_normal_fill(float *out, long n, uint64_t seed, uint32_t m, long e0,

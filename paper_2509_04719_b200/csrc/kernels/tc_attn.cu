@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // Q / K / V written by the predecessor (QKV GEMM) are complete
 
   // TMA of one tile of every head-dim chunk (row: first token coordinate)
   auto load_tile = [&](const CUtensorMap *m64, const CUtensorMap *m32, const CUtensorMap *m16,
@@ -923,8 +924,10 @@ cudaError_t launch_attn_p(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nk
   }
   dim3 grid((Nq + AQ * NQT - 1) / (AQ * NQT), H, B);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-  tc_attn_kernel<N64, N32, N16, NQT, POLY, QUAD><<<grid, C::THREADS, C::SMEM, s>>>(
-      tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], o, Nq, Nkv, B, H, hd, scale_log2, attn_flags());
+  cudaError_t el = launch_pdl(tc_attn_kernel<N64, N32, N16, NQT, POLY, QUAD>, grid,
+                              dim3(C::THREADS), C::SMEM, s, tm[0], tm[1], tm[2], tm[3], tm[4],
+                              tm[5], o, Nq, Nkv, B, H, hd, scale_log2, attn_flags());
+  if (el != cudaSuccess) return el;
   ++g_launches;
   return cudaGetLastError();
 }

@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (NCL == 2) cluster_sync();  // partner's barriers initialised before any multicast
+  pdl_wait();                    // the predecessor's outputs (A, residual) are complete
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // order every run: deterministic), then the GEMM epilogue on the column pair.
 template <int EPI>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(int M, int N, int ksplit, EpiParams ep) {
+  pdl_wait();
   const long quads = (long)M * (N / 4);
   const long plane = (long)M * N;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < quads;
@@ -614,13 +616,15 @@ cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = NCL;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   EpiParams epk = ep;
   epk.res_prefetch = res_prefetch_enabled() ? 1 : 0;
   epk.res_vec4 = res_vec4_enabled() ? 1 : 0;
@@ -631,7 +635,8 @@ cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const
   if (ksplit > 1) {
     const long quads = (long)M * (N / 4);
     const int rb = (int)std::min<long>((quads + 255) / 256, 148L * 8);
-    splitk_reduce_kernel<EPI><<<rb, 256, 0, s>>>(M, N, ksplit, ep);
+    cudaError_t e2 = launch_pdl(splitk_reduce_kernel<EPI>, dim3(rb), dim3(256), 0, s, M, N, ksplit, ep);
+    if (e2 != cudaSuccess) return e2;
     ++g_launches;
   }
   return cudaGetLastError();
@@ -717,6 +722,14 @@ GemmPlan plan_gemm(int M, int N, int K, int max_ctas, int mc, long ws_elems) {
 // two independent 128-row tiles with a multicast W tile (C5 out-proj 654 vs 613
 // TFLOP/s; 8192^3 1342 vs 1278 the other way).  STADI_GEMM_MC=0 / 2 / 3 forces
 // single-CTA tiles / multicast pairs / the cta_group::2 MMA (A/B comparisons).
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char *e = getenv("STADI_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 int gemm_pair_mode() {
   static const int v = [] {
     const char *e = getenv("STADI_GEMM_MC");

@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(256) gn_partials_kernel(const float *__restric
                                                           double *__restrict__ ws,
                                                           unsigned *__restrict__ ticket,
                                                           double *__restrict__ out) {
+  pdl_wait();
   extern __shared__ float sm[];  // [2 stats][slots][B][C]
   __shared__ bool last;
   const int nvec = C / 4;
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(
     const float *__restrict__ x, int h, int W, int B, int C, const double *__restrict__ stats,
     int G, double n_total, const float *__restrict__ gamma, const float *__restrict__ beta,
     float eps, int act, int pad, T *__restrict__ out) {
+  pdl_wait();
   __shared__ float mu[2 * GN_G], rs[2 * GN_G];
   if (stats) {
     for (int j = threadIdx.x; j < B * GN_G; j += blockDim.x) {
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(
 template <typename T>
 __global__ void latent_pad_kernel(const float *__restrict__ x, int h, int W, int Cl, int B,
                                   T *__restrict__ out) {
+  pdl_wait();
   const long total = (long)(h + 2) * (W + 2) * B * Cl;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long)gridDim.x * blockDim.x) {
@@ -176,6 +179,7 @@ template <typename T, int V>
 __global__ void __launch_bounds__(256) im2col_kernel(const T *__restrict__ P, int hin, int Win,
                                                      int B, int C, int mode, int ho, int wo,
                                                      int Kp, T *__restrict__ A) {
+  pdl_wait();
   const int kv = Kp / V;  // vectors per A row
   const long total = (long)ho * wo * B * kv;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -229,6 +233,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) halo_fill_kernel(T *__restrict__ P, int h, int W, int B,
                                                         int C, const T *__restrict__ above,
                                                         const T *__restrict__ below) {
+  pdl_wait();
   const long rowe = (long)(W + 2) * B * C;        // elements of one padded row
   const long inner = (long)W * B * C;             // interior elements of a row
   const long cell = (long)B * C;
@@ -257,6 +262,7 @@ __global__ void __launch_bounds__(256) halo_fill_kernel(T *__restrict__ P, int h
 // ------------------------------------------------------------- concat
 __global__ void concat_kernel(const float *__restrict__ a, int Ca, const float *__restrict__ b,
                               int Cb, long M, float *__restrict__ out) {
+  pdl_wait();
   const int C = Ca + Cb;
   const long total = M * (C / 4);
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -287,9 +293,10 @@ cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, doubl
   const int nb = (int)((M + rpb - 1) / rpb);
   const int nvec = C / 4, slots = nvec >= 256 ? 1 : 256 / nvec;
   const size_t smem = (size_t)2 * slots * B * C * sizeof(float);
-  gn_partials_kernel<<<nb, 256, smem, s>>>(x, M, B, C, rpb, ws, ticket, out);
+  const cudaError_t el = launch_pdl(gn_partials_kernel, dim3(nb), dim3(256), smem, s, x, M, B, C,
+                                    rpb, ws, ticket, out);
   ++g_launches;
-  return cudaGetLastError();
+  return el;
 }
 
 template <typename T>
@@ -299,10 +306,10 @@ cudaError_t gn_apply(const float *x, int h, int W, int B, int C, const double *s
   if (C % 4 || (stats && C % GN_G) || B > 2) return cudaErrorInvalidValue;
   const long work = (long)h * W * B * (C / 4);
   if (work == 0) return cudaSuccess;
-  gn_apply_kernel<T><<<grid_for(work), 256, 0, s>>>(x, h, W, B, C, stats, G, n_total, gamma,
-                                                    beta, eps, act, pad, out);
+  const cudaError_t el = launch_pdl(gn_apply_kernel<T>, dim3(grid_for(work)), dim3(256), 0, s, x,
+                                    h, W, B, C, stats, G, n_total, gamma, beta, eps, act, pad, out);
   ++g_launches;
-  return cudaGetLastError();
+  return el;
 }
 template cudaError_t gn_apply<bf16>(const float *, int, int, int, int, const double *, int,
                                     double, const float *, const float *, float, int, int, bf16 *,
@@ -316,9 +323,10 @@ cudaError_t halo_fill(T *P, int h, int W, int B, int C, const T *above, const T 
                       cudaStream_t s) {
   const long rowe = (long)(W + 2) * B * C;
   const long work = 2 * rowe / (((long)B * C) % (16 / sizeof(T)) == 0 ? 16 / sizeof(T) : 1);
-  halo_fill_kernel<T><<<grid_for(work), 256, 0, s>>>(P, h, W, B, C, above, below);
+  const cudaError_t el = launch_pdl(halo_fill_kernel<T>, dim3(grid_for(work)), dim3(256), 0, s, P,
+                                    h, W, B, C, above, below);
   ++g_launches;
-  return cudaGetLastError();
+  return el;
 }
 template cudaError_t halo_fill<bf16>(bf16 *, int, int, int, int, const bf16 *, const bf16 *,
                                      cudaStream_t);
@@ -328,9 +336,10 @@ template cudaError_t halo_fill<float>(float *, int, int, int, int, const float *
 template <typename T>
 cudaError_t latent_pad(const float *x, int h, int W, int Cl, int B, T *out, cudaStream_t s) {
   const long work = (long)(h + 2) * (W + 2) * B * Cl;
-  latent_pad_kernel<T><<<grid_for(work), 256, 0, s>>>(x, h, W, Cl, B, out);
+  const cudaError_t el = launch_pdl(latent_pad_kernel<T>, dim3(grid_for(work)), dim3(256), 0, s, x,
+                                    h, W, Cl, B, out);
   ++g_launches;
-  return cudaGetLastError();
+  return el;
 }
 template cudaError_t latent_pad<bf16>(const float *, int, int, int, int, bf16 *, cudaStream_t);
 template cudaError_t latent_pad<float>(const float *, int, int, int, int, float *, cudaStream_t);
@@ -343,10 +352,14 @@ cudaError_t im2col(const T *P, int hin, int Win, int B, int C, int mode, int Kp,
   if (Kp < 9 * C) return cudaErrorInvalidValue;
   if (C % 8 == 0 && Kp % 8 == 0 && sizeof(T) == 2) {
     const long work = (long)ho * wo * B * (Kp / 8);
-    im2col_kernel<T, 8><<<grid_for(work), 256, 0, s>>>(P, hin, Win, B, C, mode, ho, wo, Kp, A);
+    const cudaError_t el = launch_pdl(im2col_kernel<T, 8>, dim3(grid_for(work)), dim3(256), 0, s,
+                                      P, hin, Win, B, C, mode, ho, wo, Kp, A);
+    if (el != cudaSuccess) return el;
   } else {
     const long work = (long)ho * wo * B * Kp;
-    im2col_kernel<T, 1><<<grid_for(work), 256, 0, s>>>(P, hin, Win, B, C, mode, ho, wo, Kp, A);
+    const cudaError_t el = launch_pdl(im2col_kernel<T, 1>, dim3(grid_for(work)), dim3(256), 0, s,
+                                      P, hin, Win, B, C, mode, ho, wo, Kp, A);
+    if (el != cudaSuccess) return el;
   }
   ++g_launches;
   return cudaGetLastError();
@@ -361,9 +374,10 @@ cudaError_t concat_channels(const float *a, int Ca, const float *b, int Cb, long
   if (Ca % 4 || Cb % 4) return cudaErrorInvalidValue;
   const long work = M * ((Ca + Cb) / 4);
   if (work == 0) return cudaSuccess;
-  concat_kernel<<<grid_for(work), 256, 0, s>>>(a, Ca, b, Cb, M, out);
+  const cudaError_t el = launch_pdl(concat_kernel, dim3(grid_for(work)), dim3(256), 0, s, a, Ca, b,
+                                    Cb, M, out);
   ++g_launches;
-  return cudaGetLastError();
+  return el;
 }
 
 }  // namespace stadi

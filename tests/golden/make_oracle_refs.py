@@ -43,4 +43,5 @@ if __name__ == "__main__":
             t0 = time.time()
             fn()
             print(f"{mod.__name__}: {what} {time.time() - t0:.1f}s", flush=True)
-    refcache.rewrite_index()
+    if not filt:  # only a full pass has seen every case (a filtered one would drop refs)
+        refcache.rewrite_index()
