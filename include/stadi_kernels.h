@@ -113,6 +113,21 @@ stadi_status stadi_k_sampler(float *x, const float *eps_raw, int32_t rows, int32
 stadi_status stadi_k_ddpm_noise(float *out, int64_t n, uint64_t seed, uint32_t m, int64_t e0,
                                 void *stream);
 
+/* GroupNorm(32 groups) of a U-Net band (PAPER.md L80 -- the band's
+ * partial sums are the GN exchange payload): x f32 [h, W, B, C] (token-major,
+ * batch innermost), B <= 2, C % 32 == 0, C <= 3072.  Step 1 writes the band's
+ * partial sums stats f64 [B][32][{sum x, sum x^2}] (caller-owned, device; ws f64
+ * [592 * 2 * B * 32] and ticket (one zero-initialised uint32) are scratch);
+ * step 2 normalises with n_total = h * W * C / 32 elements per group (mean =
+ * S1 / n, var = max(S2 / n - mean^2, 0)), applies gamma / beta (f32 [C]), SiLU
+ * when act != 0, and writes out (T = bf16 or f32 per dtype) either plain [h, W,
+ * B, C] (pad == 0) or into the interior of the halo-padded [h+2, W+2, B, C]
+ * (pad == 1; the left / right border columns zeroed, halo rows untouched). */
+stadi_status stadi_k_groupnorm(int32_t dtype, const float *x, int32_t h, int32_t W, int32_t B,
+                               int32_t C, const float *gamma, const float *beta, float eps,
+                               int32_t act, int32_t pad, double *stats, double *ws,
+                               uint32_t *ticket, void *out, void *stream);
+
 /* Number of kernels launched by this process so far. */
 uint64_t stadi_k_launch_count(void);
 

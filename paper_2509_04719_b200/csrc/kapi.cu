@@ -101,6 +101,26 @@ extern "C" stadi_status stadi_k_ln_modulate(int32_t dtype, const float *x, void 
 
 extern "C" uint64_t stadi_k_launch_count(void) { return g_launches; }
 
+extern "C" stadi_status stadi_k_groupnorm(int32_t dtype, const float *x, int32_t h, int32_t W,
+                                          int32_t B, int32_t C, const float *gamma,
+                                          const float *beta, float eps, int32_t act, int32_t pad,
+                                          double *stats, double *ws, uint32_t *ticket, void *out,
+                                          void *stream) {
+  if (!x || !gamma || !beta || !stats || !ws || !ticket || !out || h < 0 || W <= 0 || B <= 0 ||
+      B > 2 || C <= 0 || C % 32 || C > 3072)
+    return fail(nullptr, STADI_EINVAL, "stadi_k_groupnorm: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const stadi_status sp = cu(gn_partials(x, (long)h * W * B, B, C, stats, ws, ticket, s),
+                             "gn_partials");
+  if (sp != STADI_OK) return sp;
+  const double n_total = (double)h * W * (C / 32);
+  if (dtype == STADI_DTYPE_BF16)
+    return cu(gn_apply<bf16>(x, h, W, B, C, stats, 1, n_total, gamma, beta, eps, act, pad,
+                             (bf16 *)out, s), "gn_apply");
+  return cu(gn_apply<float>(x, h, W, B, C, stats, 1, n_total, gamma, beta, eps, act, pad,
+                            (float *)out, s), "gn_apply");
+}
+
 extern "C" stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void *Wt, int32_t h,
                                         int32_t W, int32_t B, int32_t C, int32_t N, int32_t mode,
                                         int32_t implicit, const float *bias, float *out,

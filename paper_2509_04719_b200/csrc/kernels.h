@@ -81,9 +81,11 @@ cudaError_t pixart_mods(const float *t0, const float *temb, const float *sst_all
 // blocks in a fixed order (bitwise reproducible): ws = GN_PARTIAL_BLOCKS * 2 * B * 32
 // doubles of workspace, ticket = one zero-initialised unsigned (reset by the kernel);
 // one (ws, ticket) pair per stream.
+// out2 / out3 (optional): further copies of out (the exchange slots).  C <= 3072.
 constexpr int GN_PARTIAL_BLOCKS = 592;
 cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, double *ws,
-                        unsigned *ticket, cudaStream_t s);
+                        unsigned *ticket, cudaStream_t s, double *out2 = nullptr,
+                        double *out3 = nullptr);
 // Halo rows of the padded conv input P [h+2, W+2, B, C]: row 0 <- above, row h+1
 // <- below (W*B*C elements each; NULL = zeros at the image edge), corners zero.
 template <typename T>

@@ -113,9 +113,11 @@ __device__ __forceinline__ void ex2_poly_x2(uint64_t xx, float &p0, float &p1) {
 // polynomial exp2, the rest MUFU ex2.
 
 // Head-dim chunking: N64 chunks of 64, then N32 of 32, then N16 of 16.
-template <int N64, int N32, int N16, int NQT_>
+// AKTO != 0: P aliased over S (no separate P region), AKTO keys per tile.
+template <int N64, int N32, int N16, int NQT_, int AKTO = 0>
 struct AttnCfg {
   static constexpr int NQT = NQT_;
+  static constexpr bool PALIAS = AKTO != 0;
   static constexpr int HDP = 64 * N64 + 32 * N32 + 16 * N16;
   static constexpr int NCH = N64 + N32 + N16;
   // keys per tile: 112 with two query tiles so that S (2 x 112), O (2 x 80) and a
@@ -126,7 +128,7 @@ struct AttnCfg {
   static constexpr bool DUAL = NQT == 1 && 64 * N64 + 32 * N32 + 16 * N16 <= 80;
   static constexpr int MINB = DUAL ? 2 : 1;      // CTAs per SM
   static constexpr uint32_t TMEM_COLS = DUAL ? 256 : 512;
-  static constexpr int AKT = (NQT == 2 || DUAL) ? 112 : 128;
+  static constexpr int AKT = AKTO ? AKTO : ((NQT == 2 || DUAL) ? 112 : 128);
   static constexpr int QTILE = AQ * HDP * 2;   // one Q tile (128 rows), bytes
   static constexpr int KTILE = AKT * HDP * 2;  // one K or V tile, bytes
   __host__ __device__ static constexpr int cw(int c) {  // chunk width
@@ -152,7 +154,7 @@ struct AttnCfg {
 #define STADI_ATTN_MAX_STAGES 4
 #endif
   static constexpr int STAGES_FIT =
-      ((DUAL ? 100 : STADI_ATTN_SMEM_KB) * 1024 - NQT * QTILE) / (2 * KTILE);
+      ((DUAL ? 100 : (PALIAS ? 224 : STADI_ATTN_SMEM_KB)) * 1024 - NQT * QTILE) / (2 * KTILE);
   static constexpr int STAGES =
       STAGES_FIT > STADI_ATTN_MAX_STAGES ? STADI_ATTN_MAX_STAGES : STAGES_FIT;
   static constexpr int OFF_K = NQT * QTILE;
@@ -175,7 +177,8 @@ struct AttnCfg {
   __host__ __device__ static constexpr uint32_t p_col(int g) {
     return (uint32_t)(NQT * (AKT + HDP) + 64 * g);
   }
-  static_assert(NQT * (AKT + HDP + 64) <= (int)TMEM_COLS, "TMEM columns");
+  static_assert(NQT * (AKT + HDP + (PALIAS ? 0 : 64)) <= (int)TMEM_COLS, "TMEM columns");
+  static_assert(AKT % 16 == 0 && AKT <= 256, "key tile");
   static_assert(!DUAL || 2 * (SMEM + 1024) <= 228 * 1024, "two CTAs per SM");
   static_assert(NQT == 1 || HDP <= 80, "two query tiles need HDP <= 80");
   static_assert(STAGES >= 2, "smem");
@@ -244,15 +247,15 @@ __device__ __forceinline__ void tmem_store_packed(uint32_t taddr, const uint32_t
   if constexpr (NP % 16) tmem_st8(taddr + (NP - 8), pk + (NP - 8));
 }
 
-template <int N64, int N32, int N16, int NQT, int POLY, int QUAD>
-__global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT>::THREADS,
-                                  AttnCfg<N64, N32, N16, NQT>::MINB)
+template <int N64, int N32, int N16, int NQT, int POLY, int QUAD, int AKTO = 0>
+__global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
+                                  AttnCfg<N64, N32, N16, NQT, AKTO>::MINB)
     tc_attn_kernel(const __grid_constant__ CUtensorMap tq64, const __grid_constant__ CUtensorMap tq32,
                    const __grid_constant__ CUtensorMap tq16, const __grid_constant__ CUtensorMap tk64,
                    const __grid_constant__ CUtensorMap tk32, const __grid_constant__ CUtensorMap tk16,
                    bf16 *__restrict__ out, int Nq, int Nkv, int B, int H, int hd, float scale_log2,
                    int flags) {  // bit 0: exp-phase tokens, bit 1: deferred PV wait (QUAD), bit 2: MMA order
-  using C = AttnCfg<N64, N32, N16, NQT>;
+  using C = AttnCfg<N64, N32, N16, NQT, AKTO>;
   constexpr int AKT = C::AKT;
   // QUAD == 2: P aliased over S.  PV_g(j) and S_g(j+1) are issued back to back once
   // P_g(j) is stored and committed to ONE barrier (s_full), so a key tile costs each
@@ -891,10 +894,10 @@ int attn_flags() {
   }();
   return v;
 }
-template <int N64, int N32, int N16, int NQT, int POLY, int QUAD>
+template <int N64, int N32, int N16, int NQT, int POLY, int QUAD, int AKTO = 0>
 cudaError_t launch_attn_p(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B, int H,
                         int hd, cudaStream_t s) {
-  using C = AttnCfg<N64, N32, N16, NQT>;
+  using C = AttnCfg<N64, N32, N16, NQT, AKTO>;
   const int d = H * hd;
   if (d % 8) return cudaErrorInvalidValue;  // TMA: 16-byte row strides
   CUtensorMap tm[6] = {};
@@ -917,14 +920,14 @@ cudaError_t launch_attn_p(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nk
   if (!ok) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_attn_kernel<N64, N32, N16, NQT, POLY, QUAD>,
+    cudaError_t e = cudaFuncSetAttribute(tc_attn_kernel<N64, N32, N16, NQT, POLY, QUAD, AKTO>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   dim3 grid((Nq + AQ * NQT - 1) / (AQ * NQT), H, B);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-  cudaError_t el = launch_pdl(tc_attn_kernel<N64, N32, N16, NQT, POLY, QUAD>, grid,
+  cudaError_t el = launch_pdl(tc_attn_kernel<N64, N32, N16, NQT, POLY, QUAD, AKTO>, grid,
                               dim3(C::THREADS), C::SMEM, s, tm[0], tm[1], tm[2], tm[3], tm[4],
                               tm[5], o, Nq, Nkv, B, H, hd, scale_log2, attn_flags());
   if (el != cudaSuccess) return el;
@@ -962,12 +965,34 @@ int attn_alias() {
   }();
   return v;
 }
+// STADI_ATTN_AKT=144/160/176 (+1 / +2: one / two of every 8 column pairs on the
+// polynomial exp2): keys per tile of the P-over-S variant for hd 72 / 80 (TMEM
+// holds 2 x (AKT + 80) <= 512 columns without the separate P region).
+int attn_alias_akt() {
+  static const int v = [] {
+    const char *e = getenv("STADI_ATTN_AKT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 template <int N64, int N32, int N16, int NQT>
 cudaError_t launch_attn(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B, int H,
                         int hd, cudaStream_t s) {
   if (!attn_quad()) return launch_attn_p<N64, N32, N16, NQT, 0, 0>(q, kv, o, Nq, Nkv, B, H, hd, s);
-  if (NQT == 2 && attn_alias() && attn_poly() == 0)
+  if (NQT == 2 && attn_alias() && attn_poly() == 0) {
+    if constexpr (NQT == 2 && 64 * N64 + 32 * N32 + 16 * N16 == 80) {  // hd 72 / 80
+      switch (attn_alias_akt()) {
+        case 144: return launch_attn_p<N64, N32, N16, NQT, 0, 2, 144>(q, kv, o, Nq, Nkv, B, H, hd, s);
+        case 160: return launch_attn_p<N64, N32, N16, NQT, 0, 2, 160>(q, kv, o, Nq, Nkv, B, H, hd, s);
+        case 176: return launch_attn_p<N64, N32, N16, NQT, 0, 2, 176>(q, kv, o, Nq, Nkv, B, H, hd, s);
+        case 160 + 1: return launch_attn_p<N64, N32, N16, NQT, 1, 2, 160>(q, kv, o, Nq, Nkv, B, H, hd, s);
+        case 176 + 1: return launch_attn_p<N64, N32, N16, NQT, 1, 2, 176>(q, kv, o, Nq, Nkv, B, H, hd, s);
+        case 176 + 2: return launch_attn_p<N64, N32, N16, NQT, 2, 2, 176>(q, kv, o, Nq, Nkv, B, H, hd, s);
+        default: break;
+      }
+    }
     return launch_attn_p<N64, N32, N16, NQT, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+  }
   switch (attn_poly()) {
     case 0: return launch_attn_p<N64, N32, N16, NQT, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 1: return launch_attn_p<N64, N32, N16, NQT, 1, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
@@ -1000,6 +1025,14 @@ void preload_attn(cudaFuncAttributes *a) {
   cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 3, 1>);
   cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 4, 1>);
   cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 2>);
+  if constexpr (NQT == 2 && 64 * N64 + 32 * N32 + 16 * N16 == 80) {
+    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 2, 144>);
+    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 2, 160>);
+    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 2, 176>);
+    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 1, 2, 160>);
+    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 1, 2, 176>);
+    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 2, 2, 176>);
+  }
 }
 }  // namespace
 cudaError_t tc_attention_preload() {

@@ -19,80 +19,136 @@ namespace {
 constexpr int GN_G = 32;
 
 // ------------------------------------------------------------- GN partials
-// out[b][g][0] = sum x, out[b][g][1] = sum x^2 over the band, DETERMINISTIC: one
-// block = a chunk of rows; thread t owns float4 channel vector t % nvec of row
-// slots t / nvec (all 256 threads busy when nvec < 256), fp32 per thread, reduced
-// in smem per (b, channel), then per (b, group) in fp64 into the block's own
-// workspace row; the last block to finish (atomic ticket) sums the rows in block
-// order and resets the ticket -- the same bits on every run (no fp64 atomics).
-__global__ void __launch_bounds__(256) gn_partials_kernel(const float *__restrict__ x, long M,
-                                                          int B, int C, int rows_per_block,
-                                                          double *__restrict__ ws,
-                                                          unsigned *__restrict__ ticket,
-                                                          double *__restrict__ out) {
-  pdl_wait();
+// out[b][g][0] = sum x, out[b][g][1] = sum x^2 over the band, DETERMINISTIC (the
+// same bits on every run: fixed per-thread row sets, fixed-order reductions, no
+// floating-point atomics).  One block = a chunk of rpb consecutive rows (rpb even,
+// so a row's batch index is its parity when B = 2), at most GNP_MAXB blocks:
+//   thread t owns float4 channel vectors v = t % nvec (+ 256 k when nvec > 256) of
+//   the rows r0 + slot, r0 + slot + slots, ... (slot = t / nvec) and accumulates
+//   fp32 sums per (batch, channel); the block folds the slots, then two threads per
+//   (statistic, batch, group) output sum half the group's channels each in fp64 (one
+//   shuffle) into the block's workspace row.  The last block to finish (atomic
+//   ticket) sums the <= 64 rows -- two threads per output, one wave of independent
+//   loads -- and writes out and, optionally, out2 / out3 (the exchange slots, saving
+//   two copies), then resets the ticket.
+constexpr int GNP_THREADS = 256;
+constexpr int GNP_MAXV = 3;  // vectors per thread: C <= 4 * 256 * 3 = 3072
+constexpr int GNP_MAXB = 64;  // blocks per launch (the last block's reduce is one load wave)
+
+__global__ void __launch_bounds__(GNP_THREADS) gn_partials_kernel(
+    const float *__restrict__ x, int M, int B, int C, int rpb, double *__restrict__ ws,
+    unsigned *__restrict__ ticket, double *__restrict__ out, double *__restrict__ out2,
+    double *__restrict__ out3) {
   extern __shared__ float sm[];  // [2 stats][slots][B][C]
   __shared__ bool last;
+  pdl_wait();
   const int nvec = C / 4;
-  const int slots = nvec >= 256 ? 1 : 256 / nvec;
-  const long r0 = (long)blockIdx.x * rows_per_block;
-  const long r1 = min(M, r0 + rows_per_block);
-  for (int t = threadIdx.x; t < (nvec >= 256 ? nvec : slots * nvec); t += blockDim.x) {
-    const int v = t % nvec, slot = t / nvec;
-    float4 s1a = make_float4(0.f, 0.f, 0.f, 0.f), s2a = s1a, s1b = s1a, s2b = s1a;
-    for (long r = r0 + slot; r < r1; r += slots) {
-      const float4 a = reinterpret_cast<const float4 *>(x + r * C)[v];
-      if ((r % B) == 0) {
-        s1a.x += a.x; s1a.y += a.y; s1a.z += a.z; s1a.w += a.w;
-        s2a.x += a.x * a.x; s2a.y += a.y * a.y; s2a.z += a.z * a.z; s2a.w += a.w * a.w;
-      } else {
-        s1b.x += a.x; s1b.y += a.y; s1b.z += a.z; s1b.w += a.w;
-        s2b.x += a.x * a.x; s2b.y += a.y * a.y; s2b.z += a.z * a.z; s2b.w += a.w * a.w;
+  const int slots = nvec >= GNP_THREADS ? 1 : GNP_THREADS / nvec;
+  const int r0 = blockIdx.x * rpb, r1 = min(M, r0 + rpb);
+  const int t = threadIdx.x;
+  if (t < slots * nvec || nvec >= GNP_THREADS) {
+    const int slot = nvec >= GNP_THREADS ? 0 : t / nvec;
+    const int v0 = nvec >= GNP_THREADS ? t : t % nvec;
+    float4 s1[2][GNP_MAXV], s2[2][GNP_MAXV];
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+      for (int k = 0; k < GNP_MAXV; ++k)
+        s1[bb][k] = s2[bb][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = r0 + slot; r < r1; r += slots) {
+      const float4 *row = reinterpret_cast<const float4 *>(x + (long)r * C);
+      const bool odd = B == 2 && (r & 1);
+#pragma unroll
+      for (int k = 0; k < GNP_MAXV; ++k) {
+        const int v = v0 + k * GNP_THREADS;
+        if (v >= nvec) break;
+        const float4 a = row[v];
+        auto add = [&](float4 &p, float4 &q) {
+          p.x += a.x; p.y += a.y; p.z += a.z; p.w += a.w;
+          q.x += a.x * a.x; q.y += a.y * a.y; q.z += a.z * a.z; q.w += a.w * a.w;
+        };
+        if (odd) add(s1[1][k], s2[1][k]);
+        else add(s1[0][k], s2[0][k]);
       }
     }
-    float *p1 = sm + ((0 * slots + slot) * B) * C + 4 * v;
-    float *p2 = sm + ((1 * slots + slot) * B) * C + 4 * v;
-    *reinterpret_cast<float4 *>(p1) = s1a;
-    *reinterpret_cast<float4 *>(p2) = s2a;
-    if (B > 1) {
-      *reinterpret_cast<float4 *>(p1 + C) = s1b;
-      *reinterpret_cast<float4 *>(p2 + C) = s2b;
+#pragma unroll
+    for (int k = 0; k < GNP_MAXV; ++k) {
+      const int v = v0 + k * GNP_THREADS;
+      if (v >= nvec) break;
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb) {
+        if (bb >= B) break;
+        *reinterpret_cast<float4 *>(sm + ((0 * slots + slot) * B + bb) * C + 4 * v) = s1[bb][k];
+        *reinterpret_cast<float4 *>(sm + ((1 * slots + slot) * B + bb) * C + 4 * v) = s2[bb][k];
+      }
     }
   }
   __syncthreads();
-  const int cg = C / GN_G, nst = 2 * B * GN_G;
-  for (int jj = threadIdx.x; jj < nst; jj += blockDim.x) {
-    const int st = jj / (B * GN_G), b = (jj / GN_G) % B, g = jj % GN_G;
+  // slots -> slot 0 per (statistic, batch, channel), fixed order
+  if (slots > 1) {
+    for (int e = t; e < 2 * B * C; e += GNP_THREADS) {
+      const int st = e / (B * C), rem = e % (B * C);
+      float acc = sm[(st * slots) * B * C + rem];
+      for (int sl = 1; sl < slots; ++sl) acc += sm[(st * slots + sl) * B * C + rem];
+      sm[(st * slots) * B * C + rem] = acc;
+    }
+    __syncthreads();
+  }
+  // per (statistic, batch, group): two threads per output, each half the group's
+  // channels in fp64, combined by one shuffle
+  const int cg = C / GN_G, nst = 2 * B * GN_G, half = (cg + 1) / 2;
+  const int o = t >> 1, hf = t & 1;  // o = (b * 32 + g) * 2 + st
+  if (o < nst) {
+    const int st = o & 1, g = (o >> 1) % GN_G, bb = (o >> 1) / GN_G;
+    const float *src = sm + (st * slots * B + bb) * C + g * cg;
     double acc = 0.0;
-    for (int sl = 0; sl < slots; ++sl)
-      for (int c = 0; c < cg; ++c) acc += (double)sm[((st * slots + sl) * B + b) * C + g * cg + c];
-    ws[(long)blockIdx.x * nst + ((long)b * GN_G + g) * 2 + st] = acc;
+    for (int c = hf * half; c < min(cg, (hf + 1) * half); ++c) acc += (double)src[c];
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (hf == 0) ws[(long)blockIdx.x * nst + o] = acc;
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  if (t == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int jj = threadIdx.x; jj < nst; jj += blockDim.x) {
+  // the last block: two threads per output, each <= GNP_MAXB / 2 independent loads
+  if (o < nst) {
     double acc = 0.0;
-    for (unsigned k = 0; k < gridDim.x; ++k) acc += __ldcg(ws + (long)k * nst + jj);
-    out[jj] = acc;
+#pragma unroll
+    for (int k = 0; k < GNP_MAXB / 2; ++k) {
+      const int blk = hf * (GNP_MAXB / 2) + k;
+      if (blk < (int)gridDim.x) acc += __ldcg(ws + (long)blk * nst + o);
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (hf == 0) {
+      out[o] = acc;
+      if (out2) out2[o] = acc;
+      if (out3) out3[o] = acc;
+    }
   }
-  if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
+  if (t == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
 }
 
 // ------------------------------------------------------------- GN apply
-// y = (x - mean) * rstd * gamma + beta (+ SiLU), mean / var from the sum over the
+// y = (x - mean) * (rstd * gamma) + beta (+ SiLU), mean / var from the sum over the
 // G rank segments of the statistics (own fresh + others stale); stats == null:
 // plain cast.  pad: write into the halo-padded buffer (interior + zero columns).
+// One block = a chunk of rows (pixel, batch); each warp takes whole rows, lanes
+// over the float4 channel vectors (coalesced 512-byte loads), 32-bit indexing,
+// per-row (not per-element) pixel coordinates; the per-(batch, channel) mean and
+// scale live in shared memory (dynamic: 2 B C floats + C).
+constexpr int GNA_THREADS = 256;
 template <typename T>
-__global__ void __launch_bounds__(256) gn_apply_kernel(
-    const float *__restrict__ x, int h, int W, int B, int C, const double *__restrict__ stats,
-    int G, double n_total, const float *__restrict__ gamma, const float *__restrict__ beta,
-    float eps, int act, int pad, T *__restrict__ out) {
+__global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(
+    const float *__restrict__ x, int h, int W, int B, int C, int rpb,
+    const double *__restrict__ stats, int G, double n_total, const float *__restrict__ gamma,
+    const float *__restrict__ beta, float eps, int act, int pad, T *__restrict__ out) {
+  extern __shared__ float gsm[];  // mu [B][C], sc [B][C], beta [C]
+  __shared__ float mu_g[2 * GN_G], rs_g[2 * GN_G];
+  float *mu_c = gsm, *sc_c = gsm + B * C, *be_c = gsm + 2 * B * C;
   pdl_wait();
-  __shared__ float mu[2 * GN_G], rs[2 * GN_G];
+  const int cg = C / GN_G;
   if (stats) {
     for (int j = threadIdx.x; j < B * GN_G; j += blockDim.x) {
       double s1 = 0, s2 = 0;
@@ -102,52 +158,58 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(
       }
       const double m = s1 / n_total;
       const double var = fmax(s2 / n_total - m * m, 0.0);  // R17 clamp
-      mu[j] = (float)m;
-      rs[j] = (float)(1.0 / sqrt(var + (double)eps));
+      mu_g[j] = (float)m;
+      rs_g[j] = (float)(1.0 / sqrt(var + (double)eps));
     }
+    __syncthreads();
+    for (int j = threadIdx.x; j < B * C; j += blockDim.x) {
+      const int bb = j / C, c = j % C, gj = bb * GN_G + c / cg;
+      mu_c[j] = mu_g[gj];
+      sc_c[j] = rs_g[gj] * gamma[c];
+    }
+    for (int c = threadIdx.x; c < C; c += blockDim.x) be_c[c] = beta[c];
+    __syncthreads();
   }
-  __syncthreads();
-  const int nvec = C / 4, cg = C / GN_G;
-  const long total = (long)h * W * B * nvec;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long)gridDim.x * blockDim.x) {
-    const int v = (int)(i % nvec);
-    const long row = i / nvec;  // (y * W + x) * B + b
-    const int b = (int)(row % B);
-    float4 a = reinterpret_cast<const float4 *>(x + row * C)[v];
-    float e[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = 4 * v + k;
-      float y = e[k];
+  const int nvec = C / 4, M = h * W * B;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int r0 = blockIdx.x * rpb, r1 = min(M, r0 + rpb);
+  for (int row = r0 + warp; row < r1; row += GNA_THREADS / 32) {
+    const int bb = row % B, pix = row / B;
+    const int yy = pix / W, xx = pix - yy * W;
+    const long orow = pad ? ((long)(yy + 1) * (W + 2) + xx + 1) * B + bb : (long)row;
+    const float4 *src = reinterpret_cast<const float4 *>(x + (long)row * C);
+    T *o = out + orow * C;
+    for (int v = lane; v < nvec; v += 32) {
+      const float4 a = src[v];
+      float e[4] = {a.x, a.y, a.z, a.w};
       if (stats) {
-        const int j = b * GN_G + c / cg;
-        y = (y - mu[j]) * rs[j] * gamma[c] + beta[c];
+        const float4 m = *reinterpret_cast<const float4 *>(mu_c + bb * C + 4 * v);
+        const float4 s = *reinterpret_cast<const float4 *>(sc_c + bb * C + 4 * v);
+        const float4 be = *reinterpret_cast<const float4 *>(be_c + 4 * v);
+        e[0] = (e[0] - m.x) * s.x + be.x;
+        e[1] = (e[1] - m.y) * s.y + be.y;
+        e[2] = (e[2] - m.z) * s.z + be.z;
+        e[3] = (e[3] - m.w) * s.w + be.w;
       }
-      if (act) y = silu(y);
-      e[k] = y;
+      if (act) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) e[k] = silu(e[k]);
+      }
+      if constexpr (sizeof(T) == 2) {  // one 8-byte store of 4 bf16
+        __nv_bfloat162 lo = __floats2bfloat162_rn(e[0], e[1]),
+                       hi = __floats2bfloat162_rn(e[2], e[3]);
+        *reinterpret_cast<uint2 *>(o + 4 * v) =
+            make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+      } else {
+        *reinterpret_cast<float4 *>(o + 4 * v) = make_float4(e[0], e[1], e[2], e[3]);
+      }
     }
-    long orow = row;
-    if (pad) {
-      const long pix = row / B;
-      const int yy = (int)(pix / W), xx = (int)(pix % W);
-      orow = (((long)(yy + 1) * (W + 2) + xx + 1) * B + b);
-    }
-    T *o = out + orow * C + 4 * v;
-    if constexpr (sizeof(T) == 2) {  // one 8-byte store of 4 bf16
-      __nv_bfloat162 lo = __floats2bfloat162_rn(e[0], e[1]), hi = __floats2bfloat162_rn(e[2], e[3]);
-      *reinterpret_cast<uint2 *>(o) =
-          make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
-    } else {
-      *reinterpret_cast<float4 *>(o) = make_float4(e[0], e[1], e[2], e[3]);
-    }
-    if (pad) {  // zero the left / right border columns of this row
-      const long pix = row / B;
-      const int yy = (int)(pix / W), xx = (int)(pix % W);
-      if (xx == 0 || xx == W - 1) {
-        const long brow = (((long)(yy + 1) * (W + 2) + (xx == 0 ? 0 : W + 1)) * B + b);
-        T *z = out + brow * C + 4 * v;
-        z[0] = z[1] = z[2] = z[3] = from_f<T>(0.f);
+    if (pad && (xx == 0 || xx == W - 1)) {  // zero the left / right border cell(s)
+      const long prow = (long)(yy + 1) * (W + 2);
+      T *zl = out + ((prow + 0) * B + bb) * C, *zr = out + ((prow + W + 1) * B + bb) * C;
+      for (int c = lane; c < C; c += 32) {
+        if (xx == 0) zl[c] = from_f<T>(0.f);
+        if (xx == W - 1) zr[c] = from_f<T>(0.f);
       }
     }
   }
@@ -284,17 +346,28 @@ inline unsigned grid_for(long work, int per_block = 256) {
 }  // namespace
 
 cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, double *ws,
-                        unsigned *ticket, cudaStream_t s) {
-  if (C % (4 * GN_G) && C % 4) return cudaErrorInvalidValue;
-  if (B > 2 || C % 4 || C % GN_G || !ws || !ticket) return cudaErrorInvalidValue;
-  if (M == 0) return cudaMemsetAsync(out, 0, (size_t)B * GN_G * 2 * sizeof(double), s);
-  const int blocks = (int)std::min<long>(GN_PARTIAL_BLOCKS, M);
-  int rpb = (int)((M + blocks - 1) / blocks);
-  const int nb = (int)((M + rpb - 1) / rpb);
-  const int nvec = C / 4, slots = nvec >= 256 ? 1 : 256 / nvec;
+                        unsigned *ticket, cudaStream_t s, double *out2, double *out3) {
+  if (B > 2 || B < 1 || C % 4 || C % GN_G || C > 4 * GNP_THREADS * GNP_MAXV || !ws || !ticket ||
+      M > (1L << 30))
+    return cudaErrorInvalidValue;
+  if (M == 0) {
+    for (double *o : {out, out2, out3})
+      if (o) {
+        const cudaError_t e = cudaMemsetAsync(o, 0, (size_t)B * GN_G * 2 * sizeof(double), s);
+        if (e != cudaSuccess) return e;
+      }
+    return cudaSuccess;
+  }
+  // ~16 KB of X per block at least, at most GNP_MAXB blocks (the band is L2-warm)
+  const int nvec = C / 4, slots = nvec >= GNP_THREADS ? 1 : GNP_THREADS / nvec;
+  long rows_min = std::max<long>((4096 + C - 1) / C, slots);
+  long nb = std::min<long>((M + rows_min - 1) / rows_min, GNP_MAXB);
+  int rpb = (int)((M + nb - 1) / nb);
+  rpb += rpb & 1;  // even: the batch index of a row is its parity (B = 2)
+  nb = (M + rpb - 1) / rpb;
   const size_t smem = (size_t)2 * slots * B * C * sizeof(float);
-  const cudaError_t el = launch_pdl(gn_partials_kernel, dim3(nb), dim3(256), smem, s, x, M, B, C,
-                                    rpb, ws, ticket, out);
+  const cudaError_t el = launch_pdl(gn_partials_kernel, dim3((unsigned)nb), dim3(GNP_THREADS),
+                                    smem, s, x, (int)M, B, C, rpb, ws, ticket, out, out2, out3);
   ++g_launches;
   return el;
 }
@@ -303,11 +376,26 @@ template <typename T>
 cudaError_t gn_apply(const float *x, int h, int W, int B, int C, const double *stats, int G,
                      double n_total, const float *gamma, const float *beta, float eps, int act,
                      int pad, T *out, cudaStream_t s) {
-  if (C % 4 || (stats && C % GN_G) || B > 2) return cudaErrorInvalidValue;
-  const long work = (long)h * W * B * (C / 4);
-  if (work == 0) return cudaSuccess;
-  const cudaError_t el = launch_pdl(gn_apply_kernel<T>, dim3(grid_for(work)), dim3(256), 0, s, x,
-                                    h, W, B, C, stats, G, n_total, gamma, beta, eps, act, pad, out);
+  if (C % 4 || (stats && C % GN_G) || B > 2 || (long)h * W * B > (1L << 30))
+    return cudaErrorInvalidValue;
+  const long M = (long)h * W * B;
+  if (M == 0) return cudaSuccess;
+  // >= 8 rows per block (one per warp), <= 4 blocks per SM
+  const long nb = std::min<long>((M + 7) / 8, 148L * 4);
+  const int rpb = (int)((M + nb - 1) / nb);
+  const size_t smem = stats ? (size_t)(2 * B + 1) * C * sizeof(float) : 0;
+  if (smem > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      const cudaError_t e = cudaFuncSetAttribute(
+          gn_apply_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+  }
+  const cudaError_t el =
+      launch_pdl(gn_apply_kernel<T>, dim3((unsigned)((M + rpb - 1) / rpb)), dim3(GNA_THREADS),
+                 smem, s, x, h, W, B, C, rpb, stats, G, n_total, gamma, beta, eps, act, pad, out);
   ++g_launches;
   return el;
 }

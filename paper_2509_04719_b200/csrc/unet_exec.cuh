@@ -388,20 +388,19 @@ struct UBuilder {
       stadi_ctx *ctx = c;
       USite &S = ctx->un->sites[sid];
       const int pos = inc_pos(ctx->un.get(), ctx->ranks[me].g);
-      CK(timed(ctx, STADI_KCLASS_NORM, 0.0, (double)Ml * C * 4, s, [&] {
-        return gn_partials((const float *)X(), Ml, B, C, (double *)G(), ctx->un->gn_ws,
-                           ctx->un->gn_ticket, s);
-      }));
+      // own fresh partials straight into the read slot (R14) and, when it differs,
+      // the publish slot: the kernel's last block writes all copies
       if (st.pub_ver != st.read_ver) ST(u_wait(ctx, S, st.read_ver, s));
       const int64_t off = pos * S.seg_bytes;
-      CK(cudaMemcpyAsync((char *)S.slot[me][st.read_ver & 1] + off, G(), S.seg_bytes,
-                         cudaMemcpyDeviceToDevice, s));
-      if (st.pub_ver >= 0) {
-        if (st.pub_ver != st.read_ver)
-          CK(cudaMemcpyAsync((char *)S.slot[me][st.pub_ver & 1] + off, G(), S.seg_bytes,
-                             cudaMemcpyDeviceToDevice, s));
-        ST(u_publish(ctx, S, me, st.pub_ver, s));
-      }
+      double *rd = (double *)((char *)S.slot[me][st.read_ver & 1] + off);
+      double *pb = (st.pub_ver >= 0 && st.pub_ver != st.read_ver)
+                       ? (double *)((char *)S.slot[me][st.pub_ver & 1] + off)
+                       : nullptr;
+      CK(timed(ctx, STADI_KCLASS_NORM, 0.0, (double)Ml * C * 4, s, [&] {
+        return gn_partials((const float *)X(), Ml, B, C, (double *)G(), ctx->un->gn_ws,
+                           ctx->un->gn_ticket, s, rd, pb);
+      }));
+      if (st.pub_ver >= 0) ST(u_publish(ctx, S, me, st.pub_ver, s));
       return STADI_OK;
     });
     op([=](const stadi_step_t &st, cudaStream_t s) -> stadi_status {  // consume

@@ -117,7 +117,7 @@ EXPORTS = [
     "stadi_kernel_timing", "stadi_kernel_stats",
     "stadi_k_gemm", "stadi_k_gemm_ex", "stadi_k_attention", "stadi_k_ln_modulate",
     "stadi_k_conv3x3", "stadi_k_conv3x3_ex",
-    "stadi_k_sampler", "stadi_k_ddpm_noise", "stadi_k_launch_count",
+    "stadi_k_sampler", "stadi_k_ddpm_noise", "stadi_k_groupnorm", "stadi_k_launch_count",
 ]
 
 
@@ -176,6 +176,9 @@ def _load():
                                       C.c_float, C.c_float, C.c_uint64, C.c_uint32, C.c_int32,
                                       vp]),
         "stadi_k_ddpm_noise": (C.c_int, [vp, C.c_int64, C.c_uint64, C.c_uint32, C.c_int64, vp]),
+        "stadi_k_groupnorm": (C.c_int, [C.c_int32, vp, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32, vp, vp, C.c_float, C.c_int32, C.c_int32, vp,
+                                        vp, vp, vp, vp]),
         "stadi_k_launch_count": (C.c_uint64, []),
     }
     for name, (res, args) in sig.items():
@@ -442,6 +445,12 @@ def k_sampler(x, eps_raw, rows, W, C_, p, c_out, ld, B, guidance, A, Bc, Cz=0.0,
 
 def k_ddpm_noise(out, n, seed, m, e0=0, stream=None):
     _check(lib.stadi_k_ddpm_noise(ptr(out), n, seed, m, e0, stream_ptr(stream)))
+
+
+def k_groupnorm(dtype, x, h, W, B, C_, gamma, beta, eps, act, pad, stats, ws, ticket, out,
+                stream=None):
+    _check(lib.stadi_k_groupnorm(dtype, ptr(x), h, W, B, C_, ptr(gamma), ptr(beta), eps, act, pad,
+                                 ptr(stats), ptr(ws), ptr(ticket), ptr(out), stream_ptr(stream)))
 
 
 def launch_count() -> int:

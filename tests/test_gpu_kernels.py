@@ -438,8 +438,10 @@ def test_gemm_on_emulator_grid(S, max_ctas, M, N, K):
     assert _rel(res.cpu().numpy() - res0, g * ref) < tol
 
 
-def test_attention_alias_variant(S):
-    """The P-over-S variant (STADI_ATTN_ALIAS=1, QUAD == 2: two handoffs per key tile)
+@pytest.mark.parametrize("akt", ["0", "144", "160", "176", "177", "178"])
+def test_attention_alias_variant(S, akt):
+    """The P-over-S variant (STADI_ATTN_ALIAS=1, QUAD == 2: two handoffs per key tile;
+    STADI_ATTN_AKT: 144 / 160 / 176-key tiles, +1 / +2 with polynomial exp2 columns)
     against the oracle, in a subprocess (the switch is read once per process)."""
     import os
     import subprocess
@@ -457,6 +459,57 @@ def test_attention_alias_variant(S):
             "print(float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))))")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
-                       env=dict(os.environ, STADI_ATTN_ALIAS="1"), timeout=300)
+                       env=dict(os.environ, STADI_ATTN_ALIAS="1", STADI_ATTN_AKT=akt), timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) < 1e-2
+
+
+GN_SHAPES = [(3, 5, 1, 320), (7, 9, 2, 320), (64, 64, 2, 320), (16, 16, 2, 960),
+             (8, 8, 2, 2560), (32, 32, 2, 1920), (1, 1, 2, 64), (33, 17, 2, 640)]
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["bf16", "fp32"])
+@pytest.mark.parametrize("h,W,B,C", GN_SHAPES)
+def test_groupnorm(S, dtype, h, W, B, C):
+    """GroupNorm partial sums + apply (+SiLU, into the padded conv input) against
+    oracle/unet.py gn_partials / gn_apply (R17), inputs with a channel-wise mean
+    offset (the variance clamp / cancellation case); bitwise reproducible."""
+    from oracle import unet as OU
+    rng = np.random.default_rng(h * 1000 + W * 10 + C)
+    x = (rng.standard_normal((h, W, B, C)) * 2.0 + rng.standard_normal(C) * 3.0).astype(np.float32)
+    gamma = (1.0 + 0.2 * rng.standard_normal(C)).astype(np.float32)
+    beta = (0.1 * rng.standard_normal(C)).astype(np.float32)
+    xb = np.transpose(x.astype(np.float64), (2, 0, 1, 3))  # oracle layout [B, h, W, C]
+    s1, s2, n = OU.gn_partials(xb)
+    for act in (0, 1):
+        ref = OU.gn_apply(xb, (s1, s2, n), gamma.astype(np.float64), beta.astype(np.float64), 1e-5)
+        if act:
+            ref = ref / (1.0 + np.exp(-ref))
+        ref = np.transpose(ref, (1, 2, 0, 3))  # [h, W, B, C]
+        tx = torch.from_numpy(x).cuda()
+        tg, tb = torch.from_numpy(gamma).cuda(), torch.from_numpy(beta).cuda()
+        stats = torch.zeros(B * 32 * 2, device="cuda", dtype=torch.float64)
+        ws = torch.zeros(592 * 2 * B * 32, device="cuda", dtype=torch.float64)
+        ticket = torch.zeros(1, device="cuda", dtype=torch.int32)
+        odt = torch.bfloat16 if dtype == 0 else torch.float32
+        for pad in (0, 1):
+            shape = (h + 2, W + 2, B, C) if pad else (h, W, B, C)
+            out = torch.full(shape, 7.0, device="cuda", dtype=odt)
+            outs = []
+            for _ in range(2):
+                S.k_groupnorm(dtype, tx, h, W, B, C, tg, tb, 1e-5, act, pad, stats, ws, ticket,
+                              out)
+                torch.cuda.synchronize()
+                outs.append((out.float().cpu().numpy().copy(), stats.cpu().numpy().copy()))
+            assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+            st = outs[0][1].reshape(B, 32, 2)
+            assert np.allclose(st[..., 0], s1, rtol=1e-5, atol=1e-6 * n[0, 0])
+            assert np.allclose(st[..., 1], s2, rtol=1e-5)
+            got = outs[0][0]
+            if pad:
+                assert np.all(got[1:-1, 0] == 0) and np.all(got[1:-1, -1] == 0)
+                assert np.all(got[0] == 7.0) and np.all(got[-1] == 7.0)  # halo rows untouched
+                got = got[1:-1, 1:-1]
+            err = _rel(got.astype(np.float64), ref)
+            print(f"groupnorm {h}x{W}x{B}x{C} dtype={dtype} act={act} pad={pad}: {err:.2e}")
+            assert err <= (1e-2 if dtype == 0 else 1e-5), err

@@ -72,6 +72,41 @@ elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "gemm":
                        (128, 1280, 11520, S.EPI_F32), (512, 1280, 11520, S.EPI_F32),
                        (8192, 320, 2880, S.EPI_F32), (256, 1280, 1280, S.EPI_STORE)]:
         gemm(M, N, K, e)
+elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "unet":
+    # SDXL (C4) / SD-1.5 (C3) shapes at N = 1: transformer GEMMs, implicit 3x3 convs, GroupNorm
+    for M, N, K, e in [(2048, 3840, 1280, S.EPI_STORE), (2048, 1280, 1280, S.EPI_RES),
+                       (2048, 10240, 1280, S.EPI_STORE), (2048, 1280, 5120, S.EPI_RES),
+                       (8192, 1920, 640, S.EPI_STORE), (8192, 640, 640, S.EPI_RES),
+                       (8192, 5120, 640, S.EPI_STORE), (8192, 640, 2560, S.EPI_RES),
+                       (512, 3840, 1280, S.EPI_STORE), (512, 1280, 5120, S.EPI_RES)]:
+        gemm(M, N, K, e)
+    for h, W, C, N in [(128, 128, 320, 320), (64, 64, 640, 640), (32, 32, 1280, 1280),
+                       (64, 64, 320, 320), (32, 32, 640, 640), (16, 16, 1280, 1280)]:
+        B = 2
+        P = torch.randn((h + 2) * (W + 2) * B, C, device="cuda").to(torch.bfloat16)
+        kp = (9 * C + 63) // 64 * 64
+        Wt = (torch.randn(N, kp, device="cuda") / kp ** 0.5).to(torch.bfloat16)
+        out = torch.empty(h * W * B, N, device="cuda")
+        res = torch.zeros(h * W * B, N, device="cuda")
+        bias = torch.zeros(N, device="cuda")
+        ms = timeit(lambda: S.k_conv3x3_ex(0, P, Wt, h, W, B, C, N, 0, 1, bias=bias, out=out, ldo=N,
+                                           res=res, ldr=N, stream=torch.cuda.current_stream()))
+        fl = 2.0 * h * W * B * N * 9 * C
+        print(f"conv3x3 {h}x{W}x{B} C={C} N={N}: {ms * 1e3:.1f} us  {fl / ms / 1e9:.0f} TFLOP/s")
+    for h, W, C in [(128, 128, 320), (64, 64, 640), (32, 32, 1280), (32, 32, 2560), (64, 64, 320),
+                    (16, 16, 1280)]:
+        B = 2
+        x = torch.randn(h * W * B, C, device="cuda")
+        g, bt = torch.ones(C, device="cuda"), torch.zeros(C, device="cuda")
+        st = torch.zeros(B * 64, device="cuda", dtype=torch.float64)
+        ws = torch.zeros(592 * 2 * B * 32, device="cuda", dtype=torch.float64)
+        tk = torch.zeros(1, device="cuda", dtype=torch.int32)
+        y = torch.empty((h + 2) * (W + 2) * B, C, device="cuda", dtype=torch.bfloat16)
+        ms = timeit(lambda: S.k_groupnorm(0, x, h, W, B, C, g, bt, 1e-5, 1, 1, st, ws, tk, y,
+                                          stream=torch.cuda.current_stream()), reps=50)
+        by = h * W * B * C * (4 + 4 + 2)
+        print(f"groupnorm {h}x{W}x{B} C={C} (partials + apply): {ms * 1e3:.1f} us  "
+              f"{by / ms / 1e6:.0f} GB/s")
 elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ln":
     M, d = 32768, 1152
     x = torch.randn(M, d, device="cuda")
