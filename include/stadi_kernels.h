@@ -91,7 +91,8 @@ stadi_status stadi_k_conv3x3(int32_t dtype, const void *P, const void *Wt, int32
 /* As stadi_k_conv3x3 with the full EPI_CONV epilogue of the U-Net ResBlock:
  * out[f32] (row stride ep->ldo) = conv + bias + gate[row % B] (time-embedding
  * term, batch stride ep->gate_bstride; NULL = none) + res[row] (f32, row stride
- * ep->ldr; NULL = none); other ep fields ignored.  max_ctas as stadi_k_gemm_ex. */
+ * ep->ldr; NULL = none); ep->ws / ws_elems: split-K workspace (f32; NULL = allocated
+ * per call); other ep fields ignored.  max_ctas as stadi_k_gemm_ex. */
 stadi_status stadi_k_conv3x3_ex(int32_t dtype, const void *P, const void *Wt, int32_t h,
                                 int32_t W, int32_t B, int32_t C, int32_t N, int32_t mode,
                                 int32_t implicit, const stadi_k_epi *ep, int32_t max_ctas,
@@ -117,7 +118,7 @@ stadi_status stadi_k_ddpm_noise(float *out, int64_t n, uint64_t seed, uint32_t m
  * partial sums are the GN exchange payload): x f32 [h, W, B, C] (token-major,
  * batch innermost), B <= 2, C % 32 == 0, C <= 3072.  Step 1 writes the band's
  * partial sums stats f64 [B][32][{sum x, sum x^2}] (caller-owned, device; ws f64
- * [592 * 2 * B * 32] and ticket (one zero-initialised uint32) are scratch);
+ * [592 * 2 * B * 32] and ticket (32 zero-initialised uint32) are scratch);
  * step 2 normalises with n_total = h * W * C / 32 elements per group (mean =
  * S1 / n, var = max(S2 / n - mean^2, 0)), applies gamma / beta (f32 [C]), SiLU
  * when act != 0, and writes out (T = bf16 or f32 per dtype) either plain [h, W,

@@ -156,7 +156,10 @@ extern "C" stadi_status stadi_k_conv3x3_ex(int32_t dtype, const void *P, const v
   const int sms = max_ctas ? std::min(max_ctas, device_sm_count()) : device_sm_count();
   // split-K workspace (used when the conv's tiles fill at most half the SMs)
   float *ws = nullptr;
-  if (dtype == STADI_DTYPE_BF16) {
+  if (dtype == STADI_DTYPE_BF16 && ke->ws) {  // caller's workspace
+    ep.ws = ke->ws;
+    ep.ws_elems = ke->ws_elems;
+  } else if (dtype == STADI_DTYPE_BF16) {
     ep.ws_elems = (long)M * N * 16;
     cudaError_t e = cudaMallocAsync(&ws, (size_t)ep.ws_elems * 4, s);
     if (e != cudaSuccess) return cu(e, "cudaMallocAsync");

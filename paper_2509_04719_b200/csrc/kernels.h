@@ -79,7 +79,7 @@ cudaError_t pixart_mods(const float *t0, const float *temb, const float *sst_all
 // P = [h+2, W+2, B, C] halo-padded conv input (see unet_ops.cu) --------------
 // GroupNorm partial sums of the band: out[b][g][{S1, S2}] (fp64), reduced across
 // blocks in a fixed order (bitwise reproducible): ws = GN_PARTIAL_BLOCKS * 2 * B * 32
-// doubles of workspace, ticket = one zero-initialised unsigned (reset by the kernel);
+// doubles of workspace, ticket = 32 zero-initialised unsigned (reset by the kernel);
 // one (ws, ticket) pair per stream.
 // out2 / out3 (optional): further copies of out (the exchange slots).  C <= 3072.
 constexpr int GN_PARTIAL_BLOCKS = 592;

@@ -22,23 +22,44 @@ constexpr int GN_G = 32;
 // out[b][g][0] = sum x, out[b][g][1] = sum x^2 over the band, DETERMINISTIC (the
 // same bits on every run: fixed per-thread row sets, fixed-order reductions, no
 // floating-point atomics).  One block = a chunk of rpb consecutive rows (rpb even,
-// so a row's batch index is its parity when B = 2), at most GNP_MAXB blocks:
-//   thread t owns float4 channel vectors v = t % nvec (+ 256 k when nvec > 256) of
-//   the rows r0 + slot, r0 + slot + slots, ... (slot = t / nvec) and accumulates
-//   fp32 sums per (batch, channel); the block folds the slots, then two threads per
-//   (statistic, batch, group) output sum half the group's channels each in fp64 (one
-//   shuffle) into the block's workspace row.  The last block to finish (atomic
-//   ticket) sums the <= 64 rows -- two threads per output, one wave of independent
-//   loads -- and writes out and, optionally, out2 / out3 (the exchange slots, saving
-//   two copies), then resets the ticket.
+// so a row's batch index is its parity when B = 2), <= GNP_MAXB blocks:
+//   thread t owns NV float4 channel vectors v = t % nvec (+ 256 k) of the rows
+//   r0 + slot + i slots (slot = t / nvec; one slot when nvec >= 256), loads UNR
+//   rows at a time (independent loads in flight: the band is latency-, not
+//   bandwidth-bound otherwise) and accumulates fp32 sums per (batch, channel);
+//   the block folds the slots, then two threads per (statistic, batch, group)
+//   output sum half the group's channels each in fp64 (one shuffle) into the
+//   block's workspace row.
+// Cross-block, two fixed-order levels: the last block of each set of GNP_SET
+// blocks (set ticket) sums the set's rows into a set row, the last set to finish
+// (global ticket) sums the set rows and writes out and, optionally, out2 / out3
+// (the exchange slots, saving two copies); tickets reset for the next launch.
+// ticket: 1 + GNP_MAXB / GNP_SET zero-initialised unsigned.
 constexpr int GNP_THREADS = 256;
-constexpr int GNP_MAXV = 3;  // vectors per thread: C <= 4 * 256 * 3 = 3072
-constexpr int GNP_MAXB = 64;  // blocks per launch (the last block's reduce is one load wave)
+constexpr int GNP_MAXB = 296;  // blocks per launch (2 per SM)
+constexpr int GNP_SET = 16;    // blocks per first-level reduction set
+constexpr int GNP_SETROW0 = 320;  // workspace row of set 0 (after the block rows)
 
+// two threads per output: sum rows [k0, k1) of ws (row stride nst) for output o,
+// this thread taking every other row (hf) -- fixed order, one load wave
+template <int MAXR>
+__device__ __forceinline__ double gnp_sum_rows(const double *ws, int nst, int o, int hf, int k0,
+                                               int k1) {
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < MAXR; ++i) {
+    const int k = k0 + 2 * i + hf;
+    if (k < k1) acc += __ldcg(ws + (long)k * nst + o);
+  }
+  return acc + __shfl_xor_sync(0xffffffffu, acc, 1);
+}
+
+template <int NV>
 __global__ void __launch_bounds__(GNP_THREADS) gn_partials_kernel(
     const float *__restrict__ x, int M, int B, int C, int rpb, double *__restrict__ ws,
     unsigned *__restrict__ ticket, double *__restrict__ out, double *__restrict__ out2,
     double *__restrict__ out3) {
+  constexpr int UNR = NV == 1 ? 8 : 4;
   extern __shared__ float sm[];  // [2 stats][slots][B][C]
   __shared__ bool last;
   pdl_wait();
@@ -49,30 +70,40 @@ __global__ void __launch_bounds__(GNP_THREADS) gn_partials_kernel(
   if (t < slots * nvec || nvec >= GNP_THREADS) {
     const int slot = nvec >= GNP_THREADS ? 0 : t / nvec;
     const int v0 = nvec >= GNP_THREADS ? t : t % nvec;
-    float4 s1[2][GNP_MAXV], s2[2][GNP_MAXV];
+    float4 s1[2][NV], s2[2][NV];
 #pragma unroll
     for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
-      for (int k = 0; k < GNP_MAXV; ++k)
-        s1[bb][k] = s2[bb][k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int r = r0 + slot; r < r1; r += slots) {
-      const float4 *row = reinterpret_cast<const float4 *>(x + (long)r * C);
-      const bool odd = B == 2 && (r & 1);
+      for (int k = 0; k < NV; ++k) s1[bb][k] = s2[bb][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int rb = r0 + slot; rb < r1; rb += UNR * slots) {
+      float4 a[UNR][NV];
 #pragma unroll
-      for (int k = 0; k < GNP_MAXV; ++k) {
-        const int v = v0 + k * GNP_THREADS;
-        if (v >= nvec) break;
-        const float4 a = row[v];
-        auto add = [&](float4 &p, float4 &q) {
-          p.x += a.x; p.y += a.y; p.z += a.z; p.w += a.w;
-          q.x += a.x * a.x; q.y += a.y * a.y; q.z += a.z * a.z; q.w += a.w * a.w;
-        };
-        if (odd) add(s1[1][k], s2[1][k]);
-        else add(s1[0][k], s2[0][k]);
+      for (int u = 0; u < UNR; ++u) {
+        const int r = rb + u * slots;
+        const float4 *row = reinterpret_cast<const float4 *>(x + (long)r * C);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          const int v = v0 + k * GNP_THREADS;
+          a[u][k] = (r < r1 && v < nvec) ? row[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const bool odd = B == 2 && ((rb + u * slots) & 1);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          auto add = [&](float4 &p, float4 &q) {
+            const float4 e = a[u][k];
+            p.x += e.x; p.y += e.y; p.z += e.z; p.w += e.w;
+            q.x += e.x * e.x; q.y += e.y * e.y; q.z += e.z * e.z; q.w += e.w * e.w;
+          };
+          if (odd) add(s1[1][k], s2[1][k]);
+          else add(s1[0][k], s2[0][k]);
+        }
       }
     }
 #pragma unroll
-    for (int k = 0; k < GNP_MAXV; ++k) {
+    for (int k = 0; k < NV; ++k) {
       const int v = v0 + k * GNP_THREADS;
       if (v >= nvec) break;
 #pragma unroll
@@ -106,39 +137,50 @@ __global__ void __launch_bounds__(GNP_THREADS) gn_partials_kernel(
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     if (hf == 0) ws[(long)blockIdx.x * nst + o] = acc;
   }
+  // level 1: the last block of this set sums the set's block rows
+  const int set = blockIdx.x / GNP_SET, nsets = (gridDim.x + GNP_SET - 1) / GNP_SET;
+  const int k0 = set * GNP_SET, k1 = min((int)gridDim.x, k0 + GNP_SET);
   __threadfence();
   __syncthreads();
-  if (t == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  if (t == 0) last = atomicAdd(&ticket[1 + set], 1u) == (unsigned)(k1 - k0 - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // the last block: two threads per output, each <= GNP_MAXB / 2 independent loads
   if (o < nst) {
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < GNP_MAXB / 2; ++k) {
-      const int blk = hf * (GNP_MAXB / 2) + k;
-      if (blk < (int)gridDim.x) acc += __ldcg(ws + (long)blk * nst + o);
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    const double acc = gnp_sum_rows<GNP_SET / 2>(ws, nst, o, hf, k0, k1);
+    if (hf == 0) ws[(long)(GNP_SETROW0 + set) * nst + o] = acc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (t == 0) {
+    ticket[1 + set] = 0;
+    last = atomicAdd(&ticket[0], 1u) == (unsigned)(nsets - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // level 2: the last set sums the set rows
+  if (o < nst) {
+    const double acc = gnp_sum_rows<(GNP_MAXB / GNP_SET + 2) / 2>(ws, nst, o, hf, GNP_SETROW0,
+                                                                GNP_SETROW0 + nsets);
     if (hf == 0) {
       out[o] = acc;
       if (out2) out2[o] = acc;
       if (out3) out3[o] = acc;
     }
   }
-  if (t == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
+  if (t == 0) ticket[0] = 0;  // ready for the next launch (stream-ordered)
 }
 
 // ------------------------------------------------------------- GN apply
 // y = (x - mean) * (rstd * gamma) + beta (+ SiLU), mean / var from the sum over the
 // G rank segments of the statistics (own fresh + others stale); stats == null:
 // plain cast.  pad: write into the halo-padded buffer (interior + zero columns).
-// One block = a chunk of rows (pixel, batch); each warp takes whole rows, lanes
-// over the float4 channel vectors (coalesced 512-byte loads), 32-bit indexing,
-// per-row (not per-element) pixel coordinates; the per-(batch, channel) mean and
-// scale live in shared memory (dynamic: 2 B C floats + C).
+// One block = a chunk of rpb rows (pixel, batch); its (row, float4) elements are
+// walked flat, GNA_UNR per thread in flight, 32-bit indexing; the per-(batch,
+// channel) mean and scale live in shared memory (dynamic: (2 B + 1) C floats).
 constexpr int GNA_THREADS = 256;
+constexpr int GNA_UNR = 4;
 template <typename T>
 __global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(
     const float *__restrict__ x, int h, int W, int B, int C, int rpb,
@@ -171,46 +213,64 @@ __global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(
     __syncthreads();
   }
   const int nvec = C / 4, M = h * W * B;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int r0 = blockIdx.x * rpb, r1 = min(M, r0 + rpb);
-  for (int row = r0 + warp; row < r1; row += GNA_THREADS / 32) {
-    const int bb = row % B, pix = row / B;
-    const int yy = pix / W, xx = pix - yy * W;
-    const long orow = pad ? ((long)(yy + 1) * (W + 2) + xx + 1) * B + bb : (long)row;
-    const float4 *src = reinterpret_cast<const float4 *>(x + (long)row * C);
-    T *o = out + orow * C;
-    for (int v = lane; v < nvec; v += 32) {
-      const float4 a = src[v];
-      float e[4] = {a.x, a.y, a.z, a.w};
+  const int total = (r1 - r0) * nvec;
+  for (int e0 = threadIdx.x; e0 < total; e0 += GNA_UNR * GNA_THREADS) {
+    float4 a[GNA_UNR];
+#pragma unroll
+    for (int u = 0; u < GNA_UNR; ++u) {
+      const int e = e0 + u * GNA_THREADS;
+      a[u] = e < total ? reinterpret_cast<const float4 *>(x + (long)r0 * C)[e]
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < GNA_UNR; ++u) {
+      const int e = e0 + u * GNA_THREADS;
+      if (e >= total) break;
+      const int row = r0 + e / nvec, v = e % nvec;
+      const int bb = row % B;
+      float y[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
       if (stats) {
         const float4 m = *reinterpret_cast<const float4 *>(mu_c + bb * C + 4 * v);
-        const float4 s = *reinterpret_cast<const float4 *>(sc_c + bb * C + 4 * v);
+        const float4 sc = *reinterpret_cast<const float4 *>(sc_c + bb * C + 4 * v);
         const float4 be = *reinterpret_cast<const float4 *>(be_c + 4 * v);
-        e[0] = (e[0] - m.x) * s.x + be.x;
-        e[1] = (e[1] - m.y) * s.y + be.y;
-        e[2] = (e[2] - m.z) * s.z + be.z;
-        e[3] = (e[3] - m.w) * s.w + be.w;
+        y[0] = (y[0] - m.x) * sc.x + be.x;
+        y[1] = (y[1] - m.y) * sc.y + be.y;
+        y[2] = (y[2] - m.z) * sc.z + be.z;
+        y[3] = (y[3] - m.w) * sc.w + be.w;
       }
       if (act) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) e[k] = silu(e[k]);
+        for (int k = 0; k < 4; ++k) y[k] = silu(y[k]);
       }
+      long orow = row;
+      if (pad) {
+        const int pix = row / B, yy = pix / W, xx = pix - yy * W;
+        orow = ((long)(yy + 1) * (W + 2) + xx + 1) * B + bb;
+      }
+      T *o = out + orow * C + 4 * v;
       if constexpr (sizeof(T) == 2) {  // one 8-byte store of 4 bf16
-        __nv_bfloat162 lo = __floats2bfloat162_rn(e[0], e[1]),
-                       hi = __floats2bfloat162_rn(e[2], e[3]);
-        *reinterpret_cast<uint2 *>(o + 4 * v) =
+        __nv_bfloat162 lo = __floats2bfloat162_rn(y[0], y[1]),
+                       hi = __floats2bfloat162_rn(y[2], y[3]);
+        *reinterpret_cast<uint2 *>(o) =
             make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
       } else {
-        *reinterpret_cast<float4 *>(o + 4 * v) = make_float4(e[0], e[1], e[2], e[3]);
+        *reinterpret_cast<float4 *>(o) = make_float4(y[0], y[1], y[2], y[3]);
       }
     }
-    if (pad && (xx == 0 || xx == W - 1)) {  // zero the left / right border cell(s)
-      const long prow = (long)(yy + 1) * (W + 2);
-      T *zl = out + ((prow + 0) * B + bb) * C, *zr = out + ((prow + W + 1) * B + bb) * C;
-      for (int c = lane; c < C; c += 32) {
-        if (xx == 0) zl[c] = from_f<T>(0.f);
-        if (xx == W - 1) zr[c] = from_f<T>(0.f);
-      }
+  }
+  if (pad) {  // zero the left / right border cells of the chunk's image rows
+    const int p0 = r0 / B, p1 = (r1 - 1) / B;  // pixel range (inclusive)
+    const int y0 = p0 / W, ny = p1 / W - y0 + 1;
+    const int nz = ny * 2 * B * nvec;
+    for (int e = threadIdx.x; e < nz; e += GNA_THREADS) {
+      const int cand = e / (B * nvec), rem = e % (B * nvec);
+      const int yy = y0 + cand / 2, side = cand & 1;
+      const int p = yy * W + (side ? W - 1 : 0);
+      if (p < p0 || p > p1) continue;
+      const int bb = rem / nvec, v = rem % nvec;
+      T *z = out + (((long)(yy + 1) * (W + 2) + (side ? W + 1 : 0)) * B + bb) * C + 4 * v;
+      z[0] = z[1] = z[2] = z[3] = from_f<T>(0.f);
     }
   }
 }
@@ -347,9 +407,10 @@ inline unsigned grid_for(long work, int per_block = 256) {
 
 cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, double *ws,
                         unsigned *ticket, cudaStream_t s, double *out2, double *out3) {
-  if (B > 2 || B < 1 || C % 4 || C % GN_G || C > 4 * GNP_THREADS * GNP_MAXV || !ws || !ticket ||
+  if (B > 2 || B < 1 || C % 4 || C % GN_G || C > 4 * GNP_THREADS * 3 || !ws || !ticket ||
       M > (1L << 30))
     return cudaErrorInvalidValue;
+  static_assert(GNP_SETROW0 + GNP_MAXB / GNP_SET + 1 <= GN_PARTIAL_BLOCKS, "workspace rows");
   if (M == 0) {
     for (double *o : {out, out2, out3})
       if (o) {
@@ -358,16 +419,25 @@ cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, doubl
       }
     return cudaSuccess;
   }
-  // ~16 KB of X per block at least, at most GNP_MAXB blocks (the band is L2-warm)
+  // >= 8 rows per thread slot when the band allows, <= GNP_MAXB blocks
   const int nvec = C / 4, slots = nvec >= GNP_THREADS ? 1 : GNP_THREADS / nvec;
-  long rows_min = std::max<long>((4096 + C - 1) / C, slots);
-  long nb = std::min<long>((M + rows_min - 1) / rows_min, GNP_MAXB);
+  const int nv = (nvec + GNP_THREADS - 1) / GNP_THREADS;
+  const long rows_min = 8L * slots;
+  long nb = std::max<long>(1, std::min<long>((M + rows_min - 1) / rows_min, GNP_MAXB));
   int rpb = (int)((M + nb - 1) / nb);
   rpb += rpb & 1;  // even: the batch index of a row is its parity (B = 2)
   nb = (M + rpb - 1) / rpb;
   const size_t smem = (size_t)2 * slots * B * C * sizeof(float);
-  const cudaError_t el = launch_pdl(gn_partials_kernel, dim3((unsigned)nb), dim3(GNP_THREADS),
-                                    smem, s, x, (int)M, B, C, rpb, ws, ticket, out, out2, out3);
+  cudaError_t el;
+  if (nv <= 1)
+    el = launch_pdl(gn_partials_kernel<1>, dim3((unsigned)nb), dim3(GNP_THREADS), smem, s, x,
+                    (int)M, B, C, rpb, ws, ticket, out, out2, out3);
+  else if (nv == 2)
+    el = launch_pdl(gn_partials_kernel<2>, dim3((unsigned)nb), dim3(GNP_THREADS), smem, s, x,
+                    (int)M, B, C, rpb, ws, ticket, out, out2, out3);
+  else
+    el = launch_pdl(gn_partials_kernel<3>, dim3((unsigned)nb), dim3(GNP_THREADS), smem, s, x,
+                    (int)M, B, C, rpb, ws, ticket, out, out2, out3);
   ++g_launches;
   return el;
 }
@@ -376,13 +446,16 @@ template <typename T>
 cudaError_t gn_apply(const float *x, int h, int W, int B, int C, const double *stats, int G,
                      double n_total, const float *gamma, const float *beta, float eps, int act,
                      int pad, T *out, cudaStream_t s) {
-  if (C % 4 || (stats && C % GN_G) || B > 2 || (long)h * W * B > (1L << 30))
+  if (C % 4 || (stats && C % GN_G) || B > 2 || (long)h * W * B * (C / 4) > (1L << 30))
     return cudaErrorInvalidValue;
   const long M = (long)h * W * B;
   if (M == 0) return cudaSuccess;
-  // >= 8 rows per block (one per warp), <= 4 blocks per SM
-  const long nb = std::min<long>((M + 7) / 8, 148L * 4);
-  const int rpb = (int)((M + nb - 1) / nb);
+  // ~GNA_UNR float4 per thread per block, <= 4 blocks per SM; rpb even (B = 2 pairs)
+  const long vec = M * (C / 4);
+  long nb = std::max<long>(1, std::min<long>(vec / (GNA_UNR * GNA_THREADS), 148L * 4));
+  int rpb = (int)((M + nb - 1) / nb);
+  rpb += rpb & 1;
+  nb = (M + rpb - 1) / rpb;
   const size_t smem = stats ? (size_t)(2 * B + 1) * C * sizeof(float) : 0;
   if (smem > 48 * 1024) {
     static bool attr = false;
@@ -394,8 +467,8 @@ cudaError_t gn_apply(const float *x, int h, int W, int B, int C, const double *s
     }
   }
   const cudaError_t el =
-      launch_pdl(gn_apply_kernel<T>, dim3((unsigned)((M + rpb - 1) / rpb)), dim3(GNA_THREADS),
-                 smem, s, x, h, W, B, C, rpb, stats, G, n_total, gamma, beta, eps, act, pad, out);
+      launch_pdl(gn_apply_kernel<T>, dim3((unsigned)nb), dim3(GNA_THREADS), smem, s, x, h, W, B,
+                 C, rpb, stats, G, n_total, gamma, beta, eps, act, pad, out);
   ++g_launches;
   return el;
 }

@@ -89,8 +89,10 @@ elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "unet":
         out = torch.empty(h * W * B, N, device="cuda")
         res = torch.zeros(h * W * B, N, device="cuda")
         bias = torch.zeros(N, device="cuda")
+        ws = torch.empty(148 * 128 * 256, device="cuda")
         ms = timeit(lambda: S.k_conv3x3_ex(0, P, Wt, h, W, B, C, N, 0, 1, bias=bias, out=out, ldo=N,
-                                           res=res, ldr=N, stream=torch.cuda.current_stream()))
+                                           res=res, ldr=N, ws=ws, ws_elems=ws.numel(),
+                                           stream=torch.cuda.current_stream()))
         fl = 2.0 * h * W * B * N * 9 * C
         print(f"conv3x3 {h}x{W}x{B} C={C} N={N}: {ms * 1e3:.1f} us  {fl / ms / 1e9:.0f} TFLOP/s")
     for h, W, C in [(128, 128, 320), (64, 64, 640), (32, 32, 1280), (32, 32, 2560), (64, 64, 320),
@@ -100,13 +102,34 @@ elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "unet":
         g, bt = torch.ones(C, device="cuda"), torch.zeros(C, device="cuda")
         st = torch.zeros(B * 64, device="cuda", dtype=torch.float64)
         ws = torch.zeros(592 * 2 * B * 32, device="cuda", dtype=torch.float64)
-        tk = torch.zeros(1, device="cuda", dtype=torch.int32)
+        tk = torch.zeros(32, device="cuda", dtype=torch.int32)
         y = torch.empty((h + 2) * (W + 2) * B, C, device="cuda", dtype=torch.bfloat16)
         ms = timeit(lambda: S.k_groupnorm(0, x, h, W, B, C, g, bt, 1e-5, 1, 1, st, ws, tk, y,
                                           stream=torch.cuda.current_stream()), reps=50)
         by = h * W * B * C * (4 + 4 + 2)
         print(f"groupnorm {h}x{W}x{B} C={C} (partials + apply): {ms * 1e3:.1f} us  "
               f"{by / ms / 1e6:.0f} GB/s")
+elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "conv":
+    # implicit conv vs im2col + GEMM vs the plain GEMM of the same [M, N, 9C] shape;
+    # workspace allocated once (split-K allowed), inputs persistent
+    imp = int(os.environ.get("CONV_IMPLICIT", "1"))
+    for h, W, C, N in [(64, 64, 320, 320), (128, 128, 320, 320), (32, 32, 640, 640),
+                       (32, 32, 1280, 1280)]:
+        B = 2
+        M, K = h * W * B, 9 * C
+        P = torch.randn((h + 2) * (W + 2) * B, C, device="cuda").to(torch.bfloat16)
+        Wt = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+        out = torch.empty(M, N, device="cuda")
+        res = torch.zeros(M, N, device="cuda")
+        bias = torch.zeros(N, device="cuda")
+        fl = 2.0 * M * N * K
+        ws = torch.empty(148 * 128 * 256, device="cuda")
+        ms = timeit(lambda: S.k_conv3x3_ex(0, P, Wt, h, W, B, C, N, 0, imp, bias=bias, out=out,
+                                           ldo=N, res=res, ldr=N, ws=ws, ws_elems=ws.numel(),
+                                           stream=torch.cuda.current_stream()))
+        print(f"conv3x3 implicit={imp} {h}x{W}x{B} C={C} N={N}: {ms * 1e3:.1f} us  "
+              f"{fl / ms / 1e9:.0f} TFLOP/s")
+        gemm(M, N, K, S.EPI_RES)
 elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ln":
     M, d = 32768, 1152
     x = torch.randn(M, d, device="cuda")
