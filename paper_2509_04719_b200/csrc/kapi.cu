@@ -166,13 +166,24 @@ extern "C" stadi_status stadi_k_conv3x3_ex(int32_t dtype, const void *P, const v
     ep.ws = ws;
   }
   if (dtype == STADI_DTYPE_BF16 && implicit) {
-    if (mode != 0) {
-      cudaFreeAsync(ws, s);
-      return fail(nullptr, STADI_EINVAL, "implicit conv: stride 1 only");
+    // mode 2: nearest-x2 upsample into a padded buffer, then the stride-1 implicit conv
+    const int hc = mode == 2 ? 2 * h : h, Wc = mode == 2 ? 2 * W : W, mc = mode == 2 ? 0 : mode;
+    if (!tc_conv_implicit_ok(hc, Wc, B, C, N, mc)) {
+      if (ws) cudaFreeAsync(ws, s);
+      return fail(nullptr, STADI_EINVAL, "implicit conv: unsupported geometry");
     }
-    cudaError_t e =
-        tc_conv3x3_bf16((const bf16 *)P, (const bf16 *)Wt, h, W, B, C, N, EPI_CONV, ep, sms, s);
-    cudaFreeAsync(ws, s);
+    const bf16 *src = (const bf16 *)P;
+    bf16 *U = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (mode == 2) {
+      e = cudaMallocAsync(&U, (size_t)(hc + 2) * (Wc + 2) * B * C * 2, s);
+      if (e == cudaSuccess) e = upsample_pad<bf16>((const bf16 *)P, h, W, B, C, U, s);
+      src = U;
+    }
+    if (e == cudaSuccess)
+      e = tc_conv3x3_bf16(src, (const bf16 *)Wt, hc, Wc, B, C, N, EPI_CONV, ep, sms, s, mc);
+    if (U) cudaFreeAsync(U, s);
+    if (ws) cudaFreeAsync(ws, s);
     return cu(e, "tc_conv3x3_bf16");
   }
   const size_t esz = dtype == STADI_DTYPE_BF16 ? 2 : 4;

@@ -20,10 +20,19 @@ cudaError_t simt_gemm(const T *A, const T *W, int M, int N, int K, int epi, cons
 // N % 64 == 0.  max_ctas bounds the grid (SMs not pinned by the emulator).
 cudaError_t tc_gemm_bf16(const bf16 *A, const bf16 *W, int M, int N, int K, int epi,
                          const EpiParams &ep, int max_ctas, cudaStream_t s);
-// Implicit-GEMM 3x3 conv, stride 1, from the halo-padded input P [h+2, W+2, B, C]
-// (C % 64 == 0, W*B a divisor or multiple of 128); epi EPI_CONV or EPI_F32.
+// Implicit-GEMM 3x3 conv from the halo-padded input P [h+2, W+2, B, C]: mode 0 stride
+// 1, mode 1 stride 2 (h, W even); C % 64 == 0, (output width)*B a divisor or multiple of
+// 128 (tc_conv_implicit_ok); epi EPI_CONV or EPI_F32.
+bool tc_conv_implicit_ok(int h, int W, int B, int C, int N, int mode);
 cudaError_t tc_conv3x3_bf16(const bf16 *P, const bf16 *Wt, int h, int W, int B, int C, int N,
-                            int epi, const EpiParams &ep, int max_ctas, cudaStream_t s);
+                            int epi, const EpiParams &ep, int max_ctas, cudaStream_t s,
+                            int mode = 0);
+// Nearest-x2 upsample of the halo-padded P [h+2, W+2, B, C] into the halo-padded
+// U [2h+2, 2W+2, B, C]: U row Y <- P row 0 (Y = 0), h+1 (Y = 2h+1), else 1 + (Y-1)/2;
+// U column X <- P column 1 + (X-1)/2, zero for X = 0 / 2W+1 (the upsample conv's input,
+// so the conv runs as an implicit stride-1 conv instead of over a 9x im2col buffer).
+template <typename T>
+cudaError_t upsample_pad(const T *P, int h, int W, int B, int C, T *U, cudaStream_t s);
 
 // ---- attention  o = softmax(q k^T / sqrt(hd)) v  per (batch b, head h) ------
 // q, o: [Nq * B, H*hd] (row = token*B + b);  kv: [Nkv, B, 2, H*hd] (K then V).
@@ -96,10 +105,13 @@ cudaError_t halo_fill(T *P, int h, int W, int B, int C, const T *above, const T 
 template <typename T>
 cudaError_t gn_apply(const float *x, int h, int W, int B, int C, const double *stats, int G,
                      double n_total, const float *gamma, const float *beta, float eps, int act,
-                     int pad, T *out, cudaStream_t s);
-// latent band [h, W, Cl] -> P (B copies; halo rows untouched)
+                     int pad, T *out, cudaStream_t s, int zero_halo = 0);
+// latent band [h, W, Cl] -> P (B copies; halo rows untouched unless zero_halo)
+// zero_halo (pad only): bit 0 zeroes halo row 0, bit 1 row h + 1 (image-edge rows of a
+// band, so the conv of a band without neighbours needs no halo_fill)
 template <typename T>
-cudaError_t latent_pad(const float *x, int h, int W, int Cl, int B, T *out, cudaStream_t s);
+cudaError_t latent_pad(const float *x, int h, int W, int Cl, int B, T *out, cudaStream_t s,
+                       int zero_halo = 0);
 // 3x3 conv im2col from P: mode 0 stride 1, 1 stride 2, 2 nearest-x2 upsample.
 // A [(oy*Wo + ox)*B + b][Kp], column (ky*3 + kx)*C + c, zero beyond 9C.
 template <typename T>

@@ -185,7 +185,8 @@ template <typename T>
 __global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(
     const float *__restrict__ x, int h, int W, int B, int C, int rpb,
     const double *__restrict__ stats, int G, double n_total, const float *__restrict__ gamma,
-    const float *__restrict__ beta, float eps, int act, int pad, T *__restrict__ out) {
+    const float *__restrict__ beta, float eps, int act, int pad, T *__restrict__ out,
+    int zero_halo) {
   extern __shared__ float gsm[];  // mu [B][C], sc [B][C], beta [C]
   __shared__ float mu_g[2 * GN_G], rs_g[2 * GN_G];
   float *mu_c = gsm, *sc_c = gsm + B * C, *be_c = gsm + 2 * B * C;
@@ -259,6 +260,16 @@ __global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(
       }
     }
   }
+  if (pad && zero_halo) {  // image-edge halo rows (bit 0: row 0, bit 1: row h + 1), corners too
+    const int rowv = (W + 2) * B * nvec;
+    for (int e = blockIdx.x * GNA_THREADS + threadIdx.x; e < 2 * rowv;
+         e += gridDim.x * GNA_THREADS) {
+      const int r = e / rowv;
+      if (!((zero_halo >> r) & 1)) continue;
+      T *z = out + ((long)(r ? h + 1 : 0) * (W + 2) * B) * C + 4 * (long)(e % rowv);
+      z[0] = z[1] = z[2] = z[3] = from_f<T>(0.f);
+    }
+  }
   if (pad) {  // zero the left / right border cells of the chunk's image rows
     const int p0 = r0 / B, p1 = (r1 - 1) / B;  // pixel range (inclusive)
     const int y0 = p0 / W, ny = p1 / W - y0 + 1;
@@ -278,7 +289,7 @@ __global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(
 // latent band x [h, W, Cl] fp32 -> padded conv_in input [h+2, W+2, B, Cl] (B copies)
 template <typename T>
 __global__ void latent_pad_kernel(const float *__restrict__ x, int h, int W, int Cl, int B,
-                                  T *__restrict__ out) {
+                                  T *__restrict__ out, int zero_halo) {
   pdl_wait();
   const long total = (long)(h + 2) * (W + 2) * B * Cl;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -286,8 +297,13 @@ __global__ void latent_pad_kernel(const float *__restrict__ x, int h, int W, int
     const int c = (int)(i % Cl);
     const long pix = i / Cl / B;
     const int yy = (int)(pix / (W + 2)), xx = (int)(pix % (W + 2));
-    if (yy == 0 || yy == h + 1) continue;  // halo rows belong to the exchange
+    // halo rows belong to the exchange, except image-edge rows (zero_halo bit 0 / 1)
+    if ((yy == 0 && !(zero_halo & 1)) || (yy == h + 1 && !(zero_halo & 2))) continue;
     float v = 0.f;
+    if (yy == 0 || yy == h + 1) {
+      out[i] = from_f<T>(0.f);
+      continue;
+    }
     if (xx >= 1 && xx <= W) v = x[((long)(yy - 1) * W + (xx - 1)) * Cl + c];
     out[i] = from_f<T>(v);
   }
@@ -343,6 +359,33 @@ __global__ void __launch_bounds__(256) im2col_kernel(const T *__restrict__ P, in
     } else {
       dst[0] = zero ? from_f<T>(0.f) : P[src];
     }
+  }
+}
+
+// ------------------------------------------------------------- nearest-x2 upsample
+// U [2h+2, 2W+2, B, C] from P [h+2, W+2, B, C] (see kernels.h), 16-byte vectors
+template <typename T>
+__global__ void __launch_bounds__(256) upsample_pad_kernel(const T *__restrict__ P, int h, int W,
+                                                           int B, int C, T *__restrict__ U) {
+  pdl_wait();
+  constexpr int V = 16 / sizeof(T);
+  const int cv = C / V;                                   // vectors per (pixel, batch)
+  const int Wu = 2 * W + 2;
+  const long total = (long)(2 * h + 2) * Wu * B * cv;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int v = (int)(i % cv);
+    const long cell = i / cv;                             // (Y * Wu + X) * B + b
+    const int b = (int)(cell % B);
+    const long pix = cell / B;
+    const int Y = (int)(pix / Wu), X = (int)(pix % Wu);
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (X != 0 && X != Wu - 1) {
+      const int py = Y == 0 ? 0 : (Y == 2 * h + 1 ? h + 1 : 1 + (Y - 1) / 2);
+      const int px = 1 + (X - 1) / 2;
+      val = reinterpret_cast<const uint4 *>(P + (((long)py * (W + 2) + px) * B + b) * C)[v];
+    }
+    reinterpret_cast<uint4 *>(U + cell * C)[v] = val;
   }
 }
 
@@ -445,7 +488,7 @@ cudaError_t gn_partials(const float *x, long M, int B, int C, double *out, doubl
 template <typename T>
 cudaError_t gn_apply(const float *x, int h, int W, int B, int C, const double *stats, int G,
                      double n_total, const float *gamma, const float *beta, float eps, int act,
-                     int pad, T *out, cudaStream_t s) {
+                     int pad, T *out, cudaStream_t s, int zero_halo) {
   if (C % 4 || (stats && C % GN_G) || B > 2 || (long)h * W * B * (C / 4) > (1L << 30))
     return cudaErrorInvalidValue;
   const long M = (long)h * W * B;
@@ -468,16 +511,28 @@ cudaError_t gn_apply(const float *x, int h, int W, int B, int C, const double *s
   }
   const cudaError_t el =
       launch_pdl(gn_apply_kernel<T>, dim3((unsigned)nb), dim3(GNA_THREADS), smem, s, x, h, W, B,
-                 C, rpb, stats, G, n_total, gamma, beta, eps, act, pad, out);
+                 C, rpb, stats, G, n_total, gamma, beta, eps, act, pad, out, zero_halo);
   ++g_launches;
   return el;
 }
 template cudaError_t gn_apply<bf16>(const float *, int, int, int, int, const double *, int,
                                     double, const float *, const float *, float, int, int, bf16 *,
-                                    cudaStream_t);
+                                    cudaStream_t, int);
 template cudaError_t gn_apply<float>(const float *, int, int, int, int, const double *, int,
                                      double, const float *, const float *, float, int, int,
-                                     float *, cudaStream_t);
+                                     float *, cudaStream_t, int);
+
+template <typename T>
+cudaError_t upsample_pad(const T *P, int h, int W, int B, int C, T *U, cudaStream_t s) {
+  if ((C * sizeof(T)) % 16) return cudaErrorInvalidValue;
+  const long work = (long)(2 * h + 2) * (2 * W + 2) * B * (C * sizeof(T) / 16);
+  const cudaError_t el = launch_pdl(upsample_pad_kernel<T>, dim3(grid_for(work)), dim3(256), 0, s,
+                                    P, h, W, B, C, U);
+  ++g_launches;
+  return el;
+}
+template cudaError_t upsample_pad<bf16>(const bf16 *, int, int, int, int, bf16 *, cudaStream_t);
+template cudaError_t upsample_pad<float>(const float *, int, int, int, int, float *, cudaStream_t);
 
 template <typename T>
 cudaError_t halo_fill(T *P, int h, int W, int B, int C, const T *above, const T *below,
@@ -495,15 +550,18 @@ template cudaError_t halo_fill<float>(float *, int, int, int, int, const float *
                                       cudaStream_t);
 
 template <typename T>
-cudaError_t latent_pad(const float *x, int h, int W, int Cl, int B, T *out, cudaStream_t s) {
+cudaError_t latent_pad(const float *x, int h, int W, int Cl, int B, T *out, cudaStream_t s,
+                       int zero_halo) {
   const long work = (long)(h + 2) * (W + 2) * B * Cl;
   const cudaError_t el = launch_pdl(latent_pad_kernel<T>, dim3(grid_for(work)), dim3(256), 0, s, x,
-                                    h, W, Cl, B, out);
+                                    h, W, Cl, B, out, zero_halo);
   ++g_launches;
   return el;
 }
-template cudaError_t latent_pad<bf16>(const float *, int, int, int, int, bf16 *, cudaStream_t);
-template cudaError_t latent_pad<float>(const float *, int, int, int, int, float *, cudaStream_t);
+template cudaError_t latent_pad<bf16>(const float *, int, int, int, int, bf16 *, cudaStream_t,
+                                      int);
+template cudaError_t latent_pad<float>(const float *, int, int, int, int, float *, cudaStream_t,
+                                       int);
 
 template <typename T>
 cudaError_t im2col(const T *P, int hin, int Win, int B, int C, int mode, int Kp, T *A,

@@ -44,6 +44,7 @@ struct URank {
 // Work buffers of a rank (ids >= UB_COUNT are the down-path skip buffers).
 enum {
   UB_CAT = 0, UB_H, UB_H1, UB_SK, UB_TY, UB_PAD, UB_COL, UB_NB, UB_Q, UB_O, UB_FF, UB_EPS, UB_GNS,
+  UB_UPS,  // nearest-x2 upsampled padded conv input (implicit upsample conv)
   UB_COUNT
 };
 
@@ -344,6 +345,11 @@ struct UBuilder {
     return [RR, id] { return RR->buf[id]; };
   }
   const Rank &rank() const { return ctx->ranks[li]; }
+  // halo rows of this band that lie on the image edge (always zero): bit 0 top, bit 1 bottom
+  int edge_halos() const {
+    return (rank().row_begin == 0 ? 1 : 0) |
+           (rank().row_begin + rank().rows == (int)m.lat_h ? 2 : 0);
+  }
   int rows(int l) const { return rank().rows >> l; }
   int width(int l) const { return m.lat_w >> l; }
   int64_t M(int l) const { return (int64_t)rows(l) * width(l) * Bm; }
@@ -384,6 +390,7 @@ struct UBuilder {
     const int64_t Ml = M(l);
     const double n_total = (double)(m.lat_h >> l) * W * (C / 32);
     const float *gw = wF(p + ".w"), *gb = wF(p + ".b");
+    const int zh = pad ? edge_halos() : 0;
     op([=](const stadi_step_t &st, cudaStream_t s) -> stadi_status {  // publish
       stadi_ctx *ctx = c;
       USite &S = ctx->un->sites[sid];
@@ -412,9 +419,9 @@ struct UBuilder {
         const double *stats = (const double *)S.slot[me][st.read_ver & 1];
         if (ctx->dtype == STADI_DTYPE_BF16)
           return gn_apply<bf16>((const float *)X(), h, W, B, C, stats, G_, n_total, gw, gb, eps,
-                                act, pad ? 1 : 0, (bf16 *)D(), s);
+                                act, pad ? 1 : 0, (bf16 *)D(), s, zh);
         return gn_apply<float>((const float *)X(), h, W, B, C, stats, G_, n_total, gw, gb, eps,
-                               act, pad ? 1 : 0, (float *)D(), s);
+                               act, pad ? 1 : 0, (float *)D(), s, zh);
       }));
       return u_done(ctx, S, s);
     });
@@ -428,14 +435,15 @@ struct UBuilder {
     need(UB_PAD, (size_t)(h + 2) * (W + 2) * B * C * esz);
     auto X = P(x), D = P(UB_PAD);
     stadi_ctx *c = ctx;
+    const int zh = edge_halos();
     op([=](const stadi_step_t &, cudaStream_t s) -> stadi_status {
       stadi_ctx *ctx = c;
       if (ctx->dtype == STADI_DTYPE_BF16)
         CK(gn_apply<bf16>((const float *)X(), h, W, B, C, nullptr, 0, 1.0, nullptr, nullptr, 0.f,
-                          0, 1, (bf16 *)D(), s));
+                          0, 1, (bf16 *)D(), s, zh));
       else
         CK(gn_apply<float>((const float *)X(), h, W, B, C, nullptr, 0, 1.0, nullptr, nullptr,
-                           0.f, 0, 1, (float *)D(), s));
+                           0.f, 0, 1, (float *)D(), s, zh));
       return STADI_OK;
     });
   }
@@ -454,12 +462,18 @@ struct UBuilder {
     const int64_t kp = rup64(9 * C);
     const int ncols = ldo ? ldo : cout;
     const int wb = W * B;
-    const bool implicit = ctx->dtype == STADI_DTYPE_BF16 && mode == 0 && C % 64 == 0 &&
-                          (wb % 128 == 0 || 128 % wb == 0) && !conv_implicit_disabled();
+    // implicit GEMM (no im2col buffer): stride 1 and stride 2 straight from the padded
+    // input; the upsample conv as a stride-1 conv over the nearest-x2 upsampled input
+    (void)wb;
+    const bool implicit =
+        ctx->dtype == STADI_DTYPE_BF16 && !conv_implicit_disabled() &&
+        (mode == 2 ? tc_conv_implicit_ok(2 * h, 2 * W, B, C, ncols, 0)
+                   : tc_conv_implicit_ok(h, W, B, C, ncols, mode));
     need(UB_PAD, (size_t)(h + 2) * (W + 2) * B * C * esz);
     if (!implicit) need(UB_COL, (size_t)(Mo * kp) * esz);
+    if (implicit && mode == 2) need(UB_UPS, (size_t)(2 * h + 2) * (2 * W + 2) * B * C * esz);
     need(out, (size_t)(Mo * ncols) * 4);
-    auto D = P(UB_PAD), A = P(UB_COL), O = P(out);
+    auto D = P(UB_PAD), A = P(UB_COL), O = P(out), UP = P(UB_UPS);
     std::function<void *()> Rs = res >= 0 ? P(res) : std::function<void *()>();
     stadi_ctx *c = ctx;
     const int me = li;
@@ -474,6 +488,7 @@ struct UBuilder {
       const int pos = inc_pos(ctx->un.get(), ctx->ranks[me].g);
       if (st.pub_ver != st.read_ver) ST(u_wait(ctx, S, st.read_ver, s));
       if (st.pub_ver < 0) return STADI_OK;
+      if (top && bottom) return u_publish(ctx, S, me, st.pub_ver, s);  // no neighbour reads
       // own boundary rows -> own segment of the publish slot (the consumer reads
       // only the neighbours' rows, so the read slot needs no own copy).  The last
       // send from this parity (version pub - 2) completed before the read wait of
@@ -499,11 +514,15 @@ struct UBuilder {
       // rows, corner cells zero: one kernel
       const void *above = top ? nullptr : sl + (pos - 1) * S.seg_bytes + rb;
       const void *below = bottom ? nullptr : sl + (pos + 1) * S.seg_bytes;
-      if (ctx->dtype == STADI_DTYPE_BF16)
+      // a band without neighbours: its producer (GN apply / cast / latent pad) already
+      // zeroed both image-edge halo rows (zero_halo)
+      if (top && bottom) {
+      } else if (ctx->dtype == STADI_DTYPE_BF16) {
         CK(halo_fill<bf16>((bf16 *)D(), h, W, B, C, (const bf16 *)above, (const bf16 *)below, s));
-      else
+      } else {
         CK(halo_fill<float>((float *)D(), h, W, B, C, (const float *)above, (const float *)below,
                             s));
+      }
       ST(u_done(ctx, S, s));
       EpiParams ep{};
       ep.B = B;
@@ -521,9 +540,18 @@ struct UBuilder {
       if (implicit) {  // tcgen05 implicit GEMM straight from the padded input
         ep.ws = ctx->splitk_ws;
         ep.ws_elems = ctx->splitk_elems;
+        const bf16 *src = (const bf16 *)D();
+        int hc = h, Wc = W, mc = mode;
+        if (mode == 2) {
+          CK(upsample_pad<bf16>((const bf16 *)D(), h, W, B, C, (bf16 *)UP(), s));
+          src = (const bf16 *)UP();
+          hc = 2 * h;
+          Wc = 2 * W;
+          mc = 0;
+        }
         CK(timed(ctx, STADI_KCLASS_GEMM, 2.0 * Mo * ncols * kp, 0.0, s, [&] {
-          return tc_conv3x3_bf16((const bf16 *)D(), (const bf16 *)wt, h, W, B, C, ncols, epi, ep,
-                                 std::max(1, ctx->num_sms - ctx->emu_ctas), s);
+          return tc_conv3x3_bf16(src, (const bf16 *)wt, hc, Wc, B, C, ncols, epi, ep,
+                                 std::max(1, ctx->num_sms - ctx->emu_ctas), s, mc);
         }));
         return STADI_OK;
       }
@@ -713,13 +741,14 @@ struct UBuilder {
       auto D = P(UB_PAD);
       stadi_ctx *c = ctx;
       const int me = li;
+      const int zh = edge_halos();
       op([=](const stadi_step_t &, cudaStream_t s) -> stadi_status {
         stadi_ctx *ctx = c;
         const float *xb = ctx->ranks[me].x_band;
         if (ctx->dtype == STADI_DTYPE_BF16)
-          CK(latent_pad<bf16>(xb, h, W, ctx->dm.c_in, B, (bf16 *)D(), s));
+          CK(latent_pad<bf16>(xb, h, W, ctx->dm.c_in, B, (bf16 *)D(), s, zh));
         else
-          CK(latent_pad<float>(xb, h, W, ctx->dm.c_in, B, (float *)D(), s));
+          CK(latent_pad<float>(xb, h, W, ctx->dm.c_in, B, (float *)D(), s, zh));
         return STADI_OK;
       });
     }

@@ -95,6 +95,25 @@ elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "unet":
                                            stream=torch.cuda.current_stream()))
         fl = 2.0 * h * W * B * N * 9 * C
         print(f"conv3x3 {h}x{W}x{B} C={C} N={N}: {ms * 1e3:.1f} us  {fl / ms / 1e9:.0f} TFLOP/s")
+    # stride-2 (mode 1) and upsample (mode 2) convs: implicit vs im2col + GEMM
+    for h, W, C, N, mode in [(128, 128, 320, 320, 1), (64, 64, 640, 640, 1), (64, 64, 320, 320, 1),
+                             (32, 32, 1280, 1280, 2), (64, 64, 640, 640, 2),
+                             (16, 16, 1280, 1280, 2), (32, 32, 640, 640, 2)]:
+        B = 2
+        ho, wo = (h // 2, W // 2) if mode == 1 else (2 * h, 2 * W)
+        P = torch.randn((h + 2) * (W + 2) * B, C, device="cuda").to(torch.bfloat16)
+        kp = (9 * C + 63) // 64 * 64
+        Wt = (torch.randn(N, kp, device="cuda") / kp ** 0.5).to(torch.bfloat16)
+        out = torch.empty(ho * wo * B, N, device="cuda")
+        bias = torch.zeros(N, device="cuda")
+        ws = torch.empty(148 * 128 * 256, device="cuda")
+        fl = 2.0 * ho * wo * B * N * 9 * C
+        for imp in (1, 0):
+            ms = timeit(lambda: S.k_conv3x3_ex(0, P, Wt, h, W, B, C, N, mode, imp, bias=bias,
+                                               out=out, ldo=N, ws=ws, ws_elems=ws.numel(),
+                                               stream=torch.cuda.current_stream()))
+            print(f"conv3x3 mode={mode} implicit={imp} {h}x{W}x{B} C={C} N={N}: {ms * 1e3:.1f} us"
+                  f"  {fl / ms / 1e9:.0f} TFLOP/s")
     for h, W, C in [(128, 128, 320), (64, 64, 640), (32, 32, 1280), (32, 32, 2560), (64, 64, 320),
                     (16, 16, 1280)]:
         B = 2
