@@ -49,7 +49,8 @@ __device__ long long g_attn_trace[16 * 2 * 64];
 #endif
 
 bool make_tmap(CUtensorMap *m, const void *base, int rank, const uint64_t *dims,
-               const uint64_t *strides_bytes, const uint32_t *box, CUtensorMapSwizzle swz);
+               const uint64_t *strides_bytes, const uint32_t *box, CUtensorMapSwizzle swz,
+               const uint32_t *estr = nullptr);
 
 namespace {
 
@@ -113,7 +114,10 @@ __device__ __forceinline__ void ex2_poly_x2(uint64_t xx, float &p0, float &p1) {
 // polynomial exp2, the rest MUFU ex2.
 
 // Head-dim chunking: N64 chunks of 64, then N32 of 32, then N16 of 16.
-// AKTO != 0: P aliased over S (no separate P region), AKTO keys per tile.
+// AKTO != 0: P aliased over S (no separate P region), AKTO keys per tile.  Measured
+// on the C5 shape (round 2, hd 72, P over S): 112 keys 774, 144 710, 160 744, 176 529
+// TFLOP/s (register spills at 96 registers / 18 warps, fewer ring stages) against 814
+// for the separate-P default -- no instance is built; kept for such A/Bs.
 template <int N64, int N32, int N16, int NQT_, int AKTO = 0>
 struct AttnCfg {
   static constexpr int NQT = NQT_;
@@ -257,11 +261,15 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
                    int flags) {  // bit 0: exp-phase tokens, bit 1: deferred PV wait (QUAD), bit 2: MMA order
   using C = AttnCfg<N64, N32, N16, NQT, AKTO>;
   constexpr int AKT = C::AKT;
+  constexpr bool WM = C::HDP <= 48;  // warp-collective MMA issue (see the MMA issuer)
   // QUAD == 2: P aliased over S.  PV_g(j) and S_g(j+1) are issued back to back once
   // P_g(j) is stored and committed to ONE barrier (s_full), so a key tile costs each
   // group two handoffs (s_full, p_full) instead of four: s_full(j) also tells the group
   // that PV_g(j-1) is done (O may be rescaled, the S/P columns rewritten).
   constexpr bool ALIAS = QUAD == 2 && NQT == 2;
+  // P stored over S: the alias MMA order above, or (AKTO, single-tile K/V <= AKT only:
+  // the launcher guarantees n_kv == 1, so no S(j+1) can overwrite an unread P)
+  constexpr bool POS = ALIAS || C::PALIAS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -346,26 +354,51 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------ MMA issuer
+    if (WM || lane == 0) {  // ------------------------------------- MMA issuer
       constexpr uint32_t id_s = umma_idesc_bf16(128, AKT, 0, 0);
-      // Descriptors are built once per operand base and advanced by adding the
-      // (16-byte granular) start-address offset into their low field: the single
-      // issuing thread must not spend ~10 dependent ALU ops per MMA on them.
+      // WM (HDP <= 48): descriptors built once before the key loop and advanced by
+      // 16-byte offsets, issued by the whole warp (one lane elected in the asm) -- many
+      // small N <= 32 MMAs, issue-bound.  Otherwise one thread issues with per-chunk
+      // descriptors: measured faster for hd 64 / 72 (814 vs 753 TFLOP/s at C5), where
+      // back-to-back issue of the N = 112 S MMAs slows the softmax groups' TMEM traffic.
+      uint64_t qdesc[C::NQT][C::NCH], kdesc[C::NCH];
+      if constexpr (WM) {
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c) {
+          const uint32_t sbo = 8 * C::cw(c) * 2;
+#pragma unroll
+          for (int g = 0; g < C::NQT; ++g)
+            qdesc[g][c] = umma_desc(smem_u32(sQ + g * C::QTILE) + C::qoff(c), 16, sbo, C::cswz(c));
+          kdesc[c] = umma_desc(smem_u32(sK) + C::koff(c), 16, sbo, C::cswz(c));
+        }
+      }
       auto issue_s = [&](int g, int st) {
 #ifdef STADI_ATTN_NOSMMA  // timing experiment only (wrong results): no S MMAs
         if (st >= 0) return;
 #endif
         const uint32_t dt = tmem + C::s_col(g);
-        const uint32_t qa = smem_u32(sQ + g * C::QTILE), ka = smem_u32(sK + st * C::KTILE);
-        int kk = 0;
+        if constexpr (WM) {
+          const uint64_t so = (uint64_t)((uint32_t)st * (uint32_t)(C::KTILE >> 4));
+          int kk = 0;
 #pragma unroll
-        for (int c = 0; c < C::NCH; ++c) {
-          const uint32_t sbo = 8 * C::cw(c) * 2;
-          const uint64_t qd0 = umma_desc(qa + C::qoff(c), 16, sbo, C::cswz(c));
-          const uint64_t kd0 = umma_desc(ka + C::koff(c), 16, sbo, C::cswz(c));
+          for (int c = 0; c < C::NCH; ++c) {
 #pragma unroll
-          for (int k = 0; k < C::cw(c) / 16; ++k, ++kk)
-            umma_bf16(dt, qd0 + (uint64_t)(2 * k), kd0 + (uint64_t)(2 * k), id_s, kk != 0);
+            for (int k = 0; k < C::cw(c) / 16; ++k, ++kk)
+              umma_bf16_w(dt, qdesc[g][c] + (uint64_t)(2 * k), kdesc[c] + so + (uint64_t)(2 * k),
+                          id_s, kk != 0);
+          }
+        } else {
+          const uint32_t qa = smem_u32(sQ + g * C::QTILE), ka = smem_u32(sK + st * C::KTILE);
+          int kk = 0;
+#pragma unroll
+          for (int c = 0; c < C::NCH; ++c) {
+            const uint32_t sbo = 8 * C::cw(c) * 2;
+            const uint64_t qd0 = umma_desc(qa + C::qoff(c), 16, sbo, C::cswz(c));
+            const uint64_t kd0 = umma_desc(ka + C::koff(c), 16, sbo, C::cswz(c));
+#pragma unroll
+            for (int k = 0; k < C::cw(c) / 16; ++k, ++kk)
+              umma_bf16(dt, qd0 + (uint64_t)(2 * k), kd0 + (uint64_t)(2 * k), id_s, kk != 0);
+          }
         }
       };
       auto issue_pv = [&](int g, int st, int j) {
@@ -373,15 +406,17 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
         if (st >= 0) return;
 #endif
         // P: AKT / 2 columns of packed bf16 (its own region, or over S when ALIAS)
-        const uint32_t pa = tmem + (ALIAS ? C::s_col(g) : C::p_col(g));
+        const uint32_t pa = tmem + (POS ? C::s_col(g) : C::p_col(g));
         const uint32_t va = smem_u32(sV + st * C::KTILE);
         if constexpr (C::NARROW) {
           constexpr uint32_t idp = umma_idesc_bf16(128, C::HDP, 0, 1);
           const uint32_t dt = tmem + C::o_col(g);
           const uint64_t vd0 = umma_desc(va, AKT * 32, 8 * 32, SWZ_32B);
 #pragma unroll
-          for (int k = 0; k < AKT / 16; ++k)  // 16 keys x 32 B = 512 B = 32 units per step
-            umma_bf16_ts(dt, pa + k * 8, vd0 + (uint64_t)(32 * k), idp, (j | k) != 0);
+          for (int k = 0; k < AKT / 16; ++k) {  // 16 keys x 32 B = 512 B = 32 units per step
+            if constexpr (WM) umma_bf16_ts_w(dt, pa + k * 8, vd0 + (uint64_t)(32 * k), idp, (j | k) != 0);
+            else umma_bf16_ts(dt, pa + k * 8, vd0 + (uint64_t)(32 * k), idp, (j | k) != 0);
+          }
         } else {
 #pragma unroll
           for (int c = 0; c < C::NCH; ++c) {
@@ -390,10 +425,16 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
             const uint32_t dt = tmem + C::o_col(g) + C::ccol(c);
             const uint64_t vd0 = umma_desc(va + C::koff(c), AKT * rb, 8 * rb, C::cswz(c));
 #pragma unroll
-            for (int k = 0; k < AKT / 16; ++k)
-              umma_bf16_ts(dt, pa + k * 8, vd0 + (uint64_t)(k * rb), idp, (j | k) != 0);
+            for (int k = 0; k < AKT / 16; ++k) {
+              if constexpr (WM) umma_bf16_ts_w(dt, pa + k * 8, vd0 + (uint64_t)(k * rb), idp, (j | k) != 0);
+              else umma_bf16_ts(dt, pa + k * 8, vd0 + (uint64_t)(k * rb), idp, (j | k) != 0);
+            }
           }
         }
+      };
+      auto mma_commit = [&](uint64_t *bar) {
+        if constexpr (WM) umma_commit_w(bar);
+        else umma_commit(bar);
       };
       // Order per key tile j: S_g(j+1) as soon as the group has read S_g(j) (it
       // overlaps that group's exp work), then PV_g(j) once P_g(j) is stored.
@@ -403,9 +444,9 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
 #pragma unroll
       for (int g = 0; g < NQT; ++g) {
         issue_s(g, 0);
-        umma_commit(&s_full[g]);
+        mma_commit(&s_full[g]);
       }
-      umma_commit(&k_empty[0]);
+      mma_commit(&k_empty[0]);
       int ks = 1 % C::STAGES, vs = 0;
       uint32_t kph = (ks == 0), vph = 0;
       if constexpr (ALIAS) {
@@ -422,16 +463,16 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
             tc_fence_after();
             issue_pv(g, vs, j);
             if (more) issue_s(g, ks);
-            umma_commit(&s_full[g]);
+            mma_commit(&s_full[g]);
             ATTN_TRACE(8, g, j);
           }
-          umma_commit(&v_empty[vs]);
+          mma_commit(&v_empty[vs]);
           if (++vs == C::STAGES) {
             vs = 0;
             vph ^= 1;
           }
           if (more) {
-            umma_commit(&k_empty[ks]);
+            mma_commit(&k_empty[ks]);
             if (++ks == C::STAGES) {
               ks = 0;
               kph ^= 1;
@@ -450,7 +491,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
             ATTN_TRACE(0, 0, j);
             tc_fence_after();
             issue_s(0, ks);
-            umma_commit(&s_full[0]);
+            mma_commit(&s_full[0]);
             ATTN_TRACE(1, 0, j);
           }
           if (j > 0) {
@@ -458,8 +499,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
             ATTN_TRACE(2, 1, j - 1);
             tc_fence_after();
             issue_pv(1, pvs, j - 1);
-            umma_commit(&o_done[1]);
-            umma_commit(&v_empty[pvs]);
+            mma_commit(&o_done[1]);
+            mma_commit(&v_empty[pvs]);
             ATTN_TRACE(8, 1, j - 1);
           }
           if (j + 1 < n_kv) {
@@ -467,8 +508,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
             ATTN_TRACE(0, 1, j);
             tc_fence_after();
             issue_s(1, ks);
-            umma_commit(&s_full[1]);
-            umma_commit(&k_empty[ks]);
+            mma_commit(&s_full[1]);
+            mma_commit(&k_empty[ks]);
             ATTN_TRACE(1, 1, j);
             if (++ks == C::STAGES) {
               ks = 0;
@@ -480,7 +521,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
           ATTN_TRACE(2, 0, j);
           tc_fence_after();
           issue_pv(0, vs, j);
-          umma_commit(&o_done[0]);
+          mma_commit(&o_done[0]);
           ATTN_TRACE(8, 0, j);
           pvs = vs;
           if (++vs == C::STAGES) {
@@ -491,8 +532,8 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
         mbar_wait(&p_full[1], (n_kv - 1) & 1);
         tc_fence_after();
         issue_pv(1, pvs, n_kv - 1);
-        umma_commit(&o_done[1]);
-        umma_commit(&v_empty[pvs]);
+        mma_commit(&o_done[1]);
+        mma_commit(&v_empty[pvs]);
       } else {
       for (int j = 0; j < n_kv; ++j) {
         ATTN_TRACE(13, 0, j);
@@ -505,10 +546,10 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
             ATTN_TRACE(0, g, j);
             tc_fence_after();
             issue_s(g, ks);
-            umma_commit(&s_full[g]);
+            mma_commit(&s_full[g]);
             ATTN_TRACE(1, g, j);
           }
-          umma_commit(&k_empty[ks]);
+          mma_commit(&k_empty[ks]);
           if (++ks == C::STAGES) {
             ks = 0;
             kph ^= 1;
@@ -523,10 +564,10 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
           ATTN_TRACE(2, g, j);
           tc_fence_after();
           issue_pv(g, vs, j);
-          umma_commit(&o_done[g]);
+          mma_commit(&o_done[g]);
           ATTN_TRACE(8, g, j);
         }
-        umma_commit(&v_empty[vs]);
+        mma_commit(&v_empty[vs]);
         if (++vs == C::STAGES) {
           vs = 0;
           vph ^= 1;
@@ -550,7 +591,7 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
     const int cq = 2 * (lane & 3);
     const uint32_t lane_off = (uint32_t)lb << 16;
     const uint32_t s_addr = tmem + lane_off + C::s_col(g);
-    const uint32_t p_addr = tmem + lane_off + (ALIAS ? C::s_col(g) : C::p_col(g));
+    const uint32_t p_addr = tmem + lane_off + (POS ? C::s_col(g) : C::p_col(g));
     const uint32_t o_addr = tmem + lane_off + C::o_col(g);
     float m_run[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
     for (int j = 0; j < n_kv; ++j) {
@@ -577,43 +618,43 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
         for (int i = 0; i < 4 * NR; ++i)
           if (8 * (i / 4) + cq + (i & 1) >= valid) v[i] = -INFINITY;
       }
-      float mt[2];
+      uint64_t acc[2][2];
+      uint32_t pk[2 * NR];
+      // P = 2^(s scale - m_run) for this thread's pairs, partial row sums in acc; with
+      // `track` also the tile's row maxima of the raw scores (am, per row rr)
+      auto exp_pass = [&](bool track, float *am) {
+        const uint64_t sc2 = pack_f32x2(scale_log2, scale_log2);
+        const uint64_t nm2[2] = {pack_f32x2(-m_run[0], -m_run[0]),
+                                 pack_f32x2(-m_run[1], -m_run[1])};
+        acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0;
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        float a0 = -INFINITY, a1 = -INFINITY;  // two independent FMNMX3 chains
+        for (int r = 0; r < NR; ++r) {
 #pragma unroll
-        for (int r = 0; r < NR; r += 2) {
-          a0 = fmax3(a0, v[4 * r + 2 * rr], v[4 * r + 2 * rr + 1]);
-          if (r + 1 < NR) a1 = fmax3(a1, v[4 * r + 4 + 2 * rr], v[4 * r + 4 + 2 * rr + 1]);
+          for (int rr = 0; rr < 2; ++rr) {
+            if (track) am[rr] = fmax3(am[rr], v[4 * r + 2 * rr], v[4 * r + 2 * rr + 1]);
+            const uint64_t xx =
+                ffma_f32x2(pack_f32x2(v[4 * r + 2 * rr], v[4 * r + 2 * rr + 1]), sc2, nm2[rr]);
+            float p0, p1;
+#ifdef STADI_ATTN_NOEXP  // timing experiment only (wrong results): no exp work
+            if (true) {
+              unpack_f32x2(xx, p0, p1);
+            } else
+#endif
+            if (r % 8 < POLY) {
+              ex2_poly_x2(xx, p0, p1);
+            } else {
+              float x0, x1;
+              unpack_f32x2(xx, x0, x1);
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            acc[rr][r & 1] = add_f32x2(acc[rr][r & 1], pack_f32x2(p0, p1));
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
+            pk[2 * r + rr] = *reinterpret_cast<uint32_t *>(&t2);
+          }
         }
-        float m = fmaxf(a0, a1);
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-        mt[rr] = m * scale_log2;
-      }
-      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(5, g, j);
-      float factor[2] = {1.f, 1.f};
-      bool grow = false;
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        if (mt[rr] > m_run[rr] + RESCALE_THRESHOLD) {
-          factor[rr] = ex2(m_run[rr] - mt[rr]);  // 0 on the first tile
-          m_run[rr] = mt[rr];
-          grow = true;
-        }
-      }
-      // PV_g(j-1) must be complete before O is rescaled or P_g overwritten.  With
-      // `defer` the wait moves to just before the P store unless this warp rescales,
-      // so the PV latency overlaps the token wait and the exp phase.
-      const bool any_grow = __any_sync(0xffffffffu, grow);
-      // ALIAS: s_full(j) already implied PV_g(j-1) complete
-      const bool wait_now = !ALIAS && j > 0 && (!(flags & 2) || any_grow);
-      if (wait_now) {
-        mbar_wait(&o_done[g], (j - 1) & 1);
-        tc_fence_after();
-      }
-      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(9, g, j);
-      if (j > 0 && any_grow) {
+      };
+      auto rescale_o = [&](const float *factor) {
         static_assert(NO % 2 == 0, "O rescale in 16-column pieces");
 #pragma unroll
         for (int c = 0; c < NO; c += 2) {  // 16 columns at a time: S values stay live
@@ -624,48 +665,63 @@ __global__ void __launch_bounds__(AttnCfg<N64, N32, N16, NQT, AKTO>::THREADS,
           for (int i = 0; i < 8; ++i) o[i] *= factor[(i >> 1) & 1];
           tmem_st_q256_x2(o_addr + 8 * c, reinterpret_cast<const uint32_t *>(o));
         }
-      }
-      l[0] *= factor[0];
-      l[1] *= factor[1];
-      // exp-phase tokens: the two groups take turns on the exp units, per group
-      // (bit 0) or per SM sub-partition (bit 3: the two warps of each group that
-      // share an SMSP's MUFU hand over to the other group's two warps there)
-      if (NQT == 2 && (flags & 8)) {
-        if (g == 1) mbar_wait(&tok4[4 + (warp & 3)], j & 1);
-        else if (j > 0) mbar_wait(&tok4[warp & 3], (j - 1) & 1);
-      } else if (NQT == 2 && (flags & 1)) {
-        if (g == 1) mbar_wait(&tok[1], j & 1);
-        else if (j > 0) mbar_wait(&tok[0], (j - 1) & 1);
-      }
-      if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(7, g, j);
-      const uint64_t sc2 = pack_f32x2(scale_log2, scale_log2);
-      const uint64_t nm2[2] = {pack_f32x2(-m_run[0], -m_run[0]), pack_f32x2(-m_run[1], -m_run[1])};
-      uint64_t acc[2][2] = {{0, 0}, {0, 0}};
-      uint32_t pk[2 * NR];
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
+      };
+      auto token_wait = [&] {
+        // exp-phase tokens: the two groups take turns on the exp units, per group
+        // (bit 0) or per SM sub-partition (bit 3: the two warps of each group that
+        // share an SMSP's MUFU hand over to the other group's two warps there)
+        if (NQT == 2 && (flags & 8)) {
+          if (g == 1) mbar_wait(&tok4[4 + (warp & 3)], j & 1);
+          else if (j > 0) mbar_wait(&tok4[warp & 3], (j - 1) & 1);
+        } else if (NQT == 2 && (flags & 1)) {
+          if (g == 1) mbar_wait(&tok[1], j & 1);
+          else if (j > 0) mbar_wait(&tok[0], (j - 1) & 1);
+        }
+      };
+      bool wait_now = false;
+      {
+        float mt[2];
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
-          const uint64_t xx =
-              ffma_f32x2(pack_f32x2(v[4 * r + 2 * rr], v[4 * r + 2 * rr + 1]), sc2, nm2[rr]);
-          float p0, p1;
-#ifdef STADI_ATTN_NOEXP  // timing experiment only (wrong results): no exp work
-          if (true) {
-            unpack_f32x2(xx, p0, p1);
-          } else
-#endif
-          if (r % 8 < POLY) {
-            ex2_poly_x2(xx, p0, p1);
-          } else {
-            float x0, x1;
-            unpack_f32x2(xx, x0, x1);
-            p0 = ex2(x0);
-            p1 = ex2(x1);
+          float a0 = -INFINITY, a1 = -INFINITY;  // two independent FMNMX3 chains
+#pragma unroll
+          for (int r = 0; r < NR; r += 2) {
+            a0 = fmax3(a0, v[4 * r + 2 * rr], v[4 * r + 2 * rr + 1]);
+            if (r + 1 < NR) a1 = fmax3(a1, v[4 * r + 4 + 2 * rr], v[4 * r + 4 + 2 * rr + 1]);
           }
-          acc[rr][r & 1] = add_f32x2(acc[rr][r & 1], pack_f32x2(p0, p1));
-          __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
-          pk[2 * r + rr] = *reinterpret_cast<uint32_t *>(&t2);
+          float m = fmaxf(a0, a1);
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+          mt[rr] = m * scale_log2;
         }
+        if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(5, g, j);
+        float factor[2] = {1.f, 1.f};
+        bool grow = false;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          if (mt[rr] > m_run[rr] + RESCALE_THRESHOLD) {
+            factor[rr] = ex2(m_run[rr] - mt[rr]);  // 0 on the first tile
+            m_run[rr] = mt[rr];
+            grow = true;
+          }
+        }
+        // PV_g(j-1) must be complete before O is rescaled or P_g overwritten.  With
+        // `defer` the wait moves to just before the P store unless this warp rescales,
+        // so the PV latency overlaps the token wait and the exp phase.
+        const bool any_grow = __any_sync(0xffffffffu, grow);
+        // ALIAS: s_full(j) already implied PV_g(j-1) complete
+        wait_now = !ALIAS && j > 0 && (!(flags & 2) || any_grow);
+        if (wait_now) {
+          mbar_wait(&o_done[g], (j - 1) & 1);
+          tc_fence_after();
+        }
+        if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(9, g, j);
+        if (j > 0 && any_grow) rescale_o(factor);
+        l[0] *= factor[0];
+        l[1] *= factor[1];
+        token_wait();
+        if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(7, g, j);
+        exp_pass(false, nullptr);
       }
       if (hf == 0 && qd == 2 && lane == 0) ATTN_TRACE(10, g, j);
       if (!ALIAS && j > 0 && !wait_now) {
@@ -965,34 +1021,26 @@ int attn_alias() {
   }();
   return v;
 }
-// STADI_ATTN_AKT=144/160/176 (+1 / +2: one / two of every 8 column pairs on the
-// polynomial exp2): keys per tile of the P-over-S variant for hd 72 / 80 (TMEM
-// holds 2 x (AKT + 80) <= 512 columns without the separate P region).
-int attn_alias_akt() {
+// Short K/V (cross-attention, Nkv <= 128) on the two-CTAs-per-SM variant: one 128-key
+// tile with P over S (S 128 + O HDP <= 256 TMEM columns) instead of two 112-key tiles
+// (the PixArt text has 120 tokens, SD / SDXL 77).  STADI_ATTN_XTILE=0 disables.
+int attn_xtile() {
   static const int v = [] {
-    const char *e = getenv("STADI_ATTN_AKT");
-    return e ? atoi(e) : 0;
+    const char *e = getenv("STADI_ATTN_XTILE");
+    return (e && e[0] == '0') ? 0 : 1;
   }();
   return v;
 }
 template <int N64, int N32, int N16, int NQT>
 cudaError_t launch_attn(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, int Nkv, int B, int H,
                         int hd, cudaStream_t s) {
-  if (!attn_quad()) return launch_attn_p<N64, N32, N16, NQT, 0, 0>(q, kv, o, Nq, Nkv, B, H, hd, s);
-  if (NQT == 2 && attn_alias() && attn_poly() == 0) {
-    if constexpr (NQT == 2 && 64 * N64 + 32 * N32 + 16 * N16 == 80) {  // hd 72 / 80
-      switch (attn_alias_akt()) {
-        case 144: return launch_attn_p<N64, N32, N16, NQT, 0, 2, 144>(q, kv, o, Nq, Nkv, B, H, hd, s);
-        case 160: return launch_attn_p<N64, N32, N16, NQT, 0, 2, 160>(q, kv, o, Nq, Nkv, B, H, hd, s);
-        case 176: return launch_attn_p<N64, N32, N16, NQT, 0, 2, 176>(q, kv, o, Nq, Nkv, B, H, hd, s);
-        case 160 + 1: return launch_attn_p<N64, N32, N16, NQT, 1, 2, 160>(q, kv, o, Nq, Nkv, B, H, hd, s);
-        case 176 + 1: return launch_attn_p<N64, N32, N16, NQT, 1, 2, 176>(q, kv, o, Nq, Nkv, B, H, hd, s);
-        case 176 + 2: return launch_attn_p<N64, N32, N16, NQT, 2, 2, 176>(q, kv, o, Nq, Nkv, B, H, hd, s);
-        default: break;
-      }
-    }
-    return launch_attn_p<N64, N32, N16, NQT, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
+  if constexpr (NQT == 1 && 64 * N64 + 32 * N32 + 16 * N16 <= 80) {
+    if (Nkv <= 128 && attn_xtile() && attn_quad())
+      return launch_attn_p<N64, N32, N16, NQT, 0, 1, 128>(q, kv, o, Nq, Nkv, B, H, hd, s);
   }
+  if (!attn_quad()) return launch_attn_p<N64, N32, N16, NQT, 0, 0>(q, kv, o, Nq, Nkv, B, H, hd, s);
+  if (NQT == 2 && attn_alias() && attn_poly() == 0)
+    return launch_attn_p<N64, N32, N16, NQT, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
   switch (attn_poly()) {
     case 0: return launch_attn_p<N64, N32, N16, NQT, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 1: return launch_attn_p<N64, N32, N16, NQT, 1, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
@@ -1025,14 +1073,8 @@ void preload_attn(cudaFuncAttributes *a) {
   cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 3, 1>);
   cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 4, 1>);
   cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 2>);
-  if constexpr (NQT == 2 && 64 * N64 + 32 * N32 + 16 * N16 == 80) {
-    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 2, 144>);
-    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 2, 160>);
-    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 2, 176>);
-    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 1, 2, 160>);
-    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 1, 2, 176>);
-    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 2, 2, 176>);
-  }
+  if constexpr (NQT == 1 && 64 * N64 + 32 * N32 + 16 * N16 <= 80)
+    cudaFuncGetAttributes(a, tc_attn_kernel<N64, N32, N16, NQT, 0, 1, 128>);
 }
 }  // namespace
 cudaError_t tc_attention_preload() {

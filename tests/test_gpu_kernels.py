@@ -192,6 +192,7 @@ ATTN_CASES = [  # Nq, Nkv, B, H, hd
     (64, 256, 2, 8, 160), (200, 77, 2, 8, 160),    # SD-1.5 level 2 (hd 160, one Q tile/CTA)
     (500, 1500, 2, 10, 64), (255, 77, 2, 10, 64),  # SDXL level 1 self / cross (hd 64)
     (257, 129, 1, 1, 16), (300, 200, 2, 4, 80),   # the last: two-CTAs-per-SM variant, ragged
+    (200, 128, 2, 4, 80), (64, 1, 1, 2, 72),       # single 128-key tile, P over S (<= 128 keys)
 ]
 
 
@@ -311,6 +312,10 @@ CONV_CASES = [  # h, W, B, C, N, mode, implicit
     (4, 64, 2, 64, 64, 0, 1), (3, 32, 2, 128, 192, 0, 1), (5, 16, 2, 64, 128, 0, 1),
     (2, 128, 2, 320, 320, 0, 1), (7, 8, 2, 64, 64, 0, 1), (1, 64, 1, 64, 256, 0, 1),
     (4, 16, 2, 64, 128, 1, 0), (3, 8, 2, 64, 64, 2, 0), (6, 12, 2, 4, 64, 0, 0),
+    # implicit stride 2 (TMA element strides) and upsample (x2-padded input + stride 1)
+    (4, 16, 2, 64, 128, 1, 1), (8, 128, 2, 64, 64, 1, 1), (6, 256, 2, 128, 64, 1, 1),
+    (2, 64, 1, 64, 64, 1, 1), (3, 8, 2, 64, 64, 2, 1), (2, 64, 2, 128, 64, 2, 1),
+    (5, 32, 2, 64, 192, 2, 1),
 ]
 
 
@@ -353,7 +358,7 @@ def test_conv3x3(S, dtype, h, W, B, C, N, mode, implicit):
     assert _rel(got, ref) < (1e-2 if dtype == 0 else 1e-5)
 
 
-@pytest.mark.parametrize("implicit,mode", [(1, 0), (0, 0), (0, 1), (0, 2)])
+@pytest.mark.parametrize("implicit,mode", [(1, 0), (0, 0), (0, 1), (0, 2), (1, 1), (1, 2)])
 def test_conv3x3_time_bias_and_residual(S, implicit, mode):
     """The U-Net ResBlock conv epilogue (EPI_CONV): out = conv + bias + temb[row % B]
     + res, against the oracle's conv3x3_valid plus the two terms; the 16-byte path
@@ -438,11 +443,13 @@ def test_gemm_on_emulator_grid(S, max_ctas, M, N, K):
     assert _rel(res.cpu().numpy() - res0, g * ref) < tol
 
 
-@pytest.mark.parametrize("akt", ["0", "144", "160", "176", "177", "178"])
-def test_attention_alias_variant(S, akt):
-    """The P-over-S variant (STADI_ATTN_ALIAS=1, QUAD == 2: two handoffs per key tile;
-    STADI_ATTN_AKT: 144 / 160 / 176-key tiles, +1 / +2 with polynomial exp2 columns)
-    against the oracle, in a subprocess (the switch is read once per process)."""
+@pytest.mark.parametrize("switch", ["STADI_ATTN_ALIAS", "STADI_ATTN_XTILE"])
+def test_attention_alias_variant(S, switch):
+    """The P-over-S variant (STADI_ATTN_ALIAS=1, QUAD == 2: two handoffs per key tile)
+    against the oracle, in a subprocess (the switches are read once per process), keys
+    growing along the sequence so the lazy rescale fires on later tiles; XTILE=1 (the
+    default single-tile cross-attention variant) runs the same multi-tile case through
+    the unchanged self-attention path."""
     import os
     import subprocess
     import sys
@@ -450,7 +457,9 @@ def test_attention_alias_variant(S, akt):
             "from paper_2509_04719_b200 import stadi as S; from oracle import dit as OD;"
             "rng = np.random.default_rng(9); Nq, Nkv, B, H, hd = 300, 777, 2, 2, 72; d = H * hd;"
             "q = torch.from_numpy(rng.standard_normal((Nq, B, d)).astype(np.float32)).cuda().bfloat16();"
-            "kv = torch.from_numpy(rng.standard_normal((Nkv, B, 2, d)).astype(np.float32)).cuda().bfloat16();"
+            "kvn = rng.standard_normal((Nkv, B, 2, d)).astype(np.float32);"
+            "kvn[:, :, 0] *= np.linspace(0.5, 40.0, Nkv, dtype=np.float32)[:, None, None];"
+            "kv = torch.from_numpy(kvn).cuda().bfloat16();"
             "o = torch.empty(Nq * B, d, device='cuda', dtype=torch.bfloat16);"
             "S.k_attention(0, q, kv, o, Nq, Nkv, B, H, hd); torch.cuda.synchronize();"
             "nq = q.float().cpu().numpy().astype(np.float64); nkv = kv.float().cpu().numpy().astype(np.float64);"
@@ -459,7 +468,7 @@ def test_attention_alias_variant(S, akt):
             "print(float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))))")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
-                       env=dict(os.environ, STADI_ATTN_ALIAS="1", STADI_ATTN_AKT=akt), timeout=300)
+                       env=dict(os.environ, **{switch: "1"}), timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) < 1e-2
 
@@ -490,7 +499,7 @@ def test_groupnorm(S, dtype, h, W, B, C):
         tg, tb = torch.from_numpy(gamma).cuda(), torch.from_numpy(beta).cuda()
         stats = torch.zeros(B * 32 * 2, device="cuda", dtype=torch.float64)
         ws = torch.zeros(592 * 2 * B * 32, device="cuda", dtype=torch.float64)
-        ticket = torch.zeros(1, device="cuda", dtype=torch.int32)
+        ticket = torch.zeros(32, device="cuda", dtype=torch.int32)
         odt = torch.bfloat16 if dtype == 0 else torch.float32
         for pad in (0, 1):
             shape = (h + 2, W + 2, B, C) if pad else (h, W, B, C)
