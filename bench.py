@@ -585,6 +585,9 @@ def main():
     from paper_2509_04719_b200 import stadi as S
 
     assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    # one rank per GPU; more ranks than GPUs (a functional check of the N > 1 path on a
+    # smaller box) share devices round-robin -- never a performance configuration
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         # control plane only (barriers, the ncclUniqueId broadcast, max-over-ranks):

@@ -719,8 +719,19 @@ cudaError_t dispatch_conv(const bf16 *P, const bf16 *W, int h, const ConvGeo &g,
 struct GemmPlan {
   int bn, ks;
 };
+// STADI_GEMM_L2=<bytes per clock>: the cost model's chip L2 bandwidth (default 12600:
+// measured in-step, C3 334 -> 317 ms and C4 1232 -> 1180 ms / image against 6300).
+double gemm_l2_bw() {
+  static const double v = [] {
+    const char *e = getenv("STADI_GEMM_L2");
+    const double x = e ? atof(e) : 0.0;
+    return x > 0 ? x : 12600.0;
+  }();
+  return v;
+}
 GemmPlan plan_gemm(int M, int N, int K, int max_ctas, int mc, long ws_elems) {
   const int tm = (M + GBM - 1) / GBM, nkb = K / GBK;
+  const double L2 = gemm_l2_bw();
   const int ncl = mc == 1 ? 1 : 2;
   const int tmr = (tm + ncl - 1) / ncl * ncl;
   const int cands[5] = {256, 192, 160, 128, 64};
@@ -729,14 +740,14 @@ GemmPlan plan_gemm(int M, int N, int K, int max_ctas, int mc, long ws_elems) {
   for (int bn : cands) {
     if (N % bn) continue;
     const double wbytes = (mc == 1 ? 128.0 : 64.0) * bn;
-    const double per_kb = std::max(2.0 * bn, (16384.0 + wbytes) / (6300.0 / max_ctas));
+    const double per_kb = std::max(2.0 * bn, (16384.0 + wbytes) / (L2 / max_ctas));
     for (int ks = 1; ks <= 16; ++ks) {
       if (ks > 1 && (nkb / ks < 8 || (long)ks * M * N > ws_elems || splitk_disabled())) break;
       const long ctas = (long)tmr * (N / bn) * ks;
       const long waves = (ctas + max_ctas - 1) / max_ctas;
       const long per_cta = (ctas + waves - 1) / waves;  // CTAs of a wave, sharing L2
       const double kb = (double)nkb / ks;
-      const double l2 = kb * (16384.0 + wbytes) * per_cta / 6300.0;
+      const double l2 = kb * (16384.0 + wbytes) * per_cta / L2;
       double t = waves * std::max(kb * 2.0 * bn + 1500.0, l2 + 1500.0);
       if (ks > 1) t += (ks + 2.0) * M * N * 4.0 / 3300.0 + 4000.0;
       if (best_t < 0 || t < best_t * 0.97) {  // prefer the earlier (wider, unsplit) option

@@ -181,6 +181,19 @@ __global__ void __launch_bounds__(GNP_THREADS) gn_partials_kernel(
 // channel) mean and scale live in shared memory (dynamic: (2 B + 1) C floats).
 constexpr int GNA_THREADS = 256;
 constexpr int GNA_UNR = 4;
+// SiLU of the GN output: bf16 output -> x (1 + tanh(x / 2)) / 2 with the single-MUFU
+// tanh.approx (rel. error ~2^-11, 4x below the bf16 rounding of the result); fp32 (the
+// <= 1e-4 debug build) -> the accurate x / (1 + e^-x)
+template <typename T>
+__device__ __forceinline__ float silu_out(float x) {
+  if constexpr (sizeof(T) == 2) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+    return 0.5f * x * (1.f + t);
+  } else {
+    return silu(x);
+  }
+}
 template <typename T>
 __global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(
     const float *__restrict__ x, int h, int W, int B, int C, int rpb,
@@ -215,48 +228,55 @@ __global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(
   }
   const int nvec = C / 4, M = h * W * B;
   const int r0 = blockIdx.x * rpb, r1 = min(M, r0 + rpb);
-  const int total = (r1 - r0) * nvec;
-  for (int e0 = threadIdx.x; e0 < total; e0 += GNA_UNR * GNA_THREADS) {
-    float4 a[GNA_UNR];
+  // thread -> fixed float4 channel vector(s) v0 (+ 256 k), rows r0 + slot + i slots:
+  // no per-element index division; GNA_UNR rows of loads in flight
+  const int t = threadIdx.x;
+  const int slots = nvec >= GNA_THREADS ? 1 : GNA_THREADS / nvec;
+  const bool busy = nvec >= GNA_THREADS || t < slots * nvec;
+  const int slot = nvec >= GNA_THREADS ? 0 : t / nvec;
+  const int v0 = nvec >= GNA_THREADS ? t : t % nvec;
+  for (int v = v0; busy && v < nvec; v += GNA_THREADS) {
+    for (int rb = r0 + slot; rb < r1; rb += GNA_UNR * slots) {
+      float4 a[GNA_UNR];
 #pragma unroll
-    for (int u = 0; u < GNA_UNR; ++u) {
-      const int e = e0 + u * GNA_THREADS;
-      a[u] = e < total ? reinterpret_cast<const float4 *>(x + (long)r0 * C)[e]
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+      for (int u = 0; u < GNA_UNR; ++u) {
+        const int row = rb + u * slots;
+        a[u] = row < r1 ? reinterpret_cast<const float4 *>(x + (long)row * C)[v]
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-    for (int u = 0; u < GNA_UNR; ++u) {
-      const int e = e0 + u * GNA_THREADS;
-      if (e >= total) break;
-      const int row = r0 + e / nvec, v = e % nvec;
-      const int bb = row % B;
-      float y[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
-      if (stats) {
-        const float4 m = *reinterpret_cast<const float4 *>(mu_c + bb * C + 4 * v);
-        const float4 sc = *reinterpret_cast<const float4 *>(sc_c + bb * C + 4 * v);
-        const float4 be = *reinterpret_cast<const float4 *>(be_c + 4 * v);
-        y[0] = (y[0] - m.x) * sc.x + be.x;
-        y[1] = (y[1] - m.y) * sc.y + be.y;
-        y[2] = (y[2] - m.z) * sc.z + be.z;
-        y[3] = (y[3] - m.w) * sc.w + be.w;
-      }
-      if (act) {
+      for (int u = 0; u < GNA_UNR; ++u) {
+        const int row = rb + u * slots;
+        if (row >= r1) break;
+        const int bb = B == 2 ? (row & 1) : 0;
+        float y[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+        if (stats) {
+          const float4 m = *reinterpret_cast<const float4 *>(mu_c + bb * C + 4 * v);
+          const float4 sc = *reinterpret_cast<const float4 *>(sc_c + bb * C + 4 * v);
+          const float4 be = *reinterpret_cast<const float4 *>(be_c + 4 * v);
+          y[0] = (y[0] - m.x) * sc.x + be.x;
+          y[1] = (y[1] - m.y) * sc.y + be.y;
+          y[2] = (y[2] - m.z) * sc.z + be.z;
+          y[3] = (y[3] - m.w) * sc.w + be.w;
+        }
+        if (act) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) y[k] = silu(y[k]);
-      }
-      long orow = row;
-      if (pad) {
-        const int pix = row / B, yy = pix / W, xx = pix - yy * W;
-        orow = ((long)(yy + 1) * (W + 2) + xx + 1) * B + bb;
-      }
-      T *o = out + orow * C + 4 * v;
-      if constexpr (sizeof(T) == 2) {  // one 8-byte store of 4 bf16
-        __nv_bfloat162 lo = __floats2bfloat162_rn(y[0], y[1]),
-                       hi = __floats2bfloat162_rn(y[2], y[3]);
-        *reinterpret_cast<uint2 *>(o) =
-            make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
-      } else {
-        *reinterpret_cast<float4 *>(o) = make_float4(y[0], y[1], y[2], y[3]);
+          for (int k = 0; k < 4; ++k) y[k] = silu_out<T>(y[k]);
+        }
+        long orow = row;
+        if (pad) {
+          const int pix = B == 2 ? (row >> 1) : row, yy = pix / W, xx = pix - yy * W;
+          orow = ((long)(yy + 1) * (W + 2) + xx + 1) * B + bb;
+        }
+        T *o = out + orow * C + 4 * v;
+        if constexpr (sizeof(T) == 2) {  // one 8-byte store of 4 bf16
+          __nv_bfloat162 lo = __floats2bfloat162_rn(y[0], y[1]),
+                         hi = __floats2bfloat162_rn(y[2], y[3]);
+          *reinterpret_cast<uint2 *>(o) =
+              make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+        } else {
+          *reinterpret_cast<float4 *>(o) = make_float4(y[0], y[1], y[2], y[3]);
+        }
       }
     }
   }
