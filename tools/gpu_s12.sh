@@ -8,14 +8,5 @@ echo "n2 rc=$?"; tail -c 600 gpurun_out/s12_n2_c2.json; tail -3 gpurun_out/s12_n
 for v in "STADI_ATTN_POLY=0" "STADI_ATTN_POLY=1" "STADI_ATTN_POLY=2" "STADI_ATTN_POLY=1,STADI_ATTN_TOK4=0" "STADI_ATTN_POLY=2,STADI_ATTN_TOK4=0" "STADI_ATTN_TOK4=0"; do
   echo "== $v"; env ${v//,/ } timeout 120 python tools/kbench.py attn 2>&1 | grep "hd=72"
 done | tee gpurun_out/s12_poly_ab.txt
-# compute-sanitizer passes over the smoke request (C1 tiny DiT, 2 ranks, bf16 tcgen05 path)
-# and a small U-Net / kernel parity subset (SURVEY §5 race / memory checking)
-for tool in memcheck racecheck synccheck; do
-  timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool $tool --print-limit 20 \
-    python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s12_sanitizer_$tool.log 2>&1
-  echo "sanitizer $tool rc=$?"; tail -3 gpurun_out/s12_sanitizer_$tool.log
-done
-timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --print-limit 20 \
-  python -m pytest tests/test_gpu_kernels.py -m gpu -q -p no:cacheprovider -x \
-  -k "groupnorm and 7-9 or conv3x3 and 4-16 or attention and 128-120" > gpurun_out/s12_sanitizer_kernels.log 2>&1
-echo "sanitizer kernels rc=$?"; tail -3 gpurun_out/s12_sanitizer_kernels.log
+# (compute-sanitizer is closed on the GPU pool: 'runs under it have left GPUs needing a
+# reset' -- the kernels rely on bounds-checked parity tests instead)
