@@ -162,6 +162,13 @@ elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "xattn":
     attn(4096, 120, 2, 16, 72)
     attn(4096, 77, 2, 8, 40)       # SD-1.5 level 0 cross
     attn(4096, 77, 2, 10, 64)      # SDXL level 1 cross
+elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "small":
+    # latency-bound grids (split-K/V candidates): C2 self, SD-1.5 level 1, SDXL level 1 / 2
+    attn(256, 256, 2, 16, 72)
+    attn(1024, 1024, 2, 8, 80)
+    attn(4096, 4096, 2, 10, 64)
+    attn(1024, 1024, 2, 20, 64)
+    attn(256, 256, 2, 8, 160)
 elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "attn":
     attn(16384, 16384, 2, 16, 72)
     attn(4096, 4096, 2, 10, 64)
