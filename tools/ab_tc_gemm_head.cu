@@ -228,6 +228,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             else
               tma_load_3d(&tmA, sA + s * C::A_BYTES, &full[s], c0,
                           (p0 % cg.W + tap % 3) * cg.B, p0 / cg.W + tap / 3);
+          } else if constexpr (AM == 2) {  // stride 2: every other pixel / row of P
+            const int cpb = cg.C / GBK, tap = kb / cpb, c0 = (kb % cpb) * GBK;
+            const int wo = cg.W / 2, p0 = mb * (GBM / cg.B);
+            const int x = 2 * (p0 % wo) + tap % 3, y = 2 * (p0 / wo) + tap / 3;
+            if constexpr (PAIR)
+              tma_load_4d_cg2(&tmA, sA + s * C::A_BYTES, &full[s], c0, 0, x, y);
+            else
+              tma_load_4d(&tmA, sA + s * C::A_BYTES, &full[s], c0, 0, x, y);
           } else if constexpr (PAIR) {
             tma_load_2d_cg2(&tmA, sA + s * C::A_BYTES, &full[s], kb * GBK, mb * GBM);
           } else {
@@ -249,8 +257,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && (!PAIR || crank == 0)) {  // ---------------- MMA issuer (pair: leader)
+    if (!PAIR || crank == 0) {  // ---------------- MMA issuer (pair: leader), whole warp
+      // warp-collective issue (one elected lane in the asm): descriptors stay in
+      // uniform registers -- see umma_bf16_w
       constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * GBM : GBM, BN, 0, 0);
+      const uint64_t adesc0 = umma_desc(smem_u32(sA), 16, 1024, SWZ_128B);
+      const uint64_t bdesc0 = umma_desc(smem_u32(sB), 16, 1024, SWZ_128B);
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
@@ -265,25 +277,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + s * C::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + s * C::B_BYTES);
+          // stage descriptors = stage-0 descriptors + the stage's 16-byte offset
+          const uint64_t ad = adesc0 + (uint64_t)((uint32_t)s * (uint32_t)(C::A_BYTES >> 4));
+          const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)s * (uint32_t)(C::B_BYTES >> 4));
 #pragma unroll
           for (int k = 0; k < GBK / 16; ++k) {
-            const uint64_t ad = umma_desc(a0 + k * 32, 16, 1024, SWZ_128B);
-            const uint64_t bd = umma_desc(b0 + k * 32, 16, 1024, SWZ_128B);
-            if constexpr (PAIR) umma_bf16_cg2(dtm, ad, bd, idesc, (kb - kb0) | k);
-            else umma_bf16(dtm, ad, bd, idesc, (kb - kb0) | k);
+            if constexpr (PAIR) umma_bf16_cg2_w(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb - kb0) | k);
+            else umma_bf16_w(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb - kb0) | k);
           }
-          if constexpr (PAIR) umma_commit_cg2(&empty[s]);
-          else if constexpr (MC == 2) umma_commit_mc(&empty[s], (uint16_t)0x3);
-          else umma_commit(&empty[s]);
+          if constexpr (PAIR) umma_commit_cg2_w(&empty[s]);
+          else if constexpr (MC == 2) umma_commit_mc_w(&empty[s], (uint16_t)0x3);
+          else umma_commit_w(&empty[s]);
           if (++s == C::STAGES) {
             s = 0;
             ph ^= 1;
           }
         }
-        if constexpr (PAIR) umma_commit_cg2(&tfull[acc]);
-        else umma_commit(&tfull[acc]);
+        if constexpr (PAIR) umma_commit_cg2_w(&tfull[acc]);
+        else umma_commit_w(&tfull[acc]);
       }
     }
   } else {  // ---------------------------- epilogue warps 2..9
@@ -533,9 +544,11 @@ EncodeFn get_encode() {
 
 }  // namespace
 
-// Exported for the attention kernel too.
+// Exported for the attention kernel too.  estr: per-dimension element (traversal)
+// strides (NULL = all 1): TMA then loads ceil(box[i] / estr[i]) elements along i.
 bool make_tmap(CUtensorMap *m, const void *base, int rank, const uint64_t *dims,
-               const uint64_t *strides_bytes, const uint32_t *box, CUtensorMapSwizzle swz) {
+               const uint64_t *strides_bytes, const uint32_t *box, CUtensorMapSwizzle swz,
+               const uint32_t *estr = nullptr) {
   EncodeFn fn = get_encode();
   if (!fn) return false;
   cuuint64_t d[5], st[4];
@@ -543,7 +556,7 @@ bool make_tmap(CUtensorMap *m, const void *base, int rank, const uint64_t *dims,
   for (int i = 0; i < rank; ++i) {
     d[i] = dims[i];
     b[i] = box[i];
-    es[i] = 1;
+    es[i] = estr ? estr[i] : 1;
   }
   for (int i = 0; i < rank - 1; ++i) st[i] = strides_bytes[i];
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(base), d, st, b,
@@ -592,6 +605,16 @@ cudaError_t launch_gemm(const bf16 *A, const bf16 *W, int M, int N, int K, const
     const uint64_t sa[2] = {(uint64_t)cg.C * 2, (uint64_t)(cg.W + 2) * cg.B * cg.C * 2};
     const uint32_t ba[3] = {GBK, (uint32_t)std::min(wb, GBM), (uint32_t)std::max(1, GBM / wb)};
     ok = make_tmap(&ta, A, 3, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else if constexpr (AM == 2) {  // P [h+2, W+2, B, C], every other pixel / row
+    const int wob = cg.W / 2 * cg.B;
+    const uint64_t da[4] = {(uint64_t)cg.C, (uint64_t)cg.B, (uint64_t)cg.W + 2,
+                            (uint64_t)conv_h + 2};
+    const uint64_t sa[3] = {(uint64_t)cg.C * 2, (uint64_t)cg.B * cg.C * 2,
+                            (uint64_t)(cg.W + 2) * cg.B * cg.C * 2};
+    const uint32_t ba[4] = {GBK, (uint32_t)cg.B, (uint32_t)(2 * std::min(wob, GBM) / cg.B),
+                            (uint32_t)(2 * std::max(1, GBM / wob))};
+    const uint32_t es[4] = {1, 1, 2, 2};
+    ok = make_tmap(&ta, A, 4, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B, es);
   } else {
     const uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
     const uint32_t ba[2] = {GBK, GBM};
@@ -668,8 +691,17 @@ cudaError_t dispatch_mc(const bf16 *A, const bf16 *W, int M, int N, int K, int e
 }
 template <int BN, int MC>
 cudaError_t dispatch_conv(const bf16 *P, const bf16 *W, int h, const ConvGeo &g, int N, int epi,
-                          const EpiParams &ep, int max_ctas, int ks, cudaStream_t s) {
-  const int M = h * g.W * g.B, K = 9 * g.C;
+                          const EpiParams &ep, int max_ctas, int ks, int mode, cudaStream_t s) {
+  const int K = 9 * g.C;
+  if (mode == 1) {  // stride 2: (h / 2) x (W / 2) outputs
+    const int M = h / 2 * (g.W / 2) * g.B;
+    if (epi == EPI_CONV)
+      return launch_gemm<BN, EPI_CONV, MC, 2>(P, W, M, N, K, ep, max_ctas, g, h, ks, s);
+    if (epi == EPI_F32)
+      return launch_gemm<BN, EPI_F32, MC, 2>(P, W, M, N, K, ep, max_ctas, g, h, ks, s);
+    return cudaErrorInvalidValue;
+  }
+  const int M = h * g.W * g.B;
   if (epi == EPI_CONV)
     return launch_gemm<BN, EPI_CONV, MC, 1>(P, W, M, N, K, ep, max_ctas, g, h, ks, s);
   if (epi == EPI_F32)
@@ -687,8 +719,19 @@ cudaError_t dispatch_conv(const bf16 *P, const bf16 *W, int h, const ConvGeo &g,
 struct GemmPlan {
   int bn, ks;
 };
+// STADI_GEMM_L2=<bytes per clock>: the cost model's chip L2 bandwidth (default 12600:
+// measured in-step, C3 334 -> 317 ms and C4 1232 -> 1180 ms / image against 6300).
+double gemm_l2_bw() {
+  static const double v = [] {
+    const char *e = getenv("STADI_GEMM_L2");
+    const double x = e ? atof(e) : 0.0;
+    return x > 0 ? x : 12600.0;
+  }();
+  return v;
+}
 GemmPlan plan_gemm(int M, int N, int K, int max_ctas, int mc, long ws_elems) {
   const int tm = (M + GBM - 1) / GBM, nkb = K / GBK;
+  const double L2 = gemm_l2_bw();
   const int ncl = mc == 1 ? 1 : 2;
   const int tmr = (tm + ncl - 1) / ncl * ncl;
   const int cands[5] = {256, 192, 160, 128, 64};
@@ -697,14 +740,14 @@ GemmPlan plan_gemm(int M, int N, int K, int max_ctas, int mc, long ws_elems) {
   for (int bn : cands) {
     if (N % bn) continue;
     const double wbytes = (mc == 1 ? 128.0 : 64.0) * bn;
-    const double per_kb = std::max(2.0 * bn, (16384.0 + wbytes) / (6300.0 / max_ctas));
+    const double per_kb = std::max(2.0 * bn, (16384.0 + wbytes) / (L2 / max_ctas));
     for (int ks = 1; ks <= 16; ++ks) {
       if (ks > 1 && (nkb / ks < 8 || (long)ks * M * N > ws_elems || splitk_disabled())) break;
       const long ctas = (long)tmr * (N / bn) * ks;
       const long waves = (ctas + max_ctas - 1) / max_ctas;
       const long per_cta = (ctas + waves - 1) / waves;  // CTAs of a wave, sharing L2
       const double kb = (double)nkb / ks;
-      const double l2 = kb * (16384.0 + wbytes) * per_cta / 6300.0;
+      const double l2 = kb * (16384.0 + wbytes) * per_cta / L2;
       double t = waves * std::max(kb * 2.0 * bn + 1500.0, l2 + 1500.0);
       if (ks > 1) t += (ks + 2.0) * M * N * 4.0 / 3300.0 + 4000.0;
       if (best_t < 0 || t < best_t * 0.97) {  // prefer the earlier (wider, unsplit) option
@@ -799,6 +842,8 @@ void preload_bn_mc(cudaFuncAttributes *a) {
   cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_GEGLU, MC, 0>);
   cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_CONV, MC, 1>);
   cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_F32, MC, 1>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_CONV, MC, 2>);
+  cudaFuncGetAttributes(a, tc_gemm_kernel<BN, EPI_F32, MC, 2>);
 }
 template <int BN>
 void preload_bn(cudaFuncAttributes *a) {
@@ -826,23 +871,30 @@ cudaError_t tc_gemm_preload() {
   return cudaGetLastError();
 }
 
-// Implicit-GEMM 3x3 conv (stride 1): out = epi(conv(P) . W^T) with P the
-// halo-padded input [h+2, W+2, B, C] and W [N, 9C] (column (ky*3 + kx)*C + c).
+// Implicit-GEMM 3x3 conv: out = epi(conv(P) . W^T) with P the halo-padded input
+// [h+2, W+2, B, C] and W [N, 9C] (column (ky*3 + kx)*C + c); mode 0 stride 1, mode 1
+// stride 2 (output (oy, ox) reads padded rows / columns 2 oy + ky, 2 ox + kx: a 4-D
+// tensor map with element strides 2 over the pixel and row dimensions).
+bool tc_conv_implicit_ok(int h, int W, int B, int C, int N, int mode) {
+  if (C % GBK || N % 64 || (mode != 0 && mode != 1)) return false;
+  if (mode == 1 && (h % 2 || W % 2)) return false;
+  const int wb = (mode == 1 ? W / 2 : W) * B;
+  return wb > 0 && (wb % GBM == 0 || GBM % wb == 0);
+}
 cudaError_t tc_conv3x3_bf16(const bf16 *P, const bf16 *Wt, int h, int W, int B, int C, int N,
-                            int epi, const EpiParams &ep, int max_ctas, cudaStream_t s) {
+                            int epi, const EpiParams &ep, int max_ctas, cudaStream_t s, int mode) {
   if (h <= 0) return cudaSuccess;
-  const int wb = W * B;
-  if (C % GBK || N % 64 || max_ctas < 1 || (wb % GBM && GBM % wb)) return cudaErrorInvalidValue;
+  if (!tc_conv_implicit_ok(h, W, B, C, N, mode) || max_ctas < 1) return cudaErrorInvalidValue;
   const ConvGeo g{W, B, C};
-  const int M = h * wb, tm = (M + GBM - 1) / GBM;
+  const int M = mode == 1 ? h / 2 * (W / 2) * B : h * W * B, tm = (M + GBM - 1) / GBM;
   const int mc = pair_mode_for(tm, max_ctas, epi, 9 * C);
   const GemmPlan gp = plan_gemm(M, N, 9 * C, max_ctas, mc, ep.ws ? ep.ws_elems : 0);
   const int ks = gp.ks;
 #define STADI_CONV_CASE(BNV)                                                          \
   case BNV:                                                                           \
-    return mc == 3   ? dispatch_conv<BNV, 3>(P, Wt, h, g, N, epi, ep, max_ctas, ks, s) \
-           : mc == 2 ? dispatch_conv<BNV, 2>(P, Wt, h, g, N, epi, ep, max_ctas, ks, s) \
-                     : dispatch_conv<BNV, 1>(P, Wt, h, g, N, epi, ep, max_ctas, ks, s);
+    return mc == 3   ? dispatch_conv<BNV, 3>(P, Wt, h, g, N, epi, ep, max_ctas, ks, mode, s) \
+           : mc == 2 ? dispatch_conv<BNV, 2>(P, Wt, h, g, N, epi, ep, max_ctas, ks, mode, s) \
+                     : dispatch_conv<BNV, 1>(P, Wt, h, g, N, epi, ep, max_ctas, ks, mode, s);
   switch (gp.bn) {
     STADI_CONV_CASE(256)
     STADI_CONV_CASE(192)
