@@ -1062,6 +1062,14 @@ int attn_narrow() {
   return v;
 }
 
+int attn_dual40() {
+  static const int v = [] {
+    const char *e = getenv("STADI_ATTN_DUAL40");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v;
+}
+
 // Force-load every attention kernel instance (see tc_gemm_preload).
 namespace {
 template <int N64, int N32, int N16, int NQT>
@@ -1081,6 +1089,7 @@ cudaError_t tc_attention_preload() {
   cudaFuncAttributes a;
   preload_attn<0, 0, 1, 2>(&a);
   preload_attn<0, 1, 1, 2>(&a);
+  preload_attn<0, 1, 1, 1>(&a);
   preload_attn<1, 0, 0, 2>(&a);
   preload_attn<0, 0, 5, 2>(&a);
   preload_attn<0, 0, 5, 1>(&a);
@@ -1091,13 +1100,15 @@ cudaError_t tc_attention_preload() {
 }
 
 // K/V lengths up to this use the two-CTAs-per-SM variant (hd 64 / 72 / 80): a few key
-// tiles leave each CTA latency bound, so a second resident CTA hides it; for long
-// K/V the shared ping-pong CTA wins (measured 786 vs 583 TFLOP/s at 16384 keys).
-// STADI_ATTN_DUAL_KV overrides (0 = never).
+// tiles leave each CTA latency bound, so a second resident CTA hides it, and its grid
+// of 128-query CTAs fills the SMs twice as finely; for long K/V the shared ping-pong
+// CTA wins (786 vs 583 TFLOP/s at 16384 keys).  Measured round 2 (kbench, B200): 1024
+// keys hd 80 249 -> 337 TFLOP/s, 1024 keys hd 64 x 20 heads 289 -> 365, 4096 keys hd 64
+// 492 -> 603.  STADI_ATTN_DUAL_KV overrides (0 = never).
 int attn_dual_max_kv() {
   static const int v = [] {
     const char *e = getenv("STADI_ATTN_DUAL_KV");
-    return e ? atoi(e) : 256;
+    return e ? atoi(e) : 4096;
   }();
   return v;
 }
@@ -1114,7 +1125,12 @@ cudaError_t tc_attention_bf16(const bf16 *q, const bf16 *kv, bf16 *o, int Nq, in
   if (Nkv <= 0) return cudaErrorInvalidValue;
   switch (hd) {
     case 16: return launch_attn<0, 0, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
-    case 40: return launch_attn<0, 1, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);  // dual slower
+    case 40:  // dual slower for the 77-token cross-attention, faster for 128 < K/V <=
+              // STADI_ATTN_DUAL_KV (SD-1.5 level 0, 4096 keys: 329-339 -> 348-371 TFLOP/s);
+              // STADI_ATTN_DUAL40=0 keeps the ping-pong CTA
+      if (attn_dual40() && Nkv > 128 && Nkv <= attn_dual_max_kv())
+        return launch_attn<0, 1, 1, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
+      return launch_attn<0, 1, 1, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);
     case 64:  // dual: SDXL cross-attention 20 -> 16 us
       if (Nkv <= attn_dual_max_kv()) return launch_attn<1, 0, 0, 1>(q, kv, o, Nq, Nkv, B, H, hd, s);
       return launch_attn<1, 0, 0, 2>(q, kv, o, Nq, Nkv, B, H, hd, s);

@@ -443,8 +443,9 @@ def test_gemm_on_emulator_grid(S, max_ctas, M, N, K):
     assert _rel(res.cpu().numpy() - res0, g * ref) < tol
 
 
-@pytest.mark.parametrize("switch", ["STADI_ATTN_ALIAS", "STADI_ATTN_XTILE"])
-def test_attention_alias_variant(S, switch):
+@pytest.mark.parametrize("switch,hd", [("STADI_ATTN_ALIAS", 72), ("STADI_ATTN_XTILE", 72),
+                                       ("STADI_ATTN_DUAL40", 40)])  # "1": the default
+def test_attention_alias_variant(S, switch, hd):
     """The P-over-S variant (STADI_ATTN_ALIAS=1, QUAD == 2: two handoffs per key tile)
     against the oracle, in a subprocess (the switches are read once per process), keys
     growing along the sequence so the lazy rescale fires on later tiles; XTILE=1 (the
@@ -455,7 +456,7 @@ def test_attention_alias_variant(S, switch):
     import sys
     code = ("import numpy as np, torch, sys; sys.path.insert(0, '.');"
             "from paper_2509_04719_b200 import stadi as S; from oracle import dit as OD;"
-            "rng = np.random.default_rng(9); Nq, Nkv, B, H, hd = 300, 777, 2, 2, 72; d = H * hd;"
+            f"rng = np.random.default_rng(9); Nq, Nkv, B, H, hd = 300, 777, 2, 2, {hd}; d = H * hd;"
             "q = torch.from_numpy(rng.standard_normal((Nq, B, d)).astype(np.float32)).cuda().bfloat16();"
             "kvn = rng.standard_normal((Nkv, B, 2, d)).astype(np.float32);"
             "kvn[:, :, 0] *= np.linspace(0.5, 40.0, Nkv, dtype=np.float32)[:, None, None];"
