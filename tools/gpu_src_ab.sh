@@ -1,5 +1,5 @@
 # Same-box A/B of a kernel source file: the working tree's version vs an alternative
-# copy (e.g. HEAD's).  Usage: bash tools/gpu_src_ab.sh <kernel file> <alt copy> <kbench mode> <grep>
+# copy (e.g. HEAD's, written by `git show HEAD:<path> > /tmp/alt.cu`).  Usage: bash tools/gpu_src_ab.sh <kernel file> <alt copy> <kbench mode> <grep>
 k=$1; alt=$2; mode=$3; pat=$4
 d=paper_2509_04719_b200/csrc/kernels
 cp $d/$k /tmp/ab_new.cu
