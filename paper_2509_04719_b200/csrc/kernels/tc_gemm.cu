@@ -729,9 +729,20 @@ double gemm_l2_bw() {
   }();
   return v;
 }
+// STADI_GEMM_BN=<64|128|160|192|256>: force the tile width where it divides N (A/B only).
+int gemm_forced_bn() {
+  static const int v = [] {
+    const char *e = getenv("STADI_GEMM_BN");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 GemmPlan plan_gemm(int M, int N, int K, int max_ctas, int mc, long ws_elems) {
   const int tm = (M + GBM - 1) / GBM, nkb = K / GBK;
   const double L2 = gemm_l2_bw();
+  if (const int fb = gemm_forced_bn(); fb && N % fb == 0 &&
+      (fb == 64 || fb == 128 || fb == 160 || fb == 192 || fb == 256))
+    return GemmPlan{fb, 1};
   const int ncl = mc == 1 ? 1 : 2;
   const int tmr = (tm + ncl - 1) / ncl * ncl;
   const int cands[5] = {256, 192, 160, 128, 64};
