@@ -25,3 +25,27 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+# Measured parity errors in the terminal summary: the GPU parity tests print their
+# max-abs-rel (or per-case error) lines; captured stdout of passing tests is otherwise
+# dropped under -q, so the headroom under each tolerance would appear in no log.
+_PARITY_LINES = []
+
+
+def pytest_runtest_logreport(report):
+    if report.when != "call" or not report.passed:
+        return
+    for name, content in report.sections:
+        if "stdout" not in name:
+            continue
+        for line in content.splitlines():
+            if "max-abs-rel" in line or ("groupnorm" in line and ": " in line):
+                _PARITY_LINES.append(f"{report.nodeid.split('::')[-1]}: {line.strip()}")
+
+
+def pytest_terminal_summary(terminalreporter):
+    if _PARITY_LINES:
+        terminalreporter.section("measured parity errors (max |x - ref| / max |ref|)")
+        for line in _PARITY_LINES:
+            terminalreporter.write_line(line)
