@@ -34,7 +34,9 @@ def _f32(x):
 
 
 def _rel(a, b):
-    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+    v = float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+    print(f"max-abs-rel={v:.3e}")  # collected into the terminal summary (conftest.py)
+    return v
 
 
 GEMM_SHAPES = [(1, 64, 64), (77, 192, 256), (128, 128, 64), (300, 384, 1152), (1000, 256, 128),
