@@ -31,7 +31,14 @@ namespace {
 constexpr int GBM = 128, GBK = 64;
 
 constexpr int EPI_LD = 33;                       // staging row stride (floats, bank-free)
-constexpr int EPI_WARPS = 8;                     // two per TMEM lane quarter (column halves)
+// STADI_GEMM_EPI_WARPS (compile time): 8 = two per TMEM lane quarter (column halves); 4 =
+// one per quarter (6 warps per CTA, so the per-SM-sub-partition register budget allows
+// 256 registers per thread instead of 168: no epilogue spills)
+#ifndef STADI_GEMM_EPI_WARPS
+#define STADI_GEMM_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = STADI_GEMM_EPI_WARPS;
+constexpr int EPI_STEP = EPI_WARPS / 4;            // chunk stride of one epilogue warp
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int EPI_SMEM = EPI_WARPS * 32 * EPI_LD * 4;  // per warp 32 x 32 fp32 staging
 
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else {  // ---------------------------- epilogue warps 2..9
     const int qd = warp & 3;  // TMEM lane quarter this warp may access
-    const int half = (warp - 2) / 4;  // 32-column chunks half, half + 2, ... of the tile
+    const int half = (warp - 2) / 4;  // 32-column chunks half, half + EPI_STEP, ... of the tile
     constexpr int NCHUNK = BN / 32;
     static_assert(BN % 32 == 0, "epilogue chunks");
     // residual RMW epilogues use 16-byte accesses when every operand row is 16-B aligned
@@ -333,7 +340,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (ep.res_prefetch && ep.res && ksplit == 1 && row0 + lane < M) {
           const float *rp = ep.res + (long)(row0 + lane) * ep.ldr + nb * BN;
 #pragma unroll 1
-          for (int ch = half; ch < NCHUNK; ch += 2)
+          for (int ch = half; ch < NCHUNK; ch += EPI_STEP)
             asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(rp + 32 * ch));
         }
       }
@@ -342,13 +349,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + acc * BN;
       float *stg = stg_all + (warp - 2) * 32 * EPI_LD;
 #pragma unroll 1
-      for (int ch = half; ch < NCHUNK; ch += 2) {
+      for (int ch = half; ch < NCHUNK; ch += EPI_STEP) {
         const int c0 = 32 * ch;
         // TMEM -> registers (lane = row) -> smem, then coalesced: lanes cover
         // 16 column pairs of two rows per step
         float v[32];
         tmem_ld32(tbase + c0, v);
-        if (ch + 2 >= NCHUNK) {  // this warp's chunks read: release the accumulator
+        if (ch + EPI_STEP >= NCHUNK) {  // this warp's chunks read: release the accumulator
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
